@@ -1,0 +1,110 @@
+/*
+ * tkb_attn.h — C ABI of the B200-native (sm_100a) attention hot path.
+ *
+ * This is the drop-in boundary for the reference's attention entry points
+ * (reference = kittensim, /root/reference/proj/include/kittensim):
+ *
+ *   tkb_attn_fwd    replaces  attention_fwd_kernel(cfg, globals)      kernels.hpp:250-343
+ *                   + execute_functional(spec, pipeline_cfg, opts)   lcsf.hpp:779-819
+ *                   + attention_pipeline_config(cfg)                 kernels.hpp:345-355
+ *                   (paper entry: lcf::kernel<attn_fwd_template<D>>)
+ *   tkb_attn_validate replaces AttentionConfig::validate()            kernels.hpp:188-202
+ *   tkb_attn_bwd    new: the reference has no backward; it follows
+ *                   the restated oracle (oracle/attn_oracle.cpp) — dQ/dK/dV from saved L
+ *   error codes     mirror the exception taxonomy                     errors.hpp:9-46
+ *
+ * Conventions
+ *   - Tensors are row-major [B, H, N, D] bf16 (optionally strided over B, H, N;
+ *     D must be contiguous), as GlobalTensor::index (tiles.hpp:106-108).
+ *   - O is bf16 (the reference keeps fp32 O, kernels.hpp:212).
+ *   - lse is fp32 [B, H, N], contiguous: L_i = ln sum_j exp(scale * q_i . k_j)
+ *     over the unmasked keys (natural log).
+ *   - causal: key j is visible to query i iff j <= i (top-left aligned).
+ *   - All entry points are asynchronous on `stream` (a cudaStream_t), never
+ *     allocate, never throw, and are safe to call from several host threads on
+ *     distinct (device, stream) pairs. The last error message of the calling
+ *     thread is returned by tkb_last_error().
+ */
+#ifndef TKB_ATTN_H
+#define TKB_ATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TKB_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TKB_API __attribute__((visibility("default")))
+#else
+#define TKB_API
+#endif
+
+/* Error codes (errors.hpp:9-46). */
+enum tkb_status {
+    TKB_OK = 0,
+    TKB_ERR_CONFIG = 1,      /* ConfigError: bad shape/dim, non-finite input when checked */
+    TKB_ERR_SHAPE = 2,       /* ShapeError: strides / layout not supported            */
+    TKB_ERR_BOUNDS = 3,      /* BoundsError: null pointer / workspace too small        */
+    TKB_ERR_UNSUPPORTED = 4, /* device is not sm_100 (B200)                            */
+    TKB_ERR_CUDA = 5,        /* CUDA runtime / driver error                            */
+    TKB_ERR_CONTRACT = 6     /* ContractViolation: internal invariant broken           */
+};
+
+/* Problem descriptor — the AttentionConfig of kernels.hpp:168-176, minus the
+ * CPU-model knobs (kv_rows/qo_rows/num_workers are compile-time tile shapes here). */
+typedef struct tkb_attn_desc {
+    int32_t batches;      /* B >= 1 */
+    int32_t heads;        /* H >= 1 */
+    int32_t seq;          /* N >= 1 (query and key/value length) */
+    int32_t head_dim;     /* D in {64, 128} */
+    int32_t causal;       /* 0 / 1 */
+    int32_t check_finite; /* 1: scan inputs first and fail with TKB_ERR_CONFIG on inf/nan
+                             (kernels.hpp:277-284); synchronises the stream */
+    float softmax_scale;  /* <= 0: D^-1/2 */
+    int32_t reserved0;
+    /* element strides of q/k/v/o/do/dq/dk/dv; 0 = contiguous [B,H,N,D] */
+    int64_t stride_b;
+    int64_t stride_h;
+    int64_t stride_n;
+} tkb_attn_desc;
+
+/* Fill `desc` with a contiguous problem and default scale. */
+TKB_API void tkb_attn_desc_init(tkb_attn_desc* desc, int32_t batches, int32_t heads, int32_t seq, int32_t head_dim,
+                        int32_t causal);
+
+/* AttentionConfig::validate(): TKB_OK or TKB_ERR_CONFIG/SHAPE with a message. No device work. */
+TKB_API int tkb_attn_validate(const tkb_attn_desc* desc);
+
+/* Forward: o = softmax(scale * q k^T [+ causal mask]) v ; lse saved for the backward.
+ * lse may be NULL (inference). */
+TKB_API int tkb_attn_fwd(const tkb_attn_desc* desc, const void* q, const void* k, const void* v, void* o, float* lse,
+                 void* stream);
+
+/* Bytes of caller-provided device workspace the backward needs (fp32 dQ accumulator,
+ * delta = rowsum(dO * O), dQ ordering semaphores). */
+TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* desc);
+
+/* Backward from the saved lse: dq, dk, dv (bf16, same layout as q). Deterministic:
+ * repeated calls on the same inputs produce bit-identical outputs. */
+TKB_API int tkb_attn_bwd(const tkb_attn_desc* desc, const void* q, const void* k, const void* v, const void* o,
+                 const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* Multi-GPU sharding of the flattened batch x head grid:
+ * contiguous, balanced [begin, end) of `units` for `rank` of `world`. No collective. */
+TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
+
+/* Number of kernels the last successful fwd / bwd call on this thread launched. */
+TKB_API int tkb_last_launch_count(void);
+
+TKB_API const char* tkb_last_error(void);
+TKB_API int tkb_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TKB_ATTN_H */

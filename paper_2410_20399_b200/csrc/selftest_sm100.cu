@@ -1,0 +1,178 @@
+// selftest_sm100.cu — unit kernels for the tile primitives (TMA SW128 load,
+// tcgen05.mma SS/TS with K- and MN-major operands, TMEM ld/st). Each variant
+// computes one 128 x N fp32 tile that the tests compare with torch.
+//
+// These pin the descriptor encodings that fail silently:
+//   0: C = A  * B^T  A[128][K] K-major, B[N][K] K-major        (S = Q K^T)
+//   1: C = A  * B    A[128][K] K-major, B[K][N] MN-major       (O += P V, SS)
+//   2: C = A  * B    A in TMEM (bf16 pairs), B[K][N] MN-major   (O += P V, TS)
+//   3: C = A  * B    A stored transposed [K][128] (MN-major), B[K][N] MN-major (dQ = dS K)
+//   4: C = A^T * B^T-free check of TMEM st/ld round trip (C = A as fp32)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "host/tmap.hpp"
+#include "tkb/tcgen05.cuh"
+#include "tkb/tma.cuh"
+
+using namespace tkb;
+
+namespace {
+
+constexpr int M = 128;
+
+template <int N, int K, int VARIANT>
+__global__ void __launch_bounds__(128, 1)
+    selftest_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __nv_bfloat16* __restrict__ A_gmem, float* __restrict__ C) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;                 // up to 32 KB
+    uint8_t* sB = smem + 32768;         // up to 32 KB
+    __shared__ mbarrier bar_load, bar_mma;
+    __shared__ uint32_t tmem_base_slot;
+
+    const int warp = warpid();
+    const int lane = laneid();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_load, 1);
+        mbar_init(&bar_mma, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem::alloc<256>(&tmem_base_slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tbase = tmem_base_slot;
+    const uint32_t t_c = tbase;          // C: cols [0, N)
+    const uint32_t t_a = tbase + 128;    // A (TS variant): cols [128, 128 + K/2)
+
+    // A rows/cols as loaded: variant 3 stores A^T [K][128]
+    constexpr int A_ROWS = (VARIANT == 3) ? K : M;
+    constexpr int A_COLS = (VARIANT == 3) ? M : K;
+    constexpr int B_ROWS = (VARIANT == 0) ? N : K;
+    constexpr int B_COLS = (VARIANT == 0) ? K : N;
+
+    if (threadIdx.x == 0) {
+        uint32_t bytes = B_ROWS * B_COLS * 2;
+        if (VARIANT != 2) bytes += A_ROWS * A_COLS * 2;
+        mbar_arrive_expect_tx(&bar_load, bytes);
+        if (VARIANT != 2)
+            for (int a = 0; a < A_COLS / 64; ++a) tma::load_2d(sA + a * A_ROWS * 128, &tmA, &bar_load, a * 64, 0);
+        for (int a = 0; a < B_COLS / 64; ++a) tma::load_2d(sB + a * B_ROWS * 128, &tmB, &bar_load, a * 64, 0);
+    }
+    if (VARIANT == 2 || VARIANT == 4) {
+        // stage A (row = TMEM lane) into TMEM as bf16 pairs
+        const int row = warp * 32 + lane;
+        uint32_t r[64];
+#pragma unroll
+        for (int c = 0; c < K / 2; ++c) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(A_gmem + (size_t)row * K);
+            r[c] = src[c];
+        }
+        if constexpr (K == 128) {
+            tmem::st_32x32b_x64(tmem::addr(t_a, warp * 32, 0), r);
+        } else {
+            tmem::st_32x32b_x32(tmem::addr(t_a, warp * 32, 0), r);
+        }
+        tmem::wait_st();
+        tmem::fence_before();
+    }
+    __syncthreads();
+    tmem::fence_after();
+
+    if (VARIANT != 4 && warp == 0) {
+        mbar_wait(&bar_load, 0);
+        tmem::fence_after();
+        if (elect_one()) {
+            constexpr uint32_t idesc = umma::idesc_bf16<M, N, VARIANT == 3, VARIANT != 0>();
+#pragma unroll
+            for (int s = 0; s < K / 16; ++s) {
+                uint64_t bdesc;
+                if constexpr (VARIANT == 0) {
+                    bdesc = umma::desc_kmajor(smem_u32(sB + (s / 4) * (N * 128) + (s % 4) * 32));
+                } else {
+                    bdesc = umma::desc_mnmajor(smem_u32(sB + s * 16 * 128), K * 128);
+                }
+                if constexpr (VARIANT == 2) {
+                    umma::mma_ts(t_c, t_a + s * 8, bdesc, idesc, s > 0);
+                } else {
+                    uint64_t adesc;
+                    if constexpr (VARIANT == 3) {
+                        adesc = umma::desc_mnmajor(smem_u32(sA + s * 16 * 128), K * 128);
+                    } else {
+                        adesc = umma::desc_kmajor(smem_u32(sA + (s / 4) * (M * 128) + (s % 4) * 32));
+                    }
+                    umma::mma_ss(t_c, adesc, bdesc, idesc, s > 0);
+                }
+            }
+            umma::commit(&bar_mma);
+        }
+        __syncwarp();
+    }
+    if (VARIANT != 4) mbar_wait(&bar_mma, 0);
+    tmem::fence_after();
+    {
+        const int row = warp * 32 + lane;
+        uint32_t r[32];
+        if (VARIANT == 4) {
+            // read back the bf16-pair staging area and widen
+            for (int c0 = 0; c0 < K / 2; c0 += 32) {
+                tmem::ldw_32x32b_x32(tmem::addr(t_a, warp * 32, c0), r);
+                for (int j = 0; j < 32; ++j) {
+                    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&r[j]);
+                    C[(size_t)row * K + 2 * (c0 + j)] = __bfloat162float(h.x);
+                    C[(size_t)row * K + 2 * (c0 + j) + 1] = __bfloat162float(h.y);
+                }
+            }
+        } else {
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                tmem::ldw_32x32b_x32(tmem::addr(t_c, warp * 32, c0), r);
+                for (int j = 0; j < 32; ++j) C[(size_t)row * N + c0 + j] = __uint_as_float(r[j]);
+            }
+        }
+    }
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) tmem::dealloc<256>(tbase);
+}
+
+bool make_2d(CUtensorMap* tm, const void* p, int rows, int cols, std::string* err) {
+    uint64_t dims[2] = {(uint64_t)cols, (uint64_t)rows};
+    uint64_t strides[2] = {1, (uint64_t)cols};
+    uint32_t box[2] = {64, (uint32_t)rows};
+    return host::make_tmap(tm, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, strides, box,
+                           CU_TENSOR_MAP_SWIZZLE_128B, err);
+}
+
+template <int N, int K, int V>
+int launch(const void* A, const void* B, float* C, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    std::string err;
+    const int a_rows = (V == 3) ? K : M, a_cols = (V == 3) ? M : K;
+    const int b_rows = (V == 0) ? N : K, b_cols = (V == 0) ? K : N;
+    if (!make_2d(&ta, A, a_rows, a_cols, &err) || !make_2d(&tb, B, b_rows, b_cols, &err)) {
+        fprintf(stderr, "selftest tmap: %s\n", err.c_str());
+        return -1;
+    }
+    auto k = selftest_kernel<N, K, V>;
+    const int smem = 65536 + 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<<<1, 128, smem, st>>>(ta, tb, reinterpret_cast<const __nv_bfloat16*>(A), C);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_umma(int variant, int n, int k, const void* A, const void* B, float* C,
+                                 cudaStream_t stream) {
+#define TKB_ST(V, NN, KK) \
+    if (variant == V && n == NN && k == KK) return launch<NN, KK, V>(A, B, C, stream);
+    TKB_ST(0, 128, 128) TKB_ST(0, 128, 64) TKB_ST(1, 128, 128) TKB_ST(1, 64, 128) TKB_ST(2, 128, 128)
+    TKB_ST(2, 64, 128) TKB_ST(3, 128, 128) TKB_ST(3, 64, 128) TKB_ST(4, 128, 128)
+#undef TKB_ST
+    return -2;
+}

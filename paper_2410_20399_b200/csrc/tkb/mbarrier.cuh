@@ -1,0 +1,69 @@
+// mbarrier.cuh — the hardware form of the LCSF counter barrier.
+//
+// Reference semantics: kittensim::Barrier (lcsf.hpp:40-54) counts arrivals per
+// generation; a slot s of the N-stage ring is used by iteration i with
+// generation i / stages (lcsf.hpp:302-379). On Blackwell the same contract is
+// an mbarrier whose phase parity is generation & 1: a consumer waits on
+// full[s] with parity (i / stages) & 1, a producer waits on empty[s] with the
+// opposite parity before overwriting the slot.
+#pragma once
+#include "common.cuh"
+
+namespace tkb {
+
+struct alignas(8) mbarrier {
+    uint64_t word;
+};
+
+TKB_DEVICE void mbar_init(mbarrier* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+
+// Make barrier inits visible to the async proxy (TMA, tcgen05.commit).
+TKB_DEVICE void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+TKB_DEVICE void mbar_arrive(mbarrier* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+TKB_DEVICE void mbar_arrive_cnt(mbarrier* b, uint32_t cnt) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt)
+                 : "memory");
+}
+
+// Arrive once and announce `bytes` of TMA transactions for this phase.
+TKB_DEVICE void mbar_arrive_expect_tx(mbarrier* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+TKB_DEVICE bool mbar_try_wait(mbarrier* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// Blocking wait for the phase with the given parity to complete. In debug
+// builds a bounded spin traps (the DeadlockError analogue, lcsf.hpp:486-489).
+TKB_DEVICE void mbar_wait(mbarrier* b, uint32_t parity) {
+#ifdef TKB_DEBUG_DEADLOCK
+    uint64_t spins = 0;
+    while (!mbar_try_wait(b, parity)) {
+        if (++spins > (1ull << 28)) __trap();
+    }
+#else
+    while (!mbar_try_wait(b, parity)) {
+    }
+#endif
+}
+
+}  // namespace tkb
