@@ -1,0 +1,171 @@
+"""ctypes front-end of the CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module, and only as the checker or the timed CPU
+baseline. The product package (paper_2410_20399_b200) never imports it.
+
+  liboracle.so          fp64 restatement (oracle/attn_oracle.cpp), built by oracle/Makefile
+  _ref/libkittensim_ref.so  the UNMODIFIED reference attention path compiled from
+                        /root/reference/proj/include (oracle/ref_shim.cpp); prebuilt here,
+                        travels to the GPU box (git-ignored, not gpurun-ignored)
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libkittensim_ref.so")
+
+_F = ctypes.POINTER(ctypes.c_float)
+_D = ctypes.POINTER(ctypes.c_double)
+_cache = {}
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+def lib():
+    if "o" not in _cache:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = ctypes.CDLL(ORACLE_SO)
+        L.tkb_oracle_fill.argtypes = [ctypes.c_uint32, ctypes.c_float, ctypes.c_float, ctypes.c_int, _F,
+                                      ctypes.c_int64]
+        L.tkb_oracle_round_bf16.argtypes = [ctypes.c_float]
+        L.tkb_oracle_round_bf16.restype = ctypes.c_float
+        L.tkb_oracle_attn_fwd.argtypes = [_F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_double, _D, _D, ctypes.c_int]
+        L.tkb_oracle_attn_bwd.argtypes = [_F, _F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_double, _D, _D, _D, ctypes.c_int]
+        _cache["o"] = L
+    return _cache["o"]
+
+
+def ref_available():
+    return os.path.exists(REF_SO)
+
+
+def ref_lib():
+    if "r" not in _cache:
+        L = ctypes.CDLL(REF_SO)
+        L.kref_validate.argtypes = [ctypes.c_int] * 6 + [ctypes.c_char_p, ctypes.c_int]
+        L.kref_kv_tile_rows.argtypes = [ctypes.c_int]
+        L.kref_temperature_scale.argtypes = [ctypes.c_int]
+        L.kref_temperature_scale.restype = ctypes.c_double
+        L.kref_round_to_bf16.argtypes = [ctypes.c_float]
+        L.kref_round_to_bf16.restype = ctypes.c_float
+        L.kref_attention_fwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_uint64, _F, _F, _F, _F, ctypes.c_char_p,
+                                                              ctypes.c_int]
+        L.kref_oracle_attention.argtypes = [_D, _D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
+        L.kref_fill.argtypes = [ctypes.c_uint32, ctypes.c_float, ctypes.c_float, ctypes.c_int, _F, ctypes.c_int64]
+        _cache["r"] = L
+    return _cache["r"]
+
+
+def threads():
+    return max(1, os.cpu_count() or 1)
+
+
+# ------------------------------------------------------------------ generators
+
+
+def fill(seed, total, bf16=True, lo=-1.0, hi=1.0):
+    """fill_uniform (report.hpp:57-61) over one mt19937(seed) stream of `total` values."""
+    out = np.empty(total, dtype=np.float32)
+    lib().tkb_oracle_fill(seed, lo, hi, int(bf16), _ptr(out, _F), total)
+    return out
+
+
+def qkv(seed, B, H, N, D, bf16=True, scale_qk=1.0):
+    """Q then K then V from one stream, as the reference tests do (test_kernels.cpp:134-137).
+    scale_qk > 1 gives the 'peaky' distribution; values stay bf16-exact
+    for power-of-two scales."""
+    n = B * H * N * D
+    a = fill(seed, 3 * n, bf16).reshape(3, B, H, N, D)
+    q, k, v = a[0].copy(), a[1].copy(), a[2].copy()
+    if scale_qk != 1.0:
+        q *= scale_qk
+        k *= scale_qk
+    return q, k, v
+
+
+# ------------------------------------------------------------------ oracle
+
+
+def attn_fwd(q, k, v, causal=False, scale=None, nthreads=None):
+    """fp64 O [.., N, D] and L [.., N] for float32 inputs of shape [..., N, D]."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    k = np.ascontiguousarray(k, dtype=np.float32)
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    N, D = q.shape[-2:]
+    heads = int(np.prod(q.shape[:-2])) if q.ndim > 2 else 1
+    scale = scale if scale else 1.0 / np.sqrt(D)
+    o = np.empty(q.shape, dtype=np.float64)
+    lse = np.empty(q.shape[:-1], dtype=np.float64)
+    lib().tkb_oracle_attn_fwd(_ptr(q, _F), _ptr(k, _F), _ptr(v, _F), heads, N, D, int(causal), scale, _ptr(o, _D),
+                              _ptr(lse, _D), nthreads or threads())
+    return o, lse
+
+
+def attn_bwd(q, k, v, dout, causal=False, scale=None, nthreads=None):
+    q, k, v, dout = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v, dout))
+    N, D = q.shape[-2:]
+    heads = int(np.prod(q.shape[:-2])) if q.ndim > 2 else 1
+    scale = scale if scale else 1.0 / np.sqrt(D)
+    dq, dk, dv = (np.empty(q.shape, dtype=np.float64) for _ in range(3))
+    lib().tkb_oracle_attn_bwd(_ptr(q, _F), _ptr(k, _F), _ptr(v, _F), _ptr(dout, _F), heads, N, D, int(causal), scale,
+                              _ptr(dq, _D), _ptr(dk, _D), _ptr(dv, _D), nthreads or threads())
+    return dq, dk, dv
+
+
+# ------------------------------------------------------------------ reference (oracle/_ref)
+
+
+def ref_attention_fwd(q, k, v, kv_rows=0, workers=0, bf16=True, threaded=True, seed=0):
+    """The reference kernel path execute_functional(attention_fwd_kernel(cfg, g)) on [B,H,N,D] fp32."""
+    B, H, N, D = q.shape
+    q, k, v = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v))
+    o = np.empty_like(q)
+    err = ctypes.create_string_buffer(512)
+    rc = ref_lib().kref_attention_fwd(B, H, N, D, kv_rows, workers, int(bf16), int(threaded), seed, _ptr(q, _F),
+                                      _ptr(k, _F), _ptr(v, _F), _ptr(o, _F), err, 512)
+    if rc != 0:
+        raise RuntimeError(f"reference error {rc}: {err.value.decode()}")
+    return o
+
+
+def ref_oracle_attention(q, k, v):
+    """The reference fp64 oracle_attention for one head [N, D]."""
+    q, k, v = (np.ascontiguousarray(x, dtype=np.float64) for x in (q, k, v))
+    out = np.empty_like(q)
+    rc = ref_lib().kref_oracle_attention(_ptr(q, _D), _ptr(k, _D), _ptr(v, _D), q.shape[0], k.shape[0], q.shape[1],
+                                         _ptr(out, _D))
+    assert rc == 0
+    return out
+
+
+def ref_fill(seed, total, bf16=True, lo=-1.0, hi=1.0):
+    out = np.empty(total, dtype=np.float32)
+    ref_lib().kref_fill(seed, lo, hi, int(bf16), _ptr(out, _F), total)
+    return out
+
+
+# ------------------------------------------------------------------ metrics
+
+
+def max_abs(got, ref):
+    return float(np.max(np.abs(np.asarray(got, dtype=np.float64) - ref))) if np.size(ref) else 0.0
+
+
+def rel_l2(got, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    den = np.linalg.norm(ref)
+    return float(np.linalg.norm(np.asarray(got, dtype=np.float64) - ref) / (den if den > 0 else 1.0))

@@ -1,0 +1,227 @@
+"""Host-side mirror of the reference's attention interface, over the C ABI.
+
+Reference (kittensim, /root/reference/proj/include/kittensim):
+  AttentionConfig + validate()      kernels.hpp:168-203  -> AttentionConfig below
+  AttentionGlobals {q,k,v,o}        kernels.hpp:205-213  -> torch tensors [B,H,N,D] bf16
+  attention_fwd_kernel + execute_functional              -> attention_fwd()
+  exception taxonomy                errors.hpp:9-46      -> the classes below
+New (absent from the reference): causal masking, saved L,
+attention_bwd() producing dQ/dK/dV from L.
+
+Every call goes to the sm_100a kernels in libtkb.so through ctypes; there is no
+CPU or PyTorch fallback — a missing library or a non-B200 device raises.
+"""
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+from . import _lib
+
+# ---------------------------------------------------------------- errors.hpp:9-46
+
+
+class Error(RuntimeError):
+    """kittensim::Error"""
+
+
+class ConfigError(Error):
+    """kittensim::ConfigError — bad shape / dim / non-finite input."""
+
+
+class ShapeError(Error):
+    """kittensim::ShapeError — layout not supported."""
+
+
+class BoundsError(Error):
+    """kittensim::BoundsError — null pointer / workspace too small."""
+
+
+class ContractViolation(Error):
+    """kittensim::ContractViolation"""
+
+
+class UnsupportedDevice(Error):
+    """Device is not a B200 (sm_100)."""
+
+
+class CudaError(Error):
+    """CUDA runtime / driver error."""
+
+
+_CODES = {1: ConfigError, 2: ShapeError, 3: BoundsError, 4: UnsupportedDevice, 5: CudaError, 6: ContractViolation}
+
+
+class AttnDesc(ctypes.Structure):
+    """tkb_attn_desc (include/tkb_attn.h)."""
+
+    _fields_ = [
+        ("batches", ctypes.c_int32),
+        ("heads", ctypes.c_int32),
+        ("seq", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("causal", ctypes.c_int32),
+        ("check_finite", ctypes.c_int32),
+        ("softmax_scale", ctypes.c_float),
+        ("reserved0", ctypes.c_int32),
+        ("stride_b", ctypes.c_int64),
+        ("stride_h", ctypes.c_int64),
+        ("stride_n", ctypes.c_int64),
+    ]
+
+
+_VP = ctypes.c_void_p
+_SIGS = {
+    "tkb_attn_desc_init": (None, [ctypes.POINTER(AttnDesc)] + [ctypes.c_int32] * 5),
+    "tkb_attn_validate": (ctypes.c_int, [ctypes.POINTER(AttnDesc)]),
+    "tkb_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP]),
+    "tkb_attn_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
+    "tkb_attn_bwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
+    "tkb_shard_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "tkb_last_launch_count": (ctypes.c_int, []),
+    "tkb_last_error": (ctypes.c_char_p, []),
+    "tkb_abi_version": (ctypes.c_int, []),
+}
+
+
+def lib():
+    L = _lib.load()
+    if not getattr(L, "_tkb_typed", False):
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        L._tkb_typed = True
+    return L
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().tkb_last_error().decode(errors="replace")
+        raise _CODES.get(rc, Error)(msg)
+
+
+# ---------------------------------------------------------------- kernels.hpp:168-203
+
+
+@dataclass
+class AttentionConfig:
+    """The reference AttentionConfig minus its CPU-model knobs (kv_rows, qo_rows,
+    num_workers are compile-time tile shapes of the sm_100a kernels)."""
+
+    batches: int = 1
+    heads: int = 1
+    seq: int = 0
+    head_dim: int = 0
+    causal: bool = False
+    softmax_scale: Optional[float] = None
+    check_finite: bool = False
+
+    def temperature_scale(self) -> float:
+        """tau = softmax_scale * log2(e) (kernels.hpp:184-186)."""
+        s = self.softmax_scale if self.softmax_scale else 1.0 / math.sqrt(self.head_dim)
+        return s * 1.44269504089
+
+    def desc(self, strides=None) -> AttnDesc:
+        d = AttnDesc()
+        lib().tkb_attn_desc_init(ctypes.byref(d), self.batches, self.heads, self.seq, self.head_dim,
+                                 int(bool(self.causal)))
+        d.softmax_scale = float(self.softmax_scale or 0.0)
+        d.check_finite = int(bool(self.check_finite))
+        if strides is not None:
+            d.stride_b, d.stride_h, d.stride_n = strides
+        return d
+
+    def validate(self):
+        _check(lib().tkb_attn_validate(ctypes.byref(self.desc())))
+
+
+def _stream(torch_mod, dev):
+    return torch_mod.cuda.current_stream(dev).cuda_stream
+
+
+def _bhnd(t, name):
+    if t.dim() != 4:
+        raise ShapeError(f"{name} must be [B, H, N, D]")
+    if t.stride(3) != 1:
+        raise ShapeError(f"{name}: head_dim must be contiguous")
+    return t.stride(0), t.stride(1), t.stride(2)
+
+
+def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None, return_lse=True,
+                  check_finite=False):
+    """O = softmax(scale * Q K^T [causal]) V on the B200; returns (O, L) with L fp32 [B, H, N]."""
+    import torch
+
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise ConfigError("attention_fwd runs on the GPU only (no CPU fallback)")
+    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+        raise ConfigError("q, k, v must be bf16")
+    if q.shape != k.shape or q.shape != v.shape:
+        raise ShapeError("q, k, v must have the same [B, H, N, D] shape")
+    st = _bhnd(q, "q")
+    if _bhnd(k, "k") != st or _bhnd(v, "v") != st:
+        raise ShapeError("q, k, v must share strides")
+    B, H, N, D = q.shape
+    if out is None:
+        out = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+    elif _bhnd(out, "out") != st:
+        raise ShapeError("out must share q's strides")
+    if return_lse and lse is None:
+        lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
+    cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite)
+    d = cfg.desc(strides=st)
+    _check(lib().tkb_attn_fwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                              lse.data_ptr() if lse is not None else None, _stream(torch, q.device)))
+    return (out, lse) if return_lse else out
+
+
+def bwd_workspace_bytes(B, H, N, D, causal=False):
+    cfg = AttentionConfig(B, H, N, D, causal)
+    return int(lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(cfg.desc())))
+
+
+def attention_bwd(q, k, v, o, dout, lse, causal=False, softmax_scale=None, dq=None, dk=None, dv=None,
+                  workspace=None, check_finite=False):
+    """dQ, dK, dV from the saved L (deterministic)."""
+    import torch
+
+    for t, name in ((q, "q"), (k, "k"), (v, "v"), (o, "o"), (dout, "dout")):
+        if not t.is_cuda or t.dtype != torch.bfloat16:
+            raise ConfigError(f"{name} must be a bf16 CUDA tensor")
+    st = _bhnd(q, "q")
+    for t, name in ((k, "k"), (v, "v"), (o, "o"), (dout, "dout")):
+        if t.shape != q.shape or _bhnd(t, name) != st:
+            raise ShapeError(f"{name} must match q's shape and strides")
+    B, H, N, D = q.shape
+    if lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, N) or not lse.is_contiguous():
+        raise ShapeError("lse must be contiguous fp32 [B, H, N]")
+    mk = lambda: torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+    dq = mk() if dq is None else dq
+    dk = mk() if dk is None else dk
+    dv = mk() if dv is None else dv
+    cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite)
+    d = cfg.desc(strides=st)
+    ws_bytes = int(lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(d)))
+    if workspace is None or workspace.numel() * workspace.element_size() < ws_bytes:
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    _check(lib().tkb_attn_bwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                              dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                              workspace.data_ptr(), ws_bytes, _stream(torch, q.device)))
+    return dq, dk, dv
+
+
+def shard_range(units, rank, world):
+    """Contiguous balanced [begin, end) of the flattened batch x head grid for `rank`."""
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().tkb_shard_range(units, rank, world, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
+
+
+def last_launch_count():
+    return int(lib().tkb_last_launch_count())

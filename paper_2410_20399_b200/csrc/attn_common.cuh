@@ -1,0 +1,43 @@
+// attn_common.cuh — parameter blocks shared by the C-ABI layer and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tkb {
+
+// Tile shapes (compile time; the reference's runtime AttentionConfig knobs
+// kv_rows / qo_rows / num_workers, kernels.hpp:168-176, become these).
+constexpr int kBlockM = 128;   // query rows per tcgen05 M tile (one softmax warpgroup)
+constexpr int kBlockN = 128;   // key/value rows per KV tile
+constexpr int kQStages = 2;    // query tiles per CTA (ping-pong softmax warpgroups)
+constexpr int kRowsPerCta = kBlockM * kQStages;
+
+struct FwdParams {
+    CUtensorMap tm_q, tm_k, tm_v, tm_o;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128
+    float* lse;                          // [B*H, N] fp32, may be null
+    int n;                               // sequence length
+    int heads;
+    float scale_log2;                    // softmax_scale * log2(e)
+};
+
+struct BwdParams {
+    CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128
+    CUtensorMap tm_dk, tm_dv;             // stores, same layout
+    CUtensorMap tm_dqacc;                 // fp32 [B*H, Npad, D] accumulator, box {32, 128, 1}
+    const float* lse;                     // [B*H, N]
+    const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
+    float* dq_accum;                      // [B*H, Npad, D] fp32 (workspace)
+    int* dq_sema;                         // [B*H, Npad/128] ordering semaphores (workspace)
+    int n;
+    int n_pad;
+    int heads;
+    float scale;       // softmax_scale
+    float scale_log2;  // softmax_scale * log2(e)
+};
+
+// Launchers (return cudaError_t as int).
+int launch_attn_fwd(int head_dim, bool causal, const FwdParams& p, int batches, cudaStream_t stream);
+
+}  // namespace tkb

@@ -1,0 +1,234 @@
+// capi.cu — the C-ABI boundary (include/tkb_attn.h): validation with the
+// reference's error taxonomy, TMA descriptor construction, launches.
+// Never throws across the ABI; the last error message is thread-local.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "attn_common.cuh"
+#include "host/tmap.hpp"
+#include "tkb_attn.h"
+
+namespace tkb {
+int launch_attn_bwd(int head_dim, bool causal, const BwdParams& p, int batches, const void* o, const void* dout,
+                    int64_t stride_b, int64_t stride_h, int64_t stride_n, void* dq, cudaStream_t stream,
+                    int* launches);
+int launch_check_finite(const void* const* ptrs, int nptrs, int batches, int heads, int n, int d, int64_t sb,
+                        int64_t sh, int64_t sn, int* flag_dev, cudaStream_t stream);
+}  // namespace tkb
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+struct Strides {
+    int64_t b, h, n;
+};
+
+Strides strides_of(const tkb_attn_desc* d) {
+    Strides s;
+    s.n = d->stride_n ? d->stride_n : d->head_dim;
+    s.h = d->stride_h ? d->stride_h : (int64_t)d->seq * s.n;
+    s.b = d->stride_b ? d->stride_b : (int64_t)d->heads * s.h;
+    return s;
+}
+
+float scale_of(const tkb_attn_desc* d) {
+    return d->softmax_scale > 0.f ? d->softmax_scale : (float)(1.0 / std::sqrt((double)d->head_dim));
+}
+
+int check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    static thread_local int cached_dev = -1, cached_ok = 0;
+    if (cached_dev != dev) {
+        int major = 0, minor = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cached_dev = dev;
+        cached_ok = (major == 10 && minor == 0);
+        if (!cached_ok)
+            return fail(TKB_ERR_UNSUPPORTED, "device compute capability " + std::to_string(major) + "." +
+                                                 std::to_string(minor) + " is not sm_100 (B200)");
+    }
+    return cached_ok ? TKB_OK : fail(TKB_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
+}
+
+// 4-D {D, N, H, B} bf16 map with a {64, 128, 1, 1} SW128 box.
+int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, const Strides& s) {
+    uint64_t dims[4] = {(uint64_t)d->head_dim, (uint64_t)d->seq, (uint64_t)d->heads, (uint64_t)d->batches};
+    uint64_t strides[4] = {1, (uint64_t)s.n, (uint64_t)s.h, (uint64_t)s.b};
+    uint32_t box[4] = {64, 128, 1, 1};
+    std::string err;
+    if (!tkb::host::make_tmap(tm, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_128B, &err))
+        return fail(TKB_ERR_SHAPE, "tensor map: " + err);
+    return TKB_OK;
+}
+
+int finite_check(const tkb_attn_desc* d, const void* const* ptrs, int nptrs, const Strides& s, cudaStream_t st) {
+    int* flag = nullptr;
+    cudaError_t e = cudaMallocAsync(&flag, sizeof(int), st);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, "check_finite alloc failed");
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    int rc = tkb::launch_check_finite(ptrs, nptrs, d->batches, d->heads, d->seq, d->head_dim, s.b, s.h, s.n, flag,
+                                      st);
+    int host = 0;
+    cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(flag, st);
+    e = cudaStreamSynchronize(st);
+    if (rc != 0 || e != cudaSuccess) return fail(TKB_ERR_CUDA, "check_finite launch failed");
+    if (host) return fail(TKB_ERR_CONFIG, "attention inputs must be finite");  // kernels.hpp:280-283
+    return TKB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+TKB_API void tkb_attn_desc_init(tkb_attn_desc* d, int32_t batches, int32_t heads, int32_t seq, int32_t head_dim,
+                                int32_t causal) {
+    if (!d) return;
+    *d = tkb_attn_desc{};
+    d->batches = batches;
+    d->heads = heads;
+    d->seq = seq;
+    d->head_dim = head_dim;
+    d->causal = causal;
+}
+
+// AttentionConfig::validate (kernels.hpp:188-202), with the B200 tiling: any N >= 1
+// (tails are masked), D in {64, 128}.
+TKB_API int tkb_attn_validate(const tkb_attn_desc* d) {
+    if (!d) return fail(TKB_ERR_BOUNDS, "null descriptor");
+    if (d->head_dim != 64 && d->head_dim != 128) return fail(TKB_ERR_CONFIG, "head_dim must be 64 or 128");
+    if (d->batches < 1 || d->heads < 1 || d->seq < 1) return fail(TKB_ERR_CONFIG, "positive extents required");
+    if (d->causal != 0 && d->causal != 1) return fail(TKB_ERR_CONFIG, "causal must be 0 or 1");
+    if (!(std::isfinite(d->softmax_scale))) return fail(TKB_ERR_CONFIG, "softmax_scale must be finite");
+    if ((int64_t)d->batches * d->heads > (int64_t)65535 * 65535) return fail(TKB_ERR_CONFIG, "too many heads");
+    const Strides s = strides_of(d);
+    if (s.n < d->head_dim || s.h < 0 || s.b < 0 || (s.n % 8) || (s.h % 8) || (s.b % 8))
+        return fail(TKB_ERR_SHAPE, "strides must be multiples of 8 elements (16 B) with rows >= head_dim");
+    return TKB_OK;
+}
+
+TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, const void* v, void* o, float* lse,
+                         void* stream) {
+    g_launches = 0;
+    int rc = tkb_attn_validate(d);
+    if (rc) return rc;
+    if (!q || !k || !v || !o) return fail(TKB_ERR_BOUNDS, "null tensor pointer");
+    if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) & 15)
+        return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const Strides s = strides_of(d);
+    if (d->check_finite) {
+        const void* ptrs[3] = {q, k, v};
+        if ((rc = finite_check(d, ptrs, 3, s, st))) return rc;
+    }
+    tkb::FwdParams p{};
+    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, s)) ||
+        (rc = make_bhnd_map(&p.tm_v, v, d, s)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
+        return rc;
+    p.lse = lse;
+    p.n = d->seq;
+    p.heads = d->heads;
+    p.scale_log2 = scale_of(d) * 1.44269504088896340736f;
+    int e = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, st);
+    if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd launch: ") + cudaGetErrorString((cudaError_t)e));
+    g_launches = 1;
+    return TKB_OK;
+}
+
+TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* d) {
+    if (!d || d->seq < 1 || d->batches < 1 || d->heads < 1) return 0;
+    const size_t bh = (size_t)d->batches * d->heads;
+    const size_t npad = (size_t)((d->seq + 127) / 128) * 128;
+    size_t bytes = 0;
+    bytes += bh * npad * (size_t)d->head_dim * 4;  // dq accumulator fp32
+    bytes += bh * npad * 4;                        // delta
+    bytes += bh * (npad / 128) * 4;                // semaphores
+    return (bytes + 255) & ~(size_t)255;
+}
+
+TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, const void* v, const void* o,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    int rc = tkb_attn_validate(d);
+    if (rc) return rc;
+    if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv || !workspace)
+        return fail(TKB_ERR_BOUNDS, "null pointer");
+    if (workspace_bytes < tkb_attn_bwd_workspace_bytes(d)) return fail(TKB_ERR_BOUNDS, "workspace too small");
+    if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
+         (uintptr_t)dk | (uintptr_t)dv | (uintptr_t)workspace) &
+        15)
+        return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const Strides s = strides_of(d);
+    if (d->check_finite) {
+        const void* ptrs[5] = {q, k, v, o, dout};
+        if ((rc = finite_check(d, ptrs, 5, s, st))) return rc;
+    }
+    tkb::BwdParams p{};
+    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, s)) ||
+        (rc = make_bhnd_map(&p.tm_v, v, d, s)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
+        (rc = make_bhnd_map(&p.tm_dk, dk, d, s)) || (rc = make_bhnd_map(&p.tm_dv, dv, d, s)))
+        return rc;
+    const int64_t bh = (int64_t)d->batches * d->heads;
+    const int npad = (d->seq + 127) / 128 * 128;
+    uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+    p.dq_accum = reinterpret_cast<float*>(ws);
+    ws += (size_t)bh * npad * d->head_dim * 4;
+    p.delta = reinterpret_cast<float*>(ws);
+    ws += (size_t)bh * npad * 4;
+    p.dq_sema = reinterpret_cast<int*>(ws);
+    {
+        uint64_t dims[3] = {(uint64_t)d->head_dim, (uint64_t)npad, (uint64_t)bh};
+        uint64_t strides[3] = {1, (uint64_t)d->head_dim, (uint64_t)npad * d->head_dim};
+        uint32_t box[3] = {32, 128, 1};
+        std::string err;
+        if (!tkb::host::make_tmap(&p.tm_dqacc, p.dq_accum, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, dims, strides, box,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
+            return fail(TKB_ERR_SHAPE, "dq tensor map: " + err);
+    }
+    p.lse = lse;
+    p.n = d->seq;
+    p.n_pad = npad;
+    p.heads = d->heads;
+    p.scale = scale_of(d);
+    p.scale_log2 = p.scale * 1.44269504088896340736f;
+    int launches = 0;
+    int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, s.b, s.h, s.n, dq, st,
+                                 &launches);
+    if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_bwd launch: ") + cudaGetErrorString((cudaError_t)e));
+    g_launches = launches;
+    return TKB_OK;
+}
+
+TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
+    if (!begin || !end) return fail(TKB_ERR_BOUNDS, "null output");
+    if (world < 1 || rank < 0 || rank >= world || units < 0) return fail(TKB_ERR_CONFIG, "bad rank/world/units");
+    const int64_t base = units / world, rem = units % world;
+    *begin = rank * base + (rank < rem ? rank : rem);
+    *end = *begin + base + (rank < rem ? 1 : 0);
+    return TKB_OK;
+}
+
+TKB_API int tkb_last_launch_count(void) { return g_launches; }
+TKB_API const char* tkb_last_error(void) { return g_err.c_str(); }
+TKB_API int tkb_abi_version(void) { return TKB_ABI_VERSION; }
+
+}  // extern "C"
