@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""bench.py — the driver's benchmark contract for the B200 attention hot path.
+
+Metric (BASELINE.json): attention fwd/bwd TFLOPS/GPU, BF16, D=128, causal, and its
+fraction of the dense BF16 tensor peak. Workload (BASELINE configs[1]/[2]):
+B=16 H=16 N=4096 D=128 causal, one step = one forward (saving L) + one backward
+(dQ/dK/dV from L) over synthetic bf16 inputs resident in HBM (each input is 268 MB,
+larger than the 126 MB L2, so no L2 flush is needed between steps).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl tkb|reference] [--pass fwd|bwd|fwdbwd]
+
+Multi-GPU (torchrun, one process per GPU): the flattened batch x head grid of a
+global problem with B = 16 * world is sharded contiguously across ranks
+(tkb_shard_range); no collective touches the data path ("scaling": "weak").
+Time = max over ranks of the CUDA-event time of the K timed steps.
+
+FLOP convention (FlashAttention / SURVEY.md §8(d)): fwd 4 B H N^2 D, bwd 10 B H N^2 D,
+causal x 1/2.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_PER_GPU, H, N, D = 16, 16, 4096, 128
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tkb", choices=["tkb", "reference"])
+    ap.add_argument("--pass", dest="which", default="fwdbwd", choices=["fwd", "bwd", "fwdbwd"])
+    ap.add_argument("--causal", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=B_PER_GPU, help="per-GPU batch")
+    ap.add_argument("--heads", type=int, default=H)
+    ap.add_argument("--seq", type=int, default=N)
+    ap.add_argument("--head-dim", type=int, default=D)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def flops(b, h, n, d, causal, which):
+    f = 0.0
+    if "fwd" in which:
+        f += 4.0 * b * h * n * n * d
+    if "bwd" in which:
+        f += 10.0 * b * h * n * n * d
+    return f * (0.5 if causal else 1.0)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j, "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU legs (oracle / reference)
+
+
+def cpu_reference_sample(causal, which, seq, head_dim, nthreads=None):
+    """Time the reference's CPU path on a bounded sample: one (b,h) head per host thread.
+
+    fwd: the UNMODIFIED reference kernel path (oracle/_ref: execute_functional(
+         attention_fwd_kernel)) — it only supports non-causal attention, so it computes
+         the full N^2 (the FLOPs credited are the workload's own, causal-halved).
+    bwd: the reference has no backward; the oracle port's fp64 backward is timed.
+    """
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as orc
+
+    nthreads = nthreads or orc.threads()
+    heads = nthreads
+    q, k, v = orc.qkv(1234, 1, heads, seq, head_dim)
+    dout = orc.fill(99, heads * seq * head_dim).reshape(1, heads, seq, head_dim)
+    use_ref = orc.ref_available()
+    t0 = time.perf_counter()
+    if "fwd" in which:
+        if use_ref:
+            def one(hh):
+                return orc.ref_attention_fwd(q[:, hh:hh + 1], k[:, hh:hh + 1], v[:, hh:hh + 1], kv_rows=128,
+                                             workers=4, bf16=True, threaded=False)
+            with ThreadPoolExecutor(nthreads) as ex:
+                list(ex.map(one, range(heads)))
+        else:
+            orc.attn_fwd(q, k, v, causal=causal, nthreads=nthreads)
+    t1 = time.perf_counter()
+    if "bwd" in which:
+        orc.attn_bwd(q, k, v, dout, causal=causal, nthreads=nthreads)
+    t2 = time.perf_counter()
+    fl = flops(1, heads, seq, head_dim, causal, which)
+    return {
+        "value": fl / (t2 - t0) / 1e12,
+        "unit": "TFLOPS",
+        "cores": nthreads,
+        "kind": "reference" if (use_ref and "fwd" in which) else "port",
+        "sample": (f"{heads} (b,h) heads of N={seq} D={head_dim}, one per host thread; fwd = "
+                   f"{'reference execute_functional(attention_fwd_kernel) [non-causal only, bf16-emulated]' if use_ref else 'oracle port fp64'}"
+                   f" {t1 - t0:.2f}s; bwd = oracle port fp64 (reference has no backward) {t2 - t1:.2f}s"),
+        "seconds": t2 - t0,
+    }
+
+
+# ------------------------------------------------------------------ reference arm
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    causal = bool(args.causal)
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(causal, args.which, args.seq, args.head_dim)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference",
+        "metric": "attention fwd+bwd TFLOPS/GPU (BF16, D=128, causal)" if args.which == "fwdbwd"
+        else f"attention {args.which} TFLOPS/GPU (BF16, D=128, causal)",
+        "value": value,
+        "unit": "TFLOPS",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": base["seconds"] * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": workload_config(args, 1),
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world):
+    return {
+        "workload": f"attention {'fwd+bwd' if args.which == 'fwdbwd' else args.which} "
+                    f"{'causal' if args.causal else 'non-causal'} B={args.batch}/GPU H={args.heads} "
+                    f"N={args.seq} D={args.head_dim} bf16 (BASELINE configs[1]+[2])",
+        "batch_per_gpu": args.batch,
+        "global_batch": args.batch * world,
+        "heads": args.heads,
+        "seq_len": args.seq,
+        "head_dim": args.head_dim,
+        "causal": bool(args.causal),
+        "parallelism": f"bh-shard{world}",
+        "l2": "inputs larger than L2 (268 MB per tensor); no flush",
+    }
+
+
+# ------------------------------------------------------------------ tkb arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_20399_b200 import attention as A
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    causal = bool(args.causal)
+    b_loc, h, n, d = args.batch, args.heads, args.seq, args.head_dim
+    # global problem B = batch * world; this rank's contiguous (b,h) shard
+    units = b_loc * world * h
+    u0, u1 = A.shard_range(units, rank, world)
+    my_units = u1 - u0
+    gen = torch.Generator(device=dev).manual_seed(1000 + u0)  # per-shard seed: shards == the 1-GPU slices
+    shape = (1, my_units, n, d)
+    q = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
+    k = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
+    v = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
+    do = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
+    o = torch.empty_like(q)
+    lse = torch.empty((1, my_units, n), device=dev, dtype=torch.float32)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    ws = torch.empty(A.bwd_workspace_bytes(1, my_units, n, d, causal), device=dev, dtype=torch.uint8)
+    stream = torch.cuda.current_stream(dev)
+    which = args.which
+
+    launches = {"n": 0}
+
+    def step():
+        cnt = 0
+        if "fwd" in which:
+            A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse)
+            cnt += A.last_launch_count()
+        if "bwd" in which:
+            A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws)
+            cnt += A.last_launch_count()
+        launches["n"] += cnt
+
+    if "bwd" in which and "fwd" not in which:
+        A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # per-kernel timing (roofline): events around each kernel of one extra step
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    kern_ms = {}
+    for part in ("fwd", "bwd"):
+        if part not in which:
+            continue
+        e0, e1 = ev(), ev()
+        reps = 3
+        e0.record(stream)
+        for _ in range(reps):
+            if part == "fwd":
+                A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse)
+            else:
+                A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        kern_ms[part] = e0.elapsed_time(e1) / reps
+
+    # timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches["n"] = 0
+    start, end = ev(), ev()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # timing only, not on the data path
+    ms_max = float(t.item())
+    gpu_launches = launches["n"]
+
+    total_flops = flops(1, units, n, d, causal, which) * args.steps
+    value = total_flops / (ms_max / 1e3) / 1e12
+
+    # e2e through the public API with host buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
+        ho = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
+        hdq, hdk, hdv = (torch.empty(q.shape, dtype=torch.bfloat16).pin_memory() for _ in range(3))
+        h2d = d2h = 0
+
+        def e2e_step():
+            nonlocal h2d, d2h
+            h2d = d2h = 0
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            h2d += 3 * q.numel() * 2
+            if "bwd" in which:
+                do.copy_(hdo, non_blocking=True)
+                h2d += do.numel() * 2
+            if "fwd" in which:
+                A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse)
+                ho.copy_(o, non_blocking=True)
+                d2h += o.numel() * 2
+            if "bwd" in which:
+                A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws)
+                hdq.copy_(dq, non_blocking=True)
+                hdk.copy_(dk, non_blocking=True)
+                hdv.copy_(dv, non_blocking=True)
+                d2h += 3 * dq.numel() * 2
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        s2, e2 = ev(), ev()
+        s2.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2.record(stream)
+        torch.cuda.synchronize(dev)
+        t2 = torch.tensor([s2.elapsed_time(e2)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e_val = flops(1, units, n, d, causal, which) * e2e_steps / (float(t2.item()) / 1e3) / 1e12
+        e2e = {"value": e2e_val, "unit": "TFLOPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        dom = max(kern_ms, key=lambda x: kern_ms[x] * 1.0)
+        dom_flops = flops(1, my_units, n, d, causal, dom)
+        achieved = dom_flops / (kern_ms[dom] / 1e3) / 1e12
+        peak = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+        roofline = {
+            "bound": "tensor",
+            "kernel": f"attn_{dom}_kernel",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak,
+            "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)" if peak_src == "measured"
+            else "fallback 1.59 PFLOP/s (B200_PROFILING.md)",
+            "frac_of_sustained": achieved / float(peaks.get("bf16_tflops_sustained", 1400.0)),
+            "frac_of_spec_2250": achieved / 2250.0,
+            "traffic": load_traffic(dom),
+            "per_kernel_ms": kern_ms,
+            "per_kernel_tflops": {p: flops(1, my_units, n, d, causal, p) / (kern_ms[p] / 1e3) / 1e12
+                                  for p in kern_ms},
+        }
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                r = cpu_reference_sample(causal, which, n, d)
+                cpu = {k2: r[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as ex:  # the CPU leg is reported, never required
+                cpu = {"value": None, "unit": "TFLOPS", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+        line = {
+            "metric": "attention fwd+bwd TFLOPS/GPU (BF16, D=128, causal)" if which == "fwdbwd"
+            else f"attention {which} TFLOPS/GPU (BF16, D=128, causal)",
+            "value": value,
+            "unit": "TFLOPS",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic",
+            "config": workload_config(args, world),
+            "tflops_per_gpu": value / world,
+            "frac_of_peak": value / world / peak,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def load_traffic(kernel):
+    """dram bytes per launch from the committed ncu capture summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,12 +1,545 @@
-// attn_bwd_sm100.cu — attention backward (placeholder until the sm_100a kernel lands).
+// attn_bwd_sm100.cu — attention backward for B200 (sm_100a), dQ/dK/dV from the saved L.
+//
+// The reference has no backward; the math follows the restated
+// oracle (oracle/attn_oracle.cpp, bwd_head):
+//   P = exp(S - L), dV = P^T dO, dP = dO V^T, Delta = rowsum(dO o O),
+//   dS = P o (dP - Delta), dQ = scale dS K, dK = scale dS^T Q
+//
+// Three launches:
+//   bwd_prep    Delta = rowsum(dO o O), lse2 = L log2(e) (padded with +inf),
+//               reset the dQ ordering semaphores
+//   bwd_main    KV-stationary warp-specialised CTA (one 128-row K/V block per CTA,
+//               iterating over 128-row Q blocks), 5 tcgen05 GEMMs per tile pair:
+//                 S^T  = K Q^T       (SS)            -> TMEM S
+//                 dP^T = V dO^T      (SS)            -> TMEM dP
+//                 dV  += P^T dO      (TS, P in TMEM) -> TMEM dV
+//                 dK  += dS^T Q      (TS, dS in TMEM)-> TMEM dK
+//                 dQ_i = dS K        (SS, dS in SMEM)-> TMEM (aliases dP)
+//               dQ_i is reduced into an fp32 accumulator by TMA bulk stores/adds in a
+//               FIXED order per Q block (ordering semaphores) -> deterministic.
+//   bwd_convert dQ fp32 -> bf16
+//
+// Warp roles (512 threads):
+//   warps 0-7   COMPUTE: thread = (kv row r = TMEM lane, q half h); P, dS; dK/dV epilogue
+//   warps 8-11  REDUCE : thread = q row of dQ_i; TMEM -> regs -> SMEM -> TMA add
+//   warp 12     MMA    : one thread issues all tcgen05.mma
+//   warp 13     LOAD   : TMA K, V once; Q_i (+lse2) and dO_i (+Delta) rings
+//   warps 14-15 idle (complete the warpgroup for setmaxnreg)
+//
+// TMEM columns: S [0,128) | dV [128,128+D) | dP/dS/dQ [128+D, 256+D) | dK [256+D, 256+2D)
+// P^T (bf16) lives in S columns [32,96), dS^T in dP columns [32,96): each q half h
+// writes only inside the S/dP columns it has itself read ([64h, 64h+64)).
+//
+// Deterministic dQ order: CTA (bh, kv block j) visits Q blocks in the order
+//   causal:     i = j + t,            t = 0 .. nq-1-j
+//   non-causal: i = (j + t) mod nq,   t = 0 .. nq-1
+// so for every Q block the contributor at visit t is unique; it waits until the
+// block's semaphore equals t, stores (t == 0) or adds (t > 0), and bumps it.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "attn_common.cuh"
+#include "tkb/tcgen05.cuh"
+#include "tkb/tma.cuh"
 
 namespace tkb {
-int launch_attn_bwd(int, bool, const BwdParams&, int, const void*, const void*, int64_t, int64_t, int64_t, void*,
-                    cudaStream_t, int* launches) {
-    *launches = 0;
-    return (int)cudaErrorNotSupported;
+namespace bwd {
+
+template <int D>
+struct Cfg {
+    static constexpr int kAtoms = D / 64;
+    static constexpr int kAtomBytes = 128 * 128;        // 128 rows x 128 B
+    static constexpr int kTileBytes = 128 * D * 2;      // 128 x D bf16
+    static constexpr int kDoStages = (D == 128) ? 1 : 2;
+    static constexpr int kDqStageBytes = 128 * 32 * 4;  // 128 rows x 32 fp32 columns
+    static constexpr int kDqStages = (D == 128) ? 1 : 2;
+    // smem carve-up (all 1024-aligned)
+    static constexpr int kOffK = 0;
+    static constexpr int kOffV = kOffK + kTileBytes;
+    static constexpr int kOffQ = kOffV + kTileBytes;                    // 2 stages
+    static constexpr int kOffDo = kOffQ + 2 * kTileBytes;               // kDoStages
+    static constexpr int kOffDs = kOffDo + kDoStages * kTileBytes;      // 128 x 128 bf16
+    static constexpr int kOffDq = kOffDs + 128 * 128 * 2;               // kDqStages
+    static constexpr int kOffLse = kOffDq + kDqStages * kDqStageBytes;  // 2 x 128 fp32
+    static constexpr int kOffDelta = kOffLse + 2 * 128 * 4;             // kDoStages x 128 fp32
+    static constexpr int kSmemBytes = kOffDelta + kDoStages * 128 * 4 + 1024;
+    static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dv() { return 128u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 128u + D; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dk() { return 256u + D; }
+};
+
+constexpr int kThreads = 512;
+constexpr int kWarpReduce0 = 8;
+constexpr int kWarpMma = 12;
+constexpr int kWarpLoad = 13;
+constexpr int kComputeThreads = 256;
+constexpr int kReduceThreads = 128;
+constexpr int kBarCompute = 1;
+constexpr int kBarReduce = 2;
+
+TKB_DEVICE int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
+TKB_DEVICE void red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
+    using C = Cfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem + C::kOffK;
+    uint8_t* sV = smem + C::kOffV;
+    uint8_t* sQ = smem + C::kOffQ;
+    uint8_t* sDo = smem + C::kOffDo;
+    uint8_t* sDs = smem + C::kOffDs;
+    uint8_t* sDq = smem + C::kOffDq;
+    float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
+    float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
+
+    __shared__ mbarrier kv_full, q_full[2], q_empty[2], do_full[C::kDoStages], do_empty[C::kDoStages];
+    __shared__ mbarrier s_full, p_full, dp_full, ds_full, dq_full, dq_empty, dkv_full;
+    __shared__ uint32_t tmem_slot;
+
+    const int warp = warpid();
+    const int lane = laneid();
+    const int j = blockIdx.x;  // kv block
+    const int head = blockIdx.y;
+    const int batch = blockIdx.z;
+    const int bh = batch * p.heads + head;
+    const int kv0 = j * 128;
+    const int nq = p.n_pad / 128;
+    const int T = CAUSAL ? (nq - j) : nq;  // q blocks visited by this CTA
+    auto qblock = [&](int t) { return CAUSAL ? (j + t) : ((j + t) % nq); };
+
+    if (warp == kWarpLoad && lane == 0) {
+        mbar_init(&kv_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+        }
+        for (int s = 0; s < C::kDoStages; ++s) {
+            mbar_init(&do_full[s], 1);
+            mbar_init(&do_empty[s], 1 + kComputeThreads);  // MMA (dV done) + compute (Delta read)
+        }
+        mbar_init(&s_full, 1);
+        mbar_init(&p_full, kComputeThreads);
+        mbar_init(&dp_full, 1);
+        mbar_init(&ds_full, kComputeThreads);
+        mbar_init(&dq_full, 1);
+        mbar_init(&dq_empty, kReduceThreads);
+        mbar_init(&dkv_full, 1);
+        fence_barrier_init();
+        tma::prefetch_desc(&p.tm_q);
+        tma::prefetch_desc(&p.tm_k);
+        tma::prefetch_desc(&p.tm_v);
+        tma::prefetch_desc(&p.tm_do);
+    }
+    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tbase = tmem_slot;
+
+    if (warp >= kWarpMma) {
+        setmaxnreg_dec<56>();
+        if (warp == kWarpLoad && lane == 0) {
+            // ------------------------------------------------------------- LOAD
+            const uint64_t pol_stream = tma::policy_evict_first();
+            const uint64_t pol_keep = tma::policy_evict_last();
+            mbar_arrive_expect_tx(&kv_full, 2 * C::kTileBytes);
+            for (int a = 0; a < C::kAtoms; ++a) {
+                tma::load_4d(sK + a * C::kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, head, batch, pol_stream);
+                tma::load_4d(sV + a * C::kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, head, batch, pol_stream);
+            }
+            for (int t = 0; t < T; ++t) {
+                const int i = qblock(t);
+                const int qs = t & 1;
+                mbar_wait(&q_empty[qs], ((t >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&q_full[qs], C::kTileBytes + 512);
+                for (int a = 0; a < C::kAtoms; ++a)
+                    tma::load_4d(sQ + qs * C::kTileBytes + a * C::kAtomBytes, &p.tm_q, &q_full[qs], a * 64, i * 128,
+                                 head, batch, pol_keep);
+                tma::load_1d(sLse + qs * 128, p.lse2 + (size_t)bh * p.n_pad + i * 128, 512, &q_full[qs]);
+                const int ds = t % C::kDoStages;
+                mbar_wait(&do_empty[ds], ((t / C::kDoStages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&do_full[ds], C::kTileBytes + 512);
+                for (int a = 0; a < C::kAtoms; ++a)
+                    tma::load_4d(sDo + ds * C::kTileBytes + a * C::kAtomBytes, &p.tm_do, &do_full[ds], a * 64,
+                                 i * 128, head, batch, pol_keep);
+                tma::load_1d(sDelta + ds * 128, p.delta + (size_t)bh * p.n_pad + i * 128, 512, &do_full[ds]);
+            }
+        } else if (warp == kWarpMma && lane == 0) {
+            // ------------------------------------------------------------- MMA
+            constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
+            constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK (A in TMEM)
+            constexpr uint32_t id_q = umma::idesc_bf16<128, D, true, true>();      // dQ (A = dS MN-major)
+            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDs = smem_u32(sDs);
+            // X^T = A B^T with A = K or V [kv][D] and B = Q or dO [q][D], both K-major
+            auto mm_abt = [&](uint32_t dst, uint32_t a, uint32_t b) {
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint32_t off = (k / 4) * C::kAtomBytes + (k % 4) * 32;
+                    umma::mma_ss(tbase + dst, umma::desc_kmajor(a + off), umma::desc_kmajor(b + off), id_s, k > 0);
+                }
+            };
+            // acc += A[tmem] B with B = dO or Q [q][D] (MN-major)
+            auto mma_tb = [&](uint32_t dst, uint32_t a_tmem, uint32_t b, bool acc) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    umma::mma_ts(tbase + dst, tbase + a_tmem + k * 8, umma::desc_mnmajor(b + k * 2048, C::kAtomBytes),
+                                 id_kv, acc || k > 0);
+            };
+            auto mm_dq = [&]() {  // dQ = dS K : A = dS^T smem [kv][q] (MN-major), B = K [kv][D] (MN-major)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    umma::mma_ss(tbase + C::tmem_dp(), umma::desc_mnmajor(aDs + k * 2048, C::kAtomBytes),
+                                 umma::desc_mnmajor(aK + k * 2048, C::kAtomBytes), id_q, k > 0);
+            };
+            auto qaddr = [&](int t) { return smem_u32(sQ + (t & 1) * C::kTileBytes); };
+            auto doaddr = [&](int t) { return smem_u32(sDo + (t % C::kDoStages) * C::kTileBytes); };
+
+            mbar_wait(&kv_full, 0);
+            // prologue: S_0, dP_0, dV_0
+            mbar_wait(&q_full[0], 0);
+            tmem::fence_after();
+            mm_abt(C::tmem_s(), aK, qaddr(0));
+            umma::commit(&s_full);
+            mbar_wait(&do_full[0], 0);
+            tmem::fence_after();
+            mm_abt(C::tmem_dp(), aV, doaddr(0));
+            umma::commit(&dp_full);
+            mbar_wait(&p_full, 0);
+            tmem::fence_after();
+            mma_tb(C::tmem_dv(), C::tmem_s() + 32, doaddr(0), false);
+            umma::commit(&do_empty[0]);
+            for (int t = 0; t < T - 1; ++t) {
+                const uint32_t ph = (uint32_t)(t & 1);
+                const int t1 = t + 1;
+                // (1) S_{t+1}
+                mbar_wait(&q_full[t1 & 1], (t1 >> 1) & 1);
+                tmem::fence_after();
+                mm_abt(C::tmem_s(), aK, qaddr(t1));
+                umma::commit(&s_full);
+                // (2) dK += dS_t^T Q_t ; (3) dQ_t = dS_t K
+                mbar_wait(&ds_full, ph);
+                tmem::fence_after();
+                mma_tb(C::tmem_dk(), C::tmem_dp() + 32, qaddr(t), t > 0);
+                umma::commit(&q_empty[t & 1]);
+                mm_dq();
+                umma::commit(&dq_full);
+                // (4) dP_{t+1} once the reduce warps drained dQ_t
+                mbar_wait(&do_full[t1 % C::kDoStages], (t1 / C::kDoStages) & 1);
+                mbar_wait(&dq_empty, ph);
+                tmem::fence_after();
+                mm_abt(C::tmem_dp(), aV, doaddr(t1));
+                umma::commit(&dp_full);
+                // (5) dV += P_{t+1}^T dO_{t+1}
+                mbar_wait(&p_full, t1 & 1);
+                tmem::fence_after();
+                mma_tb(C::tmem_dv(), C::tmem_s() + 32, doaddr(t1), true);
+                umma::commit(&do_empty[t1 % C::kDoStages]);
+            }
+            // tail: dK, dQ of the last block
+            const int tl = T - 1;
+            mbar_wait(&ds_full, tl & 1);
+            tmem::fence_after();
+            mma_tb(C::tmem_dk(), C::tmem_dp() + 32, qaddr(tl), tl > 0);
+            umma::commit(&q_empty[tl & 1]);
+            mm_dq();
+            umma::commit(&dq_full);
+            umma::commit(&dkv_full);
+        }
+    } else if (warp >= kWarpReduce0) {
+        // ----------------------------------------------------------------- REDUCE (dQ)
+        setmaxnreg_inc<152>();
+        const int wq = warp - kWarpReduce0;
+        const int r = wq * 32 + lane;  // q row within the block == TMEM lane
+        const uint32_t tdq = tbase + ((uint32_t)(wq * 32) << 16) + C::tmem_dp();
+        const bool leader = (threadIdx.x == kWarpReduce0 * 32);
+        int* sema = p.dq_sema + (size_t)bh * nq;
+        for (int t = 0; t < T; ++t) {
+            const int i = qblock(t);
+            mbar_wait(&dq_full, t & 1);
+            tmem::fence_after();
+            uint32_t acc[D];
+#pragma unroll
+            for (int c = 0; c < D; c += 32) tmem::ld_32x32b_x32(tdq + c, acc + c);
+            tmem::wait_ld_x32(acc);  // pins acc[0..31]; later chunks are ordered by the same wait
+#pragma unroll
+            for (int c = 32; c < D; c += 32) tmem::wait_ld_x32(acc + c);
+            tmem::fence_before();
+            mbar_arrive(&dq_empty);
+            if (leader) {
+                if (t > 0) {  // release the previous block now that its adds have landed
+                    tma::wait_group<0>();
+                    tma::fence_async_global();
+                    __threadfence();
+                    red_release_add(sema + qblock(t - 1), 1);
+                }
+                while (ld_acquire(sema + i) != t) {
+                }
+                tma::fence_async_global();
+            }
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint8_t* buf = sDq + (c % C::kDqStages) * C::kDqStageBytes;
+                if (leader) tma::wait_group_read<C::kDqStages - 1>();
+                named_sync(kBarReduce, kReduceThreads);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {  // 8 chunks of 4 fp32 = 128 B row
+                    uint4 v = make_uint4(acc[c * 32 + q * 4 + 0], acc[c * 32 + q * 4 + 1], acc[c * 32 + q * 4 + 2],
+                                         acc[c * 32 + q * 4 + 3]);
+                    *reinterpret_cast<uint4*>(buf + r * 128 + ((q ^ (r & 7)) * 16)) = v;
+                }
+                tma::fence_async_smem();
+                named_sync(kBarReduce, kReduceThreads);
+                if (leader) {
+                    if (t == 0)
+                        tma::store_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
+                    else
+                        tma::reduce_add_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
+                    tma::commit_group();
+                }
+            }
+        }
+        if (leader) {
+            tma::wait_group<0>();
+            tma::fence_async_global();
+            __threadfence();
+            red_release_add(sema + qblock(T - 1), 1);
+        }
+    } else {
+        // ----------------------------------------------------------------- COMPUTE
+        setmaxnreg_inc<152>();
+        const int wq = warp & 3;
+        const int h = warp >> 2;       // q half: columns [64h, 64h+64)
+        const int r = wq * 32 + lane;  // kv row == TMEM lane
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const uint32_t tS = tbase + lane_off + C::tmem_s();
+        const uint32_t tDp = tbase + lane_off + C::tmem_dp();
+        const float tau = p.scale_log2;
+        const float scale = p.scale;
+        for (int t = 0; t < T; ++t) {
+            const int i = qblock(t);
+            const int qs = t & 1, ds = t % C::kDoStages;
+            const bool diag = CAUSAL && (i == j);
+            const float* lse = sLse + qs * 128 + 64 * h;
+            const float* dlt = sDelta + ds * 128 + 64 * h;
+            // P^T = exp2(tau S^T - lse2)
+            mbar_wait(&q_full[qs], (t >> 1) & 1);
+            mbar_wait(&s_full, t & 1);
+            tmem::fence_after();
+            float pf[64];
+            tmem::ld_32x32b_x32(tS + 64 * h, reinterpret_cast<uint32_t*>(pf));
+            tmem::ld_32x32b_x32(tS + 64 * h + 32, reinterpret_cast<uint32_t*>(pf) + 32);
+            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf));
+            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf) + 32);
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+                float p0 = ex2_approx(fmaf(pf[c], tau, -lse[c]));
+                float p1 = ex2_approx(fmaf(pf[c + 1], tau, -lse[c + 1]));
+                if (diag) {  // causal: key kv0 + r visible to query q0 + 64h + c iff r <= 64h + c
+                    if (64 * h + c < r) p0 = 0.f;
+                    if (64 * h + c + 1 < r) p1 = 0.f;
+                }
+                pf[c] = p0;
+                pf[c + 1] = p1;
+                pk[c / 2] = pack_bf16x2(p0, p1);
+            }
+            tmem::st_32x32b_x32(tS + 32 + 32 * h, pk);
+            tmem::wait_st();
+            tmem::fence_before();
+            mbar_arrive(&p_full);
+            // dS^T = P^T o (dP^T - Delta) * scale
+            mbar_wait(&do_full[ds], (t / C::kDoStages) & 1);
+            mbar_wait(&dp_full, t & 1);
+            tmem::fence_after();
+            uint8_t* dsrow = sDs + h * C::kAtomBytes + r * 128;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t dpv[32];
+                tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const int cc = 32 * half + c;
+                    const float d0 = pf[cc] * (__uint_as_float(dpv[c]) - dlt[cc]) * scale;
+                    const float d1 = pf[cc + 1] * (__uint_as_float(dpv[c + 1]) - dlt[cc + 1]) * scale;
+                    pk[cc / 2] = pack_bf16x2(d0, d1);
+                }
+            }
+            mbar_arrive(&do_empty[ds]);  // Delta consumed
+            tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                *reinterpret_cast<uint4*>(dsrow + ((q ^ (r & 7)) * 16)) =
+                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            tmem::wait_st();
+            tmem::fence_before();
+            tma::fence_async_smem();
+            mbar_arrive(&ds_full);
+        }
+        // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q ring is free) -> TMA store
+        mbar_wait(&dkv_full, 0);
+        tmem::fence_after();
+        uint8_t* stage_v = sQ;
+        uint8_t* stage_k = sQ + C::kTileBytes;
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {
+            const uint32_t tsrc = tbase + lane_off + (which == 0 ? C::tmem_dv() : C::tmem_dk());
+            uint8_t* stg = which == 0 ? stage_v : stage_k;
+#pragma unroll
+            for (int c = 0; c < D / 2; c += 32) {
+                const int col = h * (D / 2) + c;
+                uint32_t v[32];
+                tmem::ldw_32x32b_x32(tsrc + col, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int gc = col / 8 + q;  // global 16-byte chunk index within the row
+                    const int atom = gc / 8, ch = gc % 8;
+                    uint4 u;
+                    u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+                    u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+                    u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+                    u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+                    *reinterpret_cast<uint4*>(stg + atom * C::kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
+                }
+            }
+        }
+        tma::fence_async_smem();
+        named_sync(kBarCompute, kComputeThreads);
+        if (threadIdx.x == 0) {
+            for (int a = 0; a < C::kAtoms; ++a) {
+                tma::store_4d(&p.tm_dv, stage_v + a * C::kAtomBytes, a * 64, kv0, head, batch);
+                tma::store_4d(&p.tm_dk, stage_k + a * C::kAtomBytes, a * 64, kv0, head, batch);
+            }
+            tma::commit_group();
+            tma::wait_group_read<0>();
+        }
+    }
+
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
+}
+
+// Delta = rowsum(dO o O), lse2 = L log2 e (+inf / 0 on padded rows), semaphores = 0.
+template <int D>
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                                       const __nv_bfloat16* __restrict__ dout,
+                                                       const float* __restrict__ lse, float* __restrict__ lse2,
+                                                       float* __restrict__ delta, int* __restrict__ sema, int heads,
+                                                       int n, int n_pad, int64_t sb, int64_t sh, int64_t sn) {
+    constexpr int kLanesPerRow = D / 8;
+    constexpr int kRowsPerBlock = 256 / kLanesPerRow;
+    const int bh = blockIdx.y;
+    const int b = bh / heads, hh = bh % heads;
+    const int row = blockIdx.x * kRowsPerBlock + threadIdx.x / kLanesPerRow;
+    const int c = (threadIdx.x % kLanesPerRow) * 8;
+    float acc = 0.f;
+    if (row < n) {
+        const int64_t off = b * sb + hh * sh + (int64_t)row * sn + c;
+        const uint4 ov = *reinterpret_cast<const uint4*>(o + off);
+        const uint4 dv = *reinterpret_cast<const uint4*>(dout + off);
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 a = __bfloat1622float2(o2[k]);
+            const float2 g = __bfloat1622float2(d2[k]);
+            acc = fmaf(a.x, g.x, acc);
+            acc = fmaf(a.y, g.y, acc);
+        }
+    }
+#pragma unroll
+    for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
+        const size_t idx = (size_t)bh * n_pad + row;
+        delta[idx] = row < n ? acc : 0.f;
+        lse2[idx] = row < n ? lse[(size_t)bh * n + row] * 1.44269504088896340736f : INFINITY;
+    }
+    if (blockIdx.x == 0)
+        for (int k = threadIdx.x; k < n_pad / 128; k += blockDim.x) sema[(size_t)bh * (n_pad / 128) + k] = 0;
+}
+
+// dq (bf16, user layout) = dq_accum (fp32 [bh][n_pad][D])
+template <int D>
+__global__ void __launch_bounds__(256) bwd_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                                                          int heads, int n, int n_pad, int64_t sb, int64_t sh,
+                                                          int64_t sn, int64_t total_chunks) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_chunks;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(g % (D / 8)) * 8;
+        const int64_t rowg = g / (D / 8);
+        const int row = (int)(rowg % n);
+        const int bh = (int)(rowg / n);
+        const float* src = acc + ((size_t)bh * n_pad + row) * D + c;
+        const float4 a = *reinterpret_cast<const float4*>(src);
+        const float4 bq = *reinterpret_cast<const float4*>(src + 4);
+        uint4 u;
+        u.x = pack_bf16x2(a.x, a.y);
+        u.y = pack_bf16x2(a.z, a.w);
+        u.z = pack_bf16x2(bq.x, bq.y);
+        u.w = pack_bf16x2(bq.z, bq.w);
+        const int b = bh / heads, hh = bh % heads;
+        *reinterpret_cast<uint4*>(dq + b * sb + hh * sh + (int64_t)row * sn + c) = u;
+    }
+}
+
+template <int D, bool CAUSAL>
+int launch_main(const BwdParams& p, int batches, cudaStream_t stream) {
+    using C = Cfg<D>;
+    auto kern = attn_bwd_kernel<D, CAUSAL>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    dim3 grid(p.n_pad / 128, p.heads, batches);
+    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+template <int D>
+int launch_all(bool causal, const BwdParams& p, int batches, const void* o, const void* dout, const float* lse,
+               float* lse2, float* delta, float* dq_accum, int64_t sb, int64_t sh, int64_t sn, void* dq,
+               cudaStream_t stream, int* launches) {
+    constexpr int kRowsPerBlock = 256 / (D / 8);
+    const int bhs = batches * p.heads;
+    dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, bhs);
+    bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                              reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
+                                              p.dq_sema, p.heads, p.n, p.n_pad, sb, sh, sn);
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    e = causal ? launch_main<D, true>(p, batches, stream) : launch_main<D, false>(p, batches, stream);
+    if (e) return e;
+    const int64_t chunks = (int64_t)bhs * p.n * (D / 8);
+    const int blocks = (int)((chunks + 255) / 256 < 148 * 16 ? (chunks + 255) / 256 : 148 * 16);
+    bwd_convert_kernel<D><<<blocks, 256, 0, stream>>>(dq_accum, reinterpret_cast<__nv_bfloat16*>(dq), p.heads, p.n,
+                                                      p.n_pad, sb, sh, sn, chunks);
+    e = (int)cudaGetLastError();
+    if (e) return e;
+    *launches = 3;
+    return 0;
+}
+
+}  // namespace bwd
+
+int launch_attn_bwd(int head_dim, bool causal, const BwdParams& p, int batches, const void* o, const void* dout,
+                    const float* lse, float* lse2, float* delta, float* dq_accum, int64_t sb, int64_t sh, int64_t sn,
+                    void* dq, cudaStream_t stream, int* launches) {
+    if (head_dim == 128)
+        return bwd::launch_all<128>(causal, p, batches, o, dout, lse, lse2, delta, dq_accum, sb, sh, sn, dq, stream,
+                                    launches);
+    return bwd::launch_all<64>(causal, p, batches, o, dout, lse, lse2, delta, dq_accum, sb, sh, sn, dq, stream,
+                               launches);
+}
+
 }  // namespace tkb

@@ -23,13 +23,12 @@ struct FwdParams {
 };
 
 struct BwdParams {
-    CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128
-    CUtensorMap tm_dk, tm_dv;             // stores, same layout
-    CUtensorMap tm_dqacc;                 // fp32 [B*H, Npad, D] accumulator, box {32, 128, 1}
-    const float* lse;                     // [B*H, N]
+    CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128 (loads)
+    CUtensorMap tm_dk, tm_dv;             // same layout (stores)
+    CUtensorMap tm_dqacc;                 // fp32 {D, Npad, B*H}, box {32, 128, 1}, SW128
+    const float* lse2;                    // [B*H, Npad] L * log2(e); +inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
-    float* dq_accum;                      // [B*H, Npad, D] fp32 (workspace)
-    int* dq_sema;                         // [B*H, Npad/128] ordering semaphores (workspace)
+    int* dq_sema;                         // [B*H, Npad/128] dQ ordering semaphores (workspace)
     int n;
     int n_pad;
     int heads;

@@ -48,6 +48,34 @@ TKB_DEVICE void load_2d(void* smem_dst, const void* tmap, mbarrier* bar, int c0,
         : "memory");
 }
 
+// Non-tensor bulk copy global -> shared (16-byte aligned, size multiple of 16).
+TKB_DEVICE void load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, mbarrier* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+TKB_DEVICE void store_3d(const void* tmap, const void* smem_src, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(tmap)),
+        "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+TKB_DEVICE void reduce_add_3d(const void* tmap, const void* smem_src, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(tmap)),
+        "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// Order generic-proxy global accesses with async-proxy (TMA) ones.
+TKB_DEVICE void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 TKB_DEVICE void store_4d(const void* tmap, const void* smem_src, int c0, int c1, int c2, int c3) {
     asm volatile(
         "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(

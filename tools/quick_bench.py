@@ -1,0 +1,42 @@
+"""Quick kernel timing (CUDA events) of the fwd/bwd kernels at a few shapes."""
+import argparse
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2410_20399_b200 import attention as A
+
+def t_events(fn, iters=20, warmup=5):
+    for _ in range(warmup): fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for _ in range(iters):
+        s.record(); fn(); e.record(); torch.cuda.synchronize(); times.append(s.elapsed_time(e))
+    times.sort()
+    return times[len(times)//2]
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--bwd", action="store_true")
+ap.add_argument("--shapes", default="16,16,4096,128;16,16,4096,64;4,16,16384,128;16,16,1024,128")
+args = ap.parse_args()
+for sh in args.shapes.split(";"):
+    B, H, N, D = map(int, sh.split(","))
+    q, k, v = (torch.randn(B, H, N, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    for causal in (False, True):
+        o, lse = A.attention_fwd(q, k, v, causal=causal)
+        ms = t_events(lambda: A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse))
+        fl = 4 * B * H * N * N * D * (0.5 if causal else 1.0)
+        line = f"fwd B{B} H{H} N{N} D{D} causal={int(causal)}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOPS"
+        try:
+            ref = t_events(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal))
+            line += f"   | torch sdpa {fl/ref/1e9:7.1f} TFLOPS"
+        except Exception as ex:
+            line += f"   | sdpa err {ex}"
+        print(line, flush=True)
+        if args.bwd:
+            do = torch.randn_like(q)
+            ws = torch.empty(A.bwd_workspace_bytes(B, H, N, D), dtype=torch.uint8, device="cuda")
+            dq, dk, dv = A.attention_bwd(q, k, v, o, do, lse, causal=causal, workspace=ws)
+            ms = t_events(lambda: A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws))
+            fl = 10 * B * H * N * N * D * (0.5 if causal else 1.0)
+            print(f"bwd B{B} H{H} N{N} D{D} causal={int(causal)}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOPS", flush=True)
