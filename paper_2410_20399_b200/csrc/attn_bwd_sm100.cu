@@ -52,7 +52,7 @@ struct Cfg {
     static constexpr int kTileBytes = 128 * D * 2;      // 128 x D bf16
     static constexpr int kDoStages = (D == 128) ? 1 : 2;
     static constexpr int kDqStageBytes = 128 * 32 * 4;  // 128 rows x 32 fp32 columns
-    static constexpr int kDqStages = (D == 128) ? 1 : 2;
+    static constexpr int kDqStages = 2;                 // double-buffered dQ staging
     // smem carve-up (all 1024-aligned)
     static constexpr int kOffK = 0;
     static constexpr int kOffV = kOffK + kTileBytes;
@@ -62,7 +62,9 @@ struct Cfg {
     static constexpr int kOffDq = kOffDs + 128 * 128 * 2;               // kDqStages
     static constexpr int kOffLse = kOffDq + kDqStages * kDqStageBytes;  // 2 x 128 fp32
     static constexpr int kOffDelta = kOffLse + 2 * 128 * 4;             // kDoStages x 128 fp32
-    static constexpr int kSmemBytes = kOffDelta + kDoStages * 128 * 4 + 1024;
+    static constexpr int kOffBar = kOffDelta + kDoStages * 128 * 4;     // mbarriers + TMEM slot
+    static constexpr int kSmemBytes = kOffBar + 256 + 1024;             // + alignment slack
+    static_assert(kSmemBytes <= 232448, "exceeds 227 KB of shared memory");
     static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dv() { return 128u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 128u + D; }
@@ -73,6 +75,7 @@ constexpr int kThreads = 512;
 constexpr int kWarpReduce0 = 8;
 constexpr int kWarpMma = 12;
 constexpr int kWarpLoad = 13;
+constexpr int kWarpIssue0 = 14;  // warps 14, 15: dQ TMA issuers
 constexpr int kComputeThreads = 256;
 constexpr int kReduceThreads = 128;
 constexpr int kBarCompute = 1;
@@ -101,16 +104,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
     float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
 
-    __shared__ mbarrier kv_full, q_full[2], q_empty[2], do_full[C::kDoStages], do_empty[C::kDoStages];
-    __shared__ mbarrier s_full, p_full, dp_full, ds_full, dq_full, dq_empty, dkv_full;
-    __shared__ uint32_t tmem_slot;
+    // barriers live in dynamic smem (static smem would push D=128 past 227 KB)
+    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
+    mbarrier& kv_full = bars[0];
+    mbarrier* q_full = bars + 1;    // [2]
+    mbarrier* q_empty = bars + 3;   // [2]
+    mbarrier* do_full = bars + 5;   // [kDoStages <= 2]
+    mbarrier* do_empty = bars + 7;  // [kDoStages <= 2]
+    mbarrier& s_full = bars[9];
+    mbarrier& p_full = bars[10];
+    mbarrier& dp_full = bars[11];
+    mbarrier& ds_full = bars[12];
+    mbarrier& dq_full = bars[13];
+    mbarrier& dq_empty = bars[14];
+    mbarrier& dkv_full = bars[15];
+    mbarrier* chunk_full = bars + 16;   // [2] dQ staging buffer written (reduce warps)
+    mbarrier* chunk_empty = bars + 18;  // [2] dQ staging buffer read by TMA (issuer)
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 20);
+    volatile int* issued = reinterpret_cast<volatile int*>(bars + 21);  // dQ chunks handed to TMA so far
 
     const int warp = warpid();
     const int lane = laneid();
-    const int j = blockIdx.x;  // kv block
-    const int head = blockIdx.y;
-    const int batch = blockIdx.z;
-    const int bh = batch * p.heads + head;
+    // Work item from a start-order ticket rather than blockIdx: a CTA only ever waits (dQ
+    // ordering) on CTAs of its own head, and tickets guarantee every head is started
+    // contiguously, whatever order the hardware dispatches blocks in.
+    volatile int* ticket_slot = reinterpret_cast<volatile int*>(bars + 22);
+    if (threadIdx.x == 0) *ticket_slot = atomicAdd(p.ticket, 1);
+    __syncthreads();
+    const int item = *ticket_slot;
+    const int nkv_blocks = p.n_pad / 128;
+    const int bh = item / nkv_blocks;
+    const int j = item % nkv_blocks;  // kv block (heavy causal blocks first)
+    const int head = bh % p.heads;
+    const int batch = bh / p.heads;
     const int kv0 = j * 128;
     const int nq = p.n_pad / 128;
     const int T = CAUSAL ? (nq - j) : nq;  // q blocks visited by this CTA
@@ -133,6 +159,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         mbar_init(&dq_full, 1);
         mbar_init(&dq_empty, kReduceThreads);
         mbar_init(&dkv_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&chunk_full[b], kReduceThreads);
+            mbar_init(&chunk_empty[b], 1);
+        }
+        *issued = 0;
         fence_barrier_init();
         tma::prefetch_desc(&p.tm_q);
         tma::prefetch_desc(&p.tm_k);
@@ -179,26 +210,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
             constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK (A in TMEM)
             constexpr uint32_t id_q = umma::idesc_bf16<128, D, true, true>();      // dQ (A = dS MN-major)
             const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDs = smem_u32(sDs);
+            constexpr uint32_t HI = umma::desc_hi_sw128(1024);  // SBO = 8 rows x 128 B
             // X^T = A B^T with A = K or V [kv][D] and B = Q or dO [q][D], both K-major
             auto mm_abt = [&](uint32_t dst, uint32_t a, uint32_t b) {
+                a = umma::opaque(a);
+                b = umma::opaque(b);
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
                     const uint32_t off = (k / 4) * C::kAtomBytes + (k % 4) * 32;
-                    umma::mma_ss(tbase + dst, umma::desc_kmajor(a + off), umma::desc_kmajor(b + off), id_s, k > 0);
+                    umma::mma_ss_split(tbase + dst, umma::desc_lo(a + off, 16), HI, umma::desc_lo(b + off, 16), HI,
+                                       id_s, k > 0);
                 }
             };
             // acc += A[tmem] B with B = dO or Q [q][D] (MN-major)
             auto mma_tb = [&](uint32_t dst, uint32_t a_tmem, uint32_t b, bool acc) {
+                b = umma::opaque(b);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                    umma::mma_ts(tbase + dst, tbase + a_tmem + k * 8, umma::desc_mnmajor(b + k * 2048, C::kAtomBytes),
-                                 id_kv, acc || k > 0);
+                    umma::mma_ts_split(tbase + dst, tbase + a_tmem + k * 8, umma::desc_lo(b + k * 2048, C::kAtomBytes),
+                                       HI, id_kv, acc || k > 0);
             };
             auto mm_dq = [&]() {  // dQ = dS K : A = dS^T smem [kv][q] (MN-major), B = K [kv][D] (MN-major)
+                const uint32_t a = umma::opaque(aDs), b = umma::opaque(aK);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                    umma::mma_ss(tbase + C::tmem_dp(), umma::desc_mnmajor(aDs + k * 2048, C::kAtomBytes),
-                                 umma::desc_mnmajor(aK + k * 2048, C::kAtomBytes), id_q, k > 0);
+                    umma::mma_ss_split(tbase + C::tmem_dp(), umma::desc_lo(a + k * 2048, C::kAtomBytes), HI,
+                                       umma::desc_lo(b + k * 2048, C::kAtomBytes), HI, id_q, k > 0);
             };
             auto qaddr = [&](int t) { return smem_u32(sQ + (t & 1) * C::kTileBytes); };
             auto doaddr = [&](int t) { return smem_u32(sDo + (t % C::kDoStages) * C::kTileBytes); };
@@ -253,65 +290,77 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
             mm_dq();
             umma::commit(&dq_full);
             umma::commit(&dkv_full);
-        }
-    } else if (warp >= kWarpReduce0) {
-        // ----------------------------------------------------------------- REDUCE (dQ)
-        setmaxnreg_inc<152>();
-        const int wq = warp - kWarpReduce0;
-        const int r = wq * 32 + lane;  // q row within the block == TMEM lane
-        const uint32_t tdq = tbase + ((uint32_t)(wq * 32) << 16) + C::tmem_dp();
-        const bool leader = (threadIdx.x == kWarpReduce0 * 32);
-        int* sema = p.dq_sema + (size_t)bh * nq;
-        for (int t = 0; t < T; ++t) {
-            const int i = qblock(t);
-            mbar_wait(&dq_full, t & 1);
-            tmem::fence_after();
-            uint32_t acc[D];
-#pragma unroll
-            for (int c = 0; c < D; c += 32) tmem::ld_32x32b_x32(tdq + c, acc + c);
-            tmem::wait_ld_x32(acc);  // pins acc[0..31]; later chunks are ordered by the same wait
-#pragma unroll
-            for (int c = 32; c < D; c += 32) tmem::wait_ld_x32(acc + c);
-            tmem::fence_before();
-            mbar_arrive(&dq_empty);
-            if (leader) {
-                if (t > 0) {  // release the previous block now that its adds have landed
-                    tma::wait_group<0>();
-                    tma::fence_async_global();
-                    __threadfence();
-                    red_release_add(sema + qblock(t - 1), 1);
-                }
-                while (ld_acquire(sema + i) != t) {
-                }
+        } else if (warp >= kWarpIssue0 && lane == 0) {
+            // ------------------------------------------------------------- dQ TMA ISSUERS
+            // Two threads alternate Q blocks, so one can wait for its adds to land in
+            // L2 (needed before the ordering semaphore is released) while the other
+            // keeps draining staging chunks.
+            constexpr int NC = D / 32;
+            int* sema = p.dq_sema + (size_t)bh * nq;
+            for (int t = warp - kWarpIssue0; t < T; t += 2) {
+                const int i = qblock(t);
+                // visit t of block i is the t-th contributor; a lost contributor traps
+                // (~4 s) instead of hanging the GPU (DeadlockError analogue, lcsf.hpp:486-489)
+                for (long long t0 = clock64(); ld_acquire(sema + i) != t;)
+                    if (clock64() - t0 > (1ll << 33)) __trap();
                 tma::fence_async_global();
-            }
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint8_t* buf = sDq + (c % C::kDqStages) * C::kDqStageBytes;
-                if (leader) tma::wait_group_read<C::kDqStages - 1>();
-                named_sync(kBarReduce, kReduceThreads);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {  // 8 chunks of 4 fp32 = 128 B row
-                    uint4 v = make_uint4(acc[c * 32 + q * 4 + 0], acc[c * 32 + q * 4 + 1], acc[c * 32 + q * 4 + 2],
-                                         acc[c * 32 + q * 4 + 3]);
-                    *reinterpret_cast<uint4*>(buf + r * 128 + ((q ^ (r & 7)) * 16)) = v;
+                // hand-off: chunks are consumed strictly in order (mbarrier parity cannot
+                // express a wait more than one phase ahead)
+                while (*issued < t * NC) {
                 }
-                tma::fence_async_smem();
-                named_sync(kBarReduce, kReduceThreads);
-                if (leader) {
+                for (int c = 0; c < NC; ++c) {
+                    const int g = t * NC + c;
+                    const int b = g & 1;
+                    mbar_wait(&chunk_full[b], (g >> 1) & 1);
+                    const uint8_t* buf = sDq + b * C::kDqStageBytes;
                     if (t == 0)
                         tma::store_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
                     else
                         tma::reduce_add_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
                     tma::commit_group();
+                    tma::wait_group_read<0>();
+                    mbar_arrive(&chunk_empty[b]);
+                    *issued = g + 1;
                 }
+                tma::wait_group<0>();  // the adds have been performed
+                tma::fence_async_global();
+                __threadfence();
+                red_release_add(sema + i, 1);
             }
         }
-        if (leader) {
-            tma::wait_group<0>();
-            tma::fence_async_global();
-            __threadfence();
-            red_release_add(sema + qblock(T - 1), 1);
+    } else if (warp >= kWarpReduce0) {
+        // ----------------------------------------------------------------- REDUCE (dQ)
+        // TMEM -> registers (frees the dP/dQ columns at once) -> double-buffered SMEM
+        // chunks of 128 x 32 fp32; the TMA issuers (warps 14/15) drain the chunks.
+        setmaxnreg_inc<152>();
+        const int wq = warp - kWarpReduce0;
+        const int r = wq * 32 + lane;  // q row within the block == TMEM lane
+        const uint32_t tdq = tbase + ((uint32_t)(wq * 32) << 16) + C::tmem_dp();
+        constexpr int NC = D / 32;
+        for (int t = 0; t < T; ++t) {
+            mbar_wait(&dq_full, t & 1);
+            tmem::fence_after();
+            uint32_t acc[D];
+#pragma unroll
+            for (int c = 0; c < D; c += 32) tmem::ld_32x32b_x32(tdq + c, acc + c);
+#pragma unroll
+            for (int c = 0; c < D; c += 32) tmem::wait_ld_x32(acc + c);
+            tmem::fence_before();
+            mbar_arrive(&dq_empty);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int g = t * NC + c;
+                const int b = g & 1;
+                mbar_wait(&chunk_empty[b], ((g >> 1) & 1) ^ 1);
+                uint8_t* buf = sDq + b * C::kDqStageBytes;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)  // 8 chunks of 4 fp32 = one 128-B row
+                    *reinterpret_cast<uint4*>(buf + r * 128 + ((q ^ (r & 7)) * 16)) =
+                        make_uint4(acc[c * 32 + q * 4 + 0], acc[c * 32 + q * 4 + 1], acc[c * 32 + q * 4 + 2],
+                                   acc[c * 32 + q * 4 + 3]);
+                tma::fence_async_smem();
+                mbar_arrive(&chunk_full[b]);
+            }
         }
     } else {
         // ----------------------------------------------------------------- COMPUTE
@@ -433,7 +482,7 @@ template <int D>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ lse2,
-                                                       float* __restrict__ delta, int* __restrict__ sema, int heads,
+                                                       float* __restrict__ delta, int* __restrict__ sema, int* __restrict__ ticket, int heads,
                                                        int n, int n_pad, int64_t sb, int64_t sh, int64_t sn) {
     constexpr int kLanesPerRow = D / 8;
     constexpr int kRowsPerBlock = 256 / kLanesPerRow;
@@ -465,6 +514,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
     }
     if (blockIdx.x == 0)
         for (int k = threadIdx.x; k < n_pad / 128; k += blockDim.x) sema[(size_t)bh * (n_pad / 128) + k] = 0;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0;
 }
 
 // dq (bf16, user layout) = dq_accum (fp32 [bh][n_pad][D])
@@ -501,7 +551,7 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream) {
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
-    dim3 grid(p.n_pad / 128, p.heads, batches);
+    dim3 grid((p.n_pad / 128) * p.heads * batches);
     kern<<<grid, kThreads, C::kSmemBytes, stream>>>(p);
     return (int)cudaGetLastError();
 }
@@ -515,7 +565,7 @@ int launch_all(bool causal, const BwdParams& p, int batches, const void* o, cons
     dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, bhs);
     bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                               reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
-                                              p.dq_sema, p.heads, p.n, p.n_pad, sb, sh, sn);
+                                              p.dq_sema, p.ticket, p.heads, p.n, p.n_pad, sb, sh, sn);
     int e = (int)cudaGetLastError();
     if (e) return e;
     e = causal ? launch_main<D, true>(p, batches, stream) : launch_main<D, false>(p, batches, stream);

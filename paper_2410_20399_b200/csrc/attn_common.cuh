@@ -29,6 +29,7 @@ struct BwdParams {
     const float* lse2;                    // [B*H, Npad] L * log2(e); +inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
     int* dq_sema;                         // [B*H, Npad/128] dQ ordering semaphores (workspace)
+    int* ticket;                          // CTA start-order ticket (workspace, zeroed by bwd_prep)
     int n;
     int n_pad;
     int heads;

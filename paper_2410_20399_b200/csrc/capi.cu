@@ -160,6 +160,7 @@ TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* d) {
     bytes += bh * npad * 4;                        // delta
     bytes += bh * npad * 4;                        // lse2 (log2 domain, padded)
     bytes += bh * (npad / 128) * 4;                // semaphores
+    bytes += 16;                                   // CTA ticket
     return (bytes + 255) & ~(size_t)255;
 }
 
@@ -202,6 +203,8 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.delta = delta;
     p.lse2 = lse2;
     p.dq_sema = reinterpret_cast<int*>(ws);
+    ws += (size_t)bh * (npad / 128) * 4;
+    p.ticket = reinterpret_cast<int*>(ws);
     {
         uint64_t dims[3] = {(uint64_t)d->head_dim, (uint64_t)npad, (uint64_t)bh};
         uint64_t strides[3] = {1, (uint64_t)d->head_dim, (uint64_t)npad * d->head_dim};
