@@ -98,6 +98,11 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* desc, const void* q, const void* k
  * contiguous, balanced [begin, end) of `units` for `rank` of `world`. No collective. */
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
 
+/* Debug timeline of the backward kernel (the reference's Timeline, lcsf.hpp:165-224):
+ * device buffer of slots x 3 roles x 32 iterations x 8 events int64 cycle stamps for
+ * every `every`-th work item; NULL disables. Not thread-safe; debugging only. */
+TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots);
+
 /* Number of kernels the last successful fwd / bwd call on this thread launched. */
 TKB_API int tkb_last_launch_count(void);
 

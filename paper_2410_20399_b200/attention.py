@@ -80,6 +80,7 @@ _SIGS = {
     "tkb_shard_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "tkb_last_launch_count": (ctypes.c_int, []),
+    "tkb_debug_set_trace": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int]),
     "tkb_last_error": (ctypes.c_char_p, []),
     "tkb_abi_version": (ctypes.c_int, []),
 }
@@ -221,6 +222,12 @@ def shard_range(units, rank, world):
     b, e = ctypes.c_int64(), ctypes.c_int64()
     _check(lib().tkb_shard_range(units, rank, world, ctypes.byref(b), ctypes.byref(e)))
     return b.value, e.value
+
+
+def debug_set_trace(buf=None, every=1, slots=0):
+    """Enable the backward kernel's per-role cycle timeline into a device int64 tensor
+    [slots, 4, 32, 8] (debug only); buf=None disables."""
+    lib().tkb_debug_set_trace(buf.data_ptr() if buf is not None else None, every, slots)
 
 
 def last_launch_count():

@@ -25,17 +25,26 @@ struct FwdParams {
 struct BwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128 (loads)
     CUtensorMap tm_dk, tm_dv;             // same layout (stores)
-    CUtensorMap tm_dqacc;                 // fp32 {D, Npad, B*H}, box {32, 128, 1}, SW128
     const float* lse2;                    // [B*H, Npad] L * log2(e); +inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
+    float* dq_accum;                      // [B*H, Npad, D] fp32 dQ accumulator (workspace)
     int* dq_sema;                         // [B*H, Npad/128] dQ ordering semaphores (workspace)
     int* ticket;                          // CTA start-order ticket (workspace, zeroed by bwd_prep)
+    long long* trace;                     // optional per-role cycle timeline (tkb_debug_set_trace)
+    int trace_every;                      // trace work items with item % trace_every == 0
+    int trace_slots;
     int n;
     int n_pad;
     int heads;
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)
 };
+
+// Per-role cycle timeline (the Timeline of lcsf.hpp:165-224, recorded on the device):
+// trace[slot][role][iter][event] = clock64() - CTA start, roles MMA / COMPUTE / REDUCE.
+constexpr int kTraceIters = 32;
+constexpr int kTraceEvents = 8;
+constexpr int kTraceRoles = 4;  // + role 3: tensor-pipe completion stamps per GEMM
 
 // Launchers (return cudaError_t as int).
 int launch_attn_fwd(int head_dim, bool causal, const FwdParams& p, int batches, cudaStream_t stream);

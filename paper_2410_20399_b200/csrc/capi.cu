@@ -24,6 +24,8 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_trace)
+int g_trace_every = 1, g_trace_slots = 0;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -205,15 +207,10 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.dq_sema = reinterpret_cast<int*>(ws);
     ws += (size_t)bh * (npad / 128) * 4;
     p.ticket = reinterpret_cast<int*>(ws);
-    {
-        uint64_t dims[3] = {(uint64_t)d->head_dim, (uint64_t)npad, (uint64_t)bh};
-        uint64_t strides[3] = {1, (uint64_t)d->head_dim, (uint64_t)npad * d->head_dim};
-        uint32_t box[3] = {32, 128, 1};
-        std::string err;
-        if (!tkb::host::make_tmap(&p.tm_dqacc, dq_accum, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, dims, strides, box,
-                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
-            return fail(TKB_ERR_SHAPE, "dq tensor map: " + err);
-    }
+    p.dq_accum = dq_accum;
+    p.trace = g_trace;
+    p.trace_every = g_trace_every;
+    p.trace_slots = g_trace_slots;
     p.n = d->seq;
     p.n_pad = npad;
     p.heads = d->heads;
@@ -233,6 +230,13 @@ TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t*
     const int64_t base = units / world, rem = units % world;
     *begin = rank * base + (rank < rem ? rank : rem);
     *end = *begin + base + (rank < rem ? 1 : 0);
+    return TKB_OK;
+}
+
+TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots) {
+    g_trace = reinterpret_cast<long long*>(device_buf);
+    g_trace_every = every > 0 ? every : 1;
+    g_trace_slots = device_buf ? slots : 0;
     return TKB_OK;
 }
 

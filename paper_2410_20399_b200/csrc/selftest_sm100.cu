@@ -27,7 +27,8 @@ constexpr int M = 128;
 template <int N, int K, int VARIANT>
 __global__ void __launch_bounds__(128, 1)
     selftest_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __nv_bfloat16* __restrict__ A_gmem, float* __restrict__ C) {
+                    const __nv_bfloat16* __restrict__ A_gmem, float* __restrict__ C, int reps,
+                    long long* cycles) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;                 // up to 32 KB
@@ -89,6 +90,8 @@ __global__ void __launch_bounds__(128, 1)
         tmem::fence_after();
         if (elect_one()) {
             constexpr uint32_t idesc = umma::idesc_bf16<M, N, VARIANT == 3, VARIANT != 0>();
+            const long long c0 = clock64();
+            for (int rep = 0; rep < reps; ++rep)
 #pragma unroll
             for (int s = 0; s < K / 16; ++s) {
                 uint64_t bdesc;
@@ -110,6 +113,10 @@ __global__ void __launch_bounds__(128, 1)
                 }
             }
             umma::commit(&bar_mma);
+            if (cycles != nullptr) {
+                mbar_wait(&bar_mma, 0);
+                cycles[0] = clock64() - c0;
+            }
         }
         __syncwarp();
     }
@@ -149,7 +156,7 @@ bool make_2d(CUtensorMap* tm, const void* p, int rows, int cols, std::string* er
 }
 
 template <int N, int K, int V>
-int launch(const void* A, const void* B, float* C, cudaStream_t st) {
+int launch(const void* A, const void* B, float* C, cudaStream_t st, int reps, long long* cycles) {
     CUtensorMap ta, tb;
     std::string err;
     const int a_rows = (V == 3) ? K : M, a_cols = (V == 3) ? M : K;
@@ -161,16 +168,17 @@ int launch(const void* A, const void* B, float* C, cudaStream_t st) {
     auto k = selftest_kernel<N, K, V>;
     const int smem = 65536 + 1024;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<1, 128, smem, st>>>(ta, tb, reinterpret_cast<const __nv_bfloat16*>(A), C);
+    k<<<1, 128, smem, st>>>(ta, tb, reinterpret_cast<const __nv_bfloat16*>(A), C, reps, cycles);
     return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-extern "C" __attribute__((visibility("default"))) int tkb_selftest_umma(int variant, int n, int k, const void* A, const void* B, float* C,
-                                 cudaStream_t stream) {
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_umma(int variant, int n, int k, const void* A,
+                                                                       const void* B, float* C, cudaStream_t stream,
+                                                                       int reps, long long* cycles) {
 #define TKB_ST(V, NN, KK) \
-    if (variant == V && n == NN && k == KK) return launch<NN, KK, V>(A, B, C, stream);
+    if (variant == V && n == NN && k == KK) return launch<NN, KK, V>(A, B, C, stream, reps, cycles);
     TKB_ST(0, 128, 128) TKB_ST(0, 128, 64) TKB_ST(1, 128, 128) TKB_ST(1, 64, 128) TKB_ST(2, 128, 128)
     TKB_ST(2, 64, 128) TKB_ST(3, 128, 128) TKB_ST(3, 64, 128) TKB_ST(4, 128, 128)
 #undef TKB_ST

@@ -18,7 +18,7 @@ def _st():
     lib = _lib.load_selftest()
     f = lib.tkb_selftest_umma
     f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                  ctypes.c_void_p, ctypes.c_void_p]
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
     f.restype = ctypes.c_int
     return f
 
@@ -45,8 +45,25 @@ def test_umma_variant(cuda_dev, variant, n, k):
     C = torch.zeros(ref.shape, dtype=torch.float32, device=cuda_dev)
     a_ptr = A_rowmajor.data_ptr() if variant in (2, 4) else A_dev.data_ptr()
     rc = _st()(variant, n, k, a_ptr, B_dev.data_ptr(), C.data_ptr(),
-               torch.cuda.current_stream().cuda_stream)
+               torch.cuda.current_stream().cuda_stream, 1, None)
     assert rc == 0
     torch.cuda.synchronize()
     err = (C.cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), f"variant {variant}: max err {err}"
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_umma_throughput(cuda_dev, variant):
+    """Cycles per 128x128x16 tcgen05.mma for each operand flavour (single CTA, back to back)."""
+    n, k, reps = 128, 128, 200
+    A = torch.randn(128, k, device=cuda_dev).to(torch.bfloat16)
+    B = torch.randn(k, n, device=cuda_dev).to(torch.bfloat16)
+    C = torch.zeros(128, n, device=cuda_dev)
+    cyc = torch.zeros(1, dtype=torch.int64, device=cuda_dev)
+    rc = _st()(variant, n, k, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+               torch.cuda.current_stream().cuda_stream, reps, cyc.data_ptr())
+    assert rc == 0
+    torch.cuda.synchronize()
+    per_mma = cyc.item() / (reps * k / 16)
+    print(f"variant {variant}: {per_mma:.1f} cycles per 128x128x16 MMA")
+    assert per_mma < 1000

@@ -39,4 +39,12 @@ for sh in args.shapes.split(";"):
             dq, dk, dv = A.attention_bwd(q, k, v, o, do, lse, causal=causal, workspace=ws)
             ms = t_events(lambda: A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws))
             fl = 10 * B * H * N * N * D * (0.5 if causal else 1.0)
-            print(f"bwd B{B} H{H} N{N} D{D} causal={int(causal)}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOPS", flush=True)
+            line = f"bwd B{B} H{H} N{N} D{D} causal={int(causal)}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOPS"
+            try:
+                qr, kr, vr = (x.detach().clone().requires_grad_() for x in (q, k, v))
+                out = torch.nn.functional.scaled_dot_product_attention(qr, kr, vr, is_causal=causal)
+                ref = t_events(lambda: torch.autograd.grad(out, (qr, kr, vr), do, retain_graph=True))
+                line += f"   | torch sdpa bwd {fl/ref/1e9:7.1f} TFLOPS"
+            except Exception as ex:
+                line += f"   | sdpa bwd err {ex}"
+            print(line, flush=True)
