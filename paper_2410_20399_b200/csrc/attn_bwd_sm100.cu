@@ -50,18 +50,21 @@ struct Cfg {
     static constexpr int kAtoms = D / 64;
     static constexpr int kAtomBytes = 128 * 128;        // 128 rows x 128 B
     static constexpr int kTileBytes = 128 * D * 2;      // 128 x D bf16
-    static constexpr int kDoStages = 2;
+    static constexpr int kDoStages = (D == 128) ? 1 : 2;  // D=128: smem goes to dQ staging
+    static constexpr int kDqStageBytes = 128 * 32 * 4;    // 128 rows x 32 fp32 columns
+    static constexpr int kDqStages = 2;
     // smem carve-up (all 1024-aligned)
     static constexpr int kOffK = 0;
     static constexpr int kOffV = kOffK + kTileBytes;
     static constexpr int kOffQ = kOffV + kTileBytes;                    // 2 stages
     static constexpr int kOffDo = kOffQ + 2 * kTileBytes;               // kDoStages
     static constexpr int kOffDs = kOffDo + kDoStages * kTileBytes;      // 128 x 128 bf16
-    static constexpr int kOffLse = kOffDs + 128 * 128 * 2;              // 2 Q stages x 128 fp32
+    static constexpr int kOffDq = kOffDs + 128 * 128 * 2;               // kDqStages staging buffers
+    static constexpr int kOffLse = kOffDq + kDqStages * kDqStageBytes;  // 2 Q stages x 128 fp32
     static constexpr int kOffDelta = kOffLse + 2 * 128 * 4;             // 2 Q stages x 128 fp32
     static constexpr int kOffBar = kOffDelta + 2 * 128 * 4;             // mbarriers + TMEM slot
-    // No alignment slack: D=128 needs 231,680 B of the 232,448 available. The dynamic smem
-    // window starts 1 KB-aligned (after the driver's 1 KB reservation); checked at run time.
+    // No alignment slack: the dynamic smem window starts 1 KB-aligned (after the driver's
+    // 1 KB reservation); checked at run time.
     static constexpr int kSmemBytes = kOffBar + 256;  // 32 mbarrier slots
     static_assert(kSmemBytes <= 232448, "exceeds 227 KB of shared memory");
     static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
@@ -74,6 +77,7 @@ constexpr int kThreads = 512;
 constexpr int kWarpReduce0 = 8;
 constexpr int kWarpMma = 12;
 constexpr int kWarpLoad = 13;
+constexpr int kWarpIssue0 = 14;  // warps 14, 15: dQ TMA issuers
 constexpr int kComputeThreads = 256;
 constexpr int kReduceThreads = 128;
 constexpr int kBarCompute = 1;
@@ -99,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     uint8_t* sQ = smem + C::kOffQ;
     uint8_t* sDo = smem + C::kOffDo;
     uint8_t* sDs = smem + C::kOffDs;
+    uint8_t* sDq = smem + C::kOffDq;
     float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
     float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
 
@@ -117,7 +122,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbarrier& dq_empty = bars[14];
     mbarrier& dkv_full = bars[15];
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 20);
-    mbarrier* gdone = bars + 24;  // [5] debug: per-GEMM completion (S, dK, dQ, dP, dV) when tracing
+    mbarrier* chunk_full = bars + 16;   // [2] dQ staging buffer written (reduce warps)
+    mbarrier* chunk_empty = bars + 18;  // [2] dQ staging buffer read by TMA (issuers)
+    volatile int* issued = reinterpret_cast<volatile int*>(bars + 21);  // chunks handed to TMA
 
     const int warp = warpid();
     const int lane = laneid();
@@ -165,7 +172,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         mbar_init(&dq_full, 1);
         mbar_init(&dq_empty, kReduceThreads);
         mbar_init(&dkv_full, 1);
-        for (int g = 0; g < 5; ++g) mbar_init(&gdone[g], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&chunk_full[b], kReduceThreads);
+            mbar_init(&chunk_empty[b], 1);
+        }
+        *issued = 0;
         fence_barrier_init();
         tma::prefetch_desc(&p.tm_q);
         tma::prefetch_desc(&p.tm_k);
@@ -189,9 +200,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                 tma::load_4d(sK + a * C::kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, head, batch, pol_stream);
                 tma::load_4d(sV + a * C::kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, head, batch, pol_stream);
             }
-            for (int t = 0; t < T; ++t) {
-                const int i = qblock(t);
-                const int qs = t & 1;
+            // Issue order follows the order in which slots free up (dO_t after dV_t, Q_t after
+            // dK_t): dO_{t+1} is requested before Q_{t+2}, so neither waits behind the other.
+            auto load_q = [&](int t) {
+                const int i = qblock(t), qs = t & 1;
                 mbar_wait(&q_empty[qs], ((t >> 1) & 1) ^ 1);
                 mbar_arrive_expect_tx(&q_full[qs], C::kTileBytes + 1024);
                 for (int a = 0; a < C::kAtoms; ++a)
@@ -199,20 +211,60 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                                  head, batch, pol_keep);
                 tma::load_1d(sLse + qs * 128, p.lse2 + (size_t)bh * p.n_pad + i * 128, 512, &q_full[qs]);
                 tma::load_1d(sDelta + qs * 128, p.delta + (size_t)bh * p.n_pad + i * 128, 512, &q_full[qs]);
-                const int ds = t % C::kDoStages;
+            };
+            auto load_do = [&](int t) {
+                const int i = qblock(t), ds = t % C::kDoStages;
                 mbar_wait(&do_empty[ds], ((t / C::kDoStages) & 1) ^ 1);
                 mbar_arrive_expect_tx(&do_full[ds], C::kTileBytes);
                 for (int a = 0; a < C::kAtoms; ++a)
                     tma::load_4d(sDo + ds * C::kTileBytes + a * C::kAtomBytes, &p.tm_do, &do_full[ds], a * 64,
                                  i * 128, head, batch, pol_keep);
+            };
+            load_q(0);
+            load_do(0);
+            if (T > 1) load_q(1);
+            for (int t = 1; t < T; ++t) {
+                load_do(t);
+                if (t + 1 < T) load_q(t + 1);
             }
-        } else if (warp == kWarpMma + 2 && lane == 0 && tr != nullptr) {
-            // ------------------------------------------------------------- TRACE OBSERVER
-            for (int t = 0; t < T - 1; ++t)
-                for (int g = 0; g < 5; ++g) {
-                    mbar_wait(&gdone[g], t & 1);
-                    TKB_TR(3, t, g);
+        } else if (warp >= kWarpIssue0 && lane == 0) {
+            // ------------------------------------------------------------- dQ TMA ISSUERS
+            // Two threads alternate Q blocks, so one can wait for its adds to land in L2
+            // (required before the ordering semaphore is released) while the other keeps
+            // draining staging chunks. Chunks are consumed strictly in order (hand-off on
+            // `issued`): an mbarrier parity wait cannot look more than one phase ahead.
+            constexpr int NC = D / 32;
+            int* sema = p.dq_sema + (size_t)bh * nq;
+            for (int t = warp - kWarpIssue0; t < T; t += 2) {
+                const int i = qblock(t);
+                // visit t of block i is the t-th contributor; a lost contributor traps
+                // (~4 s) instead of hanging the GPU (DeadlockError analogue, lcsf.hpp:486-489)
+                for (long long t0 = clock64(); ld_acquire(sema + i) != t;)
+                    if (clock64() - t0 > (1ll << 33)) __trap();
+                tma::fence_async_global();
+                while (*issued < t * NC) {
                 }
+                if (warp == kWarpIssue0) TKB_TR(2, t, 2);
+                for (int c = 0; c < NC; ++c) {
+                    const int g = t * NC + c;
+                    const int b = g & 1;
+                    mbar_wait(&chunk_full[b], (g >> 1) & 1);
+                    const uint8_t* buf = sDq + b * C::kDqStageBytes;
+                    if (t == 0)
+                        tma::store_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
+                    else
+                        tma::reduce_add_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
+                    tma::commit_group();
+                    tma::wait_group_read<0>();
+                    mbar_arrive(&chunk_empty[b]);
+                    *issued = g + 1;
+                }
+                if (warp == kWarpIssue0) TKB_TR(2, t, 3);
+                tma::wait_group<0>();  // the adds have been performed
+                tma::fence_async_global();
+                __threadfence();
+                red_release_add(sema + i, 1);
+            }
         } else if (warp == kWarpMma && lane == 0) {
             // ------------------------------------------------------------- MMA
             constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
@@ -272,7 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                 tmem::fence_after();
                 mm_abt(C::tmem_s(), aK, qaddr(t1));
                 umma::commit(&s_full);
-                if (tr) umma::commit(&gdone[0]);
                 TKB_TR(0, t, 1);
                 // (2) dK += dS_t^T Q_t ; (3) dQ_t = dS_t K
                 mbar_wait(&ds_full, ph);
@@ -280,10 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                 tmem::fence_after();
                 mma_tb(C::tmem_dk(), C::tmem_dp() + 32, qaddr(t), t > 0);
                 umma::commit(&q_empty[t & 1]);
-                if (tr) umma::commit(&gdone[1]);
                 mm_dq();
                 umma::commit(&dq_full);
-                if (tr) umma::commit(&gdone[2]);
                 TKB_TR(0, t, 3);
                 // (4) dP_{t+1} once the reduce warps drained dQ_t
                 mbar_wait(&do_full[t1 % C::kDoStages], (t1 / C::kDoStages) & 1);
@@ -293,14 +342,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                 tmem::fence_after();
                 mm_abt(C::tmem_dp(), aV, doaddr(t1));
                 umma::commit(&dp_full);
-                if (tr) umma::commit(&gdone[3]);
                 // (5) dV += P_{t+1}^T dO_{t+1}
                 mbar_wait(&p_full, t1 & 1);
                 TKB_TR(0, t, 6);
                 tmem::fence_after();
                 mma_tb(C::tmem_dv(), C::tmem_s() + 32, doaddr(t1), true);
                 umma::commit(&do_empty[t1 % C::kDoStages]);
-                if (tr) umma::commit(&gdone[4]);
                 TKB_TR(0, t, 7);
             }
             // tail: dK, dQ of the last block
@@ -315,17 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
     } else if (warp >= kWarpReduce0) {
         // ----------------------------------------------------------------- REDUCE (dQ)
-        // TMEM -> registers (frees the dP/dQ columns at once), then the row is stored
-        // (first contributor) or added (red.global.add.v4.f32) into the fp32 accumulator,
-        // in the fixed per-block order enforced by the ordering semaphore.
+        // TMEM -> registers (frees the dP/dQ columns at once) -> double-buffered SMEM
+        // chunks of 128 x 32 fp32, drained by the TMA issuer threads (warps 14, 15).
         setmaxnreg_inc<152>();
         const int wq = warp - kWarpReduce0;
         const int r = wq * 32 + lane;  // q row within the block == TMEM lane
         const uint32_t tdq = tbase + ((uint32_t)(wq * 32) << 16) + C::tmem_dp();
         const bool leader = (threadIdx.x == kWarpReduce0 * 32);
-        int* sema = p.dq_sema + (size_t)bh * nq;
         for (int t = 0; t < T; ++t) {
-            const int i = qblock(t);
             mbar_wait(&dq_full, t & 1);
             if (leader) TKB_TR(2, t, 0);
             tmem::fence_after();
@@ -337,42 +381,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
             tmem::fence_before();
             mbar_arrive(&dq_empty);
             if (leader) TKB_TR(2, t, 1);
-            // Release the previous block only now: its adds had the whole dQ_t computation
-            // to land, so the fence is nearly free. (No cycle: the release of visit t-1
-            // depends only on this CTA's own pipeline, never on another semaphore.)
-            if (t > 0) {
-                __threadfence();  // this thread's adds of visit t-1 are performed
-                named_sync(kBarReduce, kReduceThreads);
-                if (leader) red_release_add(sema + qblock(t - 1), 1);
-            }
-            if (leader) {
-                // visit t of block i is the t-th contributor; a lost contributor traps
-                // (~4 s) instead of hanging the GPU (DeadlockError analogue, lcsf.hpp:486-489)
-                for (long long t0 = clock64(); ld_acquire(sema + i) != t;)
-                    if (clock64() - t0 > (1ll << 33)) __trap();
-            }
-            named_sync(kBarReduce, kReduceThreads);
-            if (leader) TKB_TR(2, t, 2);
-            float* dst = p.dq_accum + ((size_t)bh * p.n_pad + (size_t)i * 128 + r) * D;
-            if (t == 0) {
 #pragma unroll
-                for (int c = 0; c < D; c += 4)
-                    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c), "r"(acc[c]),
-                                 "r"(acc[c + 1]), "r"(acc[c + 2]), "r"(acc[c + 3])
-                                 : "memory");
-            } else {
+            for (int c = 0; c < D / 32; ++c) {
+                const int g = t * (D / 32) + c;
+                const int b = g & 1;
+                mbar_wait(&chunk_empty[b], ((g >> 1) & 1) ^ 1);
+                uint8_t* buf = sDq + b * C::kDqStageBytes;
 #pragma unroll
-                for (int c = 0; c < D; c += 4)
-                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c),
-                                 "f"(__uint_as_float(acc[c])), "f"(__uint_as_float(acc[c + 1])),
-                                 "f"(__uint_as_float(acc[c + 2])), "f"(__uint_as_float(acc[c + 3]))
-                                 : "memory");
+                for (int q = 0; q < 8; ++q)  // 8 chunks of 4 fp32 = one 128-B row (SW128)
+                    *reinterpret_cast<uint4*>(buf + r * 128 + ((q ^ (r & 7)) * 16)) =
+                        make_uint4(acc[c * 32 + q * 4 + 0], acc[c * 32 + q * 4 + 1], acc[c * 32 + q * 4 + 2],
+                                   acc[c * 32 + q * 4 + 3]);
+                tma::fence_async_smem();
+                mbar_arrive(&chunk_full[b]);
             }
-            if (leader) TKB_TR(2, t, 3);
         }
-        __threadfence();
-        named_sync(kBarReduce, kReduceThreads);
-        if (leader) red_release_add(sema + qblock(T - 1), 1);
     } else {
         // ----------------------------------------------------------------- COMPUTE
         setmaxnreg_inc<152>();

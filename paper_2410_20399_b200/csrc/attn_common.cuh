@@ -25,6 +25,7 @@ struct FwdParams {
 struct BwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128 (loads)
     CUtensorMap tm_dk, tm_dv;             // same layout (stores)
+    CUtensorMap tm_dqacc;                 // fp32 {D, Npad, B*H}, box {32, 128, 1}, SW128 (dQ adds)
     const float* lse2;                    // [B*H, Npad] L * log2(e); +inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
     float* dq_accum;                      // [B*H, Npad, D] fp32 dQ accumulator (workspace)
@@ -44,7 +45,7 @@ struct BwdParams {
 // trace[slot][role][iter][event] = clock64() - CTA start, roles MMA / COMPUTE / REDUCE.
 constexpr int kTraceIters = 32;
 constexpr int kTraceEvents = 8;
-constexpr int kTraceRoles = 4;  // + role 3: tensor-pipe completion stamps per GEMM
+constexpr int kTraceRoles = 4;
 
 // Launchers (return cudaError_t as int).
 int launch_attn_fwd(int head_dim, bool causal, const FwdParams& p, int batches, cudaStream_t stream);

@@ -208,6 +208,15 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     ws += (size_t)bh * (npad / 128) * 4;
     p.ticket = reinterpret_cast<int*>(ws);
     p.dq_accum = dq_accum;
+    {
+        uint64_t dims[3] = {(uint64_t)d->head_dim, (uint64_t)npad, (uint64_t)bh};
+        uint64_t strides[3] = {1, (uint64_t)d->head_dim, (uint64_t)npad * d->head_dim};
+        uint32_t box[3] = {32, 128, 1};
+        std::string err;
+        if (!tkb::host::make_tmap(&p.tm_dqacc, dq_accum, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, dims, strides, box,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
+            return fail(TKB_ERR_SHAPE, "dq tensor map: " + err);
+    }
     p.trace = g_trace;
     p.trace_every = g_trace_every;
     p.trace_slots = g_trace_slots;

@@ -184,3 +184,67 @@ extern "C" __attribute__((visibility("default"))) int tkb_selftest_umma(int vari
 #undef TKB_ST
     return -2;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Reduce-throughput microbenchmark: every CTA repeatedly adds 16 KB fp32 chunks from SMEM into
+// a global fp32 region (L2-resident), via (mode 0) the tensor TMA reduce {32 x 128 box, SW128},
+// (mode 1) the 1-D bulk reduce of a contiguous 16 KB, (mode 2) red.global.add.v4.f32 from
+// registers. `inflight` bulk groups may be outstanding. Returns nothing; time it with events.
+namespace {
+__global__ void __launch_bounds__(128, 1)
+    reduce_bench_kernel(const __grid_constant__ CUtensorMap tm, float* __restrict__ g, int mode, int iters,
+                        int inflight, int region_chunks) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    for (int i = threadIdx.x; i < 4 * 4096; i += 128) reinterpret_cast<float*>(smem)[i] = 1.0f;
+    tma::fence_async_smem();
+    __syncthreads();
+    if (mode == 2) {
+        for (int it = 0; it < iters; ++it) {
+            const int chunk = (blockIdx.x * 7 + it) % region_chunks;
+            float* dst = g + (size_t)chunk * 4096 + threadIdx.x * 32;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %1, %1, %1};" ::"l"(dst + c), "f"(1.0f) : "memory");
+        }
+        return;
+    }
+    if (threadIdx.x == 0) {
+        for (int it = 0; it < iters; ++it) {
+            const int chunk = (blockIdx.x * 7 + it) % region_chunks;
+            const uint8_t* src = smem + (it & 3) * 16384;
+            if (mode == 0) {
+                tma::reduce_add_3d(&tm, src, 0, (chunk % 64) * 128, chunk / 64);
+            } else {
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 16384;" ::"l"(
+                                 g + (size_t)chunk * 4096),
+                             "r"(smem_u32(src))
+                             : "memory");
+            }
+            tma::commit_group();
+            if (inflight <= 1) tma::wait_group_read<0>();
+            else if (inflight == 2) tma::wait_group_read<1>();
+            else tma::wait_group_read<3>();
+        }
+        tma::wait_group<0>();
+    }
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_reduce_bench(float* g, int mode, int ctas,
+                                                                               int iters, int inflight,
+                                                                               int region_chunks, cudaStream_t st) {
+    CUtensorMap tm;
+    std::string err;
+    // region viewed as {32 cols, 64*128 rows, region_chunks/64 planes}: chunk = 128 x 32 fp32 (row pitch 128 B)
+    uint64_t dims[3] = {32, 64 * 128, (uint64_t)(region_chunks / 64)};
+    uint64_t strides[3] = {1, 32, (uint64_t)64 * 128 * 32};
+    uint32_t box[3] = {32, 128, 1};
+    if (!host::make_tmap(&tm, g, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, dims, strides, box,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &err))
+        return -1;
+    const int smem = 4 * 16384 + 1024;
+    cudaFuncSetAttribute(reduce_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    reduce_bench_kernel<<<ctas, 128, smem, st>>>(tm, g, mode, iters, inflight, region_chunks);
+    return (int)cudaGetLastError();
+}

@@ -17,7 +17,7 @@ torch.cuda.synchronize()
 A.debug_set_trace(None)
 t = buf.cpu()
 names = {0: ["m.qwait", "m.S", "m.dsfull", "m.dQ", "m.dofull", "m.dqempty", "m.pfull", "m.dV"],
-         1: ["c.sfull", "c.Pdone", "c.dpfull", "c.dSdone"], 2: ["r.dqfull", "r.empty", "r.sema", "r.reds"],
+         1: ["c.sfull", "c.Pdone", "c.dpfull", "c.dSdone"], 2: ["r.dqfull", "r.empty", "i.start", "i.issued"],
          3: ["T.S", "T.dK", "T.dQ", "T.dP", "T.dV"]}
 for slot in (1, 4):
     print(f"--- slot {slot} (item {slot * every})")
