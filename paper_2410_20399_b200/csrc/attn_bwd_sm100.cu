@@ -5,36 +5,30 @@
 //   P = exp(S - L), dV = P^T dO, dP = dO V^T, Delta = rowsum(dO o O),
 //   dS = P o (dP - Delta), dQ = scale dS K, dK = scale dS^T Q
 //
-// Three launches:
-//   bwd_prep    Delta = rowsum(dO o O), lse2 = L log2(e) (padded with +inf),
-//               reset the dQ ordering semaphores
-//   bwd_main    KV-stationary warp-specialised CTA (one 128-row K/V block per CTA,
-//               iterating over 128-row Q blocks), 5 tcgen05 GEMMs per tile pair:
-//                 S^T  = K Q^T       (SS)            -> TMEM S
-//                 dP^T = V dO^T      (SS)            -> TMEM dP
-//                 dV  += P^T dO      (TS, P in TMEM) -> TMEM dV
-//                 dK  += dS^T Q      (TS, dS in TMEM)-> TMEM dK
-//                 dQ_i = dS K        (SS, dS in SMEM)-> TMEM (aliases dP)
-//               dQ_i is reduced into an fp32 accumulator by TMA bulk stores/adds in a
-//               FIXED order per Q block (ordering semaphores) -> deterministic.
-//   bwd_convert dQ fp32 -> bf16
+// Design: atomic-free, deterministic by construction. Three launches:
+//   bwd_prep   Delta = rowsum(dO o O) and lse2 = L log2(e) (+inf on padded rows)
+//   bwd_dkdv   KV-stationary: one 128-row K/V block per CTA, streaming Q/dO blocks;
+//              4 tcgen05 GEMMs per tile pair, dK/dV accumulate in TMEM:
+//                S^T  = K Q^T    (SS)            -> TMEM S
+//                dP^T = V dO^T   (SS)            -> TMEM dP
+//                dV  += P^T dO   (TS, P in TMEM)
+//                dK  += dS^T Q   (TS, dS in TMEM)
+//   bwd_dq     Q-stationary: one 128-row Q/dO block per CTA, streaming K/V blocks;
+//              3 GEMMs per tile pair, dQ accumulates in TMEM:
+//                S   = Q K^T     (SS)            -> TMEM S (double-buffered)
+//                dP  = dO V^T    (SS)            -> TMEM dP
+//                dQ += dS K      (TS, dS in TMEM)
+// A fused single kernel needs an fp32 reduction of a 128 x D dQ partial per tile pair
+// through L2; measured on this B200 the chip-wide fp32 add-reduce ceiling is ~5.6 TB/s
+// (tools/reduce_bench.py), which caps 128-row KV tiles well below the tensor rate.
+// Recomputing S and dP in bwd_dq (7 GEMMs instead of 5) costs less than that.
 //
-// Warp roles (512 threads):
-//   warps 0-7   COMPUTE: thread = (kv row r = TMEM lane, q half h); P, dS; dK/dV epilogue
-//   warps 8-11  REDUCE : thread = q row of dQ_i; TMEM -> regs -> SMEM -> TMA add
-//   warp 12     MMA    : one thread issues all tcgen05.mma
-//   warp 13     LOAD   : TMA K, V once; Q_i (+lse2) and dO_i (+Delta) rings
-//   warps 14-15 idle (complete the warpgroup for setmaxnreg)
-//
-// TMEM columns: S [0,128) | dV [128,128+D) | dP/dS/dQ [128+D, 256+D) | dK [256+D, 256+2D)
-// P^T (bf16) lives in S columns [32,96), dS^T in dP columns [32,96): each q half h
-// writes only inside the S/dP columns it has itself read ([64h, 64h+64)).
-//
-// Deterministic dQ order: CTA (bh, kv block j) visits Q blocks in the order
-//   causal:     i = j + t,            t = 0 .. nq-1-j
-//   non-causal: i = (j + t) mod nq,   t = 0 .. nq-1
-// so for every Q block the contributor at visit t is unique; it waits until the
-// block's semaphore equals t, stores (t == 0) or adds (t > 0), and bumps it.
+// Both main kernels: warps 0-7 COMPUTE (thread = (TMEM lane row, column half h)),
+// warp 8 MMA (one thread issues every tcgen05.mma), warp 9 LOAD (TMA).
+// bf16 P / dS live in TMEM next to the fp32 values they replace: half h writes only
+// columns [32 + 32h, 64 + 32h) of the S / dP region, i.e. inside the columns
+// [64h, 64h + 64) it has itself read. Tensor ops issued by one thread run in order,
+// so a GEMM that overwrites a region is always issued after the GEMM reading it.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -45,138 +39,152 @@
 namespace tkb {
 namespace bwd {
 
+constexpr int kThreads = 320;
+constexpr int kWarpMma = 8;
+constexpr int kWarpLoad = 9;
+constexpr int kComputeThreads = 256;
+constexpr int kBarCompute = 1;
+constexpr int kAtomBytes = 128 * 128;  // 128 rows x 128 B (one SW128 column block)
+
 template <int D>
-struct Cfg {
+struct Tiles {
     static constexpr int kAtoms = D / 64;
-    static constexpr int kAtomBytes = 128 * 128;        // 128 rows x 128 B
-    static constexpr int kTileBytes = 128 * D * 2;      // 128 x D bf16
-    static constexpr int kDoStages = (D == 128) ? 1 : 2;  // D=128: smem goes to dQ staging
-    static constexpr int kDqStageBytes = 128 * 32 * 4;    // 128 rows x 32 fp32 columns
-    static constexpr int kDqStages = 2;
-    // smem carve-up (all 1024-aligned)
+    static constexpr int kTileBytes = 128 * D * 2;  // 128 x D bf16
+};
+
+// ------------------------------------------------------------------------------ helpers
+
+constexpr uint32_t kDescHi = umma::desc_hi_sw128(1024);  // SBO = 8 rows x 128 B
+
+// X = A B^T with A [128 rows][D] and B [128 rows][D], both K-major (K = D)
+template <int D>
+TKB_DEVICE void mm_abt(uint32_t dst, uint32_t a, uint32_t b, uint32_t idesc) {
+    a = umma::opaque(a);
+    b = umma::opaque(b);
+#pragma unroll
+    for (int k = 0; k < D / 16; ++k) {
+        const uint32_t off = (k / 4) * kAtomBytes + (k % 4) * 32;
+        umma::mma_ss_split(dst, umma::desc_lo(a + off, 16), kDescHi, umma::desc_lo(b + off, 16), kDescHi, idesc,
+                           k > 0);
+    }
+}
+
+// acc (+)= A[tmem: 128 lanes x 128 K as bf16 pairs] B with B [128 K rows][D] MN-major
+TKB_DEVICE void mma_tmem_a(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc, bool acc) {
+    b = umma::opaque(b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        umma::mma_ts_split(dst, a_tmem + k * 8, umma::desc_lo(b + k * 2048, kAtomBytes), kDescHi, idesc,
+                           acc || k > 0);
+}
+
+// TMEM fp32 [lane r][D] -> bf16 -> SW128 smem tile: row r, columns [h*D/2, (h+1)*D/2)
+template <int D>
+TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int h) {
+#pragma unroll
+    for (int c = 0; c < D / 2; c += 32) {
+        const int col = h * (D / 2) + c;
+        uint32_t v[32];
+        tmem::ldw_32x32b_x32(tsrc + col, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int gc = col / 8 + q;  // 16-byte chunk index within the row
+            const int atom = gc / 8, ch = gc % 8;
+            uint4 u;
+            u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+            u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+            u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+            u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+            *reinterpret_cast<uint4*>(stage + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
+        }
+    }
+}
+
+TKB_DEVICE long long* trace_slot(const BwdParams& p, int lin, int kernel) {
+    if (p.trace == nullptr || lin % p.trace_every != 0 || lin / p.trace_every >= p.trace_slots) return nullptr;
+    // slot layout [slot][role][iter][event]; kernel 0 (dkdv) uses roles 0-1, kernel 1 (dq) roles 2-3
+    return p.trace + (size_t)(lin / p.trace_every) * kTraceRoles * kTraceIters * kTraceEvents +
+           (size_t)kernel * 2 * kTraceIters * kTraceEvents;
+}
+
+#define TKB_TR(role, t, ev)                                                               \
+    do {                                                                                  \
+        if (tr != nullptr && (t) < kTraceIters)                                           \
+            tr[((role) * kTraceIters + (t)) * kTraceEvents + (ev)] = clock64() - t_start; \
+    } while (0)
+
+// ================================================================== bwd_dkdv (KV-stationary)
+template <int D>
+struct CfgKV {
+    using T = Tiles<D>;
+    static constexpr int kStages = (D == 128) ? 2 : 3;  // Q and dO ring depth
     static constexpr int kOffK = 0;
-    static constexpr int kOffV = kOffK + kTileBytes;
-    static constexpr int kOffQ = kOffV + kTileBytes;                    // 2 stages
-    static constexpr int kOffDo = kOffQ + 2 * kTileBytes;               // kDoStages
-    static constexpr int kOffDs = kOffDo + kDoStages * kTileBytes;      // 128 x 128 bf16
-    static constexpr int kOffDq = kOffDs + 128 * 128 * 2;               // kDqStages staging buffers
-    static constexpr int kOffLse = kOffDq + kDqStages * kDqStageBytes;  // 2 Q stages x 128 fp32
-    static constexpr int kOffDelta = kOffLse + 2 * 128 * 4;             // 2 Q stages x 128 fp32
-    static constexpr int kOffBar = kOffDelta + 2 * 128 * 4;             // mbarriers + TMEM slot
-    // No alignment slack: the dynamic smem window starts 1 KB-aligned (after the driver's
-    // 1 KB reservation); checked at run time.
-    static constexpr int kSmemBytes = kOffBar + 256;  // 32 mbarrier slots
-    static_assert(kSmemBytes <= 232448, "exceeds 227 KB of shared memory");
+    static constexpr int kOffV = kOffK + T::kTileBytes;
+    static constexpr int kOffQ = kOffV + T::kTileBytes;
+    static constexpr int kOffDo = kOffQ + kStages * T::kTileBytes;
+    static constexpr int kOffLse = kOffDo + kStages * T::kTileBytes;  // kStages x 128 fp32
+    static constexpr int kOffDelta = kOffLse + kStages * 512;         // kStages x 128 fp32
+    static constexpr int kOffBar = kOffDelta + kStages * 512;
+    static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + alignment slack
+    static_assert(kSmemBytes <= 232448, "smem");
     static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dv() { return 128u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 128u + D; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dk() { return 256u + D; }
 };
 
-constexpr int kThreads = 512;
-constexpr int kWarpReduce0 = 8;
-constexpr int kWarpMma = 12;
-constexpr int kWarpLoad = 13;
-constexpr int kWarpIssue0 = 14;  // warps 14, 15: dQ TMA issuers
-constexpr int kComputeThreads = 256;
-constexpr int kReduceThreads = 128;
-constexpr int kBarCompute = 1;
-constexpr int kBarReduce = 2;
-
-TKB_DEVICE int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-TKB_DEVICE void red_release_add(int* p, int v) {
-    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
-    using C = Cfg<D>;
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid_constant__ BwdParams p) {
+    using C = CfgKV<D>;
+    using TL = Tiles<D>;
+    constexpr int S = C::kStages;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = smem_raw;
-    if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem + C::kOffK;
     uint8_t* sV = smem + C::kOffV;
     uint8_t* sQ = smem + C::kOffQ;
     uint8_t* sDo = smem + C::kOffDo;
-    uint8_t* sDs = smem + C::kOffDs;
-    uint8_t* sDq = smem + C::kOffDq;
     float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
     float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
-
-    // barriers live in dynamic smem (static smem would push D=128 past 227 KB)
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
     mbarrier& kv_full = bars[0];
-    mbarrier* q_full = bars + 1;    // [2]
-    mbarrier* q_empty = bars + 3;   // [2]
-    mbarrier* do_full = bars + 5;   // [kDoStages <= 2]
-    mbarrier* do_empty = bars + 7;  // [kDoStages <= 2]
-    mbarrier& s_full = bars[9];
-    mbarrier& p_full = bars[10];
-    mbarrier& dp_full = bars[11];
-    mbarrier& ds_full = bars[12];
-    mbarrier& dq_full = bars[13];
-    mbarrier& dq_empty = bars[14];
-    mbarrier& dkv_full = bars[15];
-    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 20);
-    mbarrier* chunk_full = bars + 16;   // [2] dQ staging buffer written (reduce warps)
-    mbarrier* chunk_empty = bars + 18;  // [2] dQ staging buffer read by TMA (issuers)
-    volatile int* issued = reinterpret_cast<volatile int*>(bars + 21);  // chunks handed to TMA
+    mbarrier& s_full = bars[1];
+    mbarrier& p_full = bars[2];
+    mbarrier& dp_full = bars[3];
+    mbarrier& ds_full = bars[4];
+    mbarrier& dkv_full = bars[5];
+    mbarrier* q_full = bars + 8;     // [S]
+    mbarrier* q_empty = bars + 12;   // [S]
+    mbarrier* do_full = bars + 16;   // [S]
+    mbarrier* do_empty = bars + 20;  // [S]
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
 
     const int warp = warpid();
     const int lane = laneid();
-    // Work item from a start-order ticket rather than blockIdx: a CTA only ever waits (dQ
-    // ordering) on CTAs of its own head, and tickets guarantee every head is started
-    // contiguously, whatever order the hardware dispatches blocks in.
-    volatile int* ticket_slot = reinterpret_cast<volatile int*>(bars + 22);
-    if (threadIdx.x == 0) *ticket_slot = atomicAdd(p.ticket, 1);
-    __syncthreads();
-    const int item = *ticket_slot;
-    const int nkv_blocks = p.n_pad / 128;
-    const int bh = item / nkv_blocks;
-    const int j = item % nkv_blocks;  // kv block (heavy causal blocks first)
-    const int head = bh % p.heads;
-    const int batch = bh / p.heads;
-    // optional timeline (debug): one slot per traced work item
-    long long* tr = nullptr;
-    const long long t_start = clock64();
-    if (p.trace != nullptr && item % p.trace_every == 0 && item / p.trace_every < p.trace_slots)
-        tr = p.trace + (size_t)(item / p.trace_every) * kTraceRoles * kTraceIters * kTraceEvents;
-#define TKB_TR(role, t, ev)                                                                      \
-    do {                                                                                         \
-        if (tr != nullptr && (t) < kTraceIters)                                                  \
-            tr[((role) * kTraceIters + (t)) * kTraceEvents + (ev)] = clock64() - t_start;        \
-    } while (0)
+    const int j = blockIdx.x;  // kv block; causal: small j visits the most q blocks, dispatched first
+    const int head = blockIdx.y;
+    const int batch = blockIdx.z;
+    const int bh = batch * p.heads + head;
     const int kv0 = j * 128;
     const int nq = p.n_pad / 128;
-    const int T = CAUSAL ? (nq - j) : nq;  // q blocks visited by this CTA
-    auto qblock = [&](int t) { return CAUSAL ? (j + t) : ((j + t) % nq); };
+    const int T = CAUSAL ? (nq - j) : nq;  // q blocks visited: i = j + t (causal) or t
+    auto qblock = [&](int t) { return CAUSAL ? (j + t) : t; };
+    long long* tr = trace_slot(p, bh * gridDim.x + j, 0);
+    const long long t_start = clock64();
 
     if (warp == kWarpLoad && lane == 0) {
         mbar_init(&kv_full, 1);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], 1);
-        }
-        for (int s = 0; s < C::kDoStages; ++s) {
-            mbar_init(&do_full[s], 1);
-            mbar_init(&do_empty[s], 1);  // MMA commit after dV
-        }
         mbar_init(&s_full, 1);
         mbar_init(&p_full, kComputeThreads);
         mbar_init(&dp_full, 1);
         mbar_init(&ds_full, kComputeThreads);
-        mbar_init(&dq_full, 1);
-        mbar_init(&dq_empty, kReduceThreads);
         mbar_init(&dkv_full, 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&chunk_full[b], kReduceThreads);
-            mbar_init(&chunk_empty[b], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+            mbar_init(&do_full[s], 1);
+            mbar_init(&do_empty[s], 1);
         }
-        *issued = 0;
         fence_barrier_init();
         tma::prefetch_desc(&p.tm_q);
         tma::prefetch_desc(&p.tm_k);
@@ -189,216 +197,86 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     tmem::fence_after();
     const uint32_t tbase = tmem_slot;
 
-    if (warp >= kWarpMma) {
-        setmaxnreg_dec<56>();
-        if (warp == kWarpLoad && lane == 0) {
+    if (warp == kWarpLoad) {
+        if (lane == 0) {
             // ------------------------------------------------------------- LOAD
             const uint64_t pol_stream = tma::policy_evict_first();
             const uint64_t pol_keep = tma::policy_evict_last();
-            mbar_arrive_expect_tx(&kv_full, 2 * C::kTileBytes);
-            for (int a = 0; a < C::kAtoms; ++a) {
-                tma::load_4d(sK + a * C::kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, head, batch, pol_stream);
-                tma::load_4d(sV + a * C::kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, head, batch, pol_stream);
+            mbar_arrive_expect_tx(&kv_full, 2 * TL::kTileBytes);
+            for (int a = 0; a < TL::kAtoms; ++a) {
+                tma::load_4d(sK + a * kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, head, batch, pol_stream);
+                tma::load_4d(sV + a * kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, head, batch, pol_stream);
             }
-            // Issue order follows the order in which slots free up (dO_t after dV_t, Q_t after
-            // dK_t): dO_{t+1} is requested before Q_{t+2}, so neither waits behind the other.
-            auto load_q = [&](int t) {
-                const int i = qblock(t), qs = t & 1;
-                mbar_wait(&q_empty[qs], ((t >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&q_full[qs], C::kTileBytes + 1024);
-                for (int a = 0; a < C::kAtoms; ++a)
-                    tma::load_4d(sQ + qs * C::kTileBytes + a * C::kAtomBytes, &p.tm_q, &q_full[qs], a * 64, i * 128,
+            for (int t = 0; t < T; ++t) {
+                const int i = qblock(t), s = t % S;
+                const uint32_t ph = ((t / S) & 1) ^ 1;
+                mbar_wait(&do_empty[s], ph);  // freed by dV_{t-S}, the first GEMM of its step
+                mbar_arrive_expect_tx(&do_full[s], TL::kTileBytes);
+                for (int a = 0; a < TL::kAtoms; ++a)
+                    tma::load_4d(sDo + s * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[s], a * 64, i * 128,
                                  head, batch, pol_keep);
-                tma::load_1d(sLse + qs * 128, p.lse2 + (size_t)bh * p.n_pad + i * 128, 512, &q_full[qs]);
-                tma::load_1d(sDelta + qs * 128, p.delta + (size_t)bh * p.n_pad + i * 128, 512, &q_full[qs]);
-            };
-            auto load_do = [&](int t) {
-                const int i = qblock(t), ds = t % C::kDoStages;
-                mbar_wait(&do_empty[ds], ((t / C::kDoStages) & 1) ^ 1);
-                mbar_arrive_expect_tx(&do_full[ds], C::kTileBytes);
-                for (int a = 0; a < C::kAtoms; ++a)
-                    tma::load_4d(sDo + ds * C::kTileBytes + a * C::kAtomBytes, &p.tm_do, &do_full[ds], a * 64,
-                                 i * 128, head, batch, pol_keep);
-            };
-            load_q(0);
-            load_do(0);
-            if (T > 1) load_q(1);
-            for (int t = 1; t < T; ++t) {
-                load_do(t);
-                if (t + 1 < T) load_q(t + 1);
+                mbar_wait(&q_empty[s], ph);  // freed by dK_{t-S}
+                mbar_arrive_expect_tx(&q_full[s], TL::kTileBytes + 1024);
+                for (int a = 0; a < TL::kAtoms; ++a)
+                    tma::load_4d(sQ + s * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[s], a * 64, i * 128,
+                                 head, batch, pol_keep);
+                tma::load_1d(sLse + s * 128, p.lse2 + (size_t)bh * p.n_pad + i * 128, 512, &q_full[s]);
+                tma::load_1d(sDelta + s * 128, p.delta + (size_t)bh * p.n_pad + i * 128, 512, &q_full[s]);
             }
-        } else if (warp >= kWarpIssue0 && lane == 0) {
-            // ------------------------------------------------------------- dQ TMA ISSUERS
-            // Two threads alternate Q blocks, so one can wait for its adds to land in L2
-            // (required before the ordering semaphore is released) while the other keeps
-            // draining staging chunks. Chunks are consumed strictly in order (hand-off on
-            // `issued`): an mbarrier parity wait cannot look more than one phase ahead.
-            constexpr int NC = D / 32;
-            int* sema = p.dq_sema + (size_t)bh * nq;
-            for (int t = warp - kWarpIssue0; t < T; t += 2) {
-                const int i = qblock(t);
-                // visit t of block i is the t-th contributor; a lost contributor traps
-                // (~4 s) instead of hanging the GPU (DeadlockError analogue, lcsf.hpp:486-489)
-                for (long long t0 = clock64(); ld_acquire(sema + i) != t;)
-                    if (clock64() - t0 > (1ll << 33)) __trap();
-                tma::fence_async_global();
-                while (*issued < t * NC) {
-                }
-                if (warp == kWarpIssue0) TKB_TR(2, t, 2);
-                for (int c = 0; c < NC; ++c) {
-                    const int g = t * NC + c;
-                    const int b = g & 1;
-                    mbar_wait(&chunk_full[b], (g >> 1) & 1);
-                    const uint8_t* buf = sDq + b * C::kDqStageBytes;
-                    if (t == 0)
-                        tma::store_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
-                    else
-                        tma::reduce_add_3d(&p.tm_dqacc, buf, c * 32, i * 128, bh);
-                    tma::commit_group();
-                    tma::wait_group_read<0>();
-                    mbar_arrive(&chunk_empty[b]);
-                    *issued = g + 1;
-                }
-                if (warp == kWarpIssue0) TKB_TR(2, t, 3);
-                tma::wait_group<0>();  // the adds have been performed
-                tma::fence_async_global();
-                __threadfence();
-                red_release_add(sema + i, 1);
-            }
-        } else if (warp == kWarpMma && lane == 0) {
+        }
+    } else if (warp == kWarpMma) {
+        if (lane == 0) {
             // ------------------------------------------------------------- MMA
             constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
-            constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK (A in TMEM)
-            constexpr uint32_t id_q = umma::idesc_bf16<128, D, true, true>();      // dQ (A = dS MN-major)
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDs = smem_u32(sDs);
-            constexpr uint32_t HI = umma::desc_hi_sw128(1024);  // SBO = 8 rows x 128 B
-            // X^T = A B^T with A = K or V [kv][D] and B = Q or dO [q][D], both K-major
-            auto mm_abt = [&](uint32_t dst, uint32_t a, uint32_t b) {
-                a = umma::opaque(a);
-                b = umma::opaque(b);
-#pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    const uint32_t off = (k / 4) * C::kAtomBytes + (k % 4) * 32;
-                    umma::mma_ss_split(tbase + dst, umma::desc_lo(a + off, 16), HI, umma::desc_lo(b + off, 16), HI,
-                                       id_s, k > 0);
-                }
-            };
-            // acc += A[tmem] B with B = dO or Q [q][D] (MN-major)
-            auto mma_tb = [&](uint32_t dst, uint32_t a_tmem, uint32_t b, bool acc) {
-                b = umma::opaque(b);
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    umma::mma_ts_split(tbase + dst, tbase + a_tmem + k * 8, umma::desc_lo(b + k * 2048, C::kAtomBytes),
-                                       HI, id_kv, acc || k > 0);
-            };
-            auto mm_dq = [&]() {  // dQ = dS K : A = dS^T smem [kv][q] (MN-major), B = K [kv][D] (MN-major)
-                const uint32_t a = umma::opaque(aDs), b = umma::opaque(aK);
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    umma::mma_ss_split(tbase + C::tmem_dp(), umma::desc_lo(a + k * 2048, C::kAtomBytes), HI,
-                                       umma::desc_lo(b + k * 2048, C::kAtomBytes), HI, id_q, k > 0);
-            };
-            auto qaddr = [&](int t) { return smem_u32(sQ + (t & 1) * C::kTileBytes); };
-            auto doaddr = [&](int t) { return smem_u32(sDo + (t % C::kDoStages) * C::kTileBytes); };
-
+            constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK
+            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+            auto qaddr = [&](int t) { return smem_u32(sQ + (t % S) * TL::kTileBytes); };
+            auto doaddr = [&](int t) { return smem_u32(sDo + (t % S) * TL::kTileBytes); };
             mbar_wait(&kv_full, 0);
-            // prologue: S_0, dP_0, dV_0
             mbar_wait(&q_full[0], 0);
             tmem::fence_after();
-            mm_abt(C::tmem_s(), aK, qaddr(0));
+            mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(0), id_s);
             umma::commit(&s_full);
             mbar_wait(&do_full[0], 0);
             tmem::fence_after();
-            mm_abt(C::tmem_dp(), aV, doaddr(0));
+            mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(0), id_s);
             umma::commit(&dp_full);
-            mbar_wait(&p_full, 0);
-            tmem::fence_after();
-            mma_tb(C::tmem_dv(), C::tmem_s() + 32, doaddr(0), false);
-            umma::commit(&do_empty[0]);
-            for (int t = 0; t < T - 1; ++t) {
-                const uint32_t ph = (uint32_t)(t & 1);
-                const int t1 = t + 1;
-                // (1) S_{t+1}
+            for (int t = 0; t < T; ++t) {
+                const uint32_t ph = t & 1;
+                // dV += P_t^T dO_t
                 TKB_TR(0, t, 0);
-                mbar_wait(&q_full[t1 & 1], (t1 >> 1) & 1);
-                tmem::fence_after();
-                mm_abt(C::tmem_s(), aK, qaddr(t1));
-                umma::commit(&s_full);
+                mbar_wait(&p_full, ph);
                 TKB_TR(0, t, 1);
-                // (2) dK += dS_t^T Q_t ; (3) dQ_t = dS_t K
-                mbar_wait(&ds_full, ph);
+                tmem::fence_after();
+                mma_tmem_a(tbase + C::tmem_dv(), tbase + C::tmem_s() + 32, doaddr(t), id_kv, t > 0);
+                umma::commit(&do_empty[t % S]);
+                // S_{t+1}: overwrites P_t, read by dV_t which was issued before
+                if (t + 1 < T) {
+                    mbar_wait(&q_full[(t + 1) % S], ((t + 1) / S) & 1);
+                    tmem::fence_after();
+                    mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(t + 1), id_s);
+                    umma::commit(&s_full);
+                }
+                // dK += dS_t^T Q_t
                 TKB_TR(0, t, 2);
-                tmem::fence_after();
-                mma_tb(C::tmem_dk(), C::tmem_dp() + 32, qaddr(t), t > 0);
-                umma::commit(&q_empty[t & 1]);
-                mm_dq();
-                umma::commit(&dq_full);
+                mbar_wait(&ds_full, ph);
                 TKB_TR(0, t, 3);
-                // (4) dP_{t+1} once the reduce warps drained dQ_t
-                mbar_wait(&do_full[t1 % C::kDoStages], (t1 / C::kDoStages) & 1);
+                tmem::fence_after();
+                mma_tmem_a(tbase + C::tmem_dk(), tbase + C::tmem_dp() + 32, qaddr(t), id_kv, t > 0);
+                umma::commit(&q_empty[t % S]);
+                // dP_{t+1}: overwrites dS_t, read by dK_t which was issued before
+                if (t + 1 < T) {
+                    mbar_wait(&do_full[(t + 1) % S], ((t + 1) / S) & 1);
+                    tmem::fence_after();
+                    mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(t + 1), id_s);
+                    umma::commit(&dp_full);
+                }
                 TKB_TR(0, t, 4);
-                mbar_wait(&dq_empty, ph);
-                TKB_TR(0, t, 5);
-                tmem::fence_after();
-                mm_abt(C::tmem_dp(), aV, doaddr(t1));
-                umma::commit(&dp_full);
-                // (5) dV += P_{t+1}^T dO_{t+1}
-                mbar_wait(&p_full, t1 & 1);
-                TKB_TR(0, t, 6);
-                tmem::fence_after();
-                mma_tb(C::tmem_dv(), C::tmem_s() + 32, doaddr(t1), true);
-                umma::commit(&do_empty[t1 % C::kDoStages]);
-                TKB_TR(0, t, 7);
             }
-            // tail: dK, dQ of the last block
-            const int tl = T - 1;
-            mbar_wait(&ds_full, tl & 1);
-            tmem::fence_after();
-            mma_tb(C::tmem_dk(), C::tmem_dp() + 32, qaddr(tl), tl > 0);
-            umma::commit(&q_empty[tl & 1]);
-            mm_dq();
-            umma::commit(&dq_full);
             umma::commit(&dkv_full);
-        }
-    } else if (warp >= kWarpReduce0) {
-        // ----------------------------------------------------------------- REDUCE (dQ)
-        // TMEM -> registers (frees the dP/dQ columns at once) -> double-buffered SMEM
-        // chunks of 128 x 32 fp32, drained by the TMA issuer threads (warps 14, 15).
-        setmaxnreg_inc<152>();
-        const int wq = warp - kWarpReduce0;
-        const int r = wq * 32 + lane;  // q row within the block == TMEM lane
-        const uint32_t tdq = tbase + ((uint32_t)(wq * 32) << 16) + C::tmem_dp();
-        const bool leader = (threadIdx.x == kWarpReduce0 * 32);
-        for (int t = 0; t < T; ++t) {
-            mbar_wait(&dq_full, t & 1);
-            if (leader) TKB_TR(2, t, 0);
-            tmem::fence_after();
-            uint32_t acc[D];
-#pragma unroll
-            for (int c = 0; c < D; c += 32) tmem::ld_32x32b_x32(tdq + c, acc + c);
-#pragma unroll
-            for (int c = 0; c < D; c += 32) tmem::wait_ld_x32(acc + c);
-            tmem::fence_before();
-            mbar_arrive(&dq_empty);
-            if (leader) TKB_TR(2, t, 1);
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                const int g = t * (D / 32) + c;
-                const int b = g & 1;
-                mbar_wait(&chunk_empty[b], ((g >> 1) & 1) ^ 1);
-                uint8_t* buf = sDq + b * C::kDqStageBytes;
-#pragma unroll
-                for (int q = 0; q < 8; ++q)  // 8 chunks of 4 fp32 = one 128-B row (SW128)
-                    *reinterpret_cast<uint4*>(buf + r * 128 + ((q ^ (r & 7)) * 16)) =
-                        make_uint4(acc[c * 32 + q * 4 + 0], acc[c * 32 + q * 4 + 1], acc[c * 32 + q * 4 + 2],
-                                   acc[c * 32 + q * 4 + 3]);
-                tma::fence_async_smem();
-                mbar_arrive(&chunk_full[b]);
-            }
         }
     } else {
         // ----------------------------------------------------------------- COMPUTE
-        setmaxnreg_inc<152>();
         const int wq = warp & 3;
         const int h = warp >> 2;       // q half: columns [64h, 64h+64)
         const int r = wq * 32 + lane;  // kv row == TMEM lane
@@ -409,12 +287,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         const float scale = p.scale;
         for (int t = 0; t < T; ++t) {
             const int i = qblock(t);
-            const int qs = t & 1;
+            const int s = t % S;
             const bool diag = CAUSAL && (i == j);
-            const float* lse = sLse + qs * 128 + 64 * h;
-            const float* dlt = sDelta + qs * 128 + 64 * h;
+            const float4* lse4 = reinterpret_cast<const float4*>(sLse + s * 128 + 64 * h);
+            const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + s * 128 + 64 * h);
             // P^T = exp2(tau S^T - lse2)
-            mbar_wait(&q_full[qs], (t >> 1) & 1);
+            mbar_wait(&q_full[s], (t / S) & 1);
             mbar_wait(&s_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 0);
             tmem::fence_after();
@@ -425,16 +303,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
             tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf) + 32);
             uint32_t pk[32];
 #pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-                float p0 = ex2_approx(fmaf(pf[c], tau, -lse[c]));
-                float p1 = ex2_approx(fmaf(pf[c + 1], tau, -lse[c + 1]));
-                if (diag) {  // causal: key kv0 + r visible to query q0 + 64h + c iff r <= 64h + c
-                    if (64 * h + c < r) p0 = 0.f;
-                    if (64 * h + c + 1 < r) p1 = 0.f;
+            for (int c = 0; c < 64; c += 4) {
+                const float4 l4 = lse4[c / 4];  // smem broadcast
+                float p0 = ex2_approx(fmaf(pf[c], tau, -l4.x));
+                float p1 = ex2_approx(fmaf(pf[c + 1], tau, -l4.y));
+                float p2 = ex2_approx(fmaf(pf[c + 2], tau, -l4.z));
+                float p3 = ex2_approx(fmaf(pf[c + 3], tau, -l4.w));
+                if (diag) {  // key kv0 + r visible to query kv0 + 64h + c iff r <= 64h + c
+                    const int q = 64 * h + c;
+                    p0 = (q < r) ? 0.f : p0;
+                    p1 = (q + 1 < r) ? 0.f : p1;
+                    p2 = (q + 2 < r) ? 0.f : p2;
+                    p3 = (q + 3 < r) ? 0.f : p3;
                 }
                 pf[c] = p0;
                 pf[c + 1] = p1;
+                pf[c + 2] = p2;
+                pf[c + 3] = p3;
                 pk[c / 2] = pack_bf16x2(p0, p1);
+                pk[c / 2 + 1] = pack_bf16x2(p2, p3);
             }
             tmem::st_32x32b_x32(tS + 32 + 32 * h, pk);
             tmem::wait_st();
@@ -445,63 +332,41 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
             mbar_wait(&dp_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 2);
             tmem::fence_after();
-            uint8_t* dsrow = sDs + h * C::kAtomBytes + r * 128;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 uint32_t dpv[32];
                 tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
+                for (int c = 0; c < 32; c += 4) {
                     const int cc = 32 * half + c;
-                    const float d0 = pf[cc] * (__uint_as_float(dpv[c]) - dlt[cc]) * scale;
-                    const float d1 = pf[cc + 1] * (__uint_as_float(dpv[c + 1]) - dlt[cc + 1]) * scale;
+                    const float4 d4 = dlt4[cc / 4];
+                    const float d0 = pf[cc] * (__uint_as_float(dpv[c]) - d4.x) * scale;
+                    const float d1 = pf[cc + 1] * (__uint_as_float(dpv[c + 1]) - d4.y) * scale;
+                    const float d2 = pf[cc + 2] * (__uint_as_float(dpv[c + 2]) - d4.z) * scale;
+                    const float d3 = pf[cc + 3] * (__uint_as_float(dpv[c + 3]) - d4.w) * scale;
                     pk[cc / 2] = pack_bf16x2(d0, d1);
+                    pk[cc / 2 + 1] = pack_bf16x2(d2, d3);
                 }
             }
             tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                *reinterpret_cast<uint4*>(dsrow + ((q ^ (r & 7)) * 16)) =
-                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             tmem::wait_st();
             tmem::fence_before();
-            tma::fence_async_smem();
             mbar_arrive(&ds_full);
             if (threadIdx.x == 0) TKB_TR(1, t, 3);
         }
-        // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q ring is free) -> TMA store
+        // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q and dO rings are free) -> TMA store
         mbar_wait(&dkv_full, 0);
         tmem::fence_after();
         uint8_t* stage_v = sQ;
-        uint8_t* stage_k = sQ + C::kTileBytes;
-#pragma unroll
-        for (int which = 0; which < 2; ++which) {
-            const uint32_t tsrc = tbase + lane_off + (which == 0 ? C::tmem_dv() : C::tmem_dk());
-            uint8_t* stg = which == 0 ? stage_v : stage_k;
-#pragma unroll
-            for (int c = 0; c < D / 2; c += 32) {
-                const int col = h * (D / 2) + c;
-                uint32_t v[32];
-                tmem::ldw_32x32b_x32(tsrc + col, v);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int gc = col / 8 + q;  // global 16-byte chunk index within the row
-                    const int atom = gc / 8, ch = gc % 8;
-                    uint4 u;
-                    u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
-                    u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
-                    u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
-                    u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
-                    *reinterpret_cast<uint4*>(stg + atom * C::kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
-                }
-            }
-        }
+        uint8_t* stage_k = sDo;
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dv(), stage_v, r, h);
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dk(), stage_k, r, h);
         tma::fence_async_smem();
         named_sync(kBarCompute, kComputeThreads);
         if (threadIdx.x == 0) {
-            for (int a = 0; a < C::kAtoms; ++a) {
-                tma::store_4d(&p.tm_dv, stage_v + a * C::kAtomBytes, a * 64, kv0, head, batch);
-                tma::store_4d(&p.tm_dk, stage_k + a * C::kAtomBytes, a * 64, kv0, head, batch);
+            for (int a = 0; a < TL::kAtoms; ++a) {
+                tma::store_4d(&p.tm_dv, stage_v + a * kAtomBytes, a * 64, kv0, head, batch);
+                tma::store_4d(&p.tm_dk, stage_k + a * kAtomBytes, a * 64, kv0, head, batch);
             }
             tma::commit_group();
             tma::wait_group_read<0>();
@@ -511,16 +376,234 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     tmem::fence_before();
     __syncthreads();
     if (warp == kWarpMma) tmem::dealloc<512>(tbase);
-#undef TKB_TR
 }
 
-// Delta = rowsum(dO o O), lse2 = L log2 e (+inf / 0 on padded rows), semaphores = 0.
+// ================================================================== bwd_dq (Q-stationary)
+template <int D>
+struct CfgQ {
+    using T = Tiles<D>;
+    static constexpr int kStages = (D == 128) ? 2 : 4;  // K and V ring depth
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffDo = kOffQ + T::kTileBytes;
+    static constexpr int kOffK = kOffDo + T::kTileBytes;
+    static constexpr int kOffV = kOffK + kStages * T::kTileBytes;
+    static constexpr int kOffBar = kOffV + kStages * T::kTileBytes;
+    static constexpr int kSmemBytes = kOffBar + 256 + 1024;
+    static_assert(kSmemBytes <= 232448, "smem");
+    static __device__ __forceinline__ constexpr uint32_t tmem_s(int b) { return b * 128u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 256u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dq() { return 384u; }
+};
+
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
+    using C = CfgQ<D>;
+    using TL = Tiles<D>;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem + C::kOffQ;
+    uint8_t* sDo = smem + C::kOffDo;
+    uint8_t* sK = smem + C::kOffK;
+    uint8_t* sV = smem + C::kOffV;
+    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
+    mbarrier& qdo_full = bars[0];
+    mbarrier* s_full = bars + 1;  // [2]
+    mbarrier* s_free = bars + 3;  // [2]
+    mbarrier& dp_full = bars[5];
+    mbarrier& ds_full = bars[6];
+    mbarrier& dq_full = bars[7];
+    mbarrier* k_full = bars + 8;    // [S]
+    mbarrier* k_empty = bars + 12;  // [S]
+    mbarrier* v_full = bars + 16;   // [S]
+    mbarrier* v_empty = bars + 20;  // [S]
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
+
+    const int warp = warpid();
+    const int lane = laneid();
+    const int nq = p.n_pad / 128;
+    const int i = CAUSAL ? (int)(nq - 1 - blockIdx.x) : (int)blockIdx.x;  // heavy causal blocks first
+    const int head = blockIdx.y;
+    const int batch = blockIdx.z;
+    const int bh = batch * p.heads + head;
+    const int q0 = i * 128;
+    const int nk = CAUSAL ? (i + 1) : nq;  // kv blocks visited
+    long long* tr = trace_slot(p, bh * gridDim.x + (int)blockIdx.x, 1);
+    const long long t_start = clock64();
+
+    if (warp == kWarpLoad && lane == 0) {
+        mbar_init(&qdo_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&s_free[b], kComputeThreads);
+        }
+        mbar_init(&dp_full, 1);
+        mbar_init(&ds_full, kComputeThreads);
+        mbar_init(&dq_full, 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
+        }
+        fence_barrier_init();
+        tma::prefetch_desc(&p.tm_q);
+        tma::prefetch_desc(&p.tm_k);
+        tma::prefetch_desc(&p.tm_v);
+        tma::prefetch_desc(&p.tm_do);
+    }
+    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tbase = tmem_slot;
+
+    if (warp == kWarpLoad) {
+        if (lane == 0) {
+            // ------------------------------------------------------------- LOAD
+            const uint64_t pol_stream = tma::policy_evict_first();
+            const uint64_t pol_keep = tma::policy_evict_last();
+            mbar_arrive_expect_tx(&qdo_full, 2 * TL::kTileBytes);
+            for (int a = 0; a < TL::kAtoms; ++a) {
+                tma::load_4d(sQ + a * kAtomBytes, &p.tm_q, &qdo_full, a * 64, q0, head, batch, pol_stream);
+                tma::load_4d(sDo + a * kAtomBytes, &p.tm_do, &qdo_full, a * 64, q0, head, batch, pol_stream);
+            }
+            for (int jj = 0; jj < nk; ++jj) {
+                const int s = jj % S;
+                const uint32_t ph = ((jj / S) & 1) ^ 1;
+                mbar_wait(&k_empty[s], ph);
+                mbar_arrive_expect_tx(&k_full[s], TL::kTileBytes);
+                for (int a = 0; a < TL::kAtoms; ++a)
+                    tma::load_4d(sK + s * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[s], a * 64, jj * 128,
+                                 head, batch, pol_keep);
+                mbar_wait(&v_empty[s], ph);
+                mbar_arrive_expect_tx(&v_full[s], TL::kTileBytes);
+                for (int a = 0; a < TL::kAtoms; ++a)
+                    tma::load_4d(sV + s * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[s], a * 64, jj * 128,
+                                 head, batch, pol_keep);
+            }
+        }
+    } else if (warp == kWarpMma) {
+        if (lane == 0) {
+            // ------------------------------------------------------------- MMA
+            constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
+            constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
+            const uint32_t aQ = smem_u32(sQ), aDo = smem_u32(sDo);
+            auto kaddr = [&](int jj) { return smem_u32(sK + (jj % S) * TL::kTileBytes); };
+            auto vaddr = [&](int jj) { return smem_u32(sV + (jj % S) * TL::kTileBytes); };
+            auto issue_s = [&](int jj) {  // S_j = Q K_j^T -> S[j & 1]
+                mbar_wait(&k_full[jj % S], (jj / S) & 1);
+                tmem::fence_after();
+                mm_abt<D>(tbase + C::tmem_s(jj & 1), aQ, kaddr(jj), id_s);
+                umma::commit(&s_full[jj & 1]);
+            };
+            auto issue_dp = [&](int jj) {  // dP_j = dO V_j^T
+                mbar_wait(&v_full[jj % S], (jj / S) & 1);
+                tmem::fence_after();
+                mm_abt<D>(tbase + C::tmem_dp(), aDo, vaddr(jj), id_s);
+                umma::commit(&dp_full);
+                umma::commit(&v_empty[jj % S]);
+            };
+            mbar_wait(&qdo_full, 0);
+            issue_s(0);
+            if (nk > 1) issue_s(1);
+            issue_dp(0);
+            for (int jj = 0; jj < nk; ++jj) {
+                TKB_TR(0, jj, 0);
+                mbar_wait(&ds_full, jj & 1);
+                TKB_TR(0, jj, 1);
+                tmem::fence_after();
+                mma_tmem_a(tbase + C::tmem_dq(), tbase + C::tmem_dp() + 32, kaddr(jj), id_q, jj > 0);  // dQ += dS K
+                umma::commit(&k_empty[jj % S]);
+                if (jj + 1 < nk) issue_dp(jj + 1);  // overwrites dS_j, read by dQ_j issued before
+                if (jj + 2 < nk) {
+                    mbar_wait(&s_free[jj & 1], (jj >> 1) & 1);  // S_j read out by the compute warps
+                    issue_s(jj + 2);
+                }
+                TKB_TR(0, jj, 2);
+            }
+            umma::commit(&dq_full);
+        }
+    } else {
+        // ----------------------------------------------------------------- COMPUTE
+        const int wq = warp & 3;
+        const int h = warp >> 2;       // kv half: columns [64h, 64h+64)
+        const int r = wq * 32 + lane;  // q row == TMEM lane
+        const int row = q0 + r;
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const uint32_t tDp = tbase + lane_off + C::tmem_dp();
+        const float tau = p.scale_log2;
+        const float scale = p.scale;
+        const float lse_r = p.lse2[(size_t)bh * p.n_pad + row];  // +inf on padded rows -> P = 0
+        const float dlt_r = p.delta[(size_t)bh * p.n_pad + row];
+        for (int jj = 0; jj < nk; ++jj) {
+            const int kv0 = jj * 128;
+            const uint32_t tS = tbase + lane_off + C::tmem_s(jj & 1);
+            mbar_wait(&s_full[jj & 1], (jj >> 1) & 1);
+            if (threadIdx.x == 0) TKB_TR(1, jj, 0);
+            tmem::fence_after();
+            float pf[64];
+            tmem::ld_32x32b_x32(tS + 64 * h, reinterpret_cast<uint32_t*>(pf));
+            tmem::ld_32x32b_x32(tS + 64 * h + 32, reinterpret_cast<uint32_t*>(pf) + 32);
+            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf));
+            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf) + 32);
+            tmem::fence_before();
+            mbar_arrive(&s_free[jj & 1]);
+            // visible keys: kv < n, and causal kv <= row
+            const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 64 * h;  // last visible column
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+                const float pv = ex2_approx(fmaf(pf[c], tau, -lse_r));
+                pf[c] = (c > lim) ? 0.f : pv;
+            }
+            mbar_wait(&dp_full, jj & 1);
+            if (threadIdx.x == 0) TKB_TR(1, jj, 1);
+            tmem::fence_after();
+            uint32_t pk[32];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t dpv[32];
+                tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const int cc = 32 * half + c;
+                    const float d0 = pf[cc] * (__uint_as_float(dpv[c]) - dlt_r) * scale;
+                    const float d1 = pf[cc + 1] * (__uint_as_float(dpv[c + 1]) - dlt_r) * scale;
+                    pk[cc / 2] = pack_bf16x2(d0, d1);
+                }
+            }
+            tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
+            tmem::wait_st();
+            tmem::fence_before();
+            mbar_arrive(&ds_full);
+            if (threadIdx.x == 0) TKB_TR(1, jj, 2);
+        }
+        // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM (the Q tile is free) -> TMA store
+        mbar_wait(&dq_full, 0);
+        tmem::fence_after();
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sQ, r, h);
+        tma::fence_async_smem();
+        named_sync(kBarCompute, kComputeThreads);
+        if (threadIdx.x == 0) {
+            for (int a = 0; a < TL::kAtoms; ++a) tma::store_4d(&p.tm_dq, sQ + a * kAtomBytes, a * 64, q0, head, batch);
+            tma::commit_group();
+            tma::wait_group_read<0>();
+        }
+    }
+
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
+}
+#undef TKB_TR
+
+// Delta = rowsum(dO o O), lse2 = L log2 e (+inf / 0 on padded rows).
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ lse2,
-                                                       float* __restrict__ delta, int* __restrict__ sema, int* __restrict__ ticket, int heads,
-                                                       int n, int n_pad, int64_t sb, int64_t sh, int64_t sn) {
+                                                       float* __restrict__ delta, int heads, int n, int n_pad,
+                                                       int64_t sb, int64_t sh, int64_t sn) {
     constexpr int kLanesPerRow = D / 8;
     constexpr int kRowsPerBlock = 256 / kLanesPerRow;
     const int bh = blockIdx.y;
@@ -549,69 +632,41 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
         delta[idx] = row < n ? acc : 0.f;
         lse2[idx] = row < n ? lse[(size_t)bh * n + row] * 1.44269504088896340736f : INFINITY;
     }
-    if (blockIdx.x == 0)
-        for (int k = threadIdx.x; k < n_pad / 128; k += blockDim.x) sema[(size_t)bh * (n_pad / 128) + k] = 0;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0;
 }
 
-// dq (bf16, user layout) = dq_accum (fp32 [bh][n_pad][D])
-template <int D>
-__global__ void __launch_bounds__(256) bwd_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                                                          int heads, int n, int n_pad, int64_t sb, int64_t sh,
-                                                          int64_t sn, int64_t total_chunks) {
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_chunks;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(g % (D / 8)) * 8;
-        const int64_t rowg = g / (D / 8);
-        const int row = (int)(rowg % n);
-        const int bh = (int)(rowg / n);
-        const float* src = acc + ((size_t)bh * n_pad + row) * D + c;
-        const float4 a = *reinterpret_cast<const float4*>(src);
-        const float4 bq = *reinterpret_cast<const float4*>(src + 4);
-        uint4 u;
-        u.x = pack_bf16x2(a.x, a.y);
-        u.y = pack_bf16x2(a.z, a.w);
-        u.z = pack_bf16x2(bq.x, bq.y);
-        u.w = pack_bf16x2(bq.z, bq.w);
-        const int b = bh / heads, hh = bh % heads;
-        *reinterpret_cast<uint4*>(dq + b * sb + hh * sh + (int64_t)row * sn + c) = u;
-    }
+template <class Kern>
+int set_smem(Kern k, int bytes) {
+    return (int)cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 template <int D, bool CAUSAL>
 int launch_main(const BwdParams& p, int batches, cudaStream_t stream) {
-    using C = Cfg<D>;
-    auto kern = attn_bwd_kernel<D, CAUSAL>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-        if (e != cudaSuccess) return (int)e;
+        int e = set_smem(attn_bwd_dkdv_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
+        if (!e) e = set_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes);
+        if (e) return e;
         configured = true;
     }
-    dim3 grid((p.n_pad / 128) * p.heads * batches);
-    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(p);
+    dim3 grid(p.n_pad / 128, p.heads, batches);
+    attn_bwd_dkdv_kernel<D, CAUSAL><<<grid, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    attn_bwd_dq_kernel<D, CAUSAL><<<grid, kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
     return (int)cudaGetLastError();
 }
 
 template <int D>
 int launch_all(bool causal, const BwdParams& p, int batches, const void* o, const void* dout, const float* lse,
-               float* lse2, float* delta, float* dq_accum, int64_t sb, int64_t sh, int64_t sn, void* dq,
-               cudaStream_t stream, int* launches) {
+               float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn, cudaStream_t stream, int* launches) {
     constexpr int kRowsPerBlock = 256 / (D / 8);
-    const int bhs = batches * p.heads;
-    dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, bhs);
+    dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, batches * p.heads);
     bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                               reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
-                                              p.dq_sema, p.ticket, p.heads, p.n, p.n_pad, sb, sh, sn);
+                                              p.heads, p.n, p.n_pad, sb, sh, sn);
     int e = (int)cudaGetLastError();
     if (e) return e;
     e = causal ? launch_main<D, true>(p, batches, stream) : launch_main<D, false>(p, batches, stream);
-    if (e) return e;
-    const int64_t chunks = (int64_t)bhs * p.n * (D / 8);
-    const int blocks = (int)((chunks + 255) / 256 < 148 * 16 ? (chunks + 255) / 256 : 148 * 16);
-    bwd_convert_kernel<D><<<blocks, 256, 0, stream>>>(dq_accum, reinterpret_cast<__nv_bfloat16*>(dq), p.heads, p.n,
-                                                      p.n_pad, sb, sh, sn, chunks);
-    e = (int)cudaGetLastError();
     if (e) return e;
     *launches = 3;
     return 0;
@@ -620,13 +675,11 @@ int launch_all(bool causal, const BwdParams& p, int batches, const void* o, cons
 }  // namespace bwd
 
 int launch_attn_bwd(int head_dim, bool causal, const BwdParams& p, int batches, const void* o, const void* dout,
-                    const float* lse, float* lse2, float* delta, float* dq_accum, int64_t sb, int64_t sh, int64_t sn,
-                    void* dq, cudaStream_t stream, int* launches) {
+                    const float* lse, float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn,
+                    cudaStream_t stream, int* launches) {
     if (head_dim == 128)
-        return bwd::launch_all<128>(causal, p, batches, o, dout, lse, lse2, delta, dq_accum, sb, sh, sn, dq, stream,
-                                    launches);
-    return bwd::launch_all<64>(causal, p, batches, o, dout, lse, lse2, delta, dq_accum, sb, sh, sn, dq, stream,
-                               launches);
+        return bwd::launch_all<128>(causal, p, batches, o, dout, lse, lse2, delta, sb, sh, sn, stream, launches);
+    return bwd::launch_all<64>(causal, p, batches, o, dout, lse, lse2, delta, sb, sh, sn, stream, launches);
 }
 
 }  // namespace tkb

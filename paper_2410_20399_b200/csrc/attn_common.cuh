@@ -24,15 +24,11 @@ struct FwdParams {
 
 struct BwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128 (loads)
-    CUtensorMap tm_dk, tm_dv;             // same layout (stores)
-    CUtensorMap tm_dqacc;                 // fp32 {D, Npad, B*H}, box {32, 128, 1}, SW128 (dQ adds)
+    CUtensorMap tm_dq, tm_dk, tm_dv;      // same layout (stores)
     const float* lse2;                    // [B*H, Npad] L * log2(e); +inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
-    float* dq_accum;                      // [B*H, Npad, D] fp32 dQ accumulator (workspace)
-    int* dq_sema;                         // [B*H, Npad/128] dQ ordering semaphores (workspace)
-    int* ticket;                          // CTA start-order ticket (workspace, zeroed by bwd_prep)
     long long* trace;                     // optional per-role cycle timeline (tkb_debug_set_trace)
-    int trace_every;                      // trace work items with item % trace_every == 0
+    int trace_every;                      // trace CTAs with linear id % trace_every == 0
     int trace_slots;
     int n;
     int n_pad;

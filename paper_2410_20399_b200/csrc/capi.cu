@@ -14,8 +14,8 @@
 
 namespace tkb {
 int launch_attn_bwd(int head_dim, bool causal, const BwdParams& p, int batches, const void* o, const void* dout,
-                    const float* lse, float* lse2, float* delta, float* dq_accum, int64_t sb, int64_t sh, int64_t sn,
-                    void* dq, cudaStream_t stream, int* launches);
+                    const float* lse, float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn,
+                    cudaStream_t stream, int* launches);
 int launch_check_finite(const void* const* ptrs, int nptrs, int batches, int heads, int n, int d, int64_t sb,
                         int64_t sh, int64_t sn, int* flag_dev, cudaStream_t stream);
 }  // namespace tkb
@@ -158,11 +158,8 @@ TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* d) {
     const size_t bh = (size_t)d->batches * d->heads;
     const size_t npad = (size_t)((d->seq + 127) / 128) * 128;
     size_t bytes = 0;
-    bytes += bh * npad * (size_t)d->head_dim * 4;  // dq accumulator fp32
-    bytes += bh * npad * 4;                        // delta
-    bytes += bh * npad * 4;                        // lse2 (log2 domain, padded)
-    bytes += bh * (npad / 128) * 4;                // semaphores
-    bytes += 16;                                   // CTA ticket
+    bytes += bh * npad * 4;  // delta = rowsum(dO * O)
+    bytes += bh * npad * 4;  // lse2 (log2 domain, padded)
     return (bytes + 255) & ~(size_t)255;
 }
 
@@ -175,8 +172,6 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv || !workspace)
         return fail(TKB_ERR_BOUNDS, "null pointer");
     if (workspace_bytes < tkb_attn_bwd_workspace_bytes(d)) return fail(TKB_ERR_BOUNDS, "workspace too small");
-    if ((d->seq + 127) / 128 > 144)  // deterministic dQ ordering needs a head's KV-block CTAs co-resident
-        return fail(TKB_ERR_CONFIG, "attn_bwd supports seq <= 18432 (deterministic dQ ordering)");
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
          (uintptr_t)dk | (uintptr_t)dv | (uintptr_t)workspace) &
         15)
@@ -191,32 +186,15 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     tkb::BwdParams p{};
     if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, s)) ||
         (rc = make_bhnd_map(&p.tm_v, v, d, s)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
-        (rc = make_bhnd_map(&p.tm_dk, dk, d, s)) || (rc = make_bhnd_map(&p.tm_dv, dv, d, s)))
+        (rc = make_bhnd_map(&p.tm_dq, dq, d, s)) || (rc = make_bhnd_map(&p.tm_dk, dk, d, s)) ||
+        (rc = make_bhnd_map(&p.tm_dv, dv, d, s)))
         return rc;
     const int64_t bh = (int64_t)d->batches * d->heads;
     const int npad = (d->seq + 127) / 128 * 128;
-    uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-    float* dq_accum = reinterpret_cast<float*>(ws);
-    ws += (size_t)bh * npad * d->head_dim * 4;
-    float* delta = reinterpret_cast<float*>(ws);
-    ws += (size_t)bh * npad * 4;
-    float* lse2 = reinterpret_cast<float*>(ws);
-    ws += (size_t)bh * npad * 4;
+    float* delta = reinterpret_cast<float*>(workspace);
+    float* lse2 = delta + (size_t)bh * npad;
     p.delta = delta;
     p.lse2 = lse2;
-    p.dq_sema = reinterpret_cast<int*>(ws);
-    ws += (size_t)bh * (npad / 128) * 4;
-    p.ticket = reinterpret_cast<int*>(ws);
-    p.dq_accum = dq_accum;
-    {
-        uint64_t dims[3] = {(uint64_t)d->head_dim, (uint64_t)npad, (uint64_t)bh};
-        uint64_t strides[3] = {1, (uint64_t)d->head_dim, (uint64_t)npad * d->head_dim};
-        uint32_t box[3] = {32, 128, 1};
-        std::string err;
-        if (!tkb::host::make_tmap(&p.tm_dqacc, dq_accum, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, dims, strides, box,
-                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
-            return fail(TKB_ERR_SHAPE, "dq tensor map: " + err);
-    }
     p.trace = g_trace;
     p.trace_every = g_trace_every;
     p.trace_slots = g_trace_slots;
@@ -226,8 +204,8 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.scale = scale_of(d);
     p.scale_log2 = p.scale * 1.44269504088896340736f;
     int launches = 0;
-    int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, dq_accum,
-                                 s.b, s.h, s.n, dq, st, &launches);
+    int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
+                                 s.n, st, &launches);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_bwd launch: ") + cudaGetErrorString((cudaError_t)e));
     g_launches = launches;
     return TKB_OK;

@@ -16,14 +16,15 @@ A.attention_bwd(q, k, v, o, do, lse, causal=bool(causal))
 torch.cuda.synchronize()
 A.debug_set_trace(None)
 t = buf.cpu()
-names = {0: ["m.qwait", "m.S", "m.dsfull", "m.dQ", "m.dofull", "m.dqempty", "m.pfull", "m.dV"],
-         1: ["c.sfull", "c.Pdone", "c.dpfull", "c.dSdone"], 2: ["r.dqfull", "r.empty", "i.start", "i.issued"],
-         3: ["T.S", "T.dK", "T.dQ", "T.dP", "T.dV"]}
+names = {0: ["kv.m.pwait", "kv.m.pfull", "kv.m.dswait", "kv.m.dsfull", "kv.m.end"],
+         1: ["kv.c.sfull", "kv.c.Pdone", "kv.c.dpfull", "kv.c.dSdone"],
+         2: ["q.m.dswait", "q.m.dsfull", "q.m.end"], 3: ["q.c.sfull", "q.c.dpfull", "q.c.dSdone"]}
 for slot in (1, 4):
     print(f"--- slot {slot} (item {slot * every})")
-    for it in range(8, 12):
+    for roles in ((0, 1), (2, 3)):
+      for it in range(8, 11):
         ev = []
-        for role in range(4):
+        for role in roles:
             for e, nm in enumerate(names[role]):
                 val = int(t[slot, role, it, e])
                 if val:
@@ -31,8 +32,8 @@ for slot in (1, 4):
         ev.sort()
         base = ev[0][0] if ev else 0
         print(f"iter {it}: " + "  ".join(f"{nm}+{v - base}" for v, nm in ev))
-    # average iteration period from m.S stamps
-    s_stamps = [int(t[slot, 0, i, 1]) for i in range(32) if int(t[slot, 0, i, 1])]
-    if len(s_stamps) > 4:
-        d = [b - a for a, b in zip(s_stamps, s_stamps[1:])]
-        print("iteration period (cycles):", d[2:12])
+    for role, ev_i, nm in ((0, 4, "dkdv"), (2, 2, "dq")):
+        st = [int(t[slot, role, i, ev_i]) for i in range(32) if int(t[slot, role, i, ev_i])]
+        if len(st) > 4:
+            d = [b - a for a, b in zip(st, st[1:])]
+            print(f"{nm} iteration period (cycles):", d[2:12])
