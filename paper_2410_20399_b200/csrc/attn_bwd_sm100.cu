@@ -6,7 +6,7 @@
 //   dS = P o (dP - Delta), dQ = scale dS K, dK = scale dS^T Q
 //
 // Design: atomic-free, deterministic by construction. Three launches:
-//   bwd_prep   Delta = rowsum(dO o O) and lse2 = L log2(e) (+inf on padded rows)
+//   bwd_prep   Delta = rowsum(dO o O) and -lse2 = -L log2(e) (-inf on padded rows)
 //   bwd_dkdv   KV-stationary: one 128-row K/V block per CTA, streaming Q/dO blocks;
 //              4 tcgen05 GEMMs per tile pair, dK/dV accumulate in TMEM:
 //                S^T  = K Q^T    (SS)            -> TMEM S
@@ -15,9 +15,11 @@
 //                dK  += dS^T Q   (TS, dS in TMEM)
 //   bwd_dq     Q-stationary: one 128-row Q/dO block per CTA, streaming K/V blocks;
 //              3 GEMMs per tile pair, dQ accumulates in TMEM:
-//                S   = Q K^T     (SS)            -> TMEM S (double-buffered)
-//                dP  = dO V^T    (SS)            -> TMEM dP
+//                S   = Q K^T     (TS, Q in TMEM) -> TMEM S
+//                dP  = dO V^T    (TS, dO in TMEM)-> TMEM dP
 //                dQ += dS K      (TS, dS in TMEM)
+//              (all three read only B from SMEM: an SS GEMM would need the full 128 B/clk
+//               of SMEM bandwidth and stall behind the TMA traffic)
 // A fused single kernel needs an fp32 reduction of a 128 x D dQ partial per tile pair
 // through L2; measured on this B200 the chip-wide fp32 add-reduce ceiling is ~5.6 TB/s
 // (tools/reduce_bench.py), which caps 128-row KV tiles well below the tensor rate.
@@ -67,6 +69,38 @@ TKB_DEVICE void mm_abt(uint32_t dst, uint32_t a, uint32_t b, uint32_t idesc) {
         umma::mma_ss_split(dst, umma::desc_lo(a + off, 16), kDescHi, umma::desc_lo(b + off, 16), kDescHi, idesc,
                            k > 0);
     }
+}
+
+// X = A B^T with A in TMEM (128 lanes x D, bf16 pairs) and B [128 rows][D] K-major (K = D)
+template <int D>
+TKB_DEVICE void mm_tmem_abt(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc) {
+    b = umma::opaque(b);
+#pragma unroll
+    for (int k = 0; k < D / 16; ++k) {
+        const uint32_t off = (k / 4) * kAtomBytes + (k % 4) * 32;
+        umma::mma_ts_split(dst, a_tmem + k * 8, umma::desc_lo(b + off, 16), kDescHi, idesc, k > 0);
+    }
+}
+
+// SW128 smem tile row r, columns [h*D/2, (h+1)*D/2) -> TMEM A-operand columns (bf16 pairs)
+template <int D>
+TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, int h) {
+    constexpr int kChunks = D / 16;  // 16-byte chunks per half row
+    uint32_t v[kChunks * 4];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        const int gc = h * kChunks + q;
+        const int atom = gc / 8, ch = gc % 8;
+        const uint4 u = *reinterpret_cast<const uint4*>(tile + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16));
+        v[4 * q] = u.x;
+        v[4 * q + 1] = u.y;
+        v[4 * q + 2] = u.z;
+        v[4 * q + 3] = u.w;
+    }
+    if constexpr (D == 128)
+        tmem::st_32x32b_x32(tdst + h * 32, v);
+    else
+        tmem::st_32x32b_x16(tdst + h * 16, v);
 }
 
 // acc (+)= A[tmem: 128 lanes x 128 K as bf16 pairs] B with B [128 K rows][D] MN-major
@@ -289,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             const int i = qblock(t);
             const int s = t % S;
             const bool diag = CAUSAL && (i == j);
-            const float4* lse4 = reinterpret_cast<const float4*>(sLse + s * 128 + 64 * h);
+            const float4* nlse4 = reinterpret_cast<const float4*>(sLse + s * 128 + 64 * h);
             const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + s * 128 + 64 * h);
             // P^T = exp2(tau S^T - lse2)
             mbar_wait(&q_full[s], (t / S) & 1);
@@ -304,11 +338,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < 64; c += 4) {
-                const float4 l4 = lse4[c / 4];  // smem broadcast
-                float p0 = ex2_approx(fmaf(pf[c], tau, -l4.x));
-                float p1 = ex2_approx(fmaf(pf[c + 1], tau, -l4.y));
-                float p2 = ex2_approx(fmaf(pf[c + 2], tau, -l4.z));
-                float p3 = ex2_approx(fmaf(pf[c + 3], tau, -l4.w));
+                const float4 l4 = nlse4[c / 4];  // smem broadcast; holds -lse2
+                const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(l4.x, l4.y));
+                const float2 x23 =
+                    fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(l4.z, l4.w));
+                float p0 = ex2_approx(x01.x), p1 = ex2_approx(x01.y);
+                float2 p23;
+                if ((c & 8) != 0) {  // a quarter of the exponentials on the FMA pipe (MUFU relief)
+                    p23 = ex2_poly2(x23);
+                } else {
+                    p23.x = ex2_approx(x23.x);
+                    p23.y = ex2_approx(x23.y);
+                }
+                float p2 = p23.x, p3 = p23.y;
                 if (diag) {  // key kv0 + r visible to query kv0 + 64h + c iff r <= 64h + c
                     const int q = 64 * h + c;
                     p0 = (q < r) ? 0.f : p0;
@@ -340,12 +382,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
                 for (int c = 0; c < 32; c += 4) {
                     const int cc = 32 * half + c;
                     const float4 d4 = dlt4[cc / 4];
-                    const float d0 = pf[cc] * (__uint_as_float(dpv[c]) - d4.x) * scale;
-                    const float d1 = pf[cc + 1] * (__uint_as_float(dpv[c + 1]) - d4.y) * scale;
-                    const float d2 = pf[cc + 2] * (__uint_as_float(dpv[c + 2]) - d4.z) * scale;
-                    const float d3 = pf[cc + 3] * (__uint_as_float(dpv[c + 3]) - d4.w) * scale;
-                    pk[cc / 2] = pack_bf16x2(d0, d1);
-                    pk[cc / 2 + 1] = pack_bf16x2(d2, d3);
+                    const float2 g01 = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
+                                            make_float2(d4.x, d4.y));
+                    const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
+                                            make_float2(d4.z, d4.w));
+                    const float2 s01 = mul2(mul2(make_float2(pf[cc], pf[cc + 1]), g01), make_float2(scale, scale));
+                    const float2 s23 =
+                        mul2(mul2(make_float2(pf[cc + 2], pf[cc + 3]), g23), make_float2(scale, scale));
+                    pk[cc / 2] = pack_bf16x2(s01.x, s01.y);
+                    pk[cc / 2 + 1] = pack_bf16x2(s23.x, s23.y);
                 }
             }
             tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
@@ -390,9 +435,12 @@ struct CfgQ {
     static constexpr int kOffBar = kOffV + kStages * T::kTileBytes;
     static constexpr int kSmemBytes = kOffBar + 256 + 1024;
     static_assert(kSmemBytes <= 232448, "smem");
-    static __device__ __forceinline__ constexpr uint32_t tmem_s(int b) { return b * 128u; }
-    static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 256u; }
-    static __device__ __forceinline__ constexpr uint32_t tmem_dq() { return 384u; }
+    // S | dP | dQ | Q (A operand) | dO (A operand): 128 + 128 + D + D/2 + D/2 <= 512
+    static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 128u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dq() { return 256u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_qa() { return 256u + D; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_doa() { return 256u + D + D / 2; }
 };
 
 template <int D, bool CAUSAL>
@@ -408,8 +456,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     uint8_t* sV = smem + C::kOffV;
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
     mbarrier& qdo_full = bars[0];
-    mbarrier* s_full = bars + 1;  // [2]
-    mbarrier* s_free = bars + 3;  // [2]
+    mbarrier& s_full = bars[1];
+    mbarrier& s_free = bars[2];
+    mbarrier& a_ready = bars[3];  // Q, dO copied into TMEM
     mbarrier& dp_full = bars[5];
     mbarrier& ds_full = bars[6];
     mbarrier& dq_full = bars[7];
@@ -433,10 +482,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 
     if (warp == kWarpLoad && lane == 0) {
         mbar_init(&qdo_full, 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&s_full[b], 1);
-            mbar_init(&s_free[b], kComputeThreads);
-        }
+        mbar_init(&s_full, 1);
+        mbar_init(&s_free, kComputeThreads);
+        mbar_init(&a_ready, kComputeThreads);
         mbar_init(&dp_full, 1);
         mbar_init(&ds_full, kComputeThreads);
         mbar_init(&dq_full, 1);
@@ -488,27 +536,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             // ------------------------------------------------------------- MMA
             constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
             constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
-            const uint32_t aQ = smem_u32(sQ), aDo = smem_u32(sDo);
             auto kaddr = [&](int jj) { return smem_u32(sK + (jj % S) * TL::kTileBytes); };
             auto vaddr = [&](int jj) { return smem_u32(sV + (jj % S) * TL::kTileBytes); };
-            auto issue_s = [&](int jj) {  // S_j = Q K_j^T -> S[j & 1]
+            auto issue_s = [&](int jj) {  // S_j = Q K_j^T
                 mbar_wait(&k_full[jj % S], (jj / S) & 1);
                 tmem::fence_after();
-                mm_abt<D>(tbase + C::tmem_s(jj & 1), aQ, kaddr(jj), id_s);
-                umma::commit(&s_full[jj & 1]);
+                mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(jj), id_s);
+                umma::commit(&s_full);
             };
             auto issue_dp = [&](int jj) {  // dP_j = dO V_j^T
                 mbar_wait(&v_full[jj % S], (jj / S) & 1);
                 tmem::fence_after();
-                mm_abt<D>(tbase + C::tmem_dp(), aDo, vaddr(jj), id_s);
+                mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(jj), id_s);
                 umma::commit(&dp_full);
                 umma::commit(&v_empty[jj % S]);
             };
-            mbar_wait(&qdo_full, 0);
+            mbar_wait(&a_ready, 0);
             issue_s(0);
-            if (nk > 1) issue_s(1);
             issue_dp(0);
             for (int jj = 0; jj < nk; ++jj) {
+                if (jj + 1 < nk) {
+                    mbar_wait(&s_free, jj & 1);  // S_j read out by the compute warps
+                    issue_s(jj + 1);
+                }
                 TKB_TR(0, jj, 0);
                 mbar_wait(&ds_full, jj & 1);
                 TKB_TR(0, jj, 1);
@@ -516,10 +566,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 mma_tmem_a(tbase + C::tmem_dq(), tbase + C::tmem_dp() + 32, kaddr(jj), id_q, jj > 0);  // dQ += dS K
                 umma::commit(&k_empty[jj % S]);
                 if (jj + 1 < nk) issue_dp(jj + 1);  // overwrites dS_j, read by dQ_j issued before
-                if (jj + 2 < nk) {
-                    mbar_wait(&s_free[jj & 1], (jj >> 1) & 1);  // S_j read out by the compute warps
-                    issue_s(jj + 2);
-                }
                 TKB_TR(0, jj, 2);
             }
             umma::commit(&dq_full);
@@ -534,12 +580,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         const uint32_t tDp = tbase + lane_off + C::tmem_dp();
         const float tau = p.scale_log2;
         const float scale = p.scale;
-        const float lse_r = p.lse2[(size_t)bh * p.n_pad + row];  // +inf on padded rows -> P = 0
+        const float nlse_r = p.lse2[(size_t)bh * p.n_pad + row];  // -lse2; -inf on padded rows -> P = 0
         const float dlt_r = p.delta[(size_t)bh * p.n_pad + row];
+        // Q, dO: SMEM (TMA, swizzled) -> TMEM A operands, once per CTA
+        mbar_wait(&qdo_full, 0);
+        smem_rows_to_tmem_a<D>(sQ, tbase + lane_off + C::tmem_qa(), r, h);
+        smem_rows_to_tmem_a<D>(sDo, tbase + lane_off + C::tmem_doa(), r, h);
+        tmem::wait_st();
+        tmem::fence_before();
+        mbar_arrive(&a_ready);
         for (int jj = 0; jj < nk; ++jj) {
             const int kv0 = jj * 128;
-            const uint32_t tS = tbase + lane_off + C::tmem_s(jj & 1);
-            mbar_wait(&s_full[jj & 1], (jj >> 1) & 1);
+            const uint32_t tS = tbase + lane_off + C::tmem_s();
+            mbar_wait(&s_full, jj & 1);
             if (threadIdx.x == 0) TKB_TR(1, jj, 0);
             tmem::fence_after();
             float pf[64];
@@ -548,13 +601,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf));
             tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf) + 32);
             tmem::fence_before();
-            mbar_arrive(&s_free[jj & 1]);
+            mbar_arrive(&s_free);
             // visible keys: kv < n, and causal kv <= row
             const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 64 * h;  // last visible column
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                const float pv = ex2_approx(fmaf(pf[c], tau, -lse_r));
-                pf[c] = (c > lim) ? 0.f : pv;
+            for (int c = 0; c < 64; c += 4) {
+                const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(nlse_r, nlse_r));
+                const float2 x23 =
+                    fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(nlse_r, nlse_r));
+                pf[c] = ex2_approx(x01.x);
+                pf[c + 1] = ex2_approx(x01.y);
+                float2 p23;
+                if ((c & 8) != 0) {  // a quarter of the exponentials on the FMA pipe
+                    p23 = ex2_poly2(x23);
+                } else {
+                    p23.x = ex2_approx(x23.x);
+                    p23.y = ex2_approx(x23.y);
+                }
+                pf[c + 2] = p23.x;
+                pf[c + 3] = p23.y;
+            }
+            if (lim < 63) {  // diagonal / ragged tail block only
+#pragma unroll
+                for (int c = 0; c < 64; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
             }
             mbar_wait(&dp_full, jj & 1);
             if (threadIdx.x == 0) TKB_TR(1, jj, 1);
@@ -567,9 +636,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {
                     const int cc = 32 * half + c;
-                    const float d0 = pf[cc] * (__uint_as_float(dpv[c]) - dlt_r) * scale;
-                    const float d1 = pf[cc + 1] * (__uint_as_float(dpv[c + 1]) - dlt_r) * scale;
-                    pk[cc / 2] = pack_bf16x2(d0, d1);
+                    const float2 g = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
+                                          make_float2(dlt_r, dlt_r));
+                    const float2 d = mul2(mul2(make_float2(pf[cc], pf[cc + 1]), g), make_float2(scale, scale));
+                    pk[cc / 2] = pack_bf16x2(d.x, d.y);
                 }
             }
             tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
@@ -597,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 }
 #undef TKB_TR
 
-// Delta = rowsum(dO o O), lse2 = L log2 e (+inf / 0 on padded rows).
+// Delta = rowsum(dO o O), lse2 = -L log2 e (-inf / 0 on padded rows: P = 0 there).
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
@@ -630,7 +700,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
     if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
         const size_t idx = (size_t)bh * n_pad + row;
         delta[idx] = row < n ? acc : 0.f;
-        lse2[idx] = row < n ? lse[(size_t)bh * n + row] * 1.44269504088896340736f : INFINITY;
+        lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
     }
 }
 

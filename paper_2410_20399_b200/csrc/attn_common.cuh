@@ -25,7 +25,7 @@ struct FwdParams {
 struct BwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128 (loads)
     CUtensorMap tm_dq, tm_dk, tm_dv;      // same layout (stores)
-    const float* lse2;                    // [B*H, Npad] L * log2(e); +inf on padded rows (workspace)
+    const float* lse2;                    // [B*H, Npad] -L * log2(e); -inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
     long long* trace;                     // optional per-role cycle timeline (tkb_debug_set_trace)
     int trace_every;                      // trace CTAs with linear id % trace_every == 0

@@ -8,6 +8,7 @@
 //   2: C = A  * B    A in TMEM (bf16 pairs), B[K][N] MN-major   (O += P V, TS)
 //   3: C = A  * B    A stored transposed [K][128] (MN-major), B[K][N] MN-major (dQ = dS K)
 //   4: C = A^T * B^T-free check of TMEM st/ld round trip (C = A as fp32)
+//   5: C = A  * B^T  A in TMEM (bf16 pairs), B[N][K] K-major        (S = Q K^T, Q in TMEM)
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -54,18 +55,18 @@ __global__ void __launch_bounds__(128, 1)
     // A rows/cols as loaded: variant 3 stores A^T [K][128]
     constexpr int A_ROWS = (VARIANT == 3) ? K : M;
     constexpr int A_COLS = (VARIANT == 3) ? M : K;
-    constexpr int B_ROWS = (VARIANT == 0) ? N : K;
-    constexpr int B_COLS = (VARIANT == 0) ? K : N;
+    constexpr int B_ROWS = (VARIANT == 0 || VARIANT == 5) ? N : K;
+    constexpr int B_COLS = (VARIANT == 0 || VARIANT == 5) ? K : N;
 
     if (threadIdx.x == 0) {
         uint32_t bytes = B_ROWS * B_COLS * 2;
-        if (VARIANT != 2) bytes += A_ROWS * A_COLS * 2;
+        if (VARIANT != 2 && VARIANT != 5) bytes += A_ROWS * A_COLS * 2;
         mbar_arrive_expect_tx(&bar_load, bytes);
-        if (VARIANT != 2)
+        if (VARIANT != 2 && VARIANT != 5)
             for (int a = 0; a < A_COLS / 64; ++a) tma::load_2d(sA + a * A_ROWS * 128, &tmA, &bar_load, a * 64, 0);
         for (int a = 0; a < B_COLS / 64; ++a) tma::load_2d(sB + a * B_ROWS * 128, &tmB, &bar_load, a * 64, 0);
     }
-    if (VARIANT == 2 || VARIANT == 4) {
+    if (VARIANT == 2 || VARIANT == 4 || VARIANT == 5) {
         // stage A (row = TMEM lane) into TMEM as bf16 pairs
         const int row = warp * 32 + lane;
         uint32_t r[64];
@@ -89,18 +90,18 @@ __global__ void __launch_bounds__(128, 1)
         mbar_wait(&bar_load, 0);
         tmem::fence_after();
         if (elect_one()) {
-            constexpr uint32_t idesc = umma::idesc_bf16<M, N, VARIANT == 3, VARIANT != 0>();
+            constexpr uint32_t idesc = umma::idesc_bf16<M, N, VARIANT == 3, VARIANT != 0 && VARIANT != 5>();
             const long long c0 = clock64();
             for (int rep = 0; rep < reps; ++rep)
 #pragma unroll
             for (int s = 0; s < K / 16; ++s) {
                 uint64_t bdesc;
-                if constexpr (VARIANT == 0) {
+                if constexpr (VARIANT == 0 || VARIANT == 5) {
                     bdesc = umma::desc_kmajor(smem_u32(sB + (s / 4) * (N * 128) + (s % 4) * 32));
                 } else {
                     bdesc = umma::desc_mnmajor(smem_u32(sB + s * 16 * 128), K * 128);
                 }
-                if constexpr (VARIANT == 2) {
+                if constexpr (VARIANT == 2 || VARIANT == 5) {
                     umma::mma_ts(t_c, t_a + s * 8, bdesc, idesc, s > 0);
                 } else {
                     uint64_t adesc;
@@ -160,7 +161,7 @@ int launch(const void* A, const void* B, float* C, cudaStream_t st, int reps, lo
     CUtensorMap ta, tb;
     std::string err;
     const int a_rows = (V == 3) ? K : M, a_cols = (V == 3) ? M : K;
-    const int b_rows = (V == 0) ? N : K, b_cols = (V == 0) ? K : N;
+    const int b_rows = (V == 0 || V == 5) ? N : K, b_cols = (V == 0 || V == 5) ? K : N;
     if (!make_2d(&ta, A, a_rows, a_cols, &err) || !make_2d(&tb, B, b_rows, b_cols, &err)) {
         fprintf(stderr, "selftest tmap: %s\n", err.c_str());
         return -1;
@@ -181,6 +182,7 @@ extern "C" __attribute__((visibility("default"))) int tkb_selftest_umma(int vari
     if (variant == V && n == NN && k == KK) return launch<NN, KK, V>(A, B, C, stream, reps, cycles);
     TKB_ST(0, 128, 128) TKB_ST(0, 128, 64) TKB_ST(1, 128, 128) TKB_ST(1, 64, 128) TKB_ST(2, 128, 128)
     TKB_ST(2, 64, 128) TKB_ST(3, 128, 128) TKB_ST(3, 64, 128) TKB_ST(4, 128, 128)
+    TKB_ST(5, 128, 128) TKB_ST(5, 128, 64)
 #undef TKB_ST
     return -2;
 }
@@ -246,5 +248,80 @@ extern "C" __attribute__((visibility("default"))) int tkb_selftest_reduce_bench(
     const int smem = 4 * 16384 + 1024;
     cudaFuncSetAttribute(reduce_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     reduce_bench_kernel<<<ctas, 128, smem, st>>>(tm, g, mode, iters, inflight, region_chunks);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Pipe-throughput microbenchmark for the softmax inner loop (one CTA of 256 threads):
+//   mode 0: ex2.approx (MUFU)       mode 1: cvt.rn.bf16x2.f32     mode 2: ex2 + cvt
+//   mode 3: ffma                    mode 4: fma.rn.f32x2 (packed)  mode 5: poly-3 exp2 emulation (f32x2)
+namespace {
+__global__ void __launch_bounds__(256, 1) pipe_bench_kernel(float* out, int mode, int iters, long long* cycles) {
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = -0.01f * (threadIdx.x + i);
+    uint32_t acc = 0;
+    __syncthreads();
+    const long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        if (mode == 0) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) a[i] = ex2_approx(a[i]);
+        } else if (mode == 1) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) acc += pack_bf16x2(a[i], a[i + 1]), a[i] += 1e-7f;
+        } else if (mode == 2) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+                a[i] = ex2_approx(a[i]);
+                a[i + 1] = ex2_approx(a[i + 1]);
+                acc += pack_bf16x2(a[i], a[i + 1]);
+            }
+        } else if (mode == 3) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) a[i] = fmaf(a[i], 0.999f, 1e-7f);
+        } else if (mode == 4) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+                asm volatile("{.reg .b64 x, y, z; mov.b64 x, {%0, %1}; mov.b64 y, {%2, %2}; mov.b64 z, {%3, %3};"
+                             "fma.rn.f32x2 x, x, y, z; mov.b64 {%0, %1}, x;}"
+                             : "+f"(a[i]), "+f"(a[i + 1]) : "f"(0.999f), "f"(1e-7f));
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+                float x0 = fmaxf(a[i], -127.f), x1 = fmaxf(a[i + 1], -127.f);
+                float r0, r1, f0, f1, p0, p1;
+                asm("{.reg .b64 x, rr, big, bk, fr, c3, c2, c1, c0, p;\n\t"
+                    "mov.b64 x, {%6, %7};\n\t"
+                    "mov.b64 big, {%8, %8};\n\t"
+                    "add.rm.ftz.f32x2 rr, x, big;\n\t"
+                    "sub.rn.ftz.f32x2 bk, rr, big;\n\t"
+                    "sub.rn.ftz.f32x2 fr, x, bk;\n\t"
+                    "mov.b64 c3, {%9, %9}; mov.b64 c2, {%10, %10}; mov.b64 c1, {%11, %11}; mov.b64 c0, {%12, %12};\n\t"
+                    "fma.rn.ftz.f32x2 p, fr, c3, c2;\n\t"
+                    "fma.rn.ftz.f32x2 p, p, fr, c1;\n\t"
+                    "fma.rn.ftz.f32x2 p, p, fr, c0;\n\t"
+                    "mov.b64 {%0, %1}, rr; mov.b64 {%2, %3}, fr; mov.b64 {%4, %5}, p;}"
+                    : "=f"(r0), "=f"(r1), "=f"(f0), "=f"(f1), "=f"(p0), "=f"(p1)
+                    : "f"(x0), "f"(x1), "f"(12582912.0f), "f"(0.0770954f), "f"(0.2275836f), "f"(0.6944390f),
+                      "f"(1.0f));
+                a[i] = __int_as_float((__float_as_int(r0) << 23) + __float_as_int(p0)) - 1e-3f;
+                a[i + 1] = __int_as_float((__float_as_int(r1) << 23) + __float_as_int(p1)) - 1e-3f;
+            }
+        }
+    }
+    const long long c1 = clock64();
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += a[i];
+    out[threadIdx.x] = s + (float)acc;
+    if (threadIdx.x == 0) cycles[0] = c1 - c0;
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_pipe_bench(float* out, int mode, int iters,
+                                                                             long long* cycles, cudaStream_t st) {
+    pipe_bench_kernel<<<1, 256, 0, st>>>(out, mode, iters, cycles);
     return (int)cudaGetLastError();
 }

@@ -61,6 +61,64 @@ TKB_DEVICE float ex2_approx(float x) {
     return r;
 }
 
+// Blackwell packed fp32 pair ops (one FMA-pipe instruction for two lanes of work).
+// d = a * b + c, elementwise on (x, y) pairs.
+TKB_DEVICE float2 fma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5}; mov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+TKB_DEVICE float2 mul2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+TKB_DEVICE float2 sub2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
+// 2^x for a pair on the FMA pipe (no MUFU): 2^floor(x) * p(frac(x)) with a degree-3
+// minimax polynomial (max rel. error ~9e-5, below bf16 resolution). x <= 127; x = -inf -> 0.
+TKB_DEVICE float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    float2 r, f, p;
+    asm("{.reg .b64 x, rr, big, bk, fr, c3, c2, c1, c0, p;\n\t"
+        "mov.b64 x, {%6, %7};\n\t"
+        "mov.b64 big, {%8, %8};\n\t"
+        "add.rm.ftz.f32x2 rr, x, big;\n\t"  // integer part in the low mantissa bits
+        "sub.rn.ftz.f32x2 bk, rr, big;\n\t"
+        "sub.rn.ftz.f32x2 fr, x, bk;\n\t"   // fraction in [0, 1)
+        "mov.b64 c3, {%9, %9}; mov.b64 c2, {%10, %10}; mov.b64 c1, {%11, %11}; mov.b64 c0, {%12, %12};\n\t"
+        "fma.rn.ftz.f32x2 p, fr, c3, c2;\n\t"
+        "fma.rn.ftz.f32x2 p, p, fr, c1;\n\t"
+        "fma.rn.ftz.f32x2 p, p, fr, c0;\n\t"
+        "mov.b64 {%0, %1}, rr; mov.b64 {%2, %3}, fr; mov.b64 {%4, %5}, p;}"
+        : "=f"(r.x), "=f"(r.y), "=f"(f.x), "=f"(f.y), "=f"(p.x), "=f"(p.y)
+        : "f"(x.x), "f"(x.y), "f"(12582912.0f), "f"(0.07711909f), "f"(0.22756439f), "f"(0.69514614f), "f"(1.0f));
+    float2 out;
+    out.x = __int_as_float((__float_as_int(r.x) << 23) + __float_as_int(p.x));
+    out.y = __int_as_float((__float_as_int(r.y) << 23) + __float_as_int(p.y));
+    return out;
+}
+
 template <int kRegs>
 TKB_DEVICE void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs)); }
 template <int kRegs>

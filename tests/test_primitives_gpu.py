@@ -25,12 +25,12 @@ def _st():
 
 @pytest.mark.parametrize("variant,n,k", [(0, 128, 128), (0, 128, 64), (1, 128, 128), (1, 64, 128),
                                          (2, 128, 128), (2, 64, 128), (3, 128, 128), (3, 64, 128),
-                                         (4, 128, 128)])
+                                         (4, 128, 128), (5, 128, 128), (5, 128, 64)])
 def test_umma_variant(cuda_dev, variant, n, k):
     g = torch.Generator().manual_seed(1000 * variant + n + k)
     M = 128
     A = torch.randn(M, k, generator=g).to(torch.bfloat16)
-    if variant == 0:
+    if variant in (0, 5):
         B = torch.randn(n, k, generator=g).to(torch.bfloat16)
         ref = A.float() @ B.float().t()
     elif variant == 4:
@@ -43,7 +43,7 @@ def test_umma_variant(cuda_dev, variant, n, k):
     A_rowmajor = A.to(cuda_dev)  # the TMEM-staged variants read A row-major
     B_dev = B.to(cuda_dev)
     C = torch.zeros(ref.shape, dtype=torch.float32, device=cuda_dev)
-    a_ptr = A_rowmajor.data_ptr() if variant in (2, 4) else A_dev.data_ptr()
+    a_ptr = A_rowmajor.data_ptr() if variant in (2, 4, 5) else A_dev.data_ptr()
     rc = _st()(variant, n, k, a_ptr, B_dev.data_ptr(), C.data_ptr(),
                torch.cuda.current_stream().cuda_stream, 1, None)
     assert rc == 0
