@@ -290,23 +290,30 @@ def main():
         step()
     torch.cuda.synchronize(dev)
 
-    # per-kernel timing (roofline): events around each kernel of one extra step
+    # per-kernel timing (roofline): CUDA events on the launching stream around each kernel
+    # (the backward's three kernels are isolated with the debug phase mask)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     kern_ms = {}
-    for part in ("fwd", "bwd"):
-        if part not in which:
-            continue
+
+    def time_it(fn, reps=3):
         e0, e1 = ev(), ev()
-        reps = 3
         e0.record(stream)
         for _ in range(reps):
-            if part == "fwd":
-                A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse)
-            else:
-                A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws)
+            fn()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        kern_ms[part] = e0.elapsed_time(e1) / reps
+        return e0.elapsed_time(e1) / reps
+
+    if "fwd" in which:
+        kern_ms["attn_fwd"] = time_it(lambda: A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse))
+    if "bwd" in which:
+        bwd = lambda: A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws)  # noqa
+        for name, mask in (("bwd_prep", 1), ("attn_bwd_dkdv", 2), ("attn_bwd_dq", 4)):
+            A.debug_set_bwd_phases(mask)
+            kern_ms[name] = time_it(bwd)
+        A.debug_set_bwd_phases(7)
+        bwd()  # restore complete outputs
+        torch.cuda.synchronize(dev)
 
     # timed region
     if world > 1:
@@ -315,6 +322,15 @@ def main():
     launches["n"] = 0
     start, end = ev(), ev()
     with ClockSampler(local) as clk:
+        # ~1 s of untimed steps under the sampler so the clock record covers steady load
+        t_soak = time.time()
+        while time.time() - t_soak < 1.0:
+            step()
+            torch.cuda.synchronize(dev)
+        launches["n"] = 0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
         start.record(stream)
         for _ in range(args.steps):
             step()
@@ -380,25 +396,46 @@ def main():
 
     if rank == 0:
         peaks, peak_src = load_peaks()
-        dom = max(kern_ms, key=lambda x: kern_ms[x] * 1.0)
-        dom_flops = flops(1, my_units, n, d, causal, dom)
-        achieved = dom_flops / (kern_ms[dom] / 1e3) / 1e12
-        peak = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+        # algorithmic work per launch of each kernel (the backward runs as
+        # a dK/dV kernel of 4 GEMMs and a dQ kernel of 3 GEMMs)
+        cf = 0.5 if causal else 1.0
+        work = {
+            "attn_fwd": ("tensor", 4.0 * my_units * n * n * d * cf),
+            "attn_bwd_dkdv": ("tensor", 8.0 * my_units * n * n * d * cf),
+            "attn_bwd_dq": ("tensor", 6.0 * my_units * n * n * d * cf),
+            "bwd_prep": ("hbm", (2 * 2 * my_units * n * d + 4 * my_units * n + 8 * my_units * n)),
+        }
+        dom = max(kern_ms, key=lambda x: kern_ms[x])
+        bound, amount = work[dom]
+        if bound == "tensor":
+            achieved = amount / (kern_ms[dom] / 1e3) / 1e12
+            peak = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+            unit = "TFLOP/s"
+        else:
+            achieved = amount / (kern_ms[dom] / 1e3) / 1e9
+            peak = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+            unit = "GB/s"
+        per_kernel = {}
+        for kname, ms_k in kern_ms.items():
+            b_k, amt = work[kname]
+            rate = amt / (ms_k / 1e3) / (1e12 if b_k == "tensor" else 1e9)
+            per_kernel[kname] = {"ms": ms_k, "bound": b_k, "achieved": rate,
+                                 "unit": "TFLOP/s" if b_k == "tensor" else "GB/s"}
         roofline = {
-            "bound": "tensor",
-            "kernel": f"attn_{dom}_kernel",
+            "bound": bound,
+            "kernel": dom,
             "achieved": achieved,
             "peak": peak,
-            "unit": "TFLOP/s",
+            "unit": unit,
             "frac": achieved / peak,
-            "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)" if peak_src == "measured"
-            else "fallback 1.59 PFLOP/s (B200_PROFILING.md)",
-            "frac_of_sustained": achieved / float(peaks.get("bf16_tflops_sustained", 1400.0)),
-            "frac_of_spec_2250": achieved / 2250.0,
+            "peak_source": ("measured bf16 burst, MEASURED_PEAKS.json" if bound == "tensor"
+                            else "measured HBM copy, MEASURED_PEAKS.json") if peak_src == "measured"
+            else "fallback (B200_PROFILING.md)",
+            "work_per_launch": amount,
+            "frac_of_sustained": (achieved / float(peaks.get("bf16_tflops_sustained", 1400.0))
+                                  if bound == "tensor" else None),
             "traffic": load_traffic(dom),
-            "per_kernel_ms": kern_ms,
-            "per_kernel_tflops": {p: flops(1, my_units, n, d, causal, p) / (kern_ms[p] / 1e3) / 1e12
-                                  for p in kern_ms},
+            "per_kernel": per_kernel,
         }
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -423,7 +460,7 @@ def main():
             "data": "synthetic",
             "config": workload_config(args, world),
             "tflops_per_gpu": value / world,
-            "frac_of_peak": value / world / peak,
+            "frac_of_peak": value / world / float(load_peaks()[0].get("bf16_tflops", 1590.0)),
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "roofline": roofline,

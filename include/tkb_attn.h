@@ -103,6 +103,10 @@ TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t*
  * every `every`-th work item; NULL disables. Not thread-safe; debugging only. */
 TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots);
 
+/* Debug / profiling: run only some backward stages (bit 0 prep, bit 1 dK/dV kernel,
+ * bit 2 dQ kernel; default 7). Results are only complete with 7. Not thread-safe. */
+TKB_API int tkb_debug_set_bwd_phases(int mask);
+
 /* Number of kernels the last successful fwd / bwd call on this thread launched. */
 TKB_API int tkb_last_launch_count(void);
 

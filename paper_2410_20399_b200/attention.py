@@ -81,6 +81,7 @@ _SIGS = {
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "tkb_last_launch_count": (ctypes.c_int, []),
     "tkb_debug_set_trace": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int]),
+    "tkb_debug_set_bwd_phases": (ctypes.c_int, [ctypes.c_int]),
     "tkb_last_error": (ctypes.c_char_p, []),
     "tkb_abi_version": (ctypes.c_int, []),
 }
@@ -228,6 +229,11 @@ def debug_set_trace(buf=None, every=1, slots=0):
     """Enable the backward kernel's per-role cycle timeline into a device int64 tensor
     [slots, 4, 32, 8] (debug only); buf=None disables."""
     lib().tkb_debug_set_trace(buf.data_ptr() if buf is not None else None, every, slots)
+
+
+def debug_set_bwd_phases(mask=7):
+    """Profiling only: run a subset of the backward stages (1 prep, 2 dK/dV, 4 dQ)."""
+    lib().tkb_debug_set_bwd_phases(int(mask))
 
 
 def last_launch_count():

@@ -710,7 +710,7 @@ int set_smem(Kern k, int bytes) {
 }
 
 template <int D, bool CAUSAL>
-int launch_main(const BwdParams& p, int batches, cudaStream_t stream) {
+int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases, int* launches) {
     static bool configured = false;
     if (!configured) {
         int e = set_smem(attn_bwd_dkdv_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
@@ -719,37 +719,50 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream) {
         configured = true;
     }
     dim3 grid(p.n_pad / 128, p.heads, batches);
-    attn_bwd_dkdv_kernel<D, CAUSAL><<<grid, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
-    int e = (int)cudaGetLastError();
-    if (e) return e;
-    attn_bwd_dq_kernel<D, CAUSAL><<<grid, kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
-    return (int)cudaGetLastError();
+    if (phases & 2) {
+        attn_bwd_dkdv_kernel<D, CAUSAL><<<grid, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+        int e = (int)cudaGetLastError();
+        if (e) return e;
+        ++*launches;
+    }
+    if (phases & 4) {
+        attn_bwd_dq_kernel<D, CAUSAL><<<grid, kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
+        int e = (int)cudaGetLastError();
+        if (e) return e;
+        ++*launches;
+    }
+    return 0;
 }
 
 template <int D>
 int launch_all(bool causal, const BwdParams& p, int batches, const void* o, const void* dout, const float* lse,
-               float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn, cudaStream_t stream, int* launches) {
-    constexpr int kRowsPerBlock = 256 / (D / 8);
-    dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, batches * p.heads);
-    bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                              reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
-                                              p.heads, p.n, p.n_pad, sb, sh, sn);
-    int e = (int)cudaGetLastError();
-    if (e) return e;
-    e = causal ? launch_main<D, true>(p, batches, stream) : launch_main<D, false>(p, batches, stream);
-    if (e) return e;
-    *launches = 3;
-    return 0;
+               float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn, cudaStream_t stream, int phases,
+               int* launches) {
+    *launches = 0;
+    if (phases & 1) {
+        constexpr int kRowsPerBlock = 256 / (D / 8);
+        dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, batches * p.heads);
+        bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                  reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
+                                                  p.heads, p.n, p.n_pad, sb, sh, sn);
+        int e = (int)cudaGetLastError();
+        if (e) return e;
+        ++*launches;
+    }
+    return causal ? launch_main<D, true>(p, batches, stream, phases, launches)
+                  : launch_main<D, false>(p, batches, stream, phases, launches);
 }
 
 }  // namespace bwd
 
 int launch_attn_bwd(int head_dim, bool causal, const BwdParams& p, int batches, const void* o, const void* dout,
                     const float* lse, float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn,
-                    cudaStream_t stream, int* launches) {
+                    cudaStream_t stream, int phases, int* launches) {
     if (head_dim == 128)
-        return bwd::launch_all<128>(causal, p, batches, o, dout, lse, lse2, delta, sb, sh, sn, stream, launches);
-    return bwd::launch_all<64>(causal, p, batches, o, dout, lse, lse2, delta, sb, sh, sn, stream, launches);
+        return bwd::launch_all<128>(causal, p, batches, o, dout, lse, lse2, delta, sb, sh, sn, stream, phases,
+                                    launches);
+    return bwd::launch_all<64>(causal, p, batches, o, dout, lse, lse2, delta, sb, sh, sn, stream, phases,
+                               launches);
 }
 
 }  // namespace tkb

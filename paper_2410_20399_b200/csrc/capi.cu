@@ -15,7 +15,7 @@
 namespace tkb {
 int launch_attn_bwd(int head_dim, bool causal, const BwdParams& p, int batches, const void* o, const void* dout,
                     const float* lse, float* lse2, float* delta, int64_t sb, int64_t sh, int64_t sn,
-                    cudaStream_t stream, int* launches);
+                    cudaStream_t stream, int phases, int* launches);
 int launch_check_finite(const void* const* ptrs, int nptrs, int batches, int heads, int n, int d, int64_t sb,
                         int64_t sh, int64_t sn, int* flag_dev, cudaStream_t stream);
 }  // namespace tkb
@@ -26,6 +26,7 @@ thread_local std::string g_err;
 thread_local int g_launches = 0;
 long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_trace)
 int g_trace_every = 1, g_trace_slots = 0;
+int g_bwd_phases = 7;  // debug: bit 0 prep, bit 1 dK/dV kernel, bit 2 dQ kernel
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -205,7 +206,7 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.scale_log2 = p.scale * 1.44269504088896340736f;
     int launches = 0;
     int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
-                                 s.n, st, &launches);
+                                 s.n, st, g_bwd_phases, &launches);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_bwd launch: ") + cudaGetErrorString((cudaError_t)e));
     g_launches = launches;
     return TKB_OK;
@@ -224,6 +225,11 @@ TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots) {
     g_trace = reinterpret_cast<long long*>(device_buf);
     g_trace_every = every > 0 ? every : 1;
     g_trace_slots = device_buf ? slots : 0;
+    return TKB_OK;
+}
+
+TKB_API int tkb_debug_set_bwd_phases(int mask) {
+    g_bwd_phases = mask & 7;
     return TKB_OK;
 }
 
