@@ -98,9 +98,10 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* desc, const void* q, const void* k
  * contiguous, balanced [begin, end) of `units` for `rank` of `world`. No collective. */
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
 
-/* Debug timeline of the backward kernel (the reference's Timeline, lcsf.hpp:165-224):
- * device buffer of slots x 3 roles x 32 iterations x 8 events int64 cycle stamps for
- * every `every`-th work item; NULL disables. Not thread-safe; debugging only. */
+/* Debug timeline of the kernels (the reference's Timeline, lcsf.hpp:165-224): device
+ * buffer of slots x 4 roles x 32 iterations x 8 events int64 cycle stamps; the backward
+ * traces every `every`-th work item, the persistent forward every `every`-th CTA.
+ * NULL disables. Not thread-safe; debugging only. */
 TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots);
 
 /* Debug / profiling: run only some backward stages (bit 0 prep, bit 1 dK/dV kernel,

@@ -7,7 +7,7 @@ import ctypes
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libtkb.so")
+LIB_PATH = os.environ.get("TKB_LIB_PATH") or os.path.join(PKG_DIR, "libtkb.so")
 SELFTEST_PATH = os.path.join(PKG_DIR, "libtkb_selftest.so")
 
 _cache = {}

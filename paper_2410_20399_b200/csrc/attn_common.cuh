@@ -17,8 +17,16 @@ constexpr int kRowsPerCta = kBlockM * kQStages;
 struct FwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_o;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128
     float* lse;                          // [B*H, N] fp32, may be null
+    int* sched;                          // persistent task counter pair (self-resetting)
+    long long* trace;                    // optional per-role cycle timeline (tkb_debug_set_trace)
+    int trace_every;
+    int trace_slots;
     int n;                               // sequence length
     int heads;
+    int bh;                              // batches * heads          (set by launch_attn_fwd)
+    int m_blocks;                        // 256-row query blocks     (set by launch_attn_fwd)
+    int tasks;                           // bh * m_blocks            (set by launch_attn_fwd)
+    int head_group;                      // heads per L2 group       (set by launch_attn_fwd)
     float scale_log2;                    // softmax_scale * log2(e)
 };
 
@@ -44,6 +52,6 @@ constexpr int kTraceEvents = 8;
 constexpr int kTraceRoles = 4;
 
 // Launchers (return cudaError_t as int).
-int launch_attn_fwd(int head_dim, bool causal, const FwdParams& p, int batches, cudaStream_t stream);
+int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream);
 
 }  // namespace tkb

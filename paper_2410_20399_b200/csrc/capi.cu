@@ -28,6 +28,15 @@ long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_trace)
 int g_trace_every = 1, g_trace_slots = 0;
 int g_bwd_phases = 7;  // debug: bit 0 prep, bit 1 dK/dV kernel, bit 2 dQ kernel
 
+// Per-device persistent-scheduler counters: 64 pairs used round-robin so kernels
+// running concurrently on different streams do not share a counter; each pair is
+// reset to zero by the last CTA of the grid that used it (lcsf::queue_exit).
+constexpr int kMaxDevices = 64;
+constexpr int kSchedPairs = 64;
+int* g_sched[kMaxDevices] = {};
+unsigned g_sched_next[kMaxDevices] = {};
+int g_num_sms[kMaxDevices] = {};
+
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -76,6 +85,27 @@ int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, con
     if (!tkb::host::make_tmap(tm, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, dims, strides, box,
                               CU_TENSOR_MAP_SWIZZLE_128B, &err))
         return fail(TKB_ERR_SHAPE, "tensor map: " + err);
+    return TKB_OK;
+}
+
+// One-time per-device state: SM count and the zeroed scheduler counters.
+int device_state(int* sms, int** sched) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) return fail(TKB_ERR_UNSUPPORTED, "device ordinal too large");
+    if (g_sched[dev] == nullptr) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        int* buf = nullptr;
+        cudaError_t e = cudaMalloc(&buf, kSchedPairs * 2 * sizeof(int));
+        if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("scheduler alloc: ") + cudaGetErrorString(e));
+        e = cudaMemset(buf, 0, kSchedPairs * 2 * sizeof(int));
+        if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("scheduler init: ") + cudaGetErrorString(e));
+        g_num_sms[dev] = n;
+        g_sched[dev] = buf;
+    }
+    *sms = g_num_sms[dev];
+    *sched = g_sched[dev] + 2 * (int)(__atomic_fetch_add(&g_sched_next[dev], 1u, __ATOMIC_RELAXED) % kSchedPairs);
     return TKB_OK;
 }
 
@@ -144,11 +174,16 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
     if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, s)) ||
         (rc = make_bhnd_map(&p.tm_v, v, d, s)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
         return rc;
+    int sms = 0;
+    if ((rc = device_state(&sms, &p.sched))) return rc;
     p.lse = lse;
+    p.trace = g_trace;
+    p.trace_every = g_trace_every;
+    p.trace_slots = g_trace_slots;
     p.n = d->seq;
     p.heads = d->heads;
     p.scale_log2 = scale_of(d) * 1.44269504088896340736f;
-    int e = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, st);
+    int e = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd launch: ") + cudaGetErrorString((cudaError_t)e));
     g_launches = 1;
     return TKB_OK;

@@ -39,6 +39,25 @@ TKB_DEVICE uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Explicit shared-space accesses (a generic pointer into dynamic SMEM can make the
+// compiler fall back to 64-bit generic loads/stores).
+TKB_DEVICE void sts_f32(uint32_t addr, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory"); }
+TKB_DEVICE void sts_u32(uint32_t addr, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory"); }
+TKB_DEVICE float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+TKB_DEVICE uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+TKB_DEVICE void sts_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // Named barriers (ids 1..15; id 0 is __syncthreads).
 TKB_DEVICE void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -83,6 +102,16 @@ TKB_DEVICE float2 mul2(float2 a, float2 b) {
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
 }
+TKB_DEVICE float2 add2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
 TKB_DEVICE float2 sub2(float2 a, float2 b) {
     float2 d;
     asm("{.reg .b64 ra, rb, rd;\n\t"
@@ -99,19 +128,19 @@ TKB_DEVICE float2 sub2(float2 a, float2 b) {
 TKB_DEVICE float2 ex2_poly2(float2 x) {
     x.x = fmaxf(x.x, -127.f);
     x.y = fmaxf(x.y, -127.f);
-    float2 r, f, p;
+    float2 r, p;
     asm("{.reg .b64 x, rr, big, bk, fr, c3, c2, c1, c0, p;\n\t"
-        "mov.b64 x, {%6, %7};\n\t"
-        "mov.b64 big, {%8, %8};\n\t"
+        "mov.b64 x, {%4, %5};\n\t"
+        "mov.b64 big, {%6, %6};\n\t"
         "add.rm.ftz.f32x2 rr, x, big;\n\t"  // integer part in the low mantissa bits
         "sub.rn.ftz.f32x2 bk, rr, big;\n\t"
         "sub.rn.ftz.f32x2 fr, x, bk;\n\t"   // fraction in [0, 1)
-        "mov.b64 c3, {%9, %9}; mov.b64 c2, {%10, %10}; mov.b64 c1, {%11, %11}; mov.b64 c0, {%12, %12};\n\t"
+        "mov.b64 c3, {%7, %7}; mov.b64 c2, {%8, %8}; mov.b64 c1, {%9, %9}; mov.b64 c0, {%10, %10};\n\t"
         "fma.rn.ftz.f32x2 p, fr, c3, c2;\n\t"
         "fma.rn.ftz.f32x2 p, p, fr, c1;\n\t"
         "fma.rn.ftz.f32x2 p, p, fr, c0;\n\t"
-        "mov.b64 {%0, %1}, rr; mov.b64 {%2, %3}, fr; mov.b64 {%4, %5}, p;}"
-        : "=f"(r.x), "=f"(r.y), "=f"(f.x), "=f"(f.y), "=f"(p.x), "=f"(p.y)
+        "mov.b64 {%0, %1}, rr; mov.b64 {%2, %3}, p;}"
+        : "=f"(r.x), "=f"(r.y), "=f"(p.x), "=f"(p.y)
         : "f"(x.x), "f"(x.y), "f"(12582912.0f), "f"(0.07711909f), "f"(0.22756439f), "f"(0.69514614f), "f"(1.0f));
     float2 out;
     out.x = __int_as_float((__float_as_int(r.x) << 23) + __float_as_int(p.x));

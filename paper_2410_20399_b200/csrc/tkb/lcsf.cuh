@@ -1,0 +1,98 @@
+// lcsf.cuh — the load-compute-store-finish (LCSF) template on Blackwell.
+//
+// Reference: kittensim's LCSF executor (lcsf.hpp:38-819): a producer worker fills an
+// N-slot input ring, consumer workers compute on it, each slot guarded by a counter
+// barrier with generations (Barrier lcsf.hpp:40-54; TaskRun lcsf.hpp:302-379: slot
+// = i % stages, generation = i / stages, inputs_arrived expects 1 arrival,
+// inputs_finished expects one per consumer), tasks enumerated with the sequence
+// block innermost (make_common, kernels.hpp:267-275).
+//
+// On B200 the workers are warp roles of one persistent CTA:
+//   ring<S>        the N-slot ring; full[s] completes on TMA transaction bytes (the
+//                  producer's arrive + expect_tx), empty[s] on the consumers' release
+//                  (a tcgen05.commit when the consumer is the tensor core);
+//                  phase parity = generation & 1
+//   ring_state     (slot, phase) cursor that every role advances in lockstep
+//   work_queue     the persistent task scheduler: one producer lane claims task ids
+//                  from a global atomic counter (dynamic, so heavy causal tasks first
+//                  balance across SMs) and broadcasts them through a 2-slot SMEM ring
+//                  to the other roles; the counter resets itself at grid exit.
+#pragma once
+#include "mbarrier.cuh"
+
+namespace tkb {
+namespace lcsf {
+
+// (slot, phase) cursor over an S-slot ring
+template <int S>
+struct ring_state {
+    int slot = 0;
+    uint32_t phase = 0;
+    TKB_DEVICE void advance() {
+        if (++slot == S) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+template <int S>
+struct ring {
+    mbarrier full[S];
+    mbarrier empty[S];
+    TKB_DEVICE void init(uint32_t full_count, uint32_t empty_count) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], full_count);
+            mbar_init(&empty[s], empty_count);
+        }
+    }
+    // producer side: wait until the consumers released generation (phase ^ 1) of this slot
+    TKB_DEVICE void wait_empty(const ring_state<S>& st) { mbar_wait(&empty[st.slot], st.phase ^ 1u); }
+    // consumer side: wait until the producer filled the current generation
+    TKB_DEVICE void wait_full(const ring_state<S>& st) { mbar_wait(&full[st.slot], st.phase); }
+};
+
+// Persistent task queue (ids in [0, total)); -1 terminates.
+struct work_queue {
+    static constexpr int kSlots = 2;
+    int id[kSlots];
+    mbarrier full[kSlots];
+    mbarrier empty[kSlots];
+    TKB_DEVICE void init(uint32_t consumers) {
+        for (int s = 0; s < kSlots; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], consumers);
+        }
+    }
+    // producer lane: claim the n-th task of this CTA (n = 0 is blockIdx.x) and publish it
+    TKB_DEVICE int claim(int n, int* counter, int total) {
+        int t = (n == 0) ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(counter, 1);
+        if (t >= total) t = -1;
+        const int s = n % kSlots;
+        mbar_wait(&empty[s], ((n / kSlots) & 1) ^ 1u);
+        id[s] = t;
+        mbar_arrive(&full[s]);  // release: the id store is visible to acquirers
+        return t;
+    }
+    // consumer: read the n-th task (one lane per warp calls release() after use)
+    TKB_DEVICE int get(int n) {
+        const int s = n % kSlots;
+        mbar_wait(&full[s], (n / kSlots) & 1);
+        return *reinterpret_cast<volatile int*>(&id[s]);
+    }
+    TKB_DEVICE void release(int n) { mbar_arrive(&empty[n % kSlots]); }
+};
+
+// Grid exit: the last CTA resets the task counter so the next launch starts at zero.
+// counter[0] = claims beyond the grid, counter[1] = CTAs finished.
+TKB_DEVICE void queue_exit(int* counter) {
+    __threadfence();
+    if (atomicAdd(&counter[1], 1) == (int)gridDim.x - 1) {
+        counter[0] = 0;
+        counter[1] = 0;
+        __threadfence();
+    }
+}
+
+}  // namespace lcsf
+}  // namespace tkb

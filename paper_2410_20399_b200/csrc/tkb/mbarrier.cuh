@@ -52,13 +52,28 @@ TKB_DEVICE bool mbar_try_wait(mbarrier* b, uint32_t parity) {
     return ok != 0;
 }
 
-// Blocking wait for the phase with the given parity to complete. In debug
-// builds a bounded spin traps (the DeadlockError analogue, lcsf.hpp:486-489).
+TKB_DEVICE uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Blocking wait for the phase with the given parity to complete. A wait that has spun
+// for 20 s traps instead of hanging the GPU: the DeadlockError analogue of the reference
+// (lcsf.hpp:486-489). -DTKB_NO_DEADLOCK_TRAP removes the bound.
 TKB_DEVICE void mbar_wait(mbarrier* b, uint32_t parity) {
-#ifdef TKB_DEBUG_DEADLOCK
-    uint64_t spins = 0;
+#ifndef TKB_NO_DEADLOCK_TRAP
+    if (mbar_try_wait(b, parity)) return;
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
     while (!mbar_try_wait(b, parity)) {
-        if (++spins > (1ull << 28)) __trap();
+        if ((++spins & 4095u) == 0) {
+            const uint64_t now = globaltimer_ns();
+            if (t0 == 0)
+                t0 = now;
+            else if (now - t0 > 20000000000ull)
+                __trap();
+        }
     }
 #else
     while (!mbar_try_wait(b, parity)) {

@@ -73,6 +73,14 @@ TKB_DEVICE void reduce_add_3d(const void* tmap, const void* smem_src, int c0, in
         : "memory");
 }
 
+// L2 prefetch of a 4-D tile (no SMEM destination, no barrier).
+TKB_DEVICE void prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
 // Order generic-proxy global accesses with async-proxy (TMA) ones.
 TKB_DEVICE void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 

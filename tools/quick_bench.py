@@ -17,17 +17,25 @@ def t_events(fn, iters=20, warmup=5):
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--bwd", action="store_true")
+ap.add_argument("--sdpa", action="store_true")
+ap.add_argument("--uniform", action="store_true", help="U(-1,1) inputs (bench.py data) instead of randn")
+ap.add_argument("--no-causal", action="store_true")
+ap.add_argument("--only-causal", action="store_true")
 ap.add_argument("--shapes", default="16,16,4096,128;16,16,4096,64;4,16,16384,128;16,16,1024,128")
 args = ap.parse_args()
 for sh in args.shapes.split(";"):
     B, H, N, D = map(int, sh.split(","))
-    q, k, v = (torch.randn(B, H, N, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-    for causal in (False, True):
+    if args.uniform:
+        q, k, v = (torch.empty(B, H, N, D, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1) for _ in range(3))
+    else:
+        q, k, v = (torch.randn(B, H, N, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    for causal in ((False,) if args.no_causal else (True,) if args.only_causal else (False, True)):
         o, lse = A.attention_fwd(q, k, v, causal=causal)
         ms = t_events(lambda: A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse))
         fl = 4 * B * H * N * N * D * (0.5 if causal else 1.0)
         line = f"fwd B{B} H{H} N{N} D{D} causal={int(causal)}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOPS"
         try:
+            if not args.sdpa: raise RuntimeError("skipped")
             ref = t_events(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal))
             line += f"   | torch sdpa {fl/ref/1e9:7.1f} TFLOPS"
         except Exception as ex:
@@ -41,6 +49,7 @@ for sh in args.shapes.split(";"):
             fl = 10 * B * H * N * N * D * (0.5 if causal else 1.0)
             line = f"bwd B{B} H{H} N{N} D{D} causal={int(causal)}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOPS"
             try:
+                if not args.sdpa: raise RuntimeError("skipped")
                 qr, kr, vr = (x.detach().clone().requires_grad_() for x in (q, k, v))
                 out = torch.nn.functional.scaled_dot_product_attention(qr, kr, vr, is_causal=causal)
                 ref = t_events(lambda: torch.autograd.grad(out, (qr, kr, vr), do, retain_graph=True))
