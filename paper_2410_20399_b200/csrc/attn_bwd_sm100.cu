@@ -32,6 +32,7 @@
 // [64h, 64h + 64) it has itself read. Tensor ops issued by one thread run in order,
 // so a GEMM that overwrites a region is always issued after the GEMM reading it.
 #include <cuda.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "attn_common.cuh"
@@ -61,24 +62,20 @@ constexpr uint32_t kDescHi = umma::desc_hi_sw128(1024);  // SBO = 8 rows x 128 B
 // X = A B^T with A [128 rows][D] and B [128 rows][D], both K-major (K = D)
 template <int D>
 TKB_DEVICE void mm_abt(uint32_t dst, uint32_t a, uint32_t b, uint32_t idesc) {
-    a = umma::opaque(a);
-    b = umma::opaque(b);
 #pragma unroll
     for (int k = 0; k < D / 16; ++k) {
         const uint32_t off = (k / 4) * kAtomBytes + (k % 4) * 32;
-        umma::mma_ss_split(dst, umma::desc_lo(a + off, 16), kDescHi, umma::desc_lo(b + off, 16), kDescHi, idesc,
-                           k > 0);
+        umma::mma_ss_e(dst, umma::desc_lo(a + off, 16), kDescHi, umma::desc_lo(b + off, 16), kDescHi, idesc, k > 0);
     }
 }
 
 // X = A B^T with A in TMEM (128 lanes x D, bf16 pairs) and B [128 rows][D] K-major (K = D)
 template <int D>
 TKB_DEVICE void mm_tmem_abt(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc) {
-    b = umma::opaque(b);
 #pragma unroll
     for (int k = 0; k < D / 16; ++k) {
         const uint32_t off = (k / 4) * kAtomBytes + (k % 4) * 32;
-        umma::mma_ts_split(dst, a_tmem + k * 8, umma::desc_lo(b + off, 16), kDescHi, idesc, k > 0);
+        umma::mma_ts_e(dst, a_tmem + k * 8, umma::desc_lo(b + off, 16), kDescHi, idesc, k > 0);
     }
 }
 
@@ -103,13 +100,25 @@ TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, i
         tmem::st_32x32b_x16(tdst + h * 16, v);
 }
 
-// acc (+)= A[tmem: 128 lanes x 128 K as bf16 pairs] B with B [128 K rows][D] MN-major
-TKB_DEVICE void mma_tmem_a(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc, bool acc) {
-    b = umma::opaque(b);
+// acc (+)= A[tmem: 128 lanes x 128 K as bf16 pairs] B with B [128 K rows][D] MN-major, issued
+// in kChunks K-chunks of 32 as the compute warps hand them over (chunk c = 2 * half_h + sub:
+// keys / queries [32c, 32c + 32), packed A columns [16c, 16c + 16)); the chunk order below
+// follows the order in which the two column halves finish.
+constexpr int kChunks = 4;
+template <int C0, int C1, int C2, int C3, class WaitChunk>
+TKB_DEVICE void mma_tmem_a_chunked(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc, bool acc,
+                                   WaitChunk&& wait_chunk) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        umma::mma_ts_split(dst, a_tmem + k * 8, umma::desc_lo(b + k * 2048, kAtomBytes), kDescHi, idesc,
-                           acc || k > 0);
+    for (int i = 0; i < kChunks; ++i) {
+        const int c = (i == 0) ? C0 : (i == 1) ? C1 : (i == 2) ? C2 : C3;
+        wait_chunk(c);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const int k = 2 * c + kk;
+            umma::mma_ts_e(dst, a_tmem + k * 8, umma::desc_lo(b + k * 2048, kAtomBytes), kDescHi, idesc,
+                           acc || i > 0 || kk > 0);
+        }
+    }
 }
 
 // TMEM fp32 [lane r][D] -> bf16 -> SW128 smem tile: row r, columns [h*D/2, (h+1)*D/2)
@@ -159,7 +168,7 @@ struct CfgKV {
     static constexpr int kOffLse = kOffDo + kStages * T::kTileBytes;  // kStages x 128 fp32
     static constexpr int kOffDelta = kOffLse + kStages * 512;         // kStages x 128 fp32
     static constexpr int kOffBar = kOffDelta + kStages * 512;
-    static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + alignment slack
+    static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // + alignment slack
     static_assert(kSmemBytes <= 232448, "smem");
     static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dv() { return 128u; }
@@ -183,10 +192,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
     mbarrier& kv_full = bars[0];
     mbarrier& s_full = bars[1];
-    mbarrier& p_full = bars[2];
     mbarrier& dp_full = bars[3];
-    mbarrier& ds_full = bars[4];
     mbarrier& dkv_full = bars[5];
+    mbarrier* p_full = bars + 32;   // [kChunks] P^T chunks (32 queries each)
+    mbarrier* ds_full = bars + 36;  // [kChunks] dS^T chunks
     mbarrier* q_full = bars + 8;     // [S]
     mbarrier* q_empty = bars + 12;   // [S]
     mbarrier* do_full = bars + 16;   // [S]
@@ -209,10 +218,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     if (warp == kWarpLoad && lane == 0) {
         mbar_init(&kv_full, 1);
         mbar_init(&s_full, 1);
-        mbar_init(&p_full, kComputeThreads);
         mbar_init(&dp_full, 1);
-        mbar_init(&ds_full, kComputeThreads);
         mbar_init(&dkv_full, 1);
+        for (int c = 0; c < kChunks; ++c) {
+            mbar_init(&p_full[c], kComputeThreads / 2);  // the 4 warps of one column half
+            mbar_init(&ds_full[c], kComputeThreads / 2);
+        }
         for (int s = 0; s < S; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
@@ -259,8 +270,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             }
         }
     } else if (warp == kWarpMma) {
-        if (lane == 0) {
+        {
             // ------------------------------------------------------------- MMA
+            // converged warp; one elected lane issues each tcgen05 op
             constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
             constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK
             const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
@@ -270,44 +282,48 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             mbar_wait(&q_full[0], 0);
             tmem::fence_after();
             mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(0), id_s);
-            umma::commit(&s_full);
+            umma::commit_e(&s_full);
             mbar_wait(&do_full[0], 0);
             tmem::fence_after();
             mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(0), id_s);
-            umma::commit(&dp_full);
+            umma::commit_e(&dp_full);
             for (int t = 0; t < T; ++t) {
                 const uint32_t ph = t & 1;
-                // dV += P_t^T dO_t
+                // dV += P_t^T dO_t, chunk by chunk as P^T arrives
                 TKB_TR(0, t, 0);
-                mbar_wait(&p_full, ph);
+                mma_tmem_a_chunked<0, 2, 1, 3>(tbase + C::tmem_dv(), tbase + C::tmem_s() + 32, doaddr(t), id_kv, t > 0,
+                                   [&](int c) {
+                                       mbar_wait(&p_full[c], ph);
+                                       tmem::fence_after();
+                                   });
                 TKB_TR(0, t, 1);
-                tmem::fence_after();
-                mma_tmem_a(tbase + C::tmem_dv(), tbase + C::tmem_s() + 32, doaddr(t), id_kv, t > 0);
-                umma::commit(&do_empty[t % S]);
+                umma::commit_e(&do_empty[t % S]);
                 // S_{t+1}: overwrites P_t, read by dV_t which was issued before
                 if (t + 1 < T) {
                     mbar_wait(&q_full[(t + 1) % S], ((t + 1) / S) & 1);
                     tmem::fence_after();
                     mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(t + 1), id_s);
-                    umma::commit(&s_full);
+                    umma::commit_e(&s_full);
                 }
                 // dK += dS_t^T Q_t
                 TKB_TR(0, t, 2);
-                mbar_wait(&ds_full, ph);
+                mma_tmem_a_chunked<1, 2, 0, 3>(tbase + C::tmem_dk(), tbase + C::tmem_dp() + 32, qaddr(t), id_kv, t > 0,
+                                   [&](int c) {
+                                       mbar_wait(&ds_full[c], ph);
+                                       tmem::fence_after();
+                                   });
                 TKB_TR(0, t, 3);
-                tmem::fence_after();
-                mma_tmem_a(tbase + C::tmem_dk(), tbase + C::tmem_dp() + 32, qaddr(t), id_kv, t > 0);
-                umma::commit(&q_empty[t % S]);
+                umma::commit_e(&q_empty[t % S]);
                 // dP_{t+1}: overwrites dS_t, read by dK_t which was issued before
                 if (t + 1 < T) {
                     mbar_wait(&do_full[(t + 1) % S], ((t + 1) / S) & 1);
                     tmem::fence_after();
                     mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(t + 1), id_s);
-                    umma::commit(&dp_full);
+                    umma::commit_e(&dp_full);
                 }
                 TKB_TR(0, t, 4);
             }
-            umma::commit(&dkv_full);
+            umma::commit_e(&dkv_full);
         }
     } else {
         // ----------------------------------------------------------------- COMPUTE
@@ -338,6 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < 64; c += 4) {
+                if (c == 32) {  // first 32 queries of this half are done: hand chunk 2h over
+                    tmem::st_32x32b_x16(tS + 32 + 32 * h, pk);
+                }
                 const float4 l4 = nlse4[c / 4];  // smem broadcast; holds -lse2
                 const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(l4.x, l4.y));
                 const float2 x23 =
@@ -365,17 +384,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
                 pk[c / 2] = pack_bf16x2(p0, p1);
                 pk[c / 2 + 1] = pack_bf16x2(p2, p3);
             }
-            tmem::st_32x32b_x32(tS + 32 + 32 * h, pk);
+            tmem::wait_st();  // chunk 2h (stored mid-loop)
+            tmem::fence_before();
+            mbar_arrive(&p_full[2 * h]);
+            tmem::st_32x32b_x16(tS + 32 + 32 * h + 16, pk + 16);
             tmem::wait_st();
             tmem::fence_before();
-            mbar_arrive(&p_full);
+            mbar_arrive(&p_full[2 * h + 1]);
             if (threadIdx.x == 0) TKB_TR(1, t, 1);
             // dS^T = P^T o (dP^T - Delta) * scale
             mbar_wait(&dp_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 2);
             tmem::fence_after();
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
+            // the dS^T chunk a half writes lies inside the dP^T columns of half (h == 0 ? 1 : 0):
+            // process that half first so no column is overwritten before it is read (compile-time
+            // half index: the register arrays stay in registers)
+            auto ds_half = [&](auto half_c) {
+                constexpr int half = decltype(half_c)::value;
                 uint32_t dpv[32];
                 tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
 #pragma unroll
@@ -392,11 +417,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
                     pk[cc / 2] = pack_bf16x2(s01.x, s01.y);
                     pk[cc / 2 + 1] = pack_bf16x2(s23.x, s23.y);
                 }
+                // dS^T chunk 2h + half -> TMEM; its own dP^T columns were read above
+                tmem::st_32x32b_x16(tDp + 32 + 32 * h + 16 * half, pk + 16 * half);
+                tmem::wait_st();
+                tmem::fence_before();
+                mbar_arrive(&ds_full[2 * h + half]);
+            };
+            if (h == 0) {
+                ds_half(std::integral_constant<int, 1>{});
+                ds_half(std::integral_constant<int, 0>{});
+            } else {
+                ds_half(std::integral_constant<int, 0>{});
+                ds_half(std::integral_constant<int, 1>{});
             }
-            tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
-            tmem::wait_st();
-            tmem::fence_before();
-            mbar_arrive(&ds_full);
             if (threadIdx.x == 0) TKB_TR(1, t, 3);
         }
         // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q and dO rings are free) -> TMA store
@@ -433,7 +466,7 @@ struct CfgQ {
     static constexpr int kOffK = kOffDo + T::kTileBytes;
     static constexpr int kOffV = kOffK + kStages * T::kTileBytes;
     static constexpr int kOffBar = kOffV + kStages * T::kTileBytes;
-    static constexpr int kSmemBytes = kOffBar + 256 + 1024;
+    static constexpr int kSmemBytes = kOffBar + 512 + 1024;
     static_assert(kSmemBytes <= 232448, "smem");
     // S | dP | dQ | Q (A operand) | dO (A operand): 128 + 128 + D + D/2 + D/2 <= 512
     static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
@@ -460,8 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     mbarrier& s_free = bars[2];
     mbarrier& a_ready = bars[3];  // Q, dO copied into TMEM
     mbarrier& dp_full = bars[5];
-    mbarrier& ds_full = bars[6];
     mbarrier& dq_full = bars[7];
+    mbarrier* ds_full = bars + 32;  // [kChunks] dS chunks (32 keys each)
     mbarrier* k_full = bars + 8;    // [S]
     mbarrier* k_empty = bars + 12;  // [S]
     mbarrier* v_full = bars + 16;   // [S]
@@ -486,8 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         mbar_init(&s_free, kComputeThreads);
         mbar_init(&a_ready, kComputeThreads);
         mbar_init(&dp_full, 1);
-        mbar_init(&ds_full, kComputeThreads);
         mbar_init(&dq_full, 1);
+        for (int c = 0; c < kChunks; ++c) mbar_init(&ds_full[c], kComputeThreads / 2);
         for (int s = 0; s < S; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
@@ -532,8 +565,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             }
         }
     } else if (warp == kWarpMma) {
-        if (lane == 0) {
-            // ------------------------------------------------------------- MMA
+        {
+            // ------------------------------------------------------------- MMA (converged warp)
             constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
             constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
             auto kaddr = [&](int jj) { return smem_u32(sK + (jj % S) * TL::kTileBytes); };
@@ -542,14 +575,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 mbar_wait(&k_full[jj % S], (jj / S) & 1);
                 tmem::fence_after();
                 mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(jj), id_s);
-                umma::commit(&s_full);
+                umma::commit_e(&s_full);
             };
             auto issue_dp = [&](int jj) {  // dP_j = dO V_j^T
                 mbar_wait(&v_full[jj % S], (jj / S) & 1);
                 tmem::fence_after();
                 mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(jj), id_s);
-                umma::commit(&dp_full);
-                umma::commit(&v_empty[jj % S]);
+                umma::commit_e(&dp_full);
+                umma::commit_e(&v_empty[jj % S]);
             };
             mbar_wait(&a_ready, 0);
             issue_s(0);
@@ -560,15 +593,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                     issue_s(jj + 1);
                 }
                 TKB_TR(0, jj, 0);
-                mbar_wait(&ds_full, jj & 1);
+                mma_tmem_a_chunked<1, 2, 0, 3>(tbase + C::tmem_dq(), tbase + C::tmem_dp() + 32, kaddr(jj), id_q,
+                                               jj > 0, [&](int c) {  // dQ += dS K, chunk by chunk
+                                                   mbar_wait(&ds_full[c], jj & 1);
+                                                   tmem::fence_after();
+                                               });
                 TKB_TR(0, jj, 1);
-                tmem::fence_after();
-                mma_tmem_a(tbase + C::tmem_dq(), tbase + C::tmem_dp() + 32, kaddr(jj), id_q, jj > 0);  // dQ += dS K
-                umma::commit(&k_empty[jj % S]);
+                umma::commit_e(&k_empty[jj % S]);
                 if (jj + 1 < nk) issue_dp(jj + 1);  // overwrites dS_j, read by dQ_j issued before
                 TKB_TR(0, jj, 2);
             }
-            umma::commit(&dq_full);
+            umma::commit_e(&dq_full);
         }
     } else {
         // ----------------------------------------------------------------- COMPUTE
@@ -629,8 +664,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             if (threadIdx.x == 0) TKB_TR(1, jj, 1);
             tmem::fence_after();
             uint32_t pk[32];
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
+            auto ds_half = [&](auto half_c) {  // (see bwd_dkdv: compile-time half, read-before-overwrite order)
+                constexpr int half = decltype(half_c)::value;
                 uint32_t dpv[32];
                 tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
 #pragma unroll
@@ -641,11 +676,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                     const float2 d = mul2(mul2(make_float2(pf[cc], pf[cc + 1]), g), make_float2(scale, scale));
                     pk[cc / 2] = pack_bf16x2(d.x, d.y);
                 }
+                tmem::st_32x32b_x16(tDp + 32 + 32 * h + 16 * half, pk + 16 * half);
+                tmem::wait_st();
+                tmem::fence_before();
+                mbar_arrive(&ds_full[2 * h + half]);
+            };
+            if (h == 0) {
+                ds_half(std::integral_constant<int, 1>{});
+                ds_half(std::integral_constant<int, 0>{});
+            } else {
+                ds_half(std::integral_constant<int, 0>{});
+                ds_half(std::integral_constant<int, 1>{});
             }
-            tmem::st_32x32b_x32(tDp + 32 + 32 * h, pk);
-            tmem::wait_st();
-            tmem::fence_before();
-            mbar_arrive(&ds_full);
             if (threadIdx.x == 0) TKB_TR(1, jj, 2);
         }
         // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM (the Q tile is free) -> TMA store
