@@ -25,14 +25,15 @@
 // (tools/reduce_bench.py), which caps 128-row KV tiles well below the tensor rate.
 // Recomputing S and dP in bwd_dq (7 GEMMs instead of 5) costs less than that.
 //
-// Both main kernels: warps 0-7 COMPUTE (thread = (TMEM lane row, column half h)),
-// warp 8 MMA (one thread issues every tcgen05.mma), warp 9 LOAD (TMA).
-// bf16 P / dS live in TMEM next to the fp32 values they replace: half h writes only
-// columns [32 + 32h, 64 + 32h) of the S / dP region, i.e. inside the columns
-// [64h, 64h + 64) it has itself read. Tensor ops issued by one thread run in order,
-// so a GEMM that overwrites a region is always issued after the GEMM reading it.
+// Both main kernels: warps 0-15 COMPUTE, thread = (TMEM lane row, column group g of 32),
+// four warps per SM sub-partition so the exp / FMA / MUFU work of a 128 x 128 tile is
+// spread over four instruction streams; warp 16 MMA (converged, one elected lane issues);
+// warp 17 LOAD (TMA). bf16 P / dS live in TMEM next to the fp32 values they replace:
+// group g writes packed columns [32g, 32g + 16) of the S / dP region, inside the 32
+// columns it has itself read, and hands its 32-wide K chunk to the MMA warp at once.
+// Tensor ops issued by one thread run in order, so a GEMM that overwrites a region is
+// always issued after the GEMM reading it.
 #include <cuda.h>
-#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "attn_common.cuh"
@@ -42,10 +43,11 @@
 namespace tkb {
 namespace bwd {
 
-constexpr int kThreads = 320;
-constexpr int kWarpMma = 8;
-constexpr int kWarpLoad = 9;
-constexpr int kComputeThreads = 256;
+constexpr int kGroups = 4;                          // 32-column groups per 128-wide tile
+constexpr int kComputeThreads = kGroups * 128;      // warps 0-15
+constexpr int kWarpMma = 16;
+constexpr int kWarpLoad = 17;
+constexpr int kThreads = kComputeThreads + 64;      // 576
 constexpr int kBarCompute = 1;
 constexpr int kAtomBytes = 128 * 128;  // 128 rows x 128 B (one SW128 column block)
 
@@ -79,14 +81,32 @@ TKB_DEVICE void mm_tmem_abt(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t 
     }
 }
 
-// SW128 smem tile row r, columns [h*D/2, (h+1)*D/2) -> TMEM A-operand columns (bf16 pairs)
+// acc (+)= A B over K = 128: A = bf16 pairs in TMEM, group g's 32-wide K chunk at packed
+// columns [32g, 32g + 16) of a_tmem (k-steps 2g, 2g+1); B [128 K rows][D] MN-major SMEM.
+// Each chunk is issued as soon as `wait_chunk(g)` returns.
+template <class WaitChunk>
+TKB_DEVICE void mma_tmem_a_groups(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc, bool acc,
+                                  WaitChunk&& wait_chunk) {
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+        wait_chunk(g);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const int k = 2 * g + kk;
+            umma::mma_ts_e(dst, a_tmem + 32 * g + 8 * kk, umma::desc_lo(b + k * 2048, kAtomBytes), kDescHi, idesc,
+                           acc || g > 0 || kk > 0);
+        }
+    }
+}
+
+// SW128 smem tile row r, columns [g D/4, (g+1) D/4) -> TMEM A-operand columns (bf16 pairs)
 template <int D>
-TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, int h) {
-    constexpr int kChunks = D / 16;  // 16-byte chunks per half row
+TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, int g) {
+    constexpr int kChunks = D / 32;  // 16-byte chunks per quarter row
     uint32_t v[kChunks * 4];
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) {
-        const int gc = h * kChunks + q;
+        const int gc = g * kChunks + q;
         const int atom = gc / 8, ch = gc % 8;
         const uint4 u = *reinterpret_cast<const uint4*>(tile + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16));
         v[4 * q] = u.x;
@@ -95,51 +115,31 @@ TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, i
         v[4 * q + 3] = u.w;
     }
     if constexpr (D == 128)
-        tmem::st_32x32b_x32(tdst + h * 32, v);
+        tmem::st_32x32b_x16(tdst + g * 16, v);
     else
-        tmem::st_32x32b_x16(tdst + h * 16, v);
+        tmem::st_32x32b_x8(tdst + g * 8, v);
 }
 
-// acc (+)= A[tmem: 128 lanes x 128 K as bf16 pairs] B with B [128 K rows][D] MN-major, issued
-// in kChunks K-chunks of 32 as the compute warps hand them over (chunk c = 2 * half_h + sub:
-// keys / queries [32c, 32c + 32), packed A columns [16c, 16c + 16)); the chunk order below
-// follows the order in which the two column halves finish.
-constexpr int kChunks = 4;
-template <int C0, int C1, int C2, int C3, class WaitChunk>
-TKB_DEVICE void mma_tmem_a_chunked(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc, bool acc,
-                                   WaitChunk&& wait_chunk) {
-#pragma unroll
-    for (int i = 0; i < kChunks; ++i) {
-        const int c = (i == 0) ? C0 : (i == 1) ? C1 : (i == 2) ? C2 : C3;
-        wait_chunk(c);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-            const int k = 2 * c + kk;
-            umma::mma_ts_e(dst, a_tmem + k * 8, umma::desc_lo(b + k * 2048, kAtomBytes), kDescHi, idesc,
-                           acc || i > 0 || kk > 0);
-        }
-    }
-}
-
-// TMEM fp32 [lane r][D] -> bf16 -> SW128 smem tile: row r, columns [h*D/2, (h+1)*D/2)
+// TMEM fp32 [lane r][D] -> bf16 -> SW128 smem tile: row r, columns [g D/4, (g+1) D/4)
 template <int D>
-TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int h) {
-#pragma unroll
-    for (int c = 0; c < D / 2; c += 32) {
-        const int col = h * (D / 2) + c;
-        uint32_t v[32];
+TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int g) {
+    constexpr int kCols = D / 4;
+    const int col = g * kCols;
+    uint32_t v[kCols];
+    if constexpr (D == 128)
         tmem::ldw_32x32b_x32(tsrc + col, v);
+    else
+        tmem::ldw_32x32b_x16(tsrc + col, v);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int gc = col / 8 + q;  // 16-byte chunk index within the row
-            const int atom = gc / 8, ch = gc % 8;
-            uint4 u;
-            u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
-            u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
-            u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
-            u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
-            *reinterpret_cast<uint4*>(stage + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
-        }
+    for (int q = 0; q < kCols / 8; ++q) {
+        const int gc = col / 8 + q;  // 16-byte chunk index within the row
+        const int atom = gc / 8, ch = gc % 8;
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+        u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+        u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+        u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+        *reinterpret_cast<uint4*>(stage + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
     }
 }
 
@@ -155,6 +155,30 @@ TKB_DEVICE long long* trace_slot(const BwdParams& p, int lin, int kernel) {
         if (tr != nullptr && (t) < kTraceIters)                                           \
             tr[((role) * kTraceIters + (t)) * kTraceEvents + (ev)] = clock64() - t_start; \
     } while (0)
+
+// P chunk: p = exp2(tau * s + nlse) for 32 columns; a quarter of the exponentials run as
+// a polynomial on the FMA pipe (MUFU relief). nlse4 holds -lse2 per column (dkdv) or the
+// row's -lse2 broadcast (dq, ROWCONST).
+template <bool ROWCONST>
+TKB_DEVICE void exp_chunk(float* pf, float tau, const float4* nlse4, float nlse_r) {
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+        const float4 l4 = ROWCONST ? make_float4(nlse_r, nlse_r, nlse_r, nlse_r) : nlse4[c / 4];
+        const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(l4.x, l4.y));
+        const float2 x23 = fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(l4.z, l4.w));
+        pf[c] = ex2_approx(x01.x);
+        pf[c + 1] = ex2_approx(x01.y);
+        float2 p23;
+        if ((c & 8) != 0) {
+            p23 = ex2_poly2(x23);
+        } else {
+            p23.x = ex2_approx(x23.x);
+            p23.y = ex2_approx(x23.y);
+        }
+        pf[c + 2] = p23.x;
+        pf[c + 3] = p23.y;
+    }
+}
 
 // ================================================================== bwd_dkdv (KV-stationary)
 template <int D>
@@ -194,12 +218,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     mbarrier& s_full = bars[1];
     mbarrier& dp_full = bars[3];
     mbarrier& dkv_full = bars[5];
-    mbarrier* p_full = bars + 32;   // [kChunks] P^T chunks (32 queries each)
-    mbarrier* ds_full = bars + 36;  // [kChunks] dS^T chunks
     mbarrier* q_full = bars + 8;     // [S]
     mbarrier* q_empty = bars + 12;   // [S]
     mbarrier* do_full = bars + 16;   // [S]
     mbarrier* do_empty = bars + 20;  // [S]
+    mbarrier* p_full = bars + 32;    // [kGroups] P^T chunks (32 queries each)
+    mbarrier* ds_full = bars + 36;   // [kGroups] dS^T chunks
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
 
     const int warp = warpid();
@@ -220,9 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
         mbar_init(&s_full, 1);
         mbar_init(&dp_full, 1);
         mbar_init(&dkv_full, 1);
-        for (int c = 0; c < kChunks; ++c) {
-            mbar_init(&p_full[c], kComputeThreads / 2);  // the 4 warps of one column half
-            mbar_init(&ds_full[c], kComputeThreads / 2);
+        for (int g = 0; g < kGroups; ++g) {
+            mbar_init(&p_full[g], 128);  // the 4 warps of one column group
+            mbar_init(&ds_full[g], 128);
         }
         for (int s = 0; s < S; ++s) {
             mbar_init(&q_full[s], 1);
@@ -270,166 +294,115 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             }
         }
     } else if (warp == kWarpMma) {
-        {
-            // ------------------------------------------------------------- MMA
-            // converged warp; one elected lane issues each tcgen05 op
-            constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
-            constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-            auto qaddr = [&](int t) { return smem_u32(sQ + (t % S) * TL::kTileBytes); };
-            auto doaddr = [&](int t) { return smem_u32(sDo + (t % S) * TL::kTileBytes); };
-            mbar_wait(&kv_full, 0);
-            mbar_wait(&q_full[0], 0);
-            tmem::fence_after();
-            mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(0), id_s);
-            umma::commit_e(&s_full);
-            mbar_wait(&do_full[0], 0);
-            tmem::fence_after();
-            mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(0), id_s);
-            umma::commit_e(&dp_full);
-            for (int t = 0; t < T; ++t) {
-                const uint32_t ph = t & 1;
-                // dV += P_t^T dO_t, chunk by chunk as P^T arrives
-                TKB_TR(0, t, 0);
-                mma_tmem_a_chunked<0, 2, 1, 3>(tbase + C::tmem_dv(), tbase + C::tmem_s() + 32, doaddr(t), id_kv, t > 0,
-                                   [&](int c) {
-                                       mbar_wait(&p_full[c], ph);
-                                       tmem::fence_after();
-                                   });
-                TKB_TR(0, t, 1);
-                umma::commit_e(&do_empty[t % S]);
-                // S_{t+1}: overwrites P_t, read by dV_t which was issued before
-                if (t + 1 < T) {
-                    mbar_wait(&q_full[(t + 1) % S], ((t + 1) / S) & 1);
-                    tmem::fence_after();
-                    mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(t + 1), id_s);
-                    umma::commit_e(&s_full);
-                }
-                // dK += dS_t^T Q_t
-                TKB_TR(0, t, 2);
-                mma_tmem_a_chunked<1, 2, 0, 3>(tbase + C::tmem_dk(), tbase + C::tmem_dp() + 32, qaddr(t), id_kv, t > 0,
-                                   [&](int c) {
-                                       mbar_wait(&ds_full[c], ph);
-                                       tmem::fence_after();
-                                   });
-                TKB_TR(0, t, 3);
-                umma::commit_e(&q_empty[t % S]);
-                // dP_{t+1}: overwrites dS_t, read by dK_t which was issued before
-                if (t + 1 < T) {
-                    mbar_wait(&do_full[(t + 1) % S], ((t + 1) / S) & 1);
-                    tmem::fence_after();
-                    mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(t + 1), id_s);
-                    umma::commit_e(&dp_full);
-                }
-                TKB_TR(0, t, 4);
+        // ----------------------------------------------------------------- MMA
+        // converged warp; one elected lane issues each tcgen05 op
+        constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
+        constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK
+        const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+        auto qaddr = [&](int t) { return smem_u32(sQ + (t % S) * TL::kTileBytes); };
+        auto doaddr = [&](int t) { return smem_u32(sDo + (t % S) * TL::kTileBytes); };
+        mbar_wait(&kv_full, 0);
+        mbar_wait(&q_full[0], 0);
+        tmem::fence_after();
+        mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(0), id_s);
+        umma::commit_e(&s_full);
+        mbar_wait(&do_full[0], 0);
+        tmem::fence_after();
+        mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(0), id_s);
+        umma::commit_e(&dp_full);
+        for (int t = 0; t < T; ++t) {
+            const uint32_t ph = t & 1;
+            // dV += P_t^T dO_t, one 32-query chunk per column group as it lands
+            TKB_TR(0, t, 0);
+            mma_tmem_a_groups(tbase + C::tmem_dv(), tbase + C::tmem_s(), doaddr(t), id_kv, t > 0, [&](int g) {
+                mbar_wait(&p_full[g], ph);
+                tmem::fence_after();
+            });
+            TKB_TR(0, t, 1);
+            umma::commit_e(&do_empty[t % S]);
+            // S_{t+1}: overwrites P_t, read by dV_t which was issued before
+            if (t + 1 < T) {
+                mbar_wait(&q_full[(t + 1) % S], ((t + 1) / S) & 1);
+                tmem::fence_after();
+                mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(t + 1), id_s);
+                umma::commit_e(&s_full);
             }
-            umma::commit_e(&dkv_full);
+            // dK += dS_t^T Q_t
+            TKB_TR(0, t, 2);
+            mma_tmem_a_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qaddr(t), id_kv, t > 0, [&](int g) {
+                mbar_wait(&ds_full[g], ph);
+                tmem::fence_after();
+            });
+            TKB_TR(0, t, 3);
+            umma::commit_e(&q_empty[t % S]);
+            // dP_{t+1}: overwrites dS_t, read by dK_t which was issued before
+            if (t + 1 < T) {
+                mbar_wait(&do_full[(t + 1) % S], ((t + 1) / S) & 1);
+                tmem::fence_after();
+                mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(t + 1), id_s);
+                umma::commit_e(&dp_full);
+            }
+            TKB_TR(0, t, 4);
         }
+        umma::commit_e(&dkv_full);
     } else {
         // ----------------------------------------------------------------- COMPUTE
         const int wq = warp & 3;
-        const int h = warp >> 2;       // q half: columns [64h, 64h+64)
+        const int g = warp >> 2;       // q group: columns [32g, 32g+32)
         const int r = wq * 32 + lane;  // kv row == TMEM lane
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tbase + lane_off + C::tmem_s();
-        const uint32_t tDp = tbase + lane_off + C::tmem_dp();
+        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
+        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
         const float scale = p.scale;
         for (int t = 0; t < T; ++t) {
             const int i = qblock(t);
             const int s = t % S;
             const bool diag = CAUSAL && (i == j);
-            const float4* nlse4 = reinterpret_cast<const float4*>(sLse + s * 128 + 64 * h);
-            const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + s * 128 + 64 * h);
+            const float4* nlse4 = reinterpret_cast<const float4*>(sLse + s * 128 + 32 * g);
+            const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + s * 128 + 32 * g);
             // P^T = exp2(tau S^T - lse2)
             mbar_wait(&q_full[s], (t / S) & 1);
             mbar_wait(&s_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 0);
             tmem::fence_after();
-            float pf[64];
-            tmem::ld_32x32b_x32(tS + 64 * h, reinterpret_cast<uint32_t*>(pf));
-            tmem::ld_32x32b_x32(tS + 64 * h + 32, reinterpret_cast<uint32_t*>(pf) + 32);
-            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf));
-            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf) + 32);
-            uint32_t pk[32];
+            float pf[32];
+            tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
+            exp_chunk<false>(pf, tau, nlse4, 0.f);
+            if (diag) {  // key kv0 + r visible to query kv0 + 32g + c iff r <= 32g + c
 #pragma unroll
-            for (int c = 0; c < 64; c += 4) {
-                if (c == 32) {  // first 32 queries of this half are done: hand chunk 2h over
-                    tmem::st_32x32b_x16(tS + 32 + 32 * h, pk);
-                }
-                const float4 l4 = nlse4[c / 4];  // smem broadcast; holds -lse2
-                const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(l4.x, l4.y));
-                const float2 x23 =
-                    fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(l4.z, l4.w));
-                float p0 = ex2_approx(x01.x), p1 = ex2_approx(x01.y);
-                float2 p23;
-                if ((c & 8) != 0) {  // a quarter of the exponentials on the FMA pipe (MUFU relief)
-                    p23 = ex2_poly2(x23);
-                } else {
-                    p23.x = ex2_approx(x23.x);
-                    p23.y = ex2_approx(x23.y);
-                }
-                float p2 = p23.x, p3 = p23.y;
-                if (diag) {  // key kv0 + r visible to query kv0 + 64h + c iff r <= 64h + c
-                    const int q = 64 * h + c;
-                    p0 = (q < r) ? 0.f : p0;
-                    p1 = (q + 1 < r) ? 0.f : p1;
-                    p2 = (q + 2 < r) ? 0.f : p2;
-                    p3 = (q + 3 < r) ? 0.f : p3;
-                }
-                pf[c] = p0;
-                pf[c + 1] = p1;
-                pf[c + 2] = p2;
-                pf[c + 3] = p3;
-                pk[c / 2] = pack_bf16x2(p0, p1);
-                pk[c / 2 + 1] = pack_bf16x2(p2, p3);
+                for (int c = 0; c < 32; ++c) pf[c] = (32 * g + c < r) ? 0.f : pf[c];
             }
-            tmem::wait_st();  // chunk 2h (stored mid-loop)
-            tmem::fence_before();
-            mbar_arrive(&p_full[2 * h]);
-            tmem::st_32x32b_x16(tS + 32 + 32 * h + 16, pk + 16);
+            uint32_t pk[16];
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) pk[c / 2] = pack_bf16x2(pf[c], pf[c + 1]);
+            tmem::st_32x32b_x16(tS, pk);  // inside the 32 columns this thread has read
             tmem::wait_st();
             tmem::fence_before();
-            mbar_arrive(&p_full[2 * h + 1]);
+            mbar_arrive(&p_full[g]);
             if (threadIdx.x == 0) TKB_TR(1, t, 1);
             // dS^T = P^T o (dP^T - Delta) * scale
             mbar_wait(&dp_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 2);
             tmem::fence_after();
-            // the dS^T chunk a half writes lies inside the dP^T columns of half (h == 0 ? 1 : 0):
-            // process that half first so no column is overwritten before it is read (compile-time
-            // half index: the register arrays stay in registers)
-            auto ds_half = [&](auto half_c) {
-                constexpr int half = decltype(half_c)::value;
-                uint32_t dpv[32];
-                tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
+            uint32_t dpv[32];
+            tmem::ldw_32x32b_x32(tDp, dpv);
 #pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                    const int cc = 32 * half + c;
-                    const float4 d4 = dlt4[cc / 4];
-                    const float2 g01 = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
-                                            make_float2(d4.x, d4.y));
-                    const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
-                                            make_float2(d4.z, d4.w));
-                    const float2 s01 = mul2(mul2(make_float2(pf[cc], pf[cc + 1]), g01), make_float2(scale, scale));
-                    const float2 s23 =
-                        mul2(mul2(make_float2(pf[cc + 2], pf[cc + 3]), g23), make_float2(scale, scale));
-                    pk[cc / 2] = pack_bf16x2(s01.x, s01.y);
-                    pk[cc / 2 + 1] = pack_bf16x2(s23.x, s23.y);
-                }
-                // dS^T chunk 2h + half -> TMEM; its own dP^T columns were read above
-                tmem::st_32x32b_x16(tDp + 32 + 32 * h + 16 * half, pk + 16 * half);
-                tmem::wait_st();
-                tmem::fence_before();
-                mbar_arrive(&ds_full[2 * h + half]);
-            };
-            if (h == 0) {
-                ds_half(std::integral_constant<int, 1>{});
-                ds_half(std::integral_constant<int, 0>{});
-            } else {
-                ds_half(std::integral_constant<int, 0>{});
-                ds_half(std::integral_constant<int, 1>{});
+            for (int c = 0; c < 32; c += 4) {
+                const float4 d4 = dlt4[c / 4];
+                const float2 g01 =
+                    sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(d4.x, d4.y));
+                const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
+                                        make_float2(d4.z, d4.w));
+                const float2 s01 = mul2(mul2(make_float2(pf[c], pf[c + 1]), g01), make_float2(scale, scale));
+                const float2 s23 = mul2(mul2(make_float2(pf[c + 2], pf[c + 3]), g23), make_float2(scale, scale));
+                pk[c / 2] = pack_bf16x2(s01.x, s01.y);
+                pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
             }
+            tmem::st_32x32b_x16(tDp, pk);
+            tmem::wait_st();
+            tmem::fence_before();
+            mbar_arrive(&ds_full[g]);
             if (threadIdx.x == 0) TKB_TR(1, t, 3);
         }
         // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q and dO rings are free) -> TMA store
@@ -437,8 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
         tmem::fence_after();
         uint8_t* stage_v = sQ;
         uint8_t* stage_k = sDo;
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dv(), stage_v, r, h);
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dk(), stage_k, r, h);
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dv(), stage_v, r, g);
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dk(), stage_k, r, g);
         tma::fence_async_smem();
         named_sync(kBarCompute, kComputeThreads);
         if (threadIdx.x == 0) {
@@ -494,11 +467,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     mbarrier& a_ready = bars[3];  // Q, dO copied into TMEM
     mbarrier& dp_full = bars[5];
     mbarrier& dq_full = bars[7];
-    mbarrier* ds_full = bars + 32;  // [kChunks] dS chunks (32 keys each)
     mbarrier* k_full = bars + 8;    // [S]
     mbarrier* k_empty = bars + 12;  // [S]
     mbarrier* v_full = bars + 16;   // [S]
     mbarrier* v_empty = bars + 20;  // [S]
+    mbarrier* ds_full = bars + 32;  // [kGroups] dS chunks (32 keys each)
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
 
     const int warp = warpid();
@@ -520,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         mbar_init(&a_ready, kComputeThreads);
         mbar_init(&dp_full, 1);
         mbar_init(&dq_full, 1);
-        for (int c = 0; c < kChunks; ++c) mbar_init(&ds_full[c], kComputeThreads / 2);
+        for (int g = 0; g < kGroups; ++g) mbar_init(&ds_full[g], 128);
         for (int s = 0; s < S; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
@@ -565,135 +538,103 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             }
         }
     } else if (warp == kWarpMma) {
-        {
-            // ------------------------------------------------------------- MMA (converged warp)
-            constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
-            constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
-            auto kaddr = [&](int jj) { return smem_u32(sK + (jj % S) * TL::kTileBytes); };
-            auto vaddr = [&](int jj) { return smem_u32(sV + (jj % S) * TL::kTileBytes); };
-            auto issue_s = [&](int jj) {  // S_j = Q K_j^T
-                mbar_wait(&k_full[jj % S], (jj / S) & 1);
-                tmem::fence_after();
-                mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(jj), id_s);
-                umma::commit_e(&s_full);
-            };
-            auto issue_dp = [&](int jj) {  // dP_j = dO V_j^T
-                mbar_wait(&v_full[jj % S], (jj / S) & 1);
-                tmem::fence_after();
-                mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(jj), id_s);
-                umma::commit_e(&dp_full);
-                umma::commit_e(&v_empty[jj % S]);
-            };
-            mbar_wait(&a_ready, 0);
-            issue_s(0);
-            issue_dp(0);
-            for (int jj = 0; jj < nk; ++jj) {
-                if (jj + 1 < nk) {
-                    mbar_wait(&s_free, jj & 1);  // S_j read out by the compute warps
-                    issue_s(jj + 1);
-                }
-                TKB_TR(0, jj, 0);
-                mma_tmem_a_chunked<1, 2, 0, 3>(tbase + C::tmem_dq(), tbase + C::tmem_dp() + 32, kaddr(jj), id_q,
-                                               jj > 0, [&](int c) {  // dQ += dS K, chunk by chunk
-                                                   mbar_wait(&ds_full[c], jj & 1);
-                                                   tmem::fence_after();
-                                               });
-                TKB_TR(0, jj, 1);
-                umma::commit_e(&k_empty[jj % S]);
-                if (jj + 1 < nk) issue_dp(jj + 1);  // overwrites dS_j, read by dQ_j issued before
-                TKB_TR(0, jj, 2);
+        // ----------------------------------------------------------------- MMA (converged warp)
+        constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
+        constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
+        auto kaddr = [&](int jj) { return smem_u32(sK + (jj % S) * TL::kTileBytes); };
+        auto vaddr = [&](int jj) { return smem_u32(sV + (jj % S) * TL::kTileBytes); };
+        auto issue_s = [&](int jj) {  // S_j = Q K_j^T
+            mbar_wait(&k_full[jj % S], (jj / S) & 1);
+            tmem::fence_after();
+            mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(jj), id_s);
+            umma::commit_e(&s_full);
+        };
+        auto issue_dp = [&](int jj) {  // dP_j = dO V_j^T
+            mbar_wait(&v_full[jj % S], (jj / S) & 1);
+            tmem::fence_after();
+            mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(jj), id_s);
+            umma::commit_e(&dp_full);
+            umma::commit_e(&v_empty[jj % S]);
+        };
+        mbar_wait(&a_ready, 0);
+        issue_s(0);
+        issue_dp(0);
+        for (int jj = 0; jj < nk; ++jj) {
+            if (jj + 1 < nk) {
+                mbar_wait(&s_free, jj & 1);  // S_j read out by the compute warps
+                issue_s(jj + 1);
             }
-            umma::commit_e(&dq_full);
+            TKB_TR(0, jj, 0);
+            // dQ += dS K, one 32-key chunk per column group as it lands
+            mma_tmem_a_groups(tbase + C::tmem_dq(), tbase + C::tmem_dp(), kaddr(jj), id_q, jj > 0, [&](int g) {
+                mbar_wait(&ds_full[g], jj & 1);
+                tmem::fence_after();
+            });
+            TKB_TR(0, jj, 1);
+            umma::commit_e(&k_empty[jj % S]);
+            if (jj + 1 < nk) issue_dp(jj + 1);  // overwrites dS_j, read by dQ_j issued before
+            TKB_TR(0, jj, 2);
         }
+        umma::commit_e(&dq_full);
     } else {
         // ----------------------------------------------------------------- COMPUTE
         const int wq = warp & 3;
-        const int h = warp >> 2;       // kv half: columns [64h, 64h+64)
+        const int g = warp >> 2;       // kv group: columns [32g, 32g+32)
         const int r = wq * 32 + lane;  // q row == TMEM lane
         const int row = q0 + r;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tDp = tbase + lane_off + C::tmem_dp();
+        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
+        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
         const float scale = p.scale;
         const float nlse_r = p.lse2[(size_t)bh * p.n_pad + row];  // -lse2; -inf on padded rows -> P = 0
         const float dlt_r = p.delta[(size_t)bh * p.n_pad + row];
         // Q, dO: SMEM (TMA, swizzled) -> TMEM A operands, once per CTA
         mbar_wait(&qdo_full, 0);
-        smem_rows_to_tmem_a<D>(sQ, tbase + lane_off + C::tmem_qa(), r, h);
-        smem_rows_to_tmem_a<D>(sDo, tbase + lane_off + C::tmem_doa(), r, h);
+        smem_rows_to_tmem_a<D>(sQ, tbase + lane_off + C::tmem_qa(), r, g);
+        smem_rows_to_tmem_a<D>(sDo, tbase + lane_off + C::tmem_doa(), r, g);
         tmem::wait_st();
         tmem::fence_before();
         mbar_arrive(&a_ready);
         for (int jj = 0; jj < nk; ++jj) {
             const int kv0 = jj * 128;
-            const uint32_t tS = tbase + lane_off + C::tmem_s();
             mbar_wait(&s_full, jj & 1);
             if (threadIdx.x == 0) TKB_TR(1, jj, 0);
             tmem::fence_after();
-            float pf[64];
-            tmem::ld_32x32b_x32(tS + 64 * h, reinterpret_cast<uint32_t*>(pf));
-            tmem::ld_32x32b_x32(tS + 64 * h + 32, reinterpret_cast<uint32_t*>(pf) + 32);
-            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf));
-            tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(pf) + 32);
+            float pf[32];
+            tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
             tmem::fence_before();
             mbar_arrive(&s_free);
+            exp_chunk<true>(pf, tau, nullptr, nlse_r);
             // visible keys: kv < n, and causal kv <= row
-            const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 64 * h;  // last visible column
+            const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 32 * g;  // last visible column
+            if (lim < 31) {  // diagonal / ragged tail block only
 #pragma unroll
-            for (int c = 0; c < 64; c += 4) {
-                const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(nlse_r, nlse_r));
-                const float2 x23 =
-                    fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(nlse_r, nlse_r));
-                pf[c] = ex2_approx(x01.x);
-                pf[c + 1] = ex2_approx(x01.y);
-                float2 p23;
-                if ((c & 8) != 0) {  // a quarter of the exponentials on the FMA pipe
-                    p23 = ex2_poly2(x23);
-                } else {
-                    p23.x = ex2_approx(x23.x);
-                    p23.y = ex2_approx(x23.y);
-                }
-                pf[c + 2] = p23.x;
-                pf[c + 3] = p23.y;
-            }
-            if (lim < 63) {  // diagonal / ragged tail block only
-#pragma unroll
-                for (int c = 0; c < 64; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
+                for (int c = 0; c < 32; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
             }
             mbar_wait(&dp_full, jj & 1);
             if (threadIdx.x == 0) TKB_TR(1, jj, 1);
             tmem::fence_after();
-            uint32_t pk[32];
-            auto ds_half = [&](auto half_c) {  // (see bwd_dkdv: compile-time half, read-before-overwrite order)
-                constexpr int half = decltype(half_c)::value;
-                uint32_t dpv[32];
-                tmem::ldw_32x32b_x32(tDp + 64 * h + 32 * half, dpv);
+            uint32_t dpv[32];
+            tmem::ldw_32x32b_x32(tDp, dpv);
+            uint32_t pk[16];
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                    const int cc = 32 * half + c;
-                    const float2 g = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
-                                          make_float2(dlt_r, dlt_r));
-                    const float2 d = mul2(mul2(make_float2(pf[cc], pf[cc + 1]), g), make_float2(scale, scale));
-                    pk[cc / 2] = pack_bf16x2(d.x, d.y);
-                }
-                tmem::st_32x32b_x16(tDp + 32 + 32 * h + 16 * half, pk + 16 * half);
-                tmem::wait_st();
-                tmem::fence_before();
-                mbar_arrive(&ds_full[2 * h + half]);
-            };
-            if (h == 0) {
-                ds_half(std::integral_constant<int, 1>{});
-                ds_half(std::integral_constant<int, 0>{});
-            } else {
-                ds_half(std::integral_constant<int, 0>{});
-                ds_half(std::integral_constant<int, 1>{});
+            for (int c = 0; c < 32; c += 2) {
+                const float2 gg =
+                    sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(dlt_r, dlt_r));
+                const float2 d = mul2(mul2(make_float2(pf[c], pf[c + 1]), gg), make_float2(scale, scale));
+                pk[c / 2] = pack_bf16x2(d.x, d.y);
             }
+            tmem::st_32x32b_x16(tDp, pk);  // inside the 32 dP columns this thread has read
+            tmem::wait_st();
+            tmem::fence_before();
+            mbar_arrive(&ds_full[g]);
             if (threadIdx.x == 0) TKB_TR(1, jj, 2);
         }
         // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM (the Q tile is free) -> TMA store
         mbar_wait(&dq_full, 0);
         tmem::fence_after();
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sQ, r, h);
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sQ, r, g);
         tma::fence_async_smem();
         named_sync(kBarCompute, kComputeThreads);
         if (threadIdx.x == 0) {
@@ -760,7 +701,7 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
         if (e) return e;
         configured = true;
     }
-    dim3 grid(p.n_pad / 128, p.heads, batches);
+    dim3 grid(p.n_pad / 128, p.heads, batches);  // (the dkdv/dq kernels use kThreads = 576)
     if (phases & 2) {
         attn_bwd_dkdv_kernel<D, CAUSAL><<<grid, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
         int e = (int)cudaGetLastError();
