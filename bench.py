@@ -478,7 +478,8 @@ def load_traffic(kernel):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
+        return t.get(kernel, t.get(kernel + "_kernel"))
     except Exception:
         return None
 
