@@ -67,6 +67,7 @@ struct AttentionConfig {
     bool causal = false;
     float softmax_scale = 0.f;  // 0: head_dim^-1/2
     bool check_finite = false;  // kernels.hpp:277-284, opt-in (synchronises the stream)
+    int kv_heads = 0;           // grouped-query attention: 0 = heads, else heads % kv_heads == 0
 
     double temperature_scale() const {
         const double s = softmax_scale > 0.f ? softmax_scale : 1.0 / std::sqrt((double)head_dim);
@@ -77,6 +78,7 @@ struct AttentionConfig {
         tkb_attn_desc_init(&d, batches, heads, seq, head_dim, causal ? 1 : 0);
         d.softmax_scale = softmax_scale;
         d.check_finite = check_finite ? 1 : 0;
+        d.kv_heads = kv_heads;
         return d;
     }
     void validate() const {

@@ -15,7 +15,8 @@
  *
  * Conventions
  *   - Tensors are row-major [B, H, N, D] bf16 (optionally strided over B, H, N;
- *     D must be contiguous), as GlobalTensor::index (tiles.hpp:106-108).
+ *     D must be contiguous), as GlobalTensor::index (tiles.hpp:106-108); with
+ *     grouped-query attention (desc.kv_heads) k/v/dk/dv are [B, Hkv, N, D].
  *   - O is bf16 (the reference keeps fp32 O, kernels.hpp:212).
  *   - lse is fp32 [B, H, N], contiguous: L_i = ln sum_j exp(scale * q_i . k_j)
  *     over the unmasked keys (natural log).
@@ -35,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TKB_ABI_VERSION 1
+#define TKB_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define TKB_API __attribute__((visibility("default")))
@@ -65,11 +66,16 @@ typedef struct tkb_attn_desc {
     int32_t check_finite; /* 1: scan inputs first and fail with TKB_ERR_CONFIG on inf/nan
                              (kernels.hpp:277-284); synchronises the stream */
     float softmax_scale;  /* <= 0: D^-1/2 */
-    int32_t reserved0;
-    /* element strides of q/k/v/o/do/dq/dk/dv; 0 = contiguous [B,H,N,D] */
+    int32_t kv_heads;     /* Hkv: 0 = H (multi-head); H % Hkv == 0 (grouped-query, Hkv = 1: multi-query).
+                             k/v/dk/dv are [B, Hkv, N, D]; query head h reads kv head h / (H / Hkv) */
+    /* element strides of q/o/do/dq; 0 = contiguous [B,H,N,D] */
     int64_t stride_b;
     int64_t stride_h;
     int64_t stride_n;
+    /* element strides of k/v/dk/dv; all 0 = contiguous [B,Hkv,N,D] (or q's strides when Hkv == H) */
+    int64_t kv_stride_b;
+    int64_t kv_stride_h;
+    int64_t kv_stride_n;
 } tkb_attn_desc;
 
 /* Fill `desc` with a contiguous problem and default scale. */

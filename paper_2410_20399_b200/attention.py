@@ -63,10 +63,13 @@ class AttnDesc(ctypes.Structure):
         ("causal", ctypes.c_int32),
         ("check_finite", ctypes.c_int32),
         ("softmax_scale", ctypes.c_float),
-        ("reserved0", ctypes.c_int32),
+        ("kv_heads", ctypes.c_int32),
         ("stride_b", ctypes.c_int64),
         ("stride_h", ctypes.c_int64),
         ("stride_n", ctypes.c_int64),
+        ("kv_stride_b", ctypes.c_int64),
+        ("kv_stride_h", ctypes.c_int64),
+        ("kv_stride_n", ctypes.c_int64),
     ]
 
 
@@ -123,20 +126,24 @@ class AttentionConfig:
     causal: bool = False
     softmax_scale: Optional[float] = None
     check_finite: bool = False
+    kv_heads: int = 0  # grouped-query attention: 0 = heads
 
     def temperature_scale(self) -> float:
         """tau = softmax_scale * log2(e) (kernels.hpp:184-186)."""
         s = self.softmax_scale if self.softmax_scale else 1.0 / math.sqrt(self.head_dim)
         return s * 1.44269504089
 
-    def desc(self, strides=None) -> AttnDesc:
+    def desc(self, strides=None, kv_strides=None) -> AttnDesc:
         d = AttnDesc()
         lib().tkb_attn_desc_init(ctypes.byref(d), self.batches, self.heads, self.seq, self.head_dim,
                                  int(bool(self.causal)))
         d.softmax_scale = float(self.softmax_scale or 0.0)
         d.check_finite = int(bool(self.check_finite))
+        d.kv_heads = int(self.kv_heads or 0)
         if strides is not None:
             d.stride_b, d.stride_h, d.stride_n = strides
+        if kv_strides is not None:
+            d.kv_stride_b, d.kv_stride_h, d.kv_stride_n = kv_strides
         return d
 
     def validate(self):
@@ -155,20 +162,34 @@ def _bhnd(t, name):
     return t.stride(0), t.stride(1), t.stride(2)
 
 
+def _check_kv(q, k, v):
+    """q [B, H, N, D]; k, v [B, Hkv, N, D] with H % Hkv == 0 (Hkv == H: multi-head)."""
+    if k.shape != v.shape:
+        raise ShapeError("k and v must have the same shape")
+    B, H, N, D = q.shape
+    if k.dim() != 4 or k.shape[0] != B or k.shape[2] != N or k.shape[3] != D:
+        raise ShapeError("k, v must be [B, Hkv, N, D] matching q's B, N, D")
+    hkv = k.shape[1]
+    if hkv < 1 or H % hkv:
+        raise ConfigError(f"heads ({H}) must be a multiple of kv heads ({hkv})")
+    kst = _bhnd(k, "k")
+    if _bhnd(v, "v") != kst:
+        raise ShapeError("k and v must share strides")
+    return hkv, kst
+
+
 def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None, return_lse=True,
                   check_finite=False):
-    """O = softmax(scale * Q K^T [causal]) V on the B200; returns (O, L) with L fp32 [B, H, N]."""
+    """O = softmax(scale * Q K^T [causal]) V on the B200; returns (O, L) with L fp32 [B, H, N].
+    k, v may carry fewer heads than q (grouped-query / multi-query attention)."""
     import torch
 
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ConfigError("attention_fwd runs on the GPU only (no CPU fallback)")
     if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
         raise ConfigError("q, k, v must be bf16")
-    if q.shape != k.shape or q.shape != v.shape:
-        raise ShapeError("q, k, v must have the same [B, H, N, D] shape")
     st = _bhnd(q, "q")
-    if _bhnd(k, "k") != st or _bhnd(v, "v") != st:
-        raise ShapeError("q, k, v must share strides")
+    hkv, kst = _check_kv(q, k, v)
     B, H, N, D = q.shape
     if out is None:
         out = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
@@ -176,8 +197,8 @@ def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None,
         raise ShapeError("out must share q's strides")
     if return_lse and lse is None:
         lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
-    cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite)
-    d = cfg.desc(strides=st)
+    cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite, kv_heads=hkv)
+    d = cfg.desc(strides=st, kv_strides=kst)
     _check(lib().tkb_attn_fwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr() if lse is not None else None, _stream(torch, q.device)))
     return (out, lse) if return_lse else out
@@ -190,25 +211,28 @@ def bwd_workspace_bytes(B, H, N, D, causal=False):
 
 def attention_bwd(q, k, v, o, dout, lse, causal=False, softmax_scale=None, dq=None, dk=None, dv=None,
                   workspace=None, check_finite=False):
-    """dQ, dK, dV from the saved L (deterministic)."""
+    """dQ, dK, dV from the saved L (deterministic). With grouped-query k/v, dK/dV sum the
+    contributions of every query head of the group (in TMEM, no atomics)."""
     import torch
 
     for t, name in ((q, "q"), (k, "k"), (v, "v"), (o, "o"), (dout, "dout")):
         if not t.is_cuda or t.dtype != torch.bfloat16:
             raise ConfigError(f"{name} must be a bf16 CUDA tensor")
     st = _bhnd(q, "q")
-    for t, name in ((k, "k"), (v, "v"), (o, "o"), (dout, "dout")):
+    hkv, kst = _check_kv(q, k, v)
+    for t, name in ((o, "o"), (dout, "dout")):
         if t.shape != q.shape or _bhnd(t, name) != st:
             raise ShapeError(f"{name} must match q's shape and strides")
     B, H, N, D = q.shape
     if lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, N) or not lse.is_contiguous():
         raise ShapeError("lse must be contiguous fp32 [B, H, N]")
-    mk = lambda: torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
-    dq = mk() if dq is None else dq
-    dk = mk() if dk is None else dk
-    dv = mk() if dv is None else dv
-    cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite)
-    d = cfg.desc(strides=st)
+    dq = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device) if dq is None else dq
+    dk = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device) if dk is None else dk
+    dv = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device) if dv is None else dv
+    if _bhnd(dq, "dq") != st or _bhnd(dk, "dk") != kst or _bhnd(dv, "dv") != kst:
+        raise ShapeError("dq must share q's strides and dk/dv k's")
+    cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite, kv_heads=hkv)
+    d = cfg.desc(strides=st, kv_strides=kst)
     ws_bytes = int(lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(d)))
     if workspace is None or workspace.numel() * workspace.element_size() < ws_bytes:
         workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)

@@ -229,14 +229,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     const int warp = warpid();
     const int lane = laneid();
     const int j = blockIdx.x;  // kv block; causal: small j visits the most q blocks, dispatched first
-    const int head = blockIdx.y;
+    const int head = blockIdx.y;  // kv head (== query head unless grouped-query)
     const int batch = blockIdx.z;
-    const int bh = batch * p.heads + head;
     const int kv0 = j * 128;
     const int nq = p.n_pad / 128;
-    const int T = CAUSAL ? (nq - j) : nq;  // q blocks visited: i = j + t (causal) or t
-    auto qblock = [&](int t) { return CAUSAL ? (j + t) : t; };
-    long long* tr = trace_slot(p, bh * gridDim.x + j, 0);
+    const int T1 = CAUSAL ? (nq - j) : nq;  // q blocks visited per query head: i = j + t (causal) or t
+    const int T = T1 * p.group;             // steps: the group's query heads one after the other, so
+                                            // dK/dV sum over them in TMEM (grouped-query attention)
+    auto qblock = [&](int t) { return CAUSAL ? (j + t % T1) : t % T1; };
+    auto qhead = [&](int t) { return head * p.group + t / T1; };
+    auto qbh = [&](int t) { return batch * p.heads + qhead(t); };
+    long long* tr = trace_slot(p, (batch * gridDim.y + head) * gridDim.x + j, 0);
     const long long t_start = clock64();
 
     if (warp == kWarpLoad && lane == 0) {
@@ -280,17 +283,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
                 const int i = qblock(t), s = t % S;
                 const uint32_t ph = ((t / S) & 1) ^ 1;
                 mbar_wait(&do_empty[s], ph);  // freed by dV_{t-S}, the first GEMM of its step
+                const int hq = qhead(t);
+                const size_t bhq = (size_t)qbh(t);
                 mbar_arrive_expect_tx(&do_full[s], TL::kTileBytes);
                 for (int a = 0; a < TL::kAtoms; ++a)
                     tma::load_4d(sDo + s * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[s], a * 64, i * 128,
-                                 head, batch, pol_keep);
+                                 hq, batch, pol_keep);
                 mbar_wait(&q_empty[s], ph);  // freed by dK_{t-S}
                 mbar_arrive_expect_tx(&q_full[s], TL::kTileBytes + 1024);
                 for (int a = 0; a < TL::kAtoms; ++a)
                     tma::load_4d(sQ + s * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[s], a * 64, i * 128,
-                                 head, batch, pol_keep);
-                tma::load_1d(sLse + s * 128, p.lse2 + (size_t)bh * p.n_pad + i * 128, 512, &q_full[s]);
-                tma::load_1d(sDelta + s * 128, p.delta + (size_t)bh * p.n_pad + i * 128, 512, &q_full[s]);
+                                 hq, batch, pol_keep);
+                tma::load_1d(sLse + s * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &q_full[s]);
+                tma::load_1d(sDelta + s * 128, p.delta + bhq * p.n_pad + i * 128, 512, &q_full[s]);
             }
         }
     } else if (warp == kWarpMma) {
@@ -529,12 +534,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 mbar_arrive_expect_tx(&k_full[s], TL::kTileBytes);
                 for (int a = 0; a < TL::kAtoms; ++a)
                     tma::load_4d(sK + s * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[s], a * 64, jj * 128,
-                                 head, batch, pol_keep);
+                                 head / p.group, batch, pol_keep);
                 mbar_wait(&v_empty[s], ph);
                 mbar_arrive_expect_tx(&v_full[s], TL::kTileBytes);
                 for (int a = 0; a < TL::kAtoms; ++a)
                     tma::load_4d(sV + s * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[s], a * 64, jj * 128,
-                                 head, batch, pol_keep);
+                                 head / p.group, batch, pol_keep);
             }
         }
     } else if (warp == kWarpMma) {
@@ -701,9 +706,10 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
         if (e) return e;
         configured = true;
     }
-    dim3 grid(p.n_pad / 128, p.heads, batches);  // (the dkdv/dq kernels use kThreads = 576)
+    dim3 grid(p.n_pad / 128, p.heads, batches);                 // dQ: one CTA per query block
+    dim3 grid_kv(p.n_pad / 128, p.heads / p.group, batches);    // dK/dV: one CTA per kv block
     if (phases & 2) {
-        attn_bwd_dkdv_kernel<D, CAUSAL><<<grid, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+        attn_bwd_dkdv_kernel<D, CAUSAL><<<grid_kv, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;

@@ -23,6 +23,7 @@ struct FwdParams {
     int trace_slots;
     int n;                               // sequence length
     int heads;
+    int group;                           // query heads per kv head (grouped-query attention; 1 = MHA)
     int bh;                              // batches * heads          (set by launch_attn_fwd)
     int m_blocks;                        // 256-row query blocks     (set by launch_attn_fwd)
     int tasks;                           // bh * m_blocks            (set by launch_attn_fwd)
@@ -40,7 +41,8 @@ struct BwdParams {
     int trace_slots;
     int n;
     int n_pad;
-    int heads;
+    int heads;         // query heads
+    int group;         // query heads per kv head (grouped-query attention; 1 = MHA)
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)
 };

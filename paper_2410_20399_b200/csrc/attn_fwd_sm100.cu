@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 for (int which = 0; which < 2; ++which) {
                     kv.wait_empty(st);
                     mbar_arrive_expect_tx(&kv.full[st.slot], C::kTile);
-                    load_async(sKV(st.slot), which == 0 ? gK : gV, &kv.full[st.slot], i * kBlockN, head, batch,
-                               pol_kv);
+                    load_async(sKV(st.slot), which == 0 ? gK : gV, &kv.full[st.slot], i * kBlockN, head / p.group,
+                               batch, pol_kv);  // grouped-query: kv head = head / group
                     st.advance();
                 }
             }

@@ -54,6 +54,19 @@ Strides strides_of(const tkb_attn_desc* d) {
     return s;
 }
 
+int kv_heads_of(const tkb_attn_desc* d) { return d->kv_heads > 0 ? d->kv_heads : d->heads; }
+
+// strides of k/v/dk/dv ([B, Hkv, N, D]); q's strides when multi-head and none given
+Strides kv_strides_of(const tkb_attn_desc* d) {
+    if (d->kv_stride_b == 0 && d->kv_stride_h == 0 && d->kv_stride_n == 0 && kv_heads_of(d) == d->heads)
+        return strides_of(d);
+    Strides s;
+    s.n = d->kv_stride_n ? d->kv_stride_n : d->head_dim;
+    s.h = d->kv_stride_h ? d->kv_stride_h : (int64_t)d->seq * s.n;
+    s.b = d->kv_stride_b ? d->kv_stride_b : (int64_t)kv_heads_of(d) * s.h;
+    return s;
+}
+
 float scale_of(const tkb_attn_desc* d) {
     return d->softmax_scale > 0.f ? d->softmax_scale : (float)(1.0 / std::sqrt((double)d->head_dim));
 }
@@ -76,9 +89,10 @@ int check_device() {
     return cached_ok ? TKB_OK : fail(TKB_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
 }
 
-// 4-D {D, N, H, B} bf16 map with a {64, 128, 1, 1} SW128 box.
-int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, const Strides& s) {
-    uint64_t dims[4] = {(uint64_t)d->head_dim, (uint64_t)d->seq, (uint64_t)d->heads, (uint64_t)d->batches};
+// 4-D {D, N, H, B} bf16 map with a {64, 128, 1, 1} SW128 box (heads = H, or Hkv for k/v).
+int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, const Strides& s, int heads = 0) {
+    uint64_t dims[4] = {(uint64_t)d->head_dim, (uint64_t)d->seq, (uint64_t)(heads > 0 ? heads : d->heads),
+                        (uint64_t)d->batches};
     uint64_t strides[4] = {1, (uint64_t)s.n, (uint64_t)s.h, (uint64_t)s.b};
     uint32_t box[4] = {64, 128, 1, 1};
     std::string err;
@@ -109,13 +123,13 @@ int device_state(int* sms, int** sched) {
     return TKB_OK;
 }
 
-int finite_check(const tkb_attn_desc* d, const void* const* ptrs, int nptrs, const Strides& s, cudaStream_t st) {
+int finite_check(const tkb_attn_desc* d, const void* const* ptrs, int nptrs, const Strides& s, int heads,
+                 cudaStream_t st) {
     int* flag = nullptr;
     cudaError_t e = cudaMallocAsync(&flag, sizeof(int), st);
     if (e != cudaSuccess) return fail(TKB_ERR_CUDA, "check_finite alloc failed");
     cudaMemsetAsync(flag, 0, sizeof(int), st);
-    int rc = tkb::launch_check_finite(ptrs, nptrs, d->batches, d->heads, d->seq, d->head_dim, s.b, s.h, s.n, flag,
-                                      st);
+    int rc = tkb::launch_check_finite(ptrs, nptrs, d->batches, heads, d->seq, d->head_dim, s.b, s.h, s.n, flag, st);
     int host = 0;
     cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(flag, st);
@@ -149,9 +163,11 @@ TKB_API int tkb_attn_validate(const tkb_attn_desc* d) {
     if (d->causal != 0 && d->causal != 1) return fail(TKB_ERR_CONFIG, "causal must be 0 or 1");
     if (!(std::isfinite(d->softmax_scale))) return fail(TKB_ERR_CONFIG, "softmax_scale must be finite");
     if ((int64_t)d->batches * d->heads > (int64_t)65535 * 65535) return fail(TKB_ERR_CONFIG, "too many heads");
-    const Strides s = strides_of(d);
-    if (s.n < d->head_dim || s.h < 0 || s.b < 0 || (s.n % 8) || (s.h % 8) || (s.b % 8))
-        return fail(TKB_ERR_SHAPE, "strides must be multiples of 8 elements (16 B) with rows >= head_dim");
+    if (d->kv_heads < 0 || d->heads % kv_heads_of(d) != 0)
+        return fail(TKB_ERR_CONFIG, "heads must be a multiple of kv_heads (grouped-query attention)");
+    for (const Strides& s : {strides_of(d), kv_strides_of(d)})
+        if (s.n < d->head_dim || s.h < 0 || s.b < 0 || (s.n % 8) || (s.h % 8) || (s.b % 8))
+            return fail(TKB_ERR_SHAPE, "strides must be multiples of 8 elements (16 B) with rows >= head_dim");
     return TKB_OK;
 }
 
@@ -166,14 +182,19 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
     if ((rc = check_device())) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const Strides s = strides_of(d);
+    const Strides skv = kv_strides_of(d);
+    const int hkv = kv_heads_of(d);
     if (d->check_finite) {
-        const void* ptrs[3] = {q, k, v};
-        if ((rc = finite_check(d, ptrs, 3, s, st))) return rc;
+        const void* qp[1] = {q};
+        const void* kvp[2] = {k, v};
+        if ((rc = finite_check(d, qp, 1, s, d->heads, st)) || (rc = finite_check(d, kvp, 2, skv, hkv, st)))
+            return rc;
     }
     tkb::FwdParams p{};
-    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, s)) ||
-        (rc = make_bhnd_map(&p.tm_v, v, d, s)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
+    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
+        (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
         return rc;
+    p.group = d->heads / hkv;
     int sms = 0;
     if ((rc = device_state(&sms, &p.sched))) return rc;
     p.lse = lse;
@@ -215,16 +236,21 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     if ((rc = check_device())) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const Strides s = strides_of(d);
+    const Strides skv = kv_strides_of(d);
+    const int hkv = kv_heads_of(d);
     if (d->check_finite) {
-        const void* ptrs[5] = {q, k, v, o, dout};
-        if ((rc = finite_check(d, ptrs, 5, s, st))) return rc;
+        const void* qp[3] = {q, o, dout};
+        const void* kvp[2] = {k, v};
+        if ((rc = finite_check(d, qp, 3, s, d->heads, st)) || (rc = finite_check(d, kvp, 2, skv, hkv, st)))
+            return rc;
     }
     tkb::BwdParams p{};
-    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, s)) ||
-        (rc = make_bhnd_map(&p.tm_v, v, d, s)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
-        (rc = make_bhnd_map(&p.tm_dq, dq, d, s)) || (rc = make_bhnd_map(&p.tm_dk, dk, d, s)) ||
-        (rc = make_bhnd_map(&p.tm_dv, dv, d, s)))
+    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
+        (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
+        (rc = make_bhnd_map(&p.tm_dq, dq, d, s)) || (rc = make_bhnd_map(&p.tm_dk, dk, d, skv, hkv)) ||
+        (rc = make_bhnd_map(&p.tm_dv, dv, d, skv, hkv)))
         return rc;
+    p.group = d->heads / hkv;
     const int64_t bh = (int64_t)d->batches * d->heads;
     const int npad = (d->seq + 127) / 128 * 128;
     float* delta = reinterpret_cast<float*>(workspace);

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s), s
     assert set(A.exported_symbols()) == set(declared_symbols())
-    assert A.lib().tkb_abi_version() == 1
+    assert A.lib().tkb_abi_version() == 2
 
 
 def test_library_is_built_for_sm100a():
@@ -102,3 +102,18 @@ def test_fwd_without_a_b200_fails_loudly():
 def test_null_pointers_are_bounds_errors():
     d = A.AttentionConfig(1, 1, 128, 64).desc()
     assert A.lib().tkb_attn_fwd(ctypes.byref(d), None, None, None, None, None, None) == 3
+
+
+def test_kv_heads_must_divide_heads():
+    # grouped-query attention: H % Hkv == 0 (ConfigError otherwise), checked without a GPU
+    A.AttentionConfig(1, 8, 64, 64, kv_heads=2).validate()
+    A.AttentionConfig(1, 8, 64, 64, kv_heads=1).validate()
+    with pytest.raises(A.ConfigError):
+        A.AttentionConfig(1, 8, 64, 64, kv_heads=3).validate()
+
+
+def test_desc_layout_matches_header():
+    # AttnDesc mirrors tkb_attn_desc (include/tkb_attn.h, ABI 2): 8 x 4-byte fields + 6 x int64
+    import ctypes
+    assert ctypes.sizeof(A.AttnDesc) == 8 * 4 + 6 * 8
+    assert A.AttnDesc.kv_heads.offset == 28 and A.AttnDesc.kv_stride_b.offset == 56
