@@ -100,6 +100,19 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* desc, const void* q, const void* k
                  const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
                  size_t workspace_bytes, void* stream);
 
+/* Rotary position embedding (replaces rotary_kernel, kernels.hpp:357-513; oracle
+ * oracles.hpp:66-90): for position p and i < D/2 the pair (x[p][i], x[p][i + D/2]) is
+ * rotated by the angle whose sin / cos are sin_tab / cos_tab [seq, D/2] (fp32, contiguous,
+ * shared by every batch and head). x, out: [B, H, N, D] bf16 with desc's strides; out may
+ * alias x. D must be a multiple of 16 here (any seq). */
+TKB_API int tkb_rotary(const tkb_attn_desc* desc, const void* x, const float* sin_tab, const float* cos_tab,
+                       void* out, void* stream);
+
+/* The attention prologue: Q ([B, H, N, D]) and K ([B, Hkv, N, D], desc.kv_heads / kv strides)
+ * rotated in one launch into q_out / k_out (may alias q / k). */
+TKB_API int tkb_rotary_qk(const tkb_attn_desc* desc, const void* q, const void* k, const float* sin_tab,
+                          const float* cos_tab, void* q_out, void* k_out, void* stream);
+
 /* Multi-GPU sharding of the flattened batch x head grid:
  * contiguous, balanced [begin, end) of `units` for `rank` of `world`. No collective. */
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end);

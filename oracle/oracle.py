@@ -45,6 +45,8 @@ def lib():
                                           ctypes.c_double, _D, _D, ctypes.c_int]
         L.tkb_oracle_attn_bwd.argtypes = [_F, _F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_double, _D, _D, _D, ctypes.c_int]
+        L.tkb_oracle_rotary.argtypes = [_F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _D]
+        L.tkb_oracle_gemm.argtypes = [_F, _F, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, ctypes.c_int]
         _cache["o"] = L
     return _cache["o"]
 
@@ -66,6 +68,12 @@ def ref_lib():
                                                               ctypes.c_int]
         L.kref_oracle_attention.argtypes = [_D, _D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
         L.kref_fill.argtypes = [ctypes.c_uint32, ctypes.c_float, ctypes.c_float, ctypes.c_int, _F, ctypes.c_int64]
+        L.kref_oracle_rotary.argtypes = [_D, _D, _D, ctypes.c_int, ctypes.c_int, _D]
+        L.kref_rotary.argtypes = [ctypes.c_int] * 5 + [_F, _F, _F, _F, ctypes.c_char_p, ctypes.c_int]
+        L.kref_oracle_gemm.argtypes = [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
+        L.kref_gemm.argtypes = [ctypes.c_int] * 7 + [_F, _F, _F, ctypes.c_char_p, ctypes.c_int]
+        _I = ctypes.POINTER(ctypes.c_int)
+        L.kref_supergroup_order.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I]
         _cache["r"] = L
     return _cache["r"]
 
@@ -169,3 +177,86 @@ def rel_l2(got, ref):
     ref = np.asarray(ref, dtype=np.float64)
     den = np.linalg.norm(ref)
     return float(np.linalg.norm(np.asarray(got, dtype=np.float64) - ref) / (den if den > 0 else 1.0))
+
+
+# ------------------------------------------------------------------ rotary / GEMM
+
+
+def rotary(x, sin_tab, cos_tab):
+    """fp64 oracle_rotary (oracles.hpp:66-90) on x [..., N, hd] with [N, hd/2] tables."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    n, hd = x.shape[-2:]
+    s = np.ascontiguousarray(sin_tab, dtype=np.float32)
+    c = np.ascontiguousarray(cos_tab, dtype=np.float32)
+    out = np.empty(x.shape, dtype=np.float64)
+    lib().tkb_oracle_rotary(_ptr(x, _F), _ptr(s, _F), _ptr(c, _F), x.size // hd, n, hd, _ptr(out, _D))
+    return out
+
+
+def gemm(a, b, nthreads=None):
+    """fp64 oracle_gemm (oracles.hpp:17-30): C = A B for row-major A [M, K], B [K, N]."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.float64)
+    lib().tkb_oracle_gemm(_ptr(a, _F), _ptr(b, _F), m, n, k, _ptr(c, _D), nthreads or threads())
+    return c
+
+
+def ref_rotary_oracle(x, sin_tab, cos_tab):
+    """The reference's own oracle_rotary on one [N, hd] head (oracle/_ref)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    n, hd = x.shape
+    out = np.empty_like(x)
+    rc = ref_lib().kref_oracle_rotary(_ptr(x, _D), _ptr(np.ascontiguousarray(sin_tab, np.float64), _D),
+                                      _ptr(np.ascontiguousarray(cos_tab, np.float64), _D), n, hd, _ptr(out, _D))
+    assert rc == 0
+    return out
+
+
+def ref_rotary(x, sin_tab, cos_tab, workers=4):
+    """The reference rotary_kernel through execute_functional (fp32), x [B, H, N, hd]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    B, H, N, hd = x.shape
+    out = np.empty_like(x)
+    err = ctypes.create_string_buffer(256)
+    rc = ref_lib().kref_rotary(B, H, N, hd, workers, _ptr(x, _F), _ptr(np.ascontiguousarray(sin_tab, np.float32), _F),
+                               _ptr(np.ascontiguousarray(cos_tab, np.float32), _F), _ptr(out, _F), err, 256)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return out
+
+
+def ref_gemm_oracle(a, b):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.float64)
+    assert ref_lib().kref_oracle_gemm(_ptr(a, _D), _ptr(b, _D), m, n, k, _ptr(c, _D)) == 0
+    return c
+
+
+def ref_gemm(a, b, m_block=2, n_block=4, super_m=12, bf16=False):
+    """The reference gemm_kernel through execute_functional."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.float32)
+    err = ctypes.create_string_buffer(256)
+    rc = ref_lib().kref_gemm(m, n, k, m_block, n_block, super_m, int(bf16), _ptr(a, _F), _ptr(b, _F), _ptr(c, _F),
+                             err, 256)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return c
+
+
+def ref_supergroup_order(r_blocks, c_blocks, super_m):
+    rows = np.empty(r_blocks * c_blocks, dtype=np.int32)
+    cols = np.empty_like(rows)
+    _I = ctypes.POINTER(ctypes.c_int)
+    assert ref_lib().kref_supergroup_order(r_blocks, c_blocks, super_m, rows.ctypes.data_as(_I),
+                                           cols.ctypes.data_as(_I)) == 0
+    return rows, cols

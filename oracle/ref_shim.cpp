@@ -125,3 +125,90 @@ KREF_API void kref_fill(uint32_t seed, float lo, float hi, int bf16, float* out,
     std::uniform_real_distribution<float> u(lo, hi);
     for (int64_t i = 0; i < total; ++i) out[i] = bf16 ? round_to_bf16(u(rng)) : u(rng);
 }
+
+// The reference fp64 rotary oracle (oracles.hpp:66-90) for one [n x hd] head.
+KREF_API int kref_oracle_rotary(const double* x, const double* sin_tab, const double* cos_tab, int n, int hd,
+                                double* out) {
+    try {
+        std::vector<double> xx(x, x + (size_t)n * hd), ss(sin_tab, sin_tab + (size_t)n * hd / 2),
+            cc(cos_tab, cos_tab + (size_t)n * hd / 2);
+        auto r = oracle_rotary(xx, ss, cc, n, hd);
+        std::memcpy(out, r.data(), r.size() * 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// The reference rotary kernel (kernels.hpp:413-503) through execute_functional, fp32.
+KREF_API int kref_rotary(int B, int H, int N, int hd, int workers, const float* x, const float* sin_tab,
+                         const float* cos_tab, float* o, char* err, int errlen) {
+    try {
+        RotaryConfig cfg;
+        cfg.batches = B;
+        cfg.heads = H;
+        cfg.seq = N;
+        cfg.head_dim = hd;
+        cfg.num_workers = workers;
+        auto g = std::make_shared<RotaryGlobals>(cfg);
+        std::memcpy(g->x.data.data(), x, (size_t)B * H * N * hd * 4);
+        std::memcpy(g->sin_tab.data.data(), sin_tab, (size_t)N * hd / 2 * 4);
+        std::memcpy(g->cos_tab.data.data(), cos_tab, (size_t)N * hd / 2 * 4);
+        execute_functional(rotary_kernel(cfg, g), rotary_pipeline_config(cfg));
+        std::memcpy(o, g->o.data.data(), (size_t)B * H * N * hd * 4);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return code_of(e);
+    }
+}
+
+// The reference fp64 GEMM oracle (oracles.hpp:17-30).
+KREF_API int kref_oracle_gemm(const double* a, const double* b, int m, int n, int k, double* c) {
+    try {
+        std::vector<double> aa(a, a + (size_t)m * k), bb(b, b + (size_t)k * n);
+        auto r = oracle_gemm(aa, bb, m, n, k);
+        std::memcpy(c, r.data(), r.size() * 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// The reference GEMM kernel (kernels.hpp:76-149) through execute_functional (fp32 or emulated bf16).
+KREF_API int kref_gemm(int m, int n, int k, int m_block, int n_block, int super_m, int bf16, const float* a,
+                       const float* b, float* c, char* err, int errlen) {
+    try {
+        GemmConfig cfg;
+        cfg.m = m;
+        cfg.n = n;
+        cfg.k = k;
+        cfg.m_block = m_block;
+        cfg.n_block = n_block;
+        cfg.super_m = super_m;
+        cfg.dtype = bf16 ? Dtype::Bf16 : Dtype::Fp32;
+        auto g = std::make_shared<GemmGlobals>(cfg);
+        std::memcpy(g->a.data.data(), a, (size_t)m * k * 4);
+        std::memcpy(g->b.data.data(), b, (size_t)k * n * 4);
+        execute_functional(gemm_kernel(cfg, g), gemm_pipeline_config(cfg));
+        std::memcpy(c, g->c.data.data(), (size_t)m * n * 4);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return code_of(e);
+    }
+}
+
+// supergroup_order (grid.hpp:28-47): the reference launch order, as (row, col) pairs.
+KREF_API int kref_supergroup_order(int r_blocks, int c_blocks, int super_m, int* rows, int* cols) {
+    try {
+        auto o = supergroup_order(r_blocks, c_blocks, super_m);
+        for (size_t i = 0; i < o.size(); ++i) {
+            rows[i] = o[i].row;
+            cols[i] = o[i].col;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}

@@ -80,6 +80,8 @@ _SIGS = {
     "tkb_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP]),
     "tkb_attn_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
     "tkb_attn_bwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
+    "tkb_rotary": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP]),
+    "tkb_rotary_qk": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "tkb_shard_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "tkb_last_launch_count": (ctypes.c_int, []),
@@ -178,11 +180,61 @@ def _check_kv(q, k, v):
     return hkv, kst
 
 
-def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None, return_lse=True,
-                  check_finite=False):
-    """O = softmax(scale * Q K^T [causal]) V on the B200; returns (O, L) with L fp32 [B, H, N].
-    k, v may carry fewer heads than q (grouped-query / multi-query attention)."""
+def _tables(sin_tab, cos_tab, N, D, device):
     import torch
+
+    for t in (sin_tab, cos_tab):
+        if not t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != (N, D // 2) or not t.is_contiguous():
+            raise ShapeError("sin / cos tables must be contiguous fp32 CUDA tensors [N, D/2]")
+
+
+def rotary(x, sin_tab, cos_tab, out=None):
+    """Rotary position embedding (the reference rotary_kernel, kernels.hpp:357-513): pairs
+    (x[..., p, i], x[..., p, i + D/2]) rotated by the [N, D/2] sin / cos table angles."""
+    import torch
+
+    if not x.is_cuda or x.dtype != torch.bfloat16:
+        raise ConfigError("rotary: x must be a bf16 CUDA tensor")
+    st = _bhnd(x, "x")
+    B, H, N, D = x.shape
+    _tables(sin_tab, cos_tab, N, D, x.device)
+    if out is None:
+        out = torch.empty_strided(x.shape, x.stride(), dtype=torch.bfloat16, device=x.device)
+    elif _bhnd(out, "out") != st:
+        raise ShapeError("out must share x's strides")
+    d = AttentionConfig(B, H, N, D).desc(strides=st)
+    _check(lib().tkb_rotary(ctypes.byref(d), x.data_ptr(), sin_tab.data_ptr(), cos_tab.data_ptr(), out.data_ptr(),
+                            _stream(torch, x.device)))
+    return out
+
+
+def rotary_qk(q, k, sin_tab, cos_tab):
+    """The attention prologue: rotated copies of Q and K from one launch."""
+    import torch
+
+    st = _bhnd(q, "q")
+    hkv = k.shape[1]
+    kst = _bhnd(k, "k")
+    B, H, N, D = q.shape
+    _tables(sin_tab, cos_tab, N, D, q.device)
+    qr = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+    kr = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
+    d = AttentionConfig(B, H, N, D, kv_heads=hkv).desc(strides=st, kv_strides=kst)
+    _check(lib().tkb_rotary_qk(ctypes.byref(d), q.data_ptr(), k.data_ptr(), sin_tab.data_ptr(), cos_tab.data_ptr(),
+                               qr.data_ptr(), kr.data_ptr(), _stream(torch, q.device)))
+    return qr, kr
+
+
+def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None, return_lse=True,
+                  check_finite=False, rotary_tables=None):
+    """O = softmax(scale * Q K^T [causal]) V on the B200; returns (O, L) with L fp32 [B, H, N].
+    k, v may carry fewer heads than q (grouped-query / multi-query attention).
+    rotary_tables=(sin, cos) applies the rotary embedding to Q and K first (one extra
+    HBM-bound launch; the rotated tensors are temporaries)."""
+    import torch
+
+    if rotary_tables is not None:
+        q, k = rotary_qk(q, k, *rotary_tables)
 
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ConfigError("attention_fwd runs on the GPU only (no CPU fallback)")

@@ -53,6 +53,25 @@ constexpr int kTraceIters = 32;
 constexpr int kTraceEvents = 8;
 constexpr int kTraceRoles = 4;
 
+// Rotary embedding (rotary_sm100.cu): up to two tensors (Q, K) per launch.
+namespace rope {
+struct Tensor {
+    const void* x;       // bf16 [B, heads, N, hd]
+    void* o;             // bf16, may alias x
+    int64_t xb, xh, xn;  // element strides of x
+    int64_t ob, oh, on;  // element strides of o
+    int heads;
+    int64_t items;       // B * heads * N * (hd / 16); 0 = unused slot
+};
+struct Params {
+    Tensor t[2];
+    const float* sin_tab;  // [N, hd/2] fp32
+    const float* cos_tab;
+    int n, hd;
+};
+}  // namespace rope
+int launch_rotary(const rope::Params& p, int num_sms, cudaStream_t stream);
+
 // Launchers (return cudaError_t as int).
 int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream);
 

@@ -273,6 +273,84 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     return TKB_OK;
 }
 
+// RotaryConfig::validate (kernels.hpp:367-376) relaxed to the B200 layout: even head_dim,
+// a multiple of 16 (8-pair vectors), any seq >= 1.
+int rotary_validate(const tkb_attn_desc* d) {
+    if (!d) return fail(TKB_ERR_BOUNDS, "null descriptor");
+    if (d->batches < 1 || d->heads < 1 || d->seq < 1) return fail(TKB_ERR_CONFIG, "positive extents required");
+    if (d->head_dim < 16 || d->head_dim % 16) return fail(TKB_ERR_CONFIG, "rotary head_dim must be a multiple of 16");
+    if (d->kv_heads < 0 || d->heads % kv_heads_of(d)) return fail(TKB_ERR_CONFIG, "heads % kv_heads != 0");
+    for (const Strides& s : {strides_of(d), kv_strides_of(d)})
+        if (s.n < d->head_dim || (s.n % 8) || (s.h % 8) || (s.b % 8))
+            return fail(TKB_ERR_SHAPE, "strides must be multiples of 8 elements with rows >= head_dim");
+    return TKB_OK;
+}
+
+tkb::rope::Tensor rope_tensor(const tkb_attn_desc* d, const void* x, void* o, const Strides& s, int heads) {
+    tkb::rope::Tensor t;
+    t.x = x;
+    t.o = o;
+    t.xb = t.ob = s.b;
+    t.xh = t.oh = s.h;
+    t.xn = t.on = s.n;
+    t.heads = heads;
+    t.items = (int64_t)d->batches * heads * d->seq * (d->head_dim / 16);
+    return t;
+}
+
+// Rotary embedding (rotary_kernel, kernels.hpp:413-503): out = rotate(x) by fp32 [seq, head_dim/2]
+// sin / cos tables. x, out: [B, H, N, D] bf16 with desc's strides (out may alias x).
+TKB_API int tkb_rotary(const tkb_attn_desc* d, const void* x, const float* sin_tab, const float* cos_tab, void* out,
+                       void* stream) {
+    g_launches = 0;
+    int rc = rotary_validate(d);
+    if (rc) return rc;
+    if (!x || !sin_tab || !cos_tab || !out) return fail(TKB_ERR_BOUNDS, "null pointer");
+    if (((uintptr_t)x | (uintptr_t)out | (uintptr_t)sin_tab | (uintptr_t)cos_tab) & 15)
+        return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    int sms = 0, *sched = nullptr;
+    if ((rc = device_state(&sms, &sched))) return rc;
+    tkb::rope::Params p{};
+    p.t[0] = rope_tensor(d, x, out, strides_of(d), d->heads);
+    p.sin_tab = sin_tab;
+    p.cos_tab = cos_tab;
+    p.n = d->seq;
+    p.hd = d->head_dim;
+    const int e = tkb::launch_rotary(p, sms, reinterpret_cast<cudaStream_t>(stream));
+    if (e) return fail(TKB_ERR_CUDA, std::string("rotary launch: ") + cudaGetErrorString((cudaError_t)e));
+    g_launches = 1;
+    return TKB_OK;
+}
+
+// The attention prologue: Q ([B, H, N, D], desc strides) and K ([B, Hkv, N, D], kv strides)
+// rotated in one launch into q_out / k_out (which may alias q / k).
+TKB_API int tkb_rotary_qk(const tkb_attn_desc* d, const void* q, const void* k, const float* sin_tab,
+                          const float* cos_tab, void* q_out, void* k_out, void* stream) {
+    g_launches = 0;
+    int rc = rotary_validate(d);
+    if (rc) return rc;
+    if (!q || !k || !sin_tab || !cos_tab || !q_out || !k_out) return fail(TKB_ERR_BOUNDS, "null pointer");
+    if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)q_out | (uintptr_t)k_out | (uintptr_t)sin_tab |
+         (uintptr_t)cos_tab) &
+        15)
+        return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    int sms = 0, *sched = nullptr;
+    if ((rc = device_state(&sms, &sched))) return rc;
+    tkb::rope::Params p{};
+    p.t[0] = rope_tensor(d, q, q_out, strides_of(d), d->heads);
+    p.t[1] = rope_tensor(d, k, k_out, kv_strides_of(d), kv_heads_of(d));
+    p.sin_tab = sin_tab;
+    p.cos_tab = cos_tab;
+    p.n = d->seq;
+    p.hd = d->head_dim;
+    const int e = tkb::launch_rotary(p, sms, reinterpret_cast<cudaStream_t>(stream));
+    if (e) return fail(TKB_ERR_CUDA, std::string("rotary launch: ") + cudaGetErrorString((cudaError_t)e));
+    g_launches = 1;
+    return TKB_OK;
+}
+
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
     if (!begin || !end) return fail(TKB_ERR_BOUNDS, "null output");
     if (world < 1 || rank < 0 || rank >= world || units < 0) return fail(TKB_ERR_CONFIG, "bad rank/world/units");
