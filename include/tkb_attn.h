@@ -113,6 +113,19 @@ TKB_API int tkb_rotary(const tkb_attn_desc* desc, const void* x, const float* si
 TKB_API int tkb_rotary_qk(const tkb_attn_desc* desc, const void* q, const void* k, const float* sin_tab,
                           const float* cos_tab, void* q_out, void* k_out, void* stream);
 
+/* GEMM on the same tcgen05 / TMA machinery (replaces gemm_kernel, kernels.hpp:21-164;
+ * oracle oracles.hpp:17-30): C[m, n] = A[m, k] B[k, n], bf16 row-major, fp32 accumulation,
+ * bf16 C. Tasks (128 x 256 blocks of C) run in the reference's supergrouped order
+ * (grid.hpp:28-47). Leading dimensions in elements, 0 = dense; multiples of 8. */
+typedef struct tkb_gemm_desc {
+    int32_t m, n, k;
+    int32_t super_m; /* supergroup height (GemmConfig::super_m, kernels.hpp:29); 0 = 12 */
+    int64_t lda, ldb, ldc;
+} tkb_gemm_desc;
+
+TKB_API int tkb_gemm_validate(const tkb_gemm_desc* desc);
+TKB_API int tkb_gemm(const tkb_gemm_desc* desc, const void* a, const void* b, void* c, void* stream);
+
 /* Multi-GPU sharding of the flattened batch x head grid:
  * contiguous, balanced [begin, end) of `units` for `rank` of `world`. No collective. */
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end);

@@ -73,6 +73,13 @@ class AttnDesc(ctypes.Structure):
     ]
 
 
+class GemmDesc(ctypes.Structure):
+    """tkb_gemm_desc (include/tkb_attn.h)."""
+
+    _fields_ = [("m", ctypes.c_int32), ("n", ctypes.c_int32), ("k", ctypes.c_int32), ("super_m", ctypes.c_int32),
+                ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64), ("ldc", ctypes.c_int64)]
+
+
 _VP = ctypes.c_void_p
 _SIGS = {
     "tkb_attn_desc_init": (None, [ctypes.POINTER(AttnDesc)] + [ctypes.c_int32] * 5),
@@ -82,6 +89,8 @@ _SIGS = {
     "tkb_attn_bwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
     "tkb_rotary": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP]),
     "tkb_rotary_qk": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "tkb_gemm_validate": (ctypes.c_int, [ctypes.POINTER(GemmDesc)]),
+    "tkb_gemm": (ctypes.c_int, [ctypes.POINTER(GemmDesc), _VP, _VP, _VP, _VP]),
     "tkb_shard_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "tkb_last_launch_count": (ctypes.c_int, []),
@@ -292,6 +301,43 @@ def attention_bwd(q, k, v, o, dout, lse, causal=False, softmax_scale=None, dq=No
                               dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                               workspace.data_ptr(), ws_bytes, _stream(torch, q.device)))
     return dq, dk, dv
+
+
+@dataclass
+class GemmConfig:
+    """The reference GemmConfig (kernels.hpp:23-46) minus its CPU-model knobs (m_block /
+    n_block are the compile-time 128 x 256 tile); super_m keeps its meaning (grid.hpp:28-47)."""
+
+    m: int = 0
+    n: int = 0
+    k: int = 0
+    super_m: int = 12
+
+    def desc(self, lda=0, ldb=0, ldc=0) -> GemmDesc:
+        return GemmDesc(self.m, self.n, self.k, self.super_m, lda, ldb, ldc)
+
+    def validate(self):
+        _check(lib().tkb_gemm_validate(ctypes.byref(self.desc())))
+
+
+def gemm(a, b, out=None, super_m=12):
+    """C = A B (bf16 row-major [M, K] x [K, N] -> [M, N], fp32 accumulation) on tcgen05."""
+    import torch
+
+    for t, name in ((a, "a"), (b, "b")):
+        if not t.is_cuda or t.dtype != torch.bfloat16 or t.dim() != 2 or t.stride(1) != 1:
+            raise ConfigError(f"{name} must be a row-major bf16 CUDA matrix")
+    M, K = a.shape
+    if b.shape[0] != K:
+        raise ShapeError("inner dimensions differ")
+    N = b.shape[1]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=a.device)
+    elif tuple(out.shape) != (M, N) or out.stride(1) != 1 or out.dtype != torch.bfloat16:
+        raise ShapeError("out must be a row-major bf16 [M, N] matrix")
+    d = GemmConfig(M, N, K, super_m).desc(a.stride(0), b.stride(0), out.stride(0))
+    _check(lib().tkb_gemm(ctypes.byref(d), a.data_ptr(), b.data_ptr(), out.data_ptr(), _stream(torch, a.device)))
+    return out
 
 
 def shard_range(units, rank, world):

@@ -53,6 +53,16 @@ constexpr int kTraceIters = 32;
 constexpr int kTraceEvents = 8;
 constexpr int kTraceRoles = 4;
 
+// GEMM (gemm_sm100.cu): C[m, n] = A[m, k] B[k, n], bf16 row-major, fp32 accumulation.
+struct GemmParams {
+    CUtensorMap tm_a;  // 2-D {k, m}, box {64, 128}, SW128
+    CUtensorMap tm_b;  // 2-D {n, k}, box {64, 64}, SW128 (MN-major B panels)
+    CUtensorMap tm_c;  // 2-D {n, m}, box {64, 128}, SW128
+    int m, n, k;
+    int super_m;       // supergroup height of the task order (grid.hpp:28-47)
+};
+int launch_gemm(const GemmParams& p, int num_sms, cudaStream_t stream);
+
 // Rotary embedding (rotary_sm100.cu): up to two tensors (Q, K) per launch.
 namespace rope {
 struct Tensor {

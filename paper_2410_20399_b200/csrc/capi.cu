@@ -351,6 +351,61 @@ TKB_API int tkb_rotary_qk(const tkb_attn_desc* d, const void* q, const void* k, 
     return TKB_OK;
 }
 
+// GemmConfig::validate (kernels.hpp:33-41) relaxed to the B200 layout: any m, n, k >= 1
+// (ragged edges are zero-filled / clipped by TMA), row strides multiples of 8 elements.
+TKB_API int tkb_gemm_validate(const tkb_gemm_desc* d) {
+    if (!d) return fail(TKB_ERR_BOUNDS, "null descriptor");
+    if (d->m < 1 || d->n < 1 || d->k < 1) return fail(TKB_ERR_CONFIG, "GEMM extents must be positive");
+    if (d->super_m < 0) return fail(TKB_ERR_CONFIG, "super_m must be >= 1 (0: default 12)");
+    const int64_t lda = d->lda ? d->lda : d->k, ldb = d->ldb ? d->ldb : d->n, ldc = d->ldc ? d->ldc : d->n;
+    if (lda < d->k || ldb < d->n || ldc < d->n || (lda % 8) || (ldb % 8) || (ldc % 8))
+        return fail(TKB_ERR_SHAPE, "row strides must be multiples of 8 elements covering the rows");
+    return TKB_OK;
+}
+
+TKB_API int tkb_gemm(const tkb_gemm_desc* d, const void* a, const void* b, void* c, void* stream) {
+    g_launches = 0;
+    int rc = tkb_gemm_validate(d);
+    if (rc) return rc;
+    if (!a || !b || !c) return fail(TKB_ERR_BOUNDS, "null tensor pointer");
+    if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 15) return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    int sms = 0, *sched = nullptr;
+    if ((rc = device_state(&sms, &sched))) return rc;
+    const uint64_t lda = d->lda ? d->lda : d->k, ldb = d->ldb ? d->ldb : d->n, ldc = d->ldc ? d->ldc : d->n;
+    tkb::GemmParams p{};
+    std::string err;
+    {
+        uint64_t dims[2] = {(uint64_t)d->k, (uint64_t)d->m}, str[2] = {1, lda};
+        uint32_t box[2] = {64, 128};
+        if (!tkb::host::make_tmap(&p.tm_a, a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
+            return fail(TKB_ERR_SHAPE, "tensor map A: " + err);
+    }
+    {
+        uint64_t dims[2] = {(uint64_t)d->n, (uint64_t)d->k}, str[2] = {1, ldb};
+        uint32_t box[2] = {64, 64};
+        if (!tkb::host::make_tmap(&p.tm_b, b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
+            return fail(TKB_ERR_SHAPE, "tensor map B: " + err);
+    }
+    {
+        uint64_t dims[2] = {(uint64_t)d->n, (uint64_t)d->m}, str[2] = {1, ldc};
+        uint32_t box[2] = {64, 128};
+        if (!tkb::host::make_tmap(&p.tm_c, c, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, &err))
+            return fail(TKB_ERR_SHAPE, "tensor map C: " + err);
+    }
+    p.m = d->m;
+    p.n = d->n;
+    p.k = d->k;
+    p.super_m = d->super_m > 0 ? d->super_m : 12;
+    const int e = tkb::launch_gemm(p, sms, reinterpret_cast<cudaStream_t>(stream));
+    if (e) return fail(TKB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString((cudaError_t)e));
+    g_launches = 1;
+    return TKB_OK;
+}
+
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
     if (!begin || !end) return fail(TKB_ERR_BOUNDS, "null output");
     if (world < 1 || rank < 0 || rank >= world || units < 0) return fail(TKB_ERR_CONFIG, "bad rank/world/units");

@@ -1,0 +1,211 @@
+// gemm_sm100.cu — C = A B on the same tcgen05 / TMA / LCSF machinery as attention
+// (the QKV / output projections either side of the attention).
+//
+// Reference: kittensim gemm_kernel (kernels.hpp:76-149) — one task computes a block of C
+// walking K in 64-wide panels through the LCSF ring, tasks in the supergrouped launch
+// order (supergroup_order, grid.hpp:28-47), oracle_gemm (oracles.hpp:17-30). Here:
+//   tile        128 x 256 of C per task, K panels of 64 (A: 128 x 64 K-major SW128 tile,
+//               B: 64 x 256 MN-major = four SW128 atoms), fp32 accumulation in TMEM
+//   warp 0      LOAD: TMA of the A / B panels into a 4-stage lcsf::ring (48 KB / stage)
+//   warp 1      MMA: converged warp, elected lane issues tcgen05.mma M=128 N=256 K=16
+//               (mma_ABt-style A descriptor, B MN-major = the reference's mma_AB with
+//               B row-major, kernels.hpp:124-138)
+//   warps 4-7   FINISH: TMEM -> fp32 regs -> bf16 -> SMEM atom -> TMA store, while the
+//               MMA warp already accumulates the next task into the other TMEM buffer
+//               (2 x 256 columns)
+// Persistent grid (one CTA per SM); task t -> (row block, col block) by the reference's
+// supergroup order, so concurrently running CTAs share A row panels / B column panels
+// in L2. Any M, N, K >= 1 (TMA zero-fills / clips the ragged edges); row strides must be
+// multiples of 8 elements.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "attn_common.cuh"
+#include "tkb/lcsf.cuh"
+#include "tkb/tile.cuh"
+
+namespace tkb {
+namespace gemm {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int kStages = 4;
+constexpr int kATile = BM * BK * 2;            // 16 KB
+constexpr int kBTile = BK * BN * 2;            // 32 KB: 4 atoms of 64 K rows x 64 N cols
+constexpr int kBAtom = BK * 128;               // 8 KB
+constexpr int kStage = kATile + kBTile;
+constexpr int kStaging = BM * 128;             // one 128 x 64 bf16 output atom
+constexpr int kOffBar = kStages * kStage + kStaging;
+constexpr int kSmemBytes = kOffBar + 256 + 1024;
+static_assert(kSmemBytes <= 232448, "smem");
+constexpr int kThreads = 256;  // warp 0 load, warp 1 MMA, warps 4-7 epilogue
+constexpr int kBarEpi = 1;
+
+// supergroup_order (grid.hpp:28-47): walk super_m rows down each column strip, then the
+// remainder rows column by column.
+TKB_DEVICE void supergroup(int task, int r_blocks, int c_blocks, int super_m, int& row, int& col) {
+    const int super_rows = (r_blocks / super_m) * super_m;
+    const int super_repeat = super_m * c_blocks;
+    if (task < super_rows * c_blocks) {
+        row = super_m * (task / super_repeat) + task % super_m;
+        col = (task % super_repeat) / super_m;
+    } else {
+        const int final_rows = r_blocks - super_rows;
+        const int rem = task - super_rows * c_blocks;
+        row = super_rows + rem % final_rows;
+        col = rem / final_rows;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    auto sA = [&](int s) { return st_bf<BM, BK>{smem + s * kStage}; };
+    auto sB = [&](int s) { return smem + s * kStage + kATile; };  // MN-major [BK rows][BN], 4 atoms
+    uint8_t* stage_c = smem + kStages * kStage;
+    struct Bars {
+        lcsf::ring<kStages> ab;
+        mbarrier acc_full[2], acc_empty[2];
+        uint32_t tmem_slot;
+    };
+    Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
+    static_assert(sizeof(Bars) <= 256, "barrier area");
+
+    const int warp = warpid();
+    const int lane = laneid();
+    const int r_blocks = (p.m + BM - 1) / BM, c_blocks = (p.n + BN - 1) / BN;
+    const int tasks = r_blocks * c_blocks;
+    const int k_tiles = (p.k + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        bar.ab.init(1, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar.acc_full[i], 1);
+            mbar_init(&bar.acc_empty[i], WARPGROUP_THREADS);
+        }
+        fence_barrier_init();
+        tma::prefetch_desc(&p.tm_a);
+        tma::prefetch_desc(&p.tm_b);
+        tma::prefetch_desc(&p.tm_c);
+    }
+    if (warp == 1) tmem::alloc<512>(&bar.tmem_slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tbase = bar.tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------------------------------------------------------- LOAD
+            const uint64_t pol = tma::policy_evict_last();
+            lcsf::ring_state<kStages> st;
+            for (int t = blockIdx.x; t < tasks; t += gridDim.x) {
+                int rb, cb;
+                supergroup(t, r_blocks, c_blocks, p.super_m, rb, cb);
+                for (int kt = 0; kt < k_tiles; ++kt) {
+                    bar.ab.wait_empty(st);
+                    mbar_arrive_expect_tx(&bar.ab.full[st.slot], kStage);
+                    tma::load_2d(sA(st.slot).ptr, &p.tm_a, &bar.ab.full[st.slot], kt * BK, rb * BM);
+#pragma unroll
+                    for (int a = 0; a < BN / 64; ++a)
+                        tma::load_2d(sB(st.slot) + a * kBAtom, &p.tm_b, &bar.ab.full[st.slot], cb * BN + a * 64,
+                                     kt * BK);
+                    st.advance();
+                }
+            }
+            (void)pol;
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------------------- MMA
+        constexpr uint32_t idesc = umma::idesc_bf16<BM, BN, false, true>();
+        constexpr uint32_t hi = umma::desc_hi_sw128(1024);
+        lcsf::ring_state<kStages> st;
+        int n = 0;
+        for (int t = blockIdx.x; t < tasks; t += gridDim.x, ++n) {
+            const int buf = n & 1;
+            mbar_wait(&bar.acc_empty[buf], ((n >> 1) & 1) ^ 1u);  // the epilogue drained this buffer
+            tmem::fence_after();
+            const uint32_t acc = tbase + buf * BN;
+            for (int kt = 0; kt < k_tiles; ++kt) {
+                bar.ab.wait_full(st);
+                tmem::fence_after();
+                const uint32_t a0 = sA(st.slot).addr(), b0 = smem_u32(sB(st.slot));
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                    umma::mma_ss_e(acc, umma::desc_lo(a0 + k * 32, 16), hi, umma::desc_lo(b0 + k * 16 * 128, kBAtom),
+                                   hi, idesc, (kt > 0 || k > 0) ? 1u : 0u);
+                umma::commit_e(&bar.ab.empty[st.slot]);  // panel consumed -> the producer may refill it
+                st.advance();
+            }
+            umma::commit_e(&bar.acc_full[buf]);
+        }
+    } else if (warp >= 4) {
+        // -------------------------------------------------------------------- FINISH
+        const int wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const bool leader = (warp == 4 && lane == 0);
+        const st_bf<BM, 64> stage{stage_c};
+        int n = 0;
+        for (int t = blockIdx.x; t < tasks; t += gridDim.x, ++n) {
+            int rb, cb;
+            supergroup(t, r_blocks, c_blocks, p.super_m, rb, cb);
+            const int buf = n & 1;
+            mbar_wait(&bar.acc_full[buf], (n >> 1) & 1);
+            tmem::fence_after();
+            const uint32_t acc = tbase + lane_off + buf * BN;
+#pragma unroll 1
+            for (int a = 0; a < BN / 64; ++a) {
+                rt_fl<32> v0, v1;
+                load(v0, acc + a * 64);
+                load(v1, acc + a * 64 + 32);
+                load_wait(v0);
+                load_wait(v1);
+                if (a == BN / 64 - 1) {  // accumulator drained: the MMA warp may reuse it
+                    tmem::fence_before();
+                    mbar_arrive(&bar.acc_empty[buf]);
+                }
+                rt_bf<32> b0, b1;
+                copy(b0, v0);
+                copy(b1, v1);
+                if (leader) tma::wait_group_read<0>();  // staging atom free again
+                named_sync(kBarEpi, WARPGROUP_THREADS);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    sts_v4(smem_u32(stage.chunk(r, q)), make_uint4(b0.v[4 * q], b0.v[4 * q + 1], b0.v[4 * q + 2],
+                                                                   b0.v[4 * q + 3]));
+                    sts_v4(smem_u32(stage.chunk(r, 4 + q)), make_uint4(b1.v[4 * q], b1.v[4 * q + 1],
+                                                                       b1.v[4 * q + 2], b1.v[4 * q + 3]));
+                }
+                tma::fence_async_smem();
+                named_sync(kBarEpi, WARPGROUP_THREADS);
+                if (leader) {
+                    tma::store_2d(&p.tm_c, stage.ptr, cb * BN + a * 64, rb * BM);
+                    tma::commit_group();
+                }
+            }
+        }
+        if (leader) tma::wait_group<0>();
+    }
+
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 1) tmem::dealloc<512>(tbase);
+}
+
+}  // namespace gemm
+
+int launch_gemm(const GemmParams& p, int num_sms, cudaStream_t stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e =
+            cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::kSmemBytes);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    const int tasks = ((p.m + gemm::BM - 1) / gemm::BM) * ((p.n + gemm::BN - 1) / gemm::BN);
+    const int grid = tasks < num_sms ? tasks : num_sms;
+    gemm::gemm_kernel<<<grid, gemm::kThreads, gemm::kSmemBytes, stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace tkb
