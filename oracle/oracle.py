@@ -260,3 +260,29 @@ def ref_supergroup_order(r_blocks, c_blocks, super_m):
     assert ref_lib().kref_supergroup_order(r_blocks, c_blocks, super_m, rows.ctypes.data_as(_I),
                                            cols.ctypes.data_as(_I)) == 0
     return rows, cols
+
+
+def _npy_tool():
+    return os.path.join(HERE, "_ref", "npy_tool")
+
+
+def ref_save_npy(path, arr):
+    """Write float32 `arr` with the reference's own .npy writer (npy.hpp:18-49)."""
+    import subprocess
+    import tempfile
+
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+        a.tofile(f.name)
+        subprocess.run([_npy_tool(), "save", f.name, path] + [str(d) for d in a.shape], check=True)
+
+
+def ref_load_npy(path):
+    """Read a float32 .npy with the reference's own reader (npy.hpp:51-87) -> (data, shape)."""
+    import subprocess
+    import tempfile
+
+    with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+        r = subprocess.run([_npy_tool(), "load", path, f.name], check=True, capture_output=True, text=True)
+        shape = tuple(int(x) for x in r.stdout.split())
+        return np.fromfile(f.name, dtype=np.float32).reshape(shape), shape

@@ -212,3 +212,4 @@ KREF_API int kref_supergroup_order(int r_blocks, int c_blocks, int super_m, int*
         return code_of(e);
     }
 }
+

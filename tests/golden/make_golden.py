@@ -76,6 +76,13 @@ def main():
     out["validate.d96"] = np.array(L.kref_validate(1, 1, 384, 96, 0, 0, err, 256))
     out["constants.tau"] = np.array([L.kref_temperature_scale(64), L.kref_temperature_scale(128)])
     out["constants.kv_rows"] = np.array([L.kref_kv_tile_rows(64), L.kref_kv_tile_rows(128)])
+    # .npy KAT dumps in the reference's own on-disk format (npy.hpp):
+    # the dense d=64 case (test_kernels.cpp:128-146), written by the reference's writer
+    npy_dir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "npy")
+    os.makedirs(npy_dir, exist_ok=True)
+    q, k, v = ref_fill3(164, 1, 1, 384, 64)
+    for name, arr in (("q", q[0, 0]), ("k", k[0, 0]), ("v", v[0, 0]), ("o_ref", out["dense_d64.o_kernel"][0, 0])):
+        orc.ref_save_npy(os.path.join(npy_dir, f"dense_d64_{name}.npy"), arr)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
     print("wrote", path, os.path.getsize(path), "bytes,", len(out), "arrays")
