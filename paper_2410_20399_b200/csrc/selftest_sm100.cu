@@ -17,6 +17,7 @@
 
 #include "host/tmap.hpp"
 #include "tkb/tcgen05.cuh"
+#include "tkb/tile.cuh"
 #include "tkb/tma.cuh"
 
 using namespace tkb;
@@ -185,6 +186,143 @@ extern "C" __attribute__((visibility("default"))) int tkb_selftest_umma(int vari
     TKB_ST(5, 128, 128) TKB_ST(5, 128, 64)
 #undef TKB_ST
     return -2;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Tile-API selftest (tkb/tile.cuh): one 128 x 128 attention tile written only with the
+// ThunderKittens vocabulary, checked against torch on the host (tests/test_tile_api_gpu.py):
+//   load_async(st_bf, gl)  Q, K, V (TMA, SW128)                 tiles.hpp:416-426
+//   mm_ABt(tt_fl, st_bf, st_bf)  S = Q K^T                     tiles.hpp:349
+//   load(rt_fl, tt) / row_max / sub_row / exp2 / row_sum       tiles.hpp:217-309
+//   copy(rt_bf, rt_fl)  P -> bf16 (RNE); store(tt_bf, rt_bf)   tiles.hpp:195-200
+//   mma_AB(tt_fl, tt_bf, st_bf)  O = P V (V MN-major)          tiles.hpp:350-352
+//   div_row  O / l                                             tiles.hpp:276-281
+// plus st_bf::chunk addressing against the TMA placement (the SW128 element_offset rule,
+// layouts.hpp:111-132): out_q = Q read back through chunk(r, c).
+// Outputs: O [128][128] fp32, m [128] (row max of S), l [128] (row sum of exp2(S - m)),
+// p_bf [128][128] (the bf16 P bits as float), q_back [128][128] (bf16 as float).
+__global__ void __launch_bounds__(128, 1)
+    tile_api_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, float* O, float* m_out, float* l_out, float* p_out,
+                    float* q_back) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using T = st_bf<128, 128>;
+    const T sQ{smem}, sK{smem + T::kBytes}, sV{smem + 2 * T::kBytes};
+    const gl gQ{&tmQ}, gK{&tmK}, gV{&tmV};
+    __shared__ mbarrier bar_load, bar_s, bar_o;
+    __shared__ uint32_t tslot;
+    const int warp = warpid(), lane = laneid();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_load, 1);
+        mbar_init(&bar_s, 1);
+        mbar_init(&bar_o, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem::alloc<512>(&tslot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const tt_fl<128> tS{tslot}, tO{tslot + 128};
+    const tt_bf<64> tP{tslot + 256};
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar_load, 3 * T::kBytes);
+        load_async(sQ, gQ, &bar_load, 0, 0, 0, tma::policy_evict_first());  // 2-D maps: head = batch = 0
+        load_async(sK, gK, &bar_load, 0, 0, 0, tma::policy_evict_first());
+        load_async(sV, gV, &bar_load, 0, 0, 0, tma::policy_evict_first());
+    }
+    mbar_wait(&bar_load, 0);
+    if (warp == 0) {  // converged MMA warp
+        tmem::fence_after();
+        mm_ABt(tS, sQ, sK);
+        umma::commit_e(&bar_s);
+    }
+    mbar_wait(&bar_s, 0);
+    tmem::fence_after();
+    const int r = warp * 32 + lane;
+    rt_fl<128> x;
+    load(x, tS.quarter(warp));
+    load_wait(x);
+    float mx = -INFINITY;
+    row_max(mx, x);
+    sub_row(x, mx);
+    exp2(x);
+    float l = 0.f;
+    row_sum(l, x);
+    rt_bf<128> pb;
+    copy(pb, x);
+    store(tP.quarter(warp), pb);
+    tmem::wait_st();
+    for (int c = 0; c < 128; c += 2) {
+        p_out[(size_t)r * 128 + c] = __uint_as_float(pb.v[c / 2] << 16);
+        p_out[(size_t)r * 128 + c + 1] = __uint_as_float(pb.v[c / 2] & 0xFFFF0000u);
+    }
+    m_out[r] = mx;
+    l_out[r] = l;
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem::fence_after();
+        mma_AB(tO, tP, sV, false);
+        umma::commit_e(&bar_o);
+    }
+    mbar_wait(&bar_o, 0);
+    tmem::fence_after();
+    rt_fl<128> o;
+    load(o, tO.quarter(warp));
+    load_wait(o);
+    div_row(o, l);
+    for (int c = 0; c < 128; ++c) O[(size_t)r * 128 + c] = o.v[c];
+    for (int c = 0; c < 16; ++c) {  // SW128 addressing: 16-byte chunk c of row r
+        const uint4 u = *reinterpret_cast<const uint4*>(sQ.chunk(r, c));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        for (int e = 0; e < 4; ++e) {
+            q_back[(size_t)r * 128 + 8 * c + 2 * e] = __uint_as_float(w[e] << 16);
+            q_back[(size_t)r * 128 + 8 * c + 2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+        }
+    }
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) tmem::dealloc<512>(tslot);
+}
+
+// bf16 RNE of `n` floats through copy(rt_bf, rt_fl) = cvt.rn.bf16x2.f32 (tiles.hpp:40-46, 195-200)
+__global__ void rne_kernel(const float* in, float* out, int n) {
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i + 1 < n) {
+        rt_fl<2> a;
+        a.v[0] = in[i];
+        a.v[1] = in[i + 1];
+        rt_bf<2> b;
+        copy(b, a);
+        out[i] = __uint_as_float(b.v[0] << 16);
+        out[i + 1] = __uint_as_float(b.v[0] & 0xFFFF0000u);
+    }
+}
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_tile_api(const void* Q, const void* K,
+                                                                           const void* V, float* O, float* m,
+                                                                           float* l, float* p, float* q_back,
+                                                                           cudaStream_t stream) {
+    CUtensorMap tq, tk, tv;
+    std::string err;
+    auto mk = [&](CUtensorMap* tm, const void* ptr) {  // 4-D {128, 128, 1, 1} view, box {64, 128, 1, 1}
+        uint64_t dims[4] = {128, 128, 1, 1}, strides[4] = {1, 128, 128 * 128, 128 * 128};
+        uint32_t box[4] = {64, 128, 1, 1};
+        return host::make_tmap(tm, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, dims, strides, box,
+                               CU_TENSOR_MAP_SWIZZLE_128B, &err);
+    };
+    if (!mk(&tq, Q) || !mk(&tk, K) || !mk(&tv, V)) return -1;
+    const int smem = 3 * 32768 + 1024;
+    cudaFuncSetAttribute(tile_api_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    tile_api_kernel<<<1, 128, smem, stream>>>(tq, tk, tv, O, m, l, p, q_back);
+    return (int)cudaGetLastError();
+}
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_rne(const float* in, float* out, int n,
+                                                                      cudaStream_t stream) {
+    rne_kernel<<<(n / 2 + 127) / 128, 128, 0, stream>>>(in, out, n);
+    return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------------
