@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include "attn_common.cuh"
+#include "tkb/lcsf.cuh"
 #include "tkb/tcgen05.cuh"
 #include "tkb/tma.cuh"
 
@@ -434,7 +435,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     if (warp == kWarpMma) tmem::dealloc<512>(tbase);
 }
 
-// ================================================================== bwd_dq (Q-stationary)
+// ================================================================== bwd_dq (Q-stationary, persistent)
+// One CTA per SM walks query-block tasks (b, h, i) — heads in L2-sized groups, heavy causal
+// blocks first — with every ring continuing across tasks: the next task's Q / dO are
+// TMA-loaded while this one runs, copied into TMEM as soon as this task's last S / dP GEMMs
+// retire, so its first S and dP GEMMs overlap this task's dQ finish stage.
 template <int D>
 struct CfgQ {
     using T = Tiles<D>;
@@ -443,7 +448,8 @@ struct CfgQ {
     static constexpr int kOffDo = kOffQ + T::kTileBytes;
     static constexpr int kOffK = kOffDo + T::kTileBytes;
     static constexpr int kOffV = kOffK + kStages * T::kTileBytes;
-    static constexpr int kOffBar = kOffV + kStages * T::kTileBytes;
+    static constexpr int kOffStage = kOffV + kStages * T::kTileBytes;  // dQ finish staging
+    static constexpr int kOffBar = kOffStage + T::kTileBytes;
     static constexpr int kSmemBytes = kOffBar + 512 + 1024;
     static_assert(kSmemBytes <= 232448, "smem");
     // S | dP | dQ | Q (A operand) | dO (A operand): 128 + 128 + D + D/2 + D/2 <= 512
@@ -453,6 +459,26 @@ struct CfgQ {
     static __device__ __forceinline__ constexpr uint32_t tmem_qa() { return 256u + D; }
     static __device__ __forceinline__ constexpr uint32_t tmem_doa() { return 256u + D + D / 2; }
 };
+
+struct QTask {
+    int i, bh;  // query block, batch * heads + head
+};
+
+// task t -> (query block, b*h): heads in groups of p.head_group whose K / V stay in L2,
+// inside a group the causal query blocks heavy (late) first, heads innermost
+template <bool CAUSAL>
+TKB_DEVICE QTask qtask(const BwdParams& p, int t) {
+    const int nq = p.n_pad / 128;
+    const int G = p.head_group;
+    const int sec = t / (G * nq);
+    const int r = t - sec * G * nq;
+    const int gs = min(G, p.bh - sec * G);
+    const int mi = r / gs;
+    QTask w;
+    w.bh = sec * G + (r - mi * gs);
+    w.i = CAUSAL ? (nq - 1 - mi) : mi;
+    return w;
+}
 
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
@@ -465,12 +491,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     uint8_t* sDo = smem + C::kOffDo;
     uint8_t* sK = smem + C::kOffK;
     uint8_t* sV = smem + C::kOffV;
+    uint8_t* sStage = smem + C::kOffStage;
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
-    mbarrier& qdo_full = bars[0];
+    mbarrier& qdo_full = bars[0];   // Q / dO of a task in SMEM (TMA)
     mbarrier& s_full = bars[1];
     mbarrier& s_free = bars[2];
-    mbarrier& a_ready = bars[3];  // Q, dO copied into TMEM
+    mbarrier& a_ready = bars[3];    // Q / dO of a task copied into TMEM
+    mbarrier& qdo_free = bars[4];   // SMEM Q / dO copied out: the next task's may load
     mbarrier& dp_full = bars[5];
+    mbarrier& qa_free = bars[6];    // last S / dP GEMM of a task retired: TMEM Q / dO reusable
     mbarrier& dq_full = bars[7];
     mbarrier* k_full = bars + 8;    // [S]
     mbarrier* k_empty = bars + 12;  // [S]
@@ -478,25 +507,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     mbarrier* v_empty = bars + 20;  // [S]
     mbarrier* ds_full = bars + 32;  // [kGroups] dS chunks (32 keys each)
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
+    lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);  // dynamic task claims
 
     const int warp = warpid();
     const int lane = laneid();
     const int nq = p.n_pad / 128;
-    const int i = CAUSAL ? (int)(nq - 1 - blockIdx.x) : (int)blockIdx.x;  // heavy causal blocks first
-    const int head = blockIdx.y;
-    const int batch = blockIdx.z;
-    const int bh = batch * p.heads + head;
-    const int q0 = i * 128;
-    const int nk = CAUSAL ? (i + 1) : nq;  // kv blocks visited
-    long long* tr = trace_slot(p, bh * gridDim.x + (int)blockIdx.x, 1);
+    const int tasks = p.bh * nq;
+    auto nk_of = [&](const QTask& w) { return CAUSAL ? (w.i + 1) : nq; };  // kv blocks visited
+    long long* tr = trace_slot(p, (int)blockIdx.x, 1);
     const long long t_start = clock64();
 
     if (warp == kWarpLoad && lane == 0) {
+        queue.init(1 + 16);  // the MMA warp and the 16 compute warps
         mbar_init(&qdo_full, 1);
         mbar_init(&s_full, 1);
         mbar_init(&s_free, kComputeThreads);
         mbar_init(&a_ready, kComputeThreads);
+        mbar_init(&qdo_free, kComputeThreads);
         mbar_init(&dp_full, 1);
+        mbar_init(&qa_free, 1);
         mbar_init(&dq_full, 1);
         for (int g = 0; g < kGroups; ++g) mbar_init(&ds_full[g], 128);
         for (int s = 0; s < S; ++s) {
@@ -522,136 +551,187 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             // ------------------------------------------------------------- LOAD
             const uint64_t pol_stream = tma::policy_evict_first();
             const uint64_t pol_keep = tma::policy_evict_last();
-            mbar_arrive_expect_tx(&qdo_full, 2 * TL::kTileBytes);
-            for (int a = 0; a < TL::kAtoms; ++a) {
-                tma::load_4d(sQ + a * kAtomBytes, &p.tm_q, &qdo_full, a * 64, q0, head, batch, pol_stream);
-                tma::load_4d(sDo + a * kAtomBytes, &p.tm_do, &qdo_full, a * 64, q0, head, batch, pol_stream);
-            }
-            for (int jj = 0; jj < nk; ++jj) {
-                const int s = jj % S;
-                const uint32_t ph = ((jj / S) & 1) ^ 1;
-                mbar_wait(&k_empty[s], ph);
-                mbar_arrive_expect_tx(&k_full[s], TL::kTileBytes);
-                for (int a = 0; a < TL::kAtoms; ++a)
-                    tma::load_4d(sK + s * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[s], a * 64, jj * 128,
-                                 head / p.group, batch, pol_keep);
-                mbar_wait(&v_empty[s], ph);
-                mbar_arrive_expect_tx(&v_full[s], TL::kTileBytes);
-                for (int a = 0; a < TL::kAtoms; ++a)
-                    tma::load_4d(sV + s * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[s], a * 64, jj * 128,
-                                 head / p.group, batch, pol_keep);
+            int kv = 0;  // K / V ring position, continuous across tasks
+            int n = 0;
+            int t = queue.claim(0, p.sched, tasks);
+            while (t >= 0) {
+                const QTask w = qtask<CAUSAL>(p, t);
+                const int b = w.bh / p.heads, h = w.bh - b * p.heads;
+                mbar_wait(&qdo_free, (n & 1) ^ 1u);  // the previous task's Q / dO are in TMEM
+                mbar_arrive_expect_tx(&qdo_full, 2 * TL::kTileBytes);
+                for (int a = 0; a < TL::kAtoms; ++a) {
+                    tma::load_4d(sQ + a * kAtomBytes, &p.tm_q, &qdo_full, a * 64, w.i * 128, h, b, pol_stream);
+                    tma::load_4d(sDo + a * kAtomBytes, &p.tm_do, &qdo_full, a * 64, w.i * 128, h, b, pol_stream);
+                }
+                const int nk = nk_of(w);
+                for (int jj = 0; jj < nk; ++jj, ++kv) {
+                    const int s = kv % S;
+                    const uint32_t ph = ((kv / S) & 1) ^ 1;
+                    mbar_wait(&k_empty[s], ph);
+                    mbar_arrive_expect_tx(&k_full[s], TL::kTileBytes);
+                    for (int a = 0; a < TL::kAtoms; ++a)
+                        tma::load_4d(sK + s * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[s], a * 64, jj * 128,
+                                     h / p.group, b, pol_keep);
+                    mbar_wait(&v_empty[s], ph);
+                    mbar_arrive_expect_tx(&v_full[s], TL::kTileBytes);
+                    for (int a = 0; a < TL::kAtoms; ++a)
+                        tma::load_4d(sV + s * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[s], a * 64, jj * 128,
+                                     h / p.group, b, pol_keep);
+                }
+                // claim the next task once this one's loads are all issued (the atomic counter
+                // hands the heavy causal tasks out first and balances them across SMs)
+                t = queue.claim(++n, p.sched, tasks);
             }
         }
     } else if (warp == kWarpMma) {
         // ----------------------------------------------------------------- MMA (converged warp)
         constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
         constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
-        auto kaddr = [&](int jj) { return smem_u32(sK + (jj % S) * TL::kTileBytes); };
-        auto vaddr = [&](int jj) { return smem_u32(sV + (jj % S) * TL::kTileBytes); };
-        auto issue_s = [&](int jj) {  // S_j = Q K_j^T
-            mbar_wait(&k_full[jj % S], (jj / S) & 1);
+        int kv = 0;        // K / V ring position
+        uint32_t it = 0;   // global iteration count (s_full / s_free / dp_full / ds_full phases)
+        auto kaddr = [&](int x) { return smem_u32(sK + (x % S) * TL::kTileBytes); };
+        auto vaddr = [&](int x) { return smem_u32(sV + (x % S) * TL::kTileBytes); };
+        auto issue_s = [&](int x) {  // S = Q K^T
+            mbar_wait(&k_full[x % S], (x / S) & 1);
             tmem::fence_after();
-            mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(jj), id_s);
+            mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(x), id_s);
             umma::commit_e(&s_full);
         };
-        auto issue_dp = [&](int jj) {  // dP_j = dO V_j^T
-            mbar_wait(&v_full[jj % S], (jj / S) & 1);
+        auto issue_dp = [&](int x) {  // dP = dO V^T
+            mbar_wait(&v_full[x % S], (x / S) & 1);
             tmem::fence_after();
-            mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(jj), id_s);
+            mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(x), id_s);
             umma::commit_e(&dp_full);
-            umma::commit_e(&v_empty[jj % S]);
+            umma::commit_e(&v_empty[x % S]);
         };
-        mbar_wait(&a_ready, 0);
-        issue_s(0);
-        issue_dp(0);
-        for (int jj = 0; jj < nk; ++jj) {
-            if (jj + 1 < nk) {
-                mbar_wait(&s_free, jj & 1);  // S_j read out by the compute warps
-                issue_s(jj + 1);
+        for (int n = 0;; ++n) {
+            const int t = queue.get(n);
+            if (lane == 0) queue.release(n);
+            if (t < 0) break;
+            const int nk = nk_of(qtask<CAUSAL>(p, t));
+            mbar_wait(&a_ready, n & 1);  // this task's Q / dO are in TMEM
+            issue_s(kv);
+            issue_dp(kv);
+            if (nk == 1) umma::commit_e(&qa_free);  // the task's only S and dP are issued
+            for (int jj = 0; jj < nk; ++jj, ++kv, ++it) {
+                if (jj + 1 < nk) {
+                    mbar_wait(&s_free, it & 1);  // S_j read out by the compute warps
+                    issue_s(kv + 1);
+                }
+                TKB_TR(0, (int)it, 0);
+                // dQ += dS K, one 32-key chunk per column group as it lands
+                mma_tmem_a_groups(tbase + C::tmem_dq(), tbase + C::tmem_dp(), kaddr(kv), id_q, jj > 0, [&](int g) {
+                    mbar_wait(&ds_full[g], it & 1);
+                    tmem::fence_after();
+                });
+                TKB_TR(0, (int)it, 1);
+                umma::commit_e(&k_empty[kv % S]);
+                if (jj + 1 < nk) {
+                    issue_dp(kv + 1);  // overwrites dS_j, read by dQ_j issued before
+                    if (jj + 2 == nk) umma::commit_e(&qa_free);  // the task's last S and dP are issued
+                }
+                TKB_TR(0, (int)it, 2);
             }
-            TKB_TR(0, jj, 0);
-            // dQ += dS K, one 32-key chunk per column group as it lands
-            mma_tmem_a_groups(tbase + C::tmem_dq(), tbase + C::tmem_dp(), kaddr(jj), id_q, jj > 0, [&](int g) {
-                mbar_wait(&ds_full[g], jj & 1);
-                tmem::fence_after();
-            });
-            TKB_TR(0, jj, 1);
-            umma::commit_e(&k_empty[jj % S]);
-            if (jj + 1 < nk) issue_dp(jj + 1);  // overwrites dS_j, read by dQ_j issued before
-            TKB_TR(0, jj, 2);
+            umma::commit_e(&dq_full);
         }
-        umma::commit_e(&dq_full);
     } else {
         // ----------------------------------------------------------------- COMPUTE
         const int wq = warp & 3;
         const int g = warp >> 2;       // kv group: columns [32g, 32g+32)
         const int r = wq * 32 + lane;  // q row == TMEM lane
-        const int row = q0 + r;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
         const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
         const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
         const float scale = p.scale;
-        const float nlse_r = p.lse2[(size_t)bh * p.n_pad + row];  // -lse2; -inf on padded rows -> P = 0
-        const float dlt_r = p.delta[(size_t)bh * p.n_pad + row];
-        // Q, dO: SMEM (TMA, swizzled) -> TMEM A operands, once per CTA
-        mbar_wait(&qdo_full, 0);
-        smem_rows_to_tmem_a<D>(sQ, tbase + lane_off + C::tmem_qa(), r, g);
-        smem_rows_to_tmem_a<D>(sDo, tbase + lane_off + C::tmem_doa(), r, g);
-        tmem::wait_st();
-        tmem::fence_before();
-        mbar_arrive(&a_ready);
-        for (int jj = 0; jj < nk; ++jj) {
-            const int kv0 = jj * 128;
-            mbar_wait(&s_full, jj & 1);
-            if (threadIdx.x == 0) TKB_TR(1, jj, 0);
+        uint32_t it = 0;
+        int n = 0;
+        // Q, dO of task n: SMEM (TMA, swizzled) -> TMEM A operands, once the previous task's last
+        // S / dP GEMMs retired
+        auto stage_a = [&](int nn) {
+            mbar_wait(&qdo_full, nn & 1);
+            if (nn > 0) mbar_wait(&qa_free, (nn - 1) & 1);
             tmem::fence_after();
-            float pf[32];
-            tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
-            tmem::fence_before();
-            mbar_arrive(&s_free);
-            exp_chunk<true>(pf, tau, nullptr, nlse_r);
-            // visible keys: kv < n, and causal kv <= row
-            const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 32 * g;  // last visible column
-            if (lim < 31) {  // diagonal / ragged tail block only
-#pragma unroll
-                for (int c = 0; c < 32; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
-            }
-            mbar_wait(&dp_full, jj & 1);
-            if (threadIdx.x == 0) TKB_TR(1, jj, 1);
-            tmem::fence_after();
-            uint32_t dpv[32];
-            tmem::ldw_32x32b_x32(tDp, dpv);
-            uint32_t pk[16];
-#pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-                const float2 gg =
-                    sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(dlt_r, dlt_r));
-                const float2 d = mul2(mul2(make_float2(pf[c], pf[c + 1]), gg), make_float2(scale, scale));
-                pk[c / 2] = pack_bf16x2(d.x, d.y);
-            }
-            tmem::st_32x32b_x16(tDp, pk);  // inside the 32 dP columns this thread has read
+            smem_rows_to_tmem_a<D>(sQ, tbase + lane_off + C::tmem_qa(), r, g);
+            smem_rows_to_tmem_a<D>(sDo, tbase + lane_off + C::tmem_doa(), r, g);
             tmem::wait_st();
             tmem::fence_before();
-            mbar_arrive(&ds_full[g]);
-            if (threadIdx.x == 0) TKB_TR(1, jj, 2);
+            mbar_arrive(&a_ready);
+            mbar_arrive(&qdo_free);  // SMEM Q / dO may be refilled with the next task's
+        };
+        int t = queue.get(0);
+        if (t >= 0) stage_a(0);
+        while (t >= 0) {
+            const QTask w = qtask<CAUSAL>(p, t);
+            const int b = w.bh / p.heads, h = w.bh - b * p.heads;
+            const int q0 = w.i * 128;
+            const int row = q0 + r;
+            const int nk = nk_of(w);
+            const float nlse_r = p.lse2[(size_t)w.bh * p.n_pad + row];  // -lse2; -inf on padded rows -> P = 0
+            const float dlt_r = p.delta[(size_t)w.bh * p.n_pad + row];
+            for (int jj = 0; jj < nk; ++jj, ++it) {
+                const int kv0 = jj * 128;
+                mbar_wait(&s_full, it & 1);
+                if (threadIdx.x == 0) TKB_TR(1, (int)it, 0);
+                tmem::fence_after();
+                float pf[32];
+                tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
+                tmem::fence_before();
+                mbar_arrive(&s_free);
+                exp_chunk<true>(pf, tau, nullptr, nlse_r);
+                // visible keys: kv < n, and causal kv <= row
+                const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 32 * g;  // last visible column
+                if (lim < 31) {  // diagonal / ragged tail block only
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
+                }
+                mbar_wait(&dp_full, it & 1);
+                if (threadIdx.x == 0) TKB_TR(1, (int)it, 1);
+                tmem::fence_after();
+                uint32_t dpv[32];
+                tmem::ldw_32x32b_x32(tDp, dpv);
+                uint32_t pk[16];
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const float2 gg = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
+                                           make_float2(dlt_r, dlt_r));
+                    const float2 d = mul2(mul2(make_float2(pf[c], pf[c + 1]), gg), make_float2(scale, scale));
+                    pk[c / 2] = pack_bf16x2(d.x, d.y);
+                }
+                tmem::st_32x32b_x16(tDp, pk);  // inside the 32 dP columns this thread has read
+                tmem::wait_st();
+                tmem::fence_before();
+                mbar_arrive(&ds_full[g]);
+                if (threadIdx.x == 0) TKB_TR(1, (int)it, 2);
+            }
+            // the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this finish)
+            const int t_next = queue.get(n + 1);
+            if (t_next >= 0) stage_a(n + 1);
+            // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM staging -> TMA store
+            mbar_wait(&dq_full, n & 1);
+            tmem::fence_after();
+            if (threadIdx.x == 0) tma::wait_group_read<0>();  // the previous task's store has read the staging
+            named_sync(kBarCompute, kComputeThreads);
+            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sStage, r, g);
+            tma::fence_async_smem();
+            named_sync(kBarCompute, kComputeThreads);
+            if (threadIdx.x == 0) {
+                for (int a = 0; a < TL::kAtoms; ++a)
+                    tma::store_4d(&p.tm_dq, sStage + a * kAtomBytes, a * 64, q0, h, b);
+                tma::commit_group();
+            }
+            __syncwarp();
+            if (lane == 0) queue.release(n);  // every warp read task n's id long ago
+            t = t_next;
+            ++n;
         }
-        // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM (the Q tile is free) -> TMA store
-        mbar_wait(&dq_full, 0);
-        tmem::fence_after();
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sQ, r, g);
-        tma::fence_async_smem();
-        named_sync(kBarCompute, kComputeThreads);
-        if (threadIdx.x == 0) {
-            for (int a = 0; a < TL::kAtoms; ++a) tma::store_4d(&p.tm_dq, sQ + a * kAtomBytes, a * 64, q0, head, batch);
-            tma::commit_group();
-            tma::wait_group_read<0>();
-        }
+        if (threadIdx.x == 0) tma::wait_group<0>();
     }
 
     tmem::fence_before();
     __syncthreads();
     if (warp == kWarpMma) tmem::dealloc<512>(tbase);
+    if (threadIdx.x == 0) lcsf::queue_exit(p.sched);
 }
 #undef TKB_TR
 
@@ -715,7 +795,9 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
         ++*launches;
     }
     if (phases & 4) {
-        attn_bwd_dq_kernel<D, CAUSAL><<<grid, kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
+        const int tasks = p.bh * (p.n_pad / 128);
+        attn_bwd_dq_kernel<D, CAUSAL>
+            <<<tasks < p.num_sms ? tasks : p.num_sms, kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;

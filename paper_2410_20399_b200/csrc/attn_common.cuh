@@ -43,6 +43,10 @@ struct BwdParams {
     int n_pad;
     int heads;         // query heads
     int group;         // query heads per kv head (grouped-query attention; 1 = MHA)
+    int bh;            // batches * heads (persistent task count = bh * n_pad / 128)
+    int head_group;    // heads per L2 group of the persistent task order
+    int num_sms;       // persistent grid size
+    int* sched;        // persistent task counter pair (self-resetting, lcsf::queue_exit)
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)
 };

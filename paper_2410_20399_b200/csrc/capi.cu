@@ -265,6 +265,16 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.heads = d->heads;
     p.scale = scale_of(d);
     p.scale_log2 = p.scale * 1.44269504088896340736f;
+    {
+        int sms = 0;
+        if ((rc = device_state(&sms, &p.sched))) return rc;
+        p.num_sms = sms;
+        p.bh = (int)bh;
+        // heads whose K / V (4 N D bytes each) fit in ~48 MB of L2 run together
+        const long long kv_bytes = 4ll * d->seq * d->head_dim;
+        long long hg = (48ll << 20) / (kv_bytes > 0 ? kv_bytes : 1);
+        p.head_group = (int)(hg < 1 ? 1 : (hg > bh ? bh : hg));
+    }
     int launches = 0;
     int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
                                  s.n, st, g_bwd_phases, &launches);
