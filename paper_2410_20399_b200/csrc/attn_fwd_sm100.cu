@@ -39,6 +39,12 @@
 #include "tkb/lcsf.cuh"
 #include "tkb/tile.cuh"
 
+#ifndef TKB_FWD_POLY64
+#define TKB_FWD_POLY64 2
+#endif
+#ifndef TKB_FWD_POLY128
+#define TKB_FWD_POLY128 0
+#endif
 #ifndef TKB_FWD_PCHUNKS
 #define TKB_FWD_PCHUNKS 2
 #endif
@@ -51,6 +57,11 @@ struct Cfg {
     using Tile = st_bf<128, D>;
     static constexpr int kTile = Tile::kBytes;
     static constexpr int kKvSlots = (D == 128) ? 4 : 8;  // K and V alternate in the ring
+    // exp2 of one pair in every group of four columns, on kPolyGroups of every 4 groups, runs as
+    // a polynomial on the FMA pipe: at D = 64 the MMA work per exponential halves and MUFU
+    // (16 / clk / SM) bounds the softmax; at D = 128 the single-warp exp pass is issue-bound
+    // and the polynomial does not pay
+    static constexpr int kPolyGroups = (D == 64) ? TKB_FWD_POLY64 : TKB_FWD_POLY128;
     static constexpr int kSmemQ = kQStages * kTile;
     static constexpr int kSmemKv = kKvSlots * kTile;
     static constexpr int kSmemBytes = kSmemQ + kSmemKv + 1024;  // + alignment slack (static SMEM precedes)
@@ -250,7 +261,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     const float2 xa = fma2(make_float2(x.v[j], x.v[j + 1]), tau2, nm2);
                     const float2 xb = fma2(make_float2(x.v[j + 2], x.v[j + 3]), tau2, nm2);
                     const float p0 = ex2_approx(xa.x), p1 = ex2_approx(xa.y);
-                    const float p2 = ex2_approx(xb.x), p3 = ex2_approx(xb.y);
+                    float p2, p3;
+                    if (((j / 4) % 4) < C::kPolyGroups) {  // part of the exponentials on the FMA pipe
+                        const float2 pb = ex2_poly2(xb);
+                        p2 = pb.x;
+                        p3 = pb.y;
+                    } else {
+                        p2 = ex2_approx(xb.x);
+                        p3 = ex2_approx(xb.y);
+                    }
                     l0 += p0;
                     l1 += p1;
                     l2 += p2;
