@@ -64,7 +64,9 @@ struct Cfg {
     static constexpr int kPolyGroups = (D == 64) ? TKB_FWD_POLY64 : TKB_FWD_POLY128;
     static constexpr int kSmemQ = kQStages * kTile;
     static constexpr int kSmemKv = kKvSlots * kTile;
-    static constexpr int kSmemBytes = kSmemQ + kSmemKv + 1024;  // + alignment slack (static SMEM precedes)
+    static constexpr int kStageBytes = 128 * 128;  // per-warpgroup O staging: one 128 x 64 atom
+    static constexpr int kSmemBytes = kSmemQ + kSmemKv + kQStages * kStageBytes + 1024;  // + alignment slack
+    static_assert(kSmemBytes + 512 <= 232448, "smem");
     static TKB_DEVICE constexpr uint32_t tmem_s(int s) { return s * 128u; }
     static TKB_DEVICE constexpr uint32_t tmem_o(int s) { return 256u + s * D; }
 };
@@ -88,24 +90,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     auto sKV = [&](int slot) { return Tile{smem + C::kSmemQ + slot * C::kTile}; };
     const gl gQ{&p.tm_q}, gK{&p.tm_k}, gV{&p.tm_v}, gO{&p.tm_o};
 
-    __shared__ mbarrier q_full[kQStages], s_full[kQStages], o_full[kQStages];
+    const st_bf<128, 64> sStage[kQStages] = {st_bf<128, 64>{smem + C::kSmemQ + C::kSmemKv},
+                                              st_bf<128, 64>{smem + C::kSmemQ + C::kSmemKv + C::kStageBytes}};
+
+    __shared__ mbarrier q_full[kQStages], q_empty[kQStages], s_full[kQStages], o_full[kQStages];
     __shared__ mbarrier p_full[kQStages][kPChunks];
     __shared__ lcsf::ring<C::kKvSlots> kv;
+    __shared__ lcsf::work_queue queue;
     __shared__ uint32_t tmem_slot;
 
     const int warp = warpid();
     const int lane = laneid();
-    const int mblk = CAUSAL ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;  // heavy causal tiles first
-    const int head = blockIdx.y;
-    const int batch = blockIdx.z;
-    const int q0 = mblk * kRowsPerCta;
     const int n = p.n;
-    int nkv = (n + kBlockN - 1) / kBlockN;
-    if (CAUSAL) nkv = min(nkv, (min(q0 + kRowsPerCta, n) - 1) / kBlockN + 1);
+    const int m_blocks = (n + kRowsPerCta - 1) / kRowsPerCta;
+    // task t -> (256-row query block, b, h): heads in L2-sized groups, inside a group the heavy
+    // (late) causal query blocks first, heads innermost; claimed dynamically (one CTA per SM)
+    struct Task {
+        int mblk, head, batch, nkv;
+    };
+    auto decode = [&](int t) {
+        const int G = p.head_group;
+        const int sec = t / (G * m_blocks);
+        const int r = t - sec * G * m_blocks;
+        const int gs = min(G, p.bh - sec * G);
+        const int mi = r / gs;
+        const int bh = sec * G + (r - mi * gs);
+        Task w;
+        w.mblk = CAUSAL ? (m_blocks - 1 - mi) : mi;
+        w.batch = bh / p.heads;
+        w.head = bh - w.batch * p.heads;
+        w.nkv = (n + kBlockN - 1) / kBlockN;
+        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, n) - 1) / kBlockN + 1);
+        return w;
+    };
 
     if (warp == kWarpLoad && lane == 0) {
+        queue.init(1 + 8);  // the MMA warp and the 8 softmax warps
         for (int s = 0; s < kQStages; ++s) {
             mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
             mbar_init(&s_full[s], 1);
             mbar_init(&o_full[s], 1);
             for (int c = 0; c < kPChunks; ++c) mbar_init(&p_full[s][c], WARPGROUP_THREADS);
@@ -128,20 +151,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         if (lane == 0) {
             const uint64_t pol_q = tma::policy_evict_first();
             const uint64_t pol_kv = tma::policy_evict_last();
-            for (int s = 0; s < kQStages; ++s) {
-                mbar_arrive_expect_tx(&q_full[s], C::kTile);
-                load_async(sQ[s], gQ, &q_full[s], q0 + s * kBlockM, head, batch, pol_q);
-            }
             lcsf::ring_state<C::kKvSlots> st;
-            for (int i = 0; i < nkv; ++i) {
-#pragma unroll
-                for (int which = 0; which < 2; ++which) {
-                    kv.wait_empty(st);
-                    mbar_arrive_expect_tx(&kv.full[st.slot], C::kTile);
-                    load_async(sKV(st.slot), which == 0 ? gK : gV, &kv.full[st.slot], i * kBlockN, head / p.group,
-                               batch, pol_kv);  // grouped-query: kv head = head / group
-                    st.advance();
+            int nt = 0;
+            int t = queue.claim(0, p.sched, p.tasks);
+            while (t >= 0) {
+                const Task w = decode(t);
+                const int q0 = w.mblk * kRowsPerCta;
+                for (int s = 0; s < kQStages; ++s) {  // Q_s is free once the last QK_s of the previous task retired
+                    mbar_wait(&q_empty[s], (nt & 1) ^ 1u);
+                    mbar_arrive_expect_tx(&q_full[s], C::kTile);
+                    load_async(sQ[s], gQ, &q_full[s], q0 + s * kBlockM, w.head, w.batch, pol_q);
                 }
+                const int t_next = queue.claim(nt + 1, p.sched, p.tasks);
+                if (t_next >= 0) {  // warm the next task's Q in L2
+                    const Task w2 = decode(t_next);
+                    for (int s = 0; s < kQStages; ++s)
+                        for (int a = 0; a < Tile::kAtoms; ++a)
+                            tma::prefetch_4d(gQ.tm, a * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.batch);
+                }
+                for (int i = 0; i < w.nkv; ++i) {
+#pragma unroll
+                    for (int which = 0; which < 2; ++which) {
+                        kv.wait_empty(st);
+                        mbar_arrive_expect_tx(&kv.full[st.slot], C::kTile);
+                        load_async(sKV(st.slot), which == 0 ? gK : gV, &kv.full[st.slot], i * kBlockN,
+                                   w.head / p.group, w.batch, pol_kv);  // grouped-query: kv head = head / group
+                        st.advance();
+                    }
+                }
+                t = t_next;
+                ++nt;
             }
         }
     } else if (warp == kWarpMma) {
@@ -160,62 +199,87 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                                          sKV(vslot), c * kPChunkCols, acc || c > 0);
             }
         };
-        mbar_wait(&q_full[0], 0);
-        mbar_wait(&q_full[1], 0);
         lcsf::ring_state<C::kKvSlots> st;
-        kv.wait_full(st);
-        tmem::fence_after();
-        qk(0, st.slot);
-        umma::commit_e(&s_full[0]);
-        qk(1, st.slot);
-        umma::commit_e(&s_full[1]);
-        umma::commit_e(&kv.empty[st.slot]);
-        st.advance();
-        for (int i = 1; i < nkv; ++i) {
+        uint32_t it = 0;  // global iteration count: p_full phases
+        for (int nt = 0;; ++nt) {
+            const int t = queue.get(nt);
+            if (lane == 0) queue.release(nt);
+            if (t < 0) break;
+            const int nkv = decode(t).nkv;
+            mbar_wait(&q_full[0], nt & 1);
+            mbar_wait(&q_full[1], nt & 1);
+            kv.wait_full(st);
+            tmem::fence_after();
+            // QK_s(next task) overwrites S_s, whose P was read by the previous task's last PV_s
+            // (issued before); the first PV_s below overwrites O_s only after the softmax drained it
+            qk(0, st.slot);
+            umma::commit_e(&s_full[0]);
+            qk(1, st.slot);
+            umma::commit_e(&s_full[1]);
+            if (nkv == 1) {
+                umma::commit_e(&q_empty[0]);
+                umma::commit_e(&q_empty[1]);
+            }
+            umma::commit_e(&kv.empty[st.slot]);
+            st.advance();
+            for (int i = 1; i < nkv; ++i, ++it) {
+                const int vslot = st.slot;
+                kv.wait_full(st);
+                st.advance();
+                const int kslot = st.slot;
+#pragma unroll
+                for (int s = 0; s < kQStages; ++s) {
+                    pv(s, vslot, i > 1, it & 1);
+                    if (s == 0) {
+                        kv.wait_full(st);
+                        tmem::fence_after();
+                    }
+                    qk(s, kslot);
+                    umma::commit_e(&s_full[s]);
+                    if (i == nkv - 1) umma::commit_e(&q_empty[s]);  // Q_s's last read: the next task's may load
+                }
+                umma::commit_e(&kv.empty[vslot]);
+                umma::commit_e(&kv.empty[kslot]);
+                st.advance();
+            }
             const int vslot = st.slot;
             kv.wait_full(st);
-            st.advance();
-            const int kslot = st.slot;
-            const uint32_t pphase = (uint32_t)((i - 1) & 1);
 #pragma unroll
             for (int s = 0; s < kQStages; ++s) {
-                pv(s, vslot, i > 1, pphase);
-                if (s == 0) {
-                    kv.wait_full(st);
-                    tmem::fence_after();
-                }
-                qk(s, kslot);
-                umma::commit_e(&s_full[s]);
+                pv(s, vslot, nkv > 1, it & 1);
+                umma::commit_e(&o_full[s]);
             }
             umma::commit_e(&kv.empty[vslot]);
-            umma::commit_e(&kv.empty[kslot]);
             st.advance();
+            ++it;
         }
-        const int vslot = st.slot;
-        kv.wait_full(st);
-        const uint32_t pphase = (uint32_t)((nkv - 1) & 1);
-#pragma unroll
-        for (int s = 0; s < kQStages; ++s) {
-            pv(s, vslot, nkv > 1, pphase);
-            umma::commit_e(&o_full[s]);
-        }
-        umma::commit_e(&kv.empty[vslot]);
     } else {
         // ----------------------------- SOFTMAX + FINISH ------------------------------------
         const int s = warp / 4;                  // query tile of this warpgroup
         const int wq = warp % 4;                 // TMEM lane quarter
         const int row_in_tile = wq * 32 + lane;  // == TMEM lane
-        const int row = q0 + s * kBlockM + row_in_tile;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
         const uint32_t tS = tbase + lane_off + C::tmem_s(s);
         const uint32_t tP = tS + 64;
         const uint32_t tO = tbase + lane_off + C::tmem_o(s);
         const float tau = p.scale_log2;
 
+        uint32_t sc = 0;  // s_full completions seen
+        for (int nt = 0;; ++nt) {
+        const int t = queue.get(nt);
+        __syncwarp();
+        if (lane == 0) queue.release(nt);
+        if (t < 0) break;
+        const Task w = decode(t);
+        const int q0 = w.mblk * kRowsPerCta;
+        const int row = q0 + s * kBlockM + row_in_tile;
+        const int nkv = w.nkv;
+        const int head = w.head, batch = w.batch;
         float m = -INFINITY;  // running max of tau * S (the value actually subtracted)
         float l = 0.f;        // running normaliser (fp32 sum of fp32 P, kernels.hpp:324)
         for (int i = 0; i < nkv; ++i) {
-            mbar_wait(&s_full[s], (uint32_t)(i & 1));
+            mbar_wait(&s_full[s], sc & 1);
+            ++sc;
             tmem::fence_after();
             rt_fl<kBlockN> x;
             load(x, tS);
@@ -296,43 +360,54 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             mbar_arrive(&p_full[s][kPChunks - 1]);
         }
 
-        // FINISH (kernels.hpp:335-342): O / l, store; plus L for the backward.
-        mbar_wait(&o_full[s], 0);
+        // FINISH (kernels.hpp:335-342): O / l -> bf16 -> this warpgroup's SMEM staging atom ->
+        // TMA store (one 64-column atom at a time); plus L for the backward
+        mbar_wait(&o_full[s], nt & 1);
         tmem::fence_after();
-        const float inv_l = 1.f / l;
         if (p.lse != nullptr && row < n)
             p.lse[(size_t)(batch * p.heads + head) * n + row] = (m + __log2f(l)) * kLn2;
-        const Tile stage = sQ[s];  // Q_s is dead: every QK(s) completed before o_full
+        const bool leader = (wq == 0 && lane == 0);
+#pragma unroll 1
+        for (int a = 0; a < Tile::kAtoms; ++a) {
+            rt_fl<32> o0, o1;
+            load(o0, tO + a * 64);
+            load(o1, tO + a * 64 + 32);
+            load_wait(o0);
+            load_wait(o1);
+            if (a == Tile::kAtoms - 1) tmem::fence_before();  // O_s drained: the next task's PV may overwrite it
+            div_row(o0, l);  // tiles.hpp:276-281
+            div_row(o1, l);
+            rt_bf<32> b0, b1;
+            copy(b0, o0);
+            copy(b1, o1);
+            if (leader) tma::wait_group_read<0>();  // the staging atom is free again
+            named_sync(1 + s, WARPGROUP_THREADS);
 #pragma unroll
-        for (int c = 0; c < D; c += 32) {
-            rt_fl<32> o;
-            load(o, tO + c);
-            load_wait(o);
-            div_row(o, l);  // == * inv_l (tiles.hpp:276-281)
-            (void)inv_l;
-            rt_bf<32> ob;
-            copy(ob, o);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                sts_v4(smem_u32(stage.chunk(row_in_tile, c / 8 + q)),
-                       make_uint4(ob.v[4 * q], ob.v[4 * q + 1], ob.v[4 * q + 2], ob.v[4 * q + 3]));
+            for (int q = 0; q < 4; ++q) {
+                sts_v4(smem_u32(sStage[s].chunk(row_in_tile, q)),
+                       make_uint4(b0.v[4 * q], b0.v[4 * q + 1], b0.v[4 * q + 2], b0.v[4 * q + 3]));
+                sts_v4(smem_u32(sStage[s].chunk(row_in_tile, 4 + q)),
+                       make_uint4(b1.v[4 * q], b1.v[4 * q + 1], b1.v[4 * q + 2], b1.v[4 * q + 3]));
+            }
+            tma::fence_async_smem();
+            named_sync(1 + s, WARPGROUP_THREADS);
+            if (leader) {
+                tma::store_4d(gO.tm, sStage[s].ptr, a * 64, q0 + s * kBlockM, head, batch);
+                tma::commit_group();
+            }
         }
-        tma::fence_async_smem();
-        named_sync(1 + s, WARPGROUP_THREADS);
-        if (wq == 0 && lane == 0) {
-            store_async(gO, stage, q0 + s * kBlockM, head, batch);
-            tma::commit_group();
-            tma::wait_group_read<0>();
-        }
+        }  // task loop
+        if (wq == 0 && lane == 0) tma::wait_group<0>();
     }
 
     tmem::fence_before();
     __syncthreads();
     if (warp == kWarpMma) tmem::dealloc<512>(tbase);
+    if (threadIdx.x == 0) lcsf::queue_exit(p.sched);
 }
 
 template <int D, bool CAUSAL>
-int launch(const FwdParams& p, int batches, cudaStream_t stream) {
+int launch(const FwdParams& p, int num_sms, cudaStream_t stream) {
     using C = Cfg<D>;
     auto kern = attn_fwd_kernel<D, CAUSAL>;
     static bool configured = false;  // per instantiation; attribute setting is idempotent
@@ -341,16 +416,23 @@ int launch(const FwdParams& p, int batches, cudaStream_t stream) {
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
-    dim3 grid((p.n + kRowsPerCta - 1) / kRowsPerCta, p.heads, batches);
-    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(p);
+    kern<<<p.tasks < num_sms ? p.tasks : num_sms, kThreads, C::kSmemBytes, stream>>>(p);
     return (int)cudaGetLastError();
 }
 
 }  // namespace fwd
 
-int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int /*num_sms*/, cudaStream_t stream) {
-    if (head_dim == 128) return causal ? fwd::launch<128, true>(p, batches, stream) : fwd::launch<128, false>(p, batches, stream);
-    return causal ? fwd::launch<64, true>(p, batches, stream) : fwd::launch<64, false>(p, batches, stream);
+// Fills the persistent task fields of p and launches one CTA per SM (at most one per task).
+int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream) {
+    p.bh = batches * p.heads;
+    p.m_blocks = (p.n + kRowsPerCta - 1) / kRowsPerCta;
+    p.tasks = p.bh * p.m_blocks;
+    const long long kv_bytes = 4ll * p.n * head_dim / p.group;  // K / V of one query head's kv head
+    long long g = (48ll << 20) / (kv_bytes > 0 ? kv_bytes : 1);  // heads whose K / V fit ~48 MB of L2
+    p.head_group = (int)(g < 1 ? 1 : (g > p.bh ? p.bh : g));
+    if (head_dim == 128)
+        return causal ? fwd::launch<128, true>(p, num_sms, stream) : fwd::launch<128, false>(p, num_sms, stream);
+    return causal ? fwd::launch<64, true>(p, num_sms, stream) : fwd::launch<64, false>(p, num_sms, stream);
 }
 
 }  // namespace tkb
