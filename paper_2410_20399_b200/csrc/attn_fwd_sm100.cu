@@ -123,6 +123,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, n) - 1) / kBlockN + 1);
         return w;
     };
+    // kv blocks query tile s of a task visits (causal: tile 0 skips the block only tile 1 sees)
+    auto tile_blocks = [&](const Task& w, int s) {
+        if (!CAUSAL) return w.nkv;
+        return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, n) - 1) / kBlockN + 1);
+    };
 
     if (warp == kWarpLoad && lane == 0) {
         queue.init(1 + 8);  // the MMA warp and the 8 softmax warps
@@ -200,43 +205,51 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             }
         };
         lcsf::ring_state<C::kKvSlots> st;
-        uint32_t it = 0;  // global iteration count: p_full phases
+        uint32_t it[kQStages] = {0, 0};  // PVs issued per tile: p_full phases
         for (int nt = 0;; ++nt) {
             const int t = queue.get(nt);
             if (lane == 0) queue.release(nt);
             if (t < 0) break;
-            const int nkv = decode(t).nkv;
+            const Task w = decode(t);
+            const int nkv = w.nkv;
+            const int nk[kQStages] = {tile_blocks(w, 0), tile_blocks(w, 1)};  // causal: tile 0 may stop one early
             mbar_wait(&q_full[0], nt & 1);
             mbar_wait(&q_full[1], nt & 1);
             kv.wait_full(st);
             tmem::fence_after();
             // QK_s(next task) overwrites S_s, whose P was read by the previous task's last PV_s
             // (issued before); the first PV_s below overwrites O_s only after the softmax drained it
-            qk(0, st.slot);
-            umma::commit_e(&s_full[0]);
-            qk(1, st.slot);
-            umma::commit_e(&s_full[1]);
-            if (nkv == 1) {
-                umma::commit_e(&q_empty[0]);
-                umma::commit_e(&q_empty[1]);
+#pragma unroll
+            for (int s = 0; s < kQStages; ++s) {
+                qk(s, st.slot);
+                umma::commit_e(&s_full[s]);
+                if (nk[s] == 1) umma::commit_e(&q_empty[s]);
             }
             umma::commit_e(&kv.empty[st.slot]);
             st.advance();
-            for (int i = 1; i < nkv; ++i, ++it) {
+            for (int i = 1; i < nkv; ++i) {
                 const int vslot = st.slot;
                 kv.wait_full(st);
                 st.advance();
                 const int kslot = st.slot;
+                bool k_ready = false;
 #pragma unroll
                 for (int s = 0; s < kQStages; ++s) {
-                    pv(s, vslot, i > 1, it & 1);
-                    if (s == 0) {
+                    if (i > nk[s]) continue;  // tile s is done
+                    pv(s, vslot, i > 1, it[s] & 1);
+                    ++it[s];
+                    if (i == nk[s]) {  // that was tile s's last block
+                        umma::commit_e(&o_full[s]);
+                        continue;
+                    }
+                    if (!k_ready) {
                         kv.wait_full(st);
                         tmem::fence_after();
+                        k_ready = true;
                     }
                     qk(s, kslot);
                     umma::commit_e(&s_full[s]);
-                    if (i == nkv - 1) umma::commit_e(&q_empty[s]);  // Q_s's last read: the next task's may load
+                    if (i == nk[s] - 1) umma::commit_e(&q_empty[s]);  // Q_s's last read: the next task's may load
                 }
                 umma::commit_e(&kv.empty[vslot]);
                 umma::commit_e(&kv.empty[kslot]);
@@ -246,12 +259,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             kv.wait_full(st);
 #pragma unroll
             for (int s = 0; s < kQStages; ++s) {
-                pv(s, vslot, nkv > 1, it & 1);
+                if (nk[s] != nkv) continue;
+                pv(s, vslot, nkv > 1, it[s] & 1);
+                ++it[s];
                 umma::commit_e(&o_full[s]);
             }
             umma::commit_e(&kv.empty[vslot]);
             st.advance();
-            ++it;
         }
     } else {
         // ----------------------------- SOFTMAX + FINISH ------------------------------------
@@ -273,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const Task w = decode(t);
         const int q0 = w.mblk * kRowsPerCta;
         const int row = q0 + s * kBlockM + row_in_tile;
-        const int nkv = w.nkv;
+        const int nkv = tile_blocks(w, s);
         const int head = w.head, batch = w.batch;
         float m = -INFINITY;  // running max of tau * S (the value actually subtracted)
         float l = 0.f;        // running normaliser (fp32 sum of fp32 P, kernels.hpp:324)
