@@ -121,9 +121,9 @@ TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, i
         tmem::st_32x32b_x8(tdst + g * 8, v);
 }
 
-// TMEM fp32 [lane r][D] -> bf16 -> SW128 smem tile: row r, columns [g D/4, (g+1) D/4)
+// TMEM fp32 [lane r][D] (x mul) -> bf16 -> SW128 smem tile: row r, columns [g D/4, (g+1) D/4)
 template <int D>
-TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int g) {
+TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int g, float mul = 1.f) {
     constexpr int kCols = D / 4;
     const int col = g * kCols;
     uint32_t v[kCols];
@@ -136,10 +136,10 @@ TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int
         const int gc = col / 8 + q;  // 16-byte chunk index within the row
         const int atom = gc / 8, ch = gc % 8;
         uint4 u;
-        u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
-        u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
-        u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
-        u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+        u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * mul, __uint_as_float(v[8 * q + 1]) * mul);
+        u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * mul, __uint_as_float(v[8 * q + 3]) * mul);
+        u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * mul, __uint_as_float(v[8 * q + 5]) * mul);
+        u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * mul, __uint_as_float(v[8 * q + 7]) * mul);
         *reinterpret_cast<uint4*>(stage + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
     }
 }
@@ -157,14 +157,20 @@ TKB_DEVICE long long* trace_slot(const BwdParams& p, int lin, int kernel) {
             tr[((role) * kTraceIters + (t)) * kTraceEvents + (ev)] = clock64() - t_start; \
     } while (0)
 
+TKB_DEVICE float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
 // P chunk: p = exp2(tau * s + nlse) for 32 columns; a quarter of the exponentials run as
 // a polynomial on the FMA pipe (MUFU relief). nlse4 holds -lse2 per column (dkdv) or the
 // row's -lse2 broadcast (dq, ROWCONST).
 template <bool ROWCONST>
-TKB_DEVICE void exp_chunk(float* pf, float tau, const float4* nlse4, float nlse_r) {
+TKB_DEVICE void exp_chunk(float* pf, float tau, uint32_t nlse4, float nlse_r) {
 #pragma unroll
     for (int c = 0; c < 32; c += 4) {
-        const float4 l4 = ROWCONST ? make_float4(nlse_r, nlse_r, nlse_r, nlse_r) : nlse4[c / 4];
+        const float4 l4 = ROWCONST ? make_float4(nlse_r, nlse_r, nlse_r, nlse_r) : lds_f4(nlse4 + 4 * c);
         const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(l4.x, l4.y));
         const float2 x23 = fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(l4.z, l4.w));
         pf[c] = ex2_approx(x01.x);
@@ -360,13 +366,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
         const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
         const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
-        const float scale = p.scale;
         for (int t = 0; t < T; ++t) {
-            const int i = qblock(t);
+            const int i = qblock(t);  // (t / T1 is 0 unless grouped-query: one division per step)
             const int s = t % S;
             const bool diag = CAUSAL && (i == j);
-            const float4* nlse4 = reinterpret_cast<const float4*>(sLse + s * 128 + 32 * g);
-            const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + s * 128 + 32 * g);
+            const uint32_t nlse4 = smem_u32(sLse + s * 128 + 32 * g);  // shared-space addresses
+            const uint32_t dlt4 = smem_u32(sDelta + s * 128 + 32 * g);
             // P^T = exp2(tau S^T - lse2)
             mbar_wait(&q_full[s], (t / S) & 1);
             mbar_wait(&s_full, t & 1);
@@ -395,13 +400,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
             tmem::ldw_32x32b_x32(tDp, dpv);
 #pragma unroll
             for (int c = 0; c < 32; c += 4) {
-                const float4 d4 = dlt4[c / 4];
+                const float4 d4 = lds_f4(dlt4 + 4 * c);
                 const float2 g01 =
                     sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(d4.x, d4.y));
                 const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
                                         make_float2(d4.z, d4.w));
-                const float2 s01 = mul2(mul2(make_float2(pf[c], pf[c + 1]), g01), make_float2(scale, scale));
-                const float2 s23 = mul2(mul2(make_float2(pf[c + 2], pf[c + 3]), g23), make_float2(scale, scale));
+                // dS^T / scale: the softmax scale is applied to dK once, in the finish stage
+                const float2 s01 = mul2(make_float2(pf[c], pf[c + 1]), g01);
+                const float2 s23 = mul2(make_float2(pf[c + 2], pf[c + 3]), g23);
                 pk[c / 2] = pack_bf16x2(s01.x, s01.y);
                 pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
             }
@@ -417,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
         uint8_t* stage_v = sQ;
         uint8_t* stage_k = sDo;
         tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dv(), stage_v, r, g);
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dk(), stage_k, r, g);
+        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dk(), stage_k, r, g, p.scale);  // dK = scale dS^T Q
         tma::fence_async_smem();
         named_sync(kBarCompute, kComputeThreads);
         if (threadIdx.x == 0) {
@@ -643,7 +649,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
         const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
-        const float scale = p.scale;
         uint32_t it = 0;
         int n = 0;
         // Q, dO of task n: SMEM (TMA, swizzled) -> TMEM A operands, once the previous task's last
@@ -678,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
                 tmem::fence_before();
                 mbar_arrive(&s_free);
-                exp_chunk<true>(pf, tau, nullptr, nlse_r);
+                exp_chunk<true>(pf, tau, 0u, nlse_r);
                 // visible keys: kv < n, and causal kv <= row
                 const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 32 * g;  // last visible column
                 if (lim < 31) {  // diagonal / ragged tail block only
@@ -695,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 for (int c = 0; c < 32; c += 2) {
                     const float2 gg = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
                                            make_float2(dlt_r, dlt_r));
-                    const float2 d = mul2(mul2(make_float2(pf[c], pf[c + 1]), gg), make_float2(scale, scale));
+                    const float2 d = mul2(make_float2(pf[c], pf[c + 1]), gg);  // dS / scale (scale in the finish)
                     pk[c / 2] = pack_bf16x2(d.x, d.y);
                 }
                 tmem::st_32x32b_x16(tDp, pk);  // inside the 32 dP columns this thread has read
@@ -712,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             tmem::fence_after();
             if (threadIdx.x == 0) tma::wait_group_read<0>();  // the previous task's store has read the staging
             named_sync(kBarCompute, kComputeThreads);
-            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sStage, r, g);
+            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sStage, r, g, p.scale);  // dQ = scale dS K
             tma::fence_async_smem();
             named_sync(kBarCompute, kComputeThreads);
             if (threadIdx.x == 0) {
