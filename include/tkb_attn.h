@@ -140,6 +140,12 @@ TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots);
  * bit 2 dQ kernel; default 7). Results are only complete with 7. Not thread-safe. */
 TKB_API int tkb_debug_set_bwd_phases(int mask);
 
+/* Backward dK/dV kernel selection at D = 128 (process-wide; not thread-safe): 0 = one CTA
+ * per kv block (default), 1 = CTA pairs (clusters of 2, tcgen05 cta_group::2, M = 256
+ * MMAs over two kv blocks; half the per-SM operand traffic). Same results, bit for bit
+ * within each variant's own summation order. */
+TKB_API int tkb_set_bwd_pairs(int on);
+
 /* Number of kernels the last successful fwd / bwd call on this thread launched. */
 TKB_API int tkb_last_launch_count(void);
 

@@ -96,6 +96,7 @@ _SIGS = {
     "tkb_last_launch_count": (ctypes.c_int, []),
     "tkb_debug_set_trace": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int]),
     "tkb_debug_set_bwd_phases": (ctypes.c_int, [ctypes.c_int]),
+    "tkb_set_bwd_pairs": (ctypes.c_int, [ctypes.c_int]),
     "tkb_last_error": (ctypes.c_char_p, []),
     "tkb_abi_version": (ctypes.c_int, []),
 }
@@ -356,6 +357,12 @@ def debug_set_trace(buf=None, every=1, slots=0):
 def debug_set_bwd_phases(mask=7):
     """Profiling only: run a subset of the backward stages (1 prep, 2 dK/dV, 4 dQ)."""
     lib().tkb_debug_set_bwd_phases(int(mask))
+
+
+def set_bwd_pairs(on=True):
+    """D = 128 backward: run dK/dV on CTA pairs (cta_group::2 clusters) instead of one CTA
+    per kv block. Process-wide switch; results match the oracle either way."""
+    lib().tkb_set_bwd_pairs(1 if on else 0)
 
 
 def last_launch_count():

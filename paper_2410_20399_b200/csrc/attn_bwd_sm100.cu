@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include "attn_common.cuh"
+#include "tkb/cluster.cuh"
 #include "tkb/lcsf.cuh"
 #include "tkb/tcgen05.cuh"
 #include "tkb/tma.cuh"
@@ -441,6 +442,335 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     if (warp == kWarpMma) tmem::dealloc<512>(tbase);
 }
 
+// ================================================================== bwd_dkdv on CTA pairs (D = 128)
+// The single-CTA bwd_dkdv moves 256 KB through each SM's shared-memory port per step (the
+// SS GEMMs S^T / dP^T read 8 KB per MMA, the TS GEMMs 4 KB, TMA writes 64 KB of Q / dO) —
+// more than the 128 B/clk port delivers in the 2048 clk the 32 MMAs need. A cluster of two
+// CTAs (kv blocks 2p, 2p + 1) runs every GEMM as one M = 256 pair MMA over their 256 kv rows
+// (cluster.cuh): B is split between the CTAs, so per SM an S^T / dP^T MMA reads 4 + 2 KB and
+// a dV / dK MMA 2 KB, and the step costs 192 KB of SMEM traffic. The two CTAs stream the
+// same Q / dO blocks; each holds
+//   Q_s  its 64-query half of the block, all D   (B of S^T  = K Q^T, N = queries)
+//   Q_t  its 64-column half of D, all 128 queries (B of dK += dS^T Q, N = D)
+// (and dO likewise). Causal: the pair visits q blocks >= 2p; block 2p is fully masked for
+// the odd CTA (P = 0 there).
+// TMEM per CTA as bwd_dkdv (kvP order): S^T | dV | dP^T (P^T / dS^T packed into it) | dK.
+struct CfgKV2 {
+    static constexpr int D = 128;
+    static constexpr int kTile = 128 * D * 2;   // K / V: 32 KB
+    static constexpr int kHalf = kTile / 2;     // Q_s, Q_t, dO_s, dO_t: 16 KB
+    static constexpr int kStages = 2;
+    static constexpr int kOffK = 0;
+    static constexpr int kOffV = kOffK + kTile;
+    static constexpr int kOffQ = kOffV + kTile;               // [S] x (Q_s | Q_t)
+    static constexpr int kOffDo = kOffQ + kStages * kTile;    // [S] x (dO_s | dO_t)
+    static constexpr int kOffLse = kOffDo + kStages * kTile;  // [S] x 128 fp32
+    static constexpr int kOffDelta = kOffLse + kStages * 512;
+    static constexpr int kOffBar = kOffDelta + kStages * 512;
+    static constexpr int kSmemBytes = kOffBar + 512 + 1024;
+    static_assert(kSmemBytes <= 232448, "smem");
+    static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dv() { return 128u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 256u; }
+    static __device__ __forceinline__ constexpr uint32_t tmem_dk() { return 384u; }
+};
+
+// X^T (+)= A[128 own rows][128] B_half[64 rows][128]^T over the pair: A atoms 16 KB apart,
+// B (a 64-row half tile) atoms 8 KB apart; both K-major
+TKB_DEVICE void mm2_abt(uint32_t dst, uint32_t a, uint32_t b, uint32_t idesc) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t offa = (k / 4) * kAtomBytes + (k % 4) * 32;
+        const uint32_t offb = (k / 4) * (kAtomBytes / 2) + (k % 4) * 32;
+        umma::mma2_ss_e(dst, umma::desc_lo(a + offa, 16), kDescHi, umma::desc_lo(b + offb, 16), kDescHi, idesc, k > 0);
+    }
+}
+
+template <bool CAUSAL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    attn_bwd_dkdv2_kernel(const __grid_constant__ BwdParams p) {
+    using C = CfgKV2;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem + C::kOffK;
+    uint8_t* sV = smem + C::kOffV;
+    uint8_t* sQ = smem + C::kOffQ;
+    uint8_t* sDo = smem + C::kOffDo;
+    float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
+    float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
+    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
+    mbarrier& kv_full = bars[0];     // leader: K / V of both CTAs
+    mbarrier& s_full = bars[1];      // both (multicast commit)
+    mbarrier& s_free = bars[2];      // leader: S^T read out in both CTAs
+    mbarrier& dp_full = bars[3];     // both
+    mbarrier& dkv_full = bars[5];    // both
+    // operand rings, full on the leader (both CTAs' TMA), empty on both (multicast commit):
+    // the S^T / dP^T operands (Q_s, dO_s) are released as soon as that GEMM retires, a step
+    // before the dK / dV operands (Q_t, dO_t), so the next S^T's Q is loaded early
+    mbarrier* qs_full = bars + 8;     // [S]
+    mbarrier* qs_empty = bars + 10;   // [S]
+    mbarrier* qt_full = bars + 12;    // [S]
+    mbarrier* qt_empty = bars + 14;   // [S]
+    mbarrier* dos_full = bars + 16;   // [S]
+    mbarrier* dos_empty = bars + 18;  // [S]
+    mbarrier* dot_full = bars + 20;   // [S]
+    mbarrier* dot_empty = bars + 22;  // [S]
+    mbarrier* aux_full = bars + 24;   // [S] own: lse2 / delta of the q block
+    mbarrier* p_full = bars + 32;    // [kGroups] leader: P^T chunks of both CTAs
+    mbarrier* ds_full = bars + 36;   // [kGroups] leader: dS^T chunks
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
+
+    const int warp = warpid();
+    const int lane = laneid();
+    const uint32_t rank = cluster::ctarank();
+    const bool leader = rank == 0;
+    const int j = blockIdx.x;  // kv block; the pair is (j0, j0 + 1)
+    const int j0 = j & ~1;
+    const int head = blockIdx.y;
+    const int batch = blockIdx.z;
+    const int kv0 = j * 128;
+    const int nq = p.n_pad / 128;
+    const int T1 = CAUSAL ? (nq - j0) : nq;
+    const int T = T1 * p.group;
+    auto qblock = [&](int t) { return CAUSAL ? (j0 + t % T1) : t % T1; };
+    auto qhead = [&](int t) { return head * p.group + t / T1; };
+    long long* tr = trace_slot(p, (batch * gridDim.y + head) * gridDim.x + j, 0);
+    const long long t_start = clock64();
+
+    if (warp == kWarpLoad && lane == 0) {
+        mbar_init(&kv_full, 1);
+        mbar_init(&s_full, 1);
+        mbar_init(&s_free, 2 * 16);  // one lane per compute warp of both CTAs
+        mbar_init(&dp_full, 1);
+        mbar_init(&dkv_full, 1);
+        for (int g = 0; g < kGroups; ++g) {
+            mbar_init(&p_full[g], 2 * 4);  // the 4 warps of one column group, both CTAs
+            mbar_init(&ds_full[g], 2 * 4);
+        }
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&qs_full[s], 1);
+            mbar_init(&qs_empty[s], 1);
+            mbar_init(&qt_full[s], 1);
+            mbar_init(&qt_empty[s], 1);
+            mbar_init(&dos_full[s], 1);
+            mbar_init(&dos_empty[s], 1);
+            mbar_init(&dot_full[s], 1);
+            mbar_init(&dot_empty[s], 1);
+            mbar_init(&aux_full[s], 1);
+        }
+        fence_barrier_init();
+        tma::prefetch_desc(&p.tm_q);
+        tma::prefetch_desc(&p.tm_q64);
+        tma::prefetch_desc(&p.tm_k);
+        tma::prefetch_desc(&p.tm_v);
+        tma::prefetch_desc(&p.tm_do);
+        tma::prefetch_desc(&p.tm_do64);
+    }
+    if (warp == kWarpMma) tmem::alloc2<512>(&tmem_slot);
+    tmem::fence_before();
+    cluster::sync();  // barriers of both CTAs initialised before any remote arrive / complete_tx
+    tmem::fence_after();
+    const uint32_t tbase = tmem_slot;
+
+    if (warp == kWarpLoad) {
+        if (lane == 0) {
+            // ------------------------------------------------------------- LOAD (both CTAs)
+            const uint64_t pol_stream = tma::policy_evict_first();
+            const uint64_t pol_keep = tma::policy_evict_last();
+            const uint32_t kv_bar = cluster::map(&kv_full, 0);
+            if (leader) mbar_arrive_expect_tx(&kv_full, 4 * C::kTile);
+            for (int a = 0; a < 2; ++a) {
+                cluster::load_4d(sK + a * kAtomBytes, &p.tm_k, kv_bar, a * 64, kv0, head, batch, pol_stream);
+                cluster::load_4d(sV + a * kAtomBytes, &p.tm_v, kv_bar, a * 64, kv0, head, batch, pol_stream);
+            }
+            const int r64 = 64 * (int)rank;
+            // one half tile (16 KB) into this CTA, counted on the leader's barrier
+            auto half = [&](mbarrier* full, mbarrier* empty, uint32_t ph, uint8_t* dst, const CUtensorMap* rows64,
+                            const CUtensorMap* rows128, bool qhalf, int i, int hq) {
+                mbar_wait(empty, ph);
+                const uint32_t bar = cluster::map(full, 0);
+                if (leader) mbar_arrive_expect_tx(full, 2 * C::kHalf);
+                if (qhalf) {  // query rows [64 rank, +64) of the block, all D (two 8 KB atoms)
+                    for (int a = 0; a < 2; ++a)
+                        cluster::load_4d(dst + a * (kAtomBytes / 2), rows64, bar, a * 64, i * 128 + r64, hq, batch,
+                                         pol_keep);
+                } else {  // D columns [64 rank, +64), all 128 queries (one atom)
+                    cluster::load_4d(dst, rows128, bar, r64, i * 128, hq, batch, pol_keep);
+                }
+            };
+            for (int t = 0; t < T; ++t) {
+                const int i = qblock(t), s = t % S, hq = qhead(t);
+                const size_t bhq = (size_t)batch * p.heads + hq;
+                const uint32_t ph = ((t / S) & 1) ^ 1;
+                uint8_t* dos = sDo + s * C::kTile;
+                uint8_t* qs = sQ + s * C::kTile;
+                half(&qs_full[s], &qs_empty[s], ph, qs, &p.tm_q64, &p.tm_q, true, i, hq);
+                half(&dos_full[s], &dos_empty[s], ph, dos, &p.tm_do64, &p.tm_do, true, i, hq);
+                half(&qt_full[s], &qt_empty[s], ph, qs + C::kHalf, &p.tm_q64, &p.tm_q, false, i, hq);
+                mbar_arrive_expect_tx(&aux_full[s], 1024);  // slot freed with Q_t (dK_{t-S})
+                tma::load_1d(sLse + s * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &aux_full[s]);
+                tma::load_1d(sDelta + s * 128, p.delta + bhq * p.n_pad + i * 128, 512, &aux_full[s]);
+                half(&dot_full[s], &dot_empty[s], ph, dos + C::kHalf, &p.tm_do64, &p.tm_do, false, i, hq);
+            }
+        }
+    } else if (warp == kWarpMma) {
+        if (leader) {
+            // ------------------------------------------------------------- MMA (leader, converged)
+            constexpr uint32_t id_s = umma::idesc_bf16_m256<128, false, false>();  // S^T, dP^T
+            constexpr uint32_t id_kv = umma::idesc_bf16_m256<128, false, true>();  // dV, dK
+            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+            auto qs = [&](int t) { return smem_u32(sQ + (t % S) * C::kTile); };
+            auto dos = [&](int t) { return smem_u32(sDo + (t % S) * C::kTile); };
+            // acc (+)= A[TMEM packed chunks] B_t[128 query rows][64 D cols] (MN-major, one atom)
+            auto mma_groups = [&](uint32_t dst, uint32_t a_tmem, uint32_t b, bool acc, mbarrier* ready,
+                                  uint32_t ph) {
+#pragma unroll
+                for (int g = 0; g < kGroups; ++g) {
+                    cluster::wait(&ready[g], ph);
+                    tmem::fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const int k = 2 * g + kk;
+                        umma::mma2_ts_e(dst, a_tmem + 32 * g + 8 * kk, umma::desc_lo(b + k * 2048, kAtomBytes),
+                                        kDescHi, id_kv, acc || g > 0 || kk > 0);
+                    }
+                }
+            };
+            auto issue_s = [&](int x) {  // S^T_x = K Q_x^T
+                cluster::wait(&qs_full[x % S], (x / S) & 1);
+                tmem::fence_after();
+                mm2_abt(tbase + C::tmem_s(), aK, qs(x), id_s);
+                umma::commit2_e(&s_full);
+                umma::commit2_e(&qs_empty[x % S]);
+            };
+            auto issue_dp = [&](int x) {  // dP^T_x = V dO_x^T
+                cluster::wait(&dos_full[x % S], (x / S) & 1);
+                tmem::fence_after();
+                mm2_abt(tbase + C::tmem_dp(), aV, dos(x), id_s);
+                umma::commit2_e(&dp_full);
+                umma::commit2_e(&dos_empty[x % S]);
+            };
+            cluster::wait(&kv_full, 0);
+            issue_s(0);
+            issue_dp(0);
+            for (int t = 0; t < T; ++t) {
+                const uint32_t ph = t & 1;
+                TKB_TR(0, t, 0);
+                if (t + 1 < T) {  // S_{t+1} once both CTAs read S_t out
+                    cluster::wait(&s_free, ph);
+                    issue_s(t + 1);
+                }
+                // dV += P_t^T dO_t   (P^T in packed columns [32g + 16, 32g + 32) of the dP region)
+                TKB_TR(0, t, 1);
+                cluster::wait(&dot_full[t % S], (t / S) & 1);
+                mma_groups(tbase + C::tmem_dv(), tbase + C::tmem_dp() + 16, dos(t) + C::kHalf, t > 0, p_full, ph);
+                umma::commit2_e(&dot_empty[t % S]);
+                // dK += dS_t^T Q_t   (dS^T in packed columns [32g, 32g + 16))
+                TKB_TR(0, t, 2);
+                cluster::wait(&qt_full[t % S], (t / S) & 1);
+                mma_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qs(t) + C::kHalf, t > 0, ds_full, ph);
+                umma::commit2_e(&qt_empty[t % S]);
+                TKB_TR(0, t, 3);
+                if (t + 1 < T) issue_dp(t + 1);  // overwrites P_t / dS_t, read by dV_t / dK_t issued before
+                TKB_TR(0, t, 4);
+            }
+            umma::commit2_e(&dkv_full);
+        }
+    } else {
+        // ----------------------------------------------------------------- COMPUTE (both CTAs)
+        const int wq = warp & 3;
+        const int g = warp >> 2;       // q group: columns [32g, 32g+32)
+        const int r = wq * 32 + lane;  // kv row == TMEM lane
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
+        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
+        const float tau = p.scale_log2;
+        const uint32_t s_free_l = cluster::map(&s_free, 0);
+        const uint32_t p_full_l = cluster::map(&p_full[g], 0);
+        const uint32_t ds_full_l = cluster::map(&ds_full[g], 0);
+        // all lanes' TMEM accesses retired, then one lane arrives on the leader's barrier
+        auto warp_arrive = [&](uint32_t bar) {
+            tmem::fence_before();
+            __syncwarp();
+            if (lane == 0) cluster::arrive_remote(bar);
+        };
+        for (int t = 0; t < T; ++t) {
+            const int i = qblock(t);
+            const int s = t % S;
+            // key kv0 + r visible to query 128 i + 32 g + c iff c >= lim
+            const int lim = kv0 + r - i * 128 - 32 * g;
+            const bool diag = CAUSAL && (i * 128 < kv0 + 128);
+            const uint32_t nlse4 = smem_u32(sLse + s * 128 + 32 * g);
+            const uint32_t dlt4 = smem_u32(sDelta + s * 128 + 32 * g);
+            mbar_wait(&aux_full[s], (t / S) & 1);
+            cluster::wait(&s_full, t & 1);
+            if (threadIdx.x == 0) TKB_TR(1, t, 0);
+            tmem::fence_after();
+            float pf[32];
+            tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
+            warp_arrive(s_free_l);  // S_{t+1} may now overwrite S_t
+            exp_chunk<false>(pf, tau, nlse4, 0.f);
+            if (diag) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) pf[c] = (c < lim) ? 0.f : pf[c];
+            }
+            if (threadIdx.x == 0) TKB_TR(1, t, 1);
+            cluster::wait(&dp_full, t & 1);
+            if (threadIdx.x == 0) TKB_TR(1, t, 2);
+            tmem::fence_after();
+            uint32_t dpv[32];
+            tmem::ldw_32x32b_x32(tDp, dpv);
+            uint32_t pk[16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int c = 0; c < 16; c += 2) pk[8 * h + c / 2] = pack_bf16x2(pf[16 * h + c], pf[16 * h + c + 1]);
+                tmem::st_32x32b_x8(tDp + 16 + 8 * h, pk + 8 * h);
+            }
+            tmem::wait_st();
+            warp_arrive(p_full_l);
+            // dS^T = P^T o (dP^T - Delta)   (the softmax scale is applied to dK at the finish)
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+                const float4 d4 = lds_f4(dlt4 + 4 * c);
+                const float2 g01 =
+                    sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(d4.x, d4.y));
+                const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
+                                        make_float2(d4.z, d4.w));
+                const float2 s01 = mul2(make_float2(pf[c], pf[c + 1]), g01);
+                const float2 s23 = mul2(make_float2(pf[c + 2], pf[c + 3]), g23);
+                pk[c / 2] = pack_bf16x2(s01.x, s01.y);
+                pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
+            }
+            tmem::st_32x32b_x16(tDp, pk);
+            tmem::wait_st();
+            warp_arrive(ds_full_l);
+            if (threadIdx.x == 0) TKB_TR(1, t, 3);
+        }
+        // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q and dO rings are free) -> TMA store
+        cluster::wait(&dkv_full, 0);
+        tmem::fence_after();
+        tmem_rows_to_smem_bf16<128>(tbase + lane_off + C::tmem_dv(), sQ, r, g);
+        tmem_rows_to_smem_bf16<128>(tbase + lane_off + C::tmem_dk(), sDo, r, g, p.scale);  // dK = scale dS^T Q
+        tma::fence_async_smem();
+        named_sync(kBarCompute, kComputeThreads);
+        if (threadIdx.x == 0) {
+            for (int a = 0; a < 2; ++a) {
+                tma::store_4d(&p.tm_dv, sQ + a * kAtomBytes, a * 64, kv0, head, batch);
+                tma::store_4d(&p.tm_dk, sDo + a * kAtomBytes, a * 64, kv0, head, batch);
+            }
+            tma::commit_group();
+            tma::wait_group_read<0>();
+            TKB_TR(1, kTraceIters - 1, 7);  // CTA finish
+        }
+    }
+
+    tmem::fence_before();
+    cluster::sync();  // the pair's MMAs / remote arrives are all done before TMEM goes away
+    if (warp == kWarpMma) tmem::dealloc2<512>(tbase);
+}
+
 // ================================================================== bwd_dq (Q-stationary, persistent)
 // One CTA per SM walks query-block tasks (b, h, i) — heads in L2-sized groups, heavy causal
 // blocks first — with every ring continuing across tasks: the next task's Q / dO are
@@ -788,13 +1118,19 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
     if (!configured) {
         int e = set_smem(attn_bwd_dkdv_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
         if (!e) e = set_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes);
+        if (!e && D == 128) e = set_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes);
         if (e) return e;
         configured = true;
     }
     dim3 grid(p.n_pad / 128, p.heads, batches);                 // dQ: one CTA per query block
     dim3 grid_kv(p.n_pad / 128, p.heads / p.group, batches);    // dK/dV: one CTA per kv block
     if (phases & 2) {
-        attn_bwd_dkdv_kernel<D, CAUSAL><<<grid_kv, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+        if (D == 128 && p.pairs) {  // CTA pairs: kv blocks rounded up to an even count
+            dim3 grid2((p.n_pad / 128 + 1) & ~1, p.heads / p.group, batches);
+            attn_bwd_dkdv2_kernel<CAUSAL><<<grid2, kThreads, CfgKV2::kSmemBytes, stream>>>(p);
+        } else {
+            attn_bwd_dkdv_kernel<D, CAUSAL><<<grid_kv, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+        }
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;

@@ -34,6 +34,7 @@ struct FwdParams {
 struct BwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_do;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128 (loads)
     CUtensorMap tm_dq, tm_dk, tm_dv;      // same layout (stores)
+    CUtensorMap tm_q64, tm_do64;          // Q / dO with a {64, 64, 1, 1} box (CTA-pair query halves)
     const float* lse2;                    // [B*H, Npad] -L * log2(e); -inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
     long long* trace;                     // optional per-role cycle timeline (tkb_debug_set_trace)
@@ -46,6 +47,7 @@ struct BwdParams {
     int bh;            // batches * heads (persistent task count = bh * n_pad / 128)
     int head_group;    // heads per L2 group of the persistent task order
     int num_sms;       // persistent grid size
+    int pairs;         // D = 128: dK/dV on CTA pairs (attn_bwd_dkdv2_kernel)
     int* sched;        // persistent task counter pair (self-resetting, lcsf::queue_exit)
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)

@@ -27,6 +27,7 @@ thread_local int g_launches = 0;
 long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_trace)
 int g_trace_every = 1, g_trace_slots = 0;
 int g_bwd_phases = 7;  // debug: bit 0 prep, bit 1 dK/dV kernel, bit 2 dQ kernel
+int g_bwd_pairs = 0;   // D = 128 dK/dV on CTA pairs (tkb_set_bwd_pairs)
 
 // Per-device persistent-scheduler counters: 64 pairs used round-robin so kernels
 // running concurrently on different streams do not share a counter; each pair is
@@ -89,12 +90,13 @@ int check_device() {
     return cached_ok ? TKB_OK : fail(TKB_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
 }
 
-// 4-D {D, N, H, B} bf16 map with a {64, 128, 1, 1} SW128 box (heads = H, or Hkv for k/v).
-int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, const Strides& s, int heads = 0) {
+// 4-D {D, N, H, B} bf16 map with a {64, box_rows, 1, 1} SW128 box (heads = H, or Hkv for k/v).
+int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, const Strides& s, int heads = 0,
+                  uint32_t box_rows = 128) {
     uint64_t dims[4] = {(uint64_t)d->head_dim, (uint64_t)d->seq, (uint64_t)(heads > 0 ? heads : d->heads),
                         (uint64_t)d->batches};
     uint64_t strides[4] = {1, (uint64_t)s.n, (uint64_t)s.h, (uint64_t)s.b};
-    uint32_t box[4] = {64, 128, 1, 1};
+    uint32_t box[4] = {64, box_rows, 1, 1};
     std::string err;
     if (!tkb::host::make_tmap(tm, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, dims, strides, box,
                               CU_TENSOR_MAP_SWIZZLE_128B, &err))
@@ -248,7 +250,8 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
         (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
         (rc = make_bhnd_map(&p.tm_dq, dq, d, s)) || (rc = make_bhnd_map(&p.tm_dk, dk, d, skv, hkv)) ||
-        (rc = make_bhnd_map(&p.tm_dv, dv, d, skv, hkv)))
+        (rc = make_bhnd_map(&p.tm_dv, dv, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_q64, q, d, s, 0, 64)) ||
+        (rc = make_bhnd_map(&p.tm_do64, dout, d, s, 0, 64)))
         return rc;
     p.group = d->heads / hkv;
     const int64_t bh = (int64_t)d->batches * d->heads;
@@ -275,6 +278,7 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
         long long hg = (48ll << 20) / (kv_bytes > 0 ? kv_bytes : 1);
         p.head_group = (int)(hg < 1 ? 1 : (hg > bh ? bh : hg));
     }
+    p.pairs = g_bwd_pairs;
     int launches = 0;
     int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
                                  s.n, st, g_bwd_phases, &launches);
@@ -434,6 +438,11 @@ TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots) {
 
 TKB_API int tkb_debug_set_bwd_phases(int mask) {
     g_bwd_phases = mask & 7;
+    return TKB_OK;
+}
+
+TKB_API int tkb_set_bwd_pairs(int on) {
+    g_bwd_pairs = on ? 1 : 0;
     return TKB_OK;
 }
 

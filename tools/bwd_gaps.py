@@ -6,11 +6,12 @@ import torch
 from paper_2410_20399_b200 import attention as A
 
 B, H, N, D = 16, 16, 4096, 128
+CAUSAL = bool(int(sys.argv[1])) if len(sys.argv) > 1 else True
 q, k, v, do = (torch.empty(B, H, N, D, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1) for _ in range(4))
-o, lse = A.attention_fwd(q, k, v, causal=True)
+o, lse = A.attention_fwd(q, k, v, causal=CAUSAL)
 dq, dk, dv = (torch.empty_like(q) for _ in range(3))
 ws = torch.empty(A.bwd_workspace_bytes(B, H, N, D), dtype=torch.uint8, device="cuda")
-bwd = lambda: A.attention_bwd(q, k, v, o, do, lse, causal=True, dq=dq, dk=dk, dv=dv, workspace=ws)  # noqa
+bwd = lambda: A.attention_bwd(q, k, v, o, do, lse, causal=CAUSAL, dq=dq, dk=dk, dv=dv, workspace=ws)  # noqa
 for _ in range(3):
     bwd()
 torch.cuda.synchronize()

@@ -16,8 +16,8 @@ A.attention_bwd(q, k, v, o, do, lse, causal=bool(causal))
 torch.cuda.synchronize()
 A.debug_set_trace(None)
 t = buf.cpu()
-names = {0: ["kv.m.pwait", "kv.m.pfull", "kv.m.dswait", "kv.m.dsfull", "kv.m.end"],
-         1: ["kv.c.sfull", "kv.c.Pdone", "kv.c.dpfull", "kv.c.dSdone"],
+names = {0: ["kv.m.top", "kv.m.Sissued", "kv.m.dVissued", "kv.m.dKissued", "kv.m.end", "kv.m.sfree_ok", "kv.m.p0_ok", "kv.m.ds0_ok"],
+         1: ["kv.c.sfull", "kv.c.expdone", "kv.c.dpfull", "kv.c.dSdone"],
          2: ["q.m.dswait", "q.m.dsfull", "q.m.end"], 3: ["q.c.sfull", "q.c.dpfull", "q.c.dSdone"]}
 for slot in (1, 4):
     print(f"--- slot {slot} (item {slot * every})")
@@ -37,3 +37,11 @@ for slot in (1, 4):
         if len(st) > 4:
             d = [b - a for a, b in zip(st, st[1:])]
             print(f"{nm} iteration period (cycles):", d[2:12])
+
+# CTA timeline: first S^T ready, last step, finish (cycles from CTA start)
+for slot in range(slots):
+    first = int(t[slot, 1, 0, 0])
+    fin = int(t[slot, 1, 31, 7])
+    last = max(int(t[slot, 1, it, 3]) for it in range(31))
+    if first or fin:
+        print(f"slot {slot}: first s_full {first}, last traced dS {last}, finish {fin}")
