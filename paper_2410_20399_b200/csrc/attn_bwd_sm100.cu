@@ -442,6 +442,314 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
     if (warp == kWarpMma) tmem::dealloc<512>(tbase);
 }
 
+// ================================================================== bwd_dkdv, persistent
+// bwd_dkdv with one CTA per SM walking (kv block, kv head, batch) tasks from the atomic
+// queue, so that a task's prologue / finish overlap its neighbours instead of costing a CTA
+// turnover (~4000 clk start-up + ~4400 clk finish per CTA, ~9 % of a 32-step task):
+//   - K / V of the next task are loaded as soon as this task's last S^T / dP^T retire
+//     (kv_empty), i.e. under its last dV / dK GEMMs and finish;
+//   - the Q / dO rings and the per-step barriers run on a step counter continuous across
+//     tasks, so the next task's first S^T / dP^T GEMMs are issued right behind this task's
+//     last dV / dK (they write the S / dP regions, which hold nothing live by then);
+//   - the finish reads dV / dK out of TMEM, releases them at once (dv_free / dk_free: the
+//     next task's first dV / dK overwrite them) and stores bf16 rows straight from registers.
+TKB_DEVICE void st_global_v4(void* ptr, uint4 v) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// TMEM fp32 [lane][D/4 columns of group g] -> registers; the caller releases TMEM, then
+// rows_store_bf16 writes them (x mul) as bf16 to row `dst` (columns [g D/4, (g+1) D/4)).
+template <int D>
+TKB_DEVICE void rows_store_bf16(const uint32_t* v, __nv_bfloat16* dst, float mul) {
+#pragma unroll
+    for (int q = 0; q < D / 32; ++q) {
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * mul, __uint_as_float(v[8 * q + 1]) * mul);
+        u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * mul, __uint_as_float(v[8 * q + 3]) * mul);
+        u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * mul, __uint_as_float(v[8 * q + 5]) * mul);
+        u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * mul, __uint_as_float(v[8 * q + 7]) * mul);
+        st_global_v4(dst + 8 * q, u);
+    }
+}
+
+struct KvTask {
+    int j, head, batch;
+};
+
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __grid_constant__ BwdParams p) {
+    using C = CfgKV<D>;
+    using TL = Tiles<D>;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem + C::kOffK;
+    uint8_t* sV = smem + C::kOffV;
+    uint8_t* sQ = smem + C::kOffQ;
+    uint8_t* sDo = smem + C::kOffDo;
+    float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
+    float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
+    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
+    mbarrier& kv_full = bars[0];
+    mbarrier& s_full = bars[1];
+    mbarrier& kv_empty = bars[2];   // the task's last S^T / dP^T retired: K / V reloadable
+    mbarrier& dp_full = bars[3];
+    mbarrier& dv_free = bars[4];    // the finish has read dV out of TMEM
+    mbarrier& dkv_full = bars[5];
+    mbarrier& dk_free = bars[6];
+    mbarrier* q_full = bars + 8;     // [S]
+    mbarrier* q_empty = bars + 12;   // [S]
+    mbarrier* do_full = bars + 16;   // [S]
+    mbarrier* do_empty = bars + 20;  // [S]
+    mbarrier* p_full = bars + 32;    // [kGroups]
+    mbarrier* ds_full = bars + 36;   // [kGroups]
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
+    lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);
+
+    const int warp = warpid();
+    const int lane = laneid();
+    const int nq = p.n_pad / 128;
+    const int hkv = p.heads / p.group;
+    const int tasks = nq * hkv * (p.bh / p.heads);
+    // task id -> (kv block fastest, kv head, batch): the CTAs running together share heads
+    auto decode = [&](int id) {
+        KvTask w;
+        w.j = id % nq;
+        const int r = id / nq;
+        w.head = r % hkv;
+        w.batch = r / hkv;
+        return w;
+    };
+    auto steps = [&](const KvTask& w) { return (CAUSAL ? (nq - w.j) : nq) * p.group; };
+    long long* tr = trace_slot(p, (int)blockIdx.x, 0);
+    const long long t_start = clock64();
+
+    if (warp == kWarpLoad && lane == 0) {
+        queue.init(1 + 16);
+        mbar_init(&kv_full, 1);
+        mbar_init(&s_full, 1);
+        mbar_init(&kv_empty, 1);
+        mbar_init(&dp_full, 1);
+        mbar_init(&dv_free, kComputeThreads);
+        mbar_init(&dkv_full, 1);
+        mbar_init(&dk_free, kComputeThreads);
+        for (int g = 0; g < kGroups; ++g) {
+            mbar_init(&p_full[g], 128);
+            mbar_init(&ds_full[g], 128);
+        }
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+            mbar_init(&do_full[s], 1);
+            mbar_init(&do_empty[s], 1);
+        }
+        fence_barrier_init();
+        tma::prefetch_desc(&p.tm_q);
+        tma::prefetch_desc(&p.tm_k);
+        tma::prefetch_desc(&p.tm_v);
+        tma::prefetch_desc(&p.tm_do);
+    }
+    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tbase = tmem_slot;
+
+    if (warp == kWarpLoad) {
+        if (lane == 0) {
+            // ------------------------------------------------------------- LOAD
+            const uint64_t pol_stream = tma::policy_evict_first();
+            const uint64_t pol_keep = tma::policy_evict_last();
+            int x = 0;  // global step (ring position)
+            int n = 0;
+            int id = queue.claim(0, p.sched, tasks);
+            while (id >= 0) {
+                const KvTask w = decode(id);
+                const int T = steps(w), T1 = T / p.group;
+                const int kv0 = w.j * 128;
+                mbar_wait(&kv_empty, (n & 1) ^ 1u);
+                mbar_arrive_expect_tx(&kv_full, 2 * TL::kTileBytes);
+                for (int a = 0; a < TL::kAtoms; ++a) {
+                    tma::load_4d(sK + a * kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, w.head, w.batch, pol_stream);
+                    tma::load_4d(sV + a * kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, w.head, w.batch, pol_stream);
+                }
+                for (int t = 0; t < T; ++t, ++x) {
+                    const int i = (CAUSAL ? w.j : 0) + t % T1;
+                    const int hq = w.head * p.group + t / T1;
+                    const size_t bhq = (size_t)w.batch * p.heads + hq;
+                    const int s = x % S;
+                    const uint32_t ph = ((x / S) & 1) ^ 1;
+                    mbar_wait(&do_empty[s], ph);
+                    mbar_arrive_expect_tx(&do_full[s], TL::kTileBytes);
+                    for (int a = 0; a < TL::kAtoms; ++a)
+                        tma::load_4d(sDo + s * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[s], a * 64,
+                                     i * 128, hq, w.batch, pol_keep);
+                    mbar_wait(&q_empty[s], ph);
+                    mbar_arrive_expect_tx(&q_full[s], TL::kTileBytes + 1024);
+                    for (int a = 0; a < TL::kAtoms; ++a)
+                        tma::load_4d(sQ + s * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[s], a * 64,
+                                     i * 128, hq, w.batch, pol_keep);
+                    tma::load_1d(sLse + s * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &q_full[s]);
+                    tma::load_1d(sDelta + s * 128, p.delta + bhq * p.n_pad + i * 128, 512, &q_full[s]);
+                }
+                id = queue.claim(++n, p.sched, tasks);
+            }
+        }
+    } else if (warp == kWarpMma) {
+        // ----------------------------------------------------------------- MMA (converged warp)
+        constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();
+        constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();
+        const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+        auto qaddr = [&](int x) { return smem_u32(sQ + (x % S) * TL::kTileBytes); };
+        auto doaddr = [&](int x) { return smem_u32(sDo + (x % S) * TL::kTileBytes); };
+        auto issue_s = [&](int x) {
+            mbar_wait(&q_full[x % S], (x / S) & 1);
+            tmem::fence_after();
+            mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(x), id_s);
+            umma::commit_e(&s_full);
+        };
+        auto issue_dp = [&](int x) {
+            mbar_wait(&do_full[x % S], (x / S) & 1);
+            tmem::fence_after();
+            mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(x), id_s);
+            umma::commit_e(&dp_full);
+        };
+        int x0 = 0;  // first global step of the task
+        for (int n = 0;; ++n) {
+            const int id = queue.get_warp(n);
+            if (lane == 0) queue.release(n);
+            if (id < 0) break;
+            const int T = steps(decode(id));
+            mbar_wait(&kv_full, n & 1);
+            issue_s(x0);
+            issue_dp(x0);
+            if (T == 1) umma::commit_e(&kv_empty);
+            for (int t = 0; t < T; ++t) {
+                const int x = x0 + t;
+                const uint32_t ph = x & 1;
+                TKB_TR(0, x, 0);
+                if (t == 0 && n > 0) mbar_wait(&dv_free, (n - 1) & 1);  // previous task's dV read out
+                mma_tmem_a_groups(tbase + C::tmem_dv(), tbase + C::tmem_s(), doaddr(x), id_kv, t > 0, [&](int g) {
+                    mbar_wait(&p_full[g], ph);
+                    tmem::fence_after();
+                });
+                TKB_TR(0, x, 1);
+                umma::commit_e(&do_empty[x % S]);
+                if (t + 1 < T) issue_s(x + 1);  // overwrites P_t, read by dV_t issued before
+                TKB_TR(0, x, 2);
+                if (t == 0 && n > 0) mbar_wait(&dk_free, (n - 1) & 1);
+                mma_tmem_a_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qaddr(x), id_kv, t > 0, [&](int g) {
+                    mbar_wait(&ds_full[g], ph);
+                    tmem::fence_after();
+                });
+                TKB_TR(0, x, 3);
+                umma::commit_e(&q_empty[x % S]);
+                if (t + 1 < T) {
+                    issue_dp(x + 1);  // overwrites dS_t, read by dK_t issued before
+                    if (t + 2 == T) umma::commit_e(&kv_empty);  // the task's last S^T / dP^T issued
+                }
+                TKB_TR(0, x, 4);
+            }
+            umma::commit_e(&dkv_full);
+            x0 += T;
+        }
+    } else {
+        // ----------------------------------------------------------------- COMPUTE
+        const int wq = warp & 3;
+        const int g = warp >> 2;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
+        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
+        const float tau = p.scale_log2;
+        int x0 = 0;
+        for (int n = 0;; ++n) {
+            const int id = queue.get_warp(n);
+            if (id < 0) break;
+            const KvTask w = decode(id);
+            const int T = steps(w), T1 = T / p.group;
+            const int kv0 = w.j * 128;
+            for (int t = 0; t < T; ++t) {
+                const int x = x0 + t;
+                const int s = x % S;
+                const bool diag = CAUSAL && (t % T1 == 0);  // q block i == j
+                const uint32_t nlse4 = smem_u32(sLse + s * 128 + 32 * g);
+                const uint32_t dlt4 = smem_u32(sDelta + s * 128 + 32 * g);
+                mbar_wait(&q_full[s], (x / S) & 1);
+                mbar_wait(&s_full, x & 1);
+                if (threadIdx.x == 0) TKB_TR(1, x, 0);
+                tmem::fence_after();
+                float pf[32];
+                tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
+                exp_chunk<false>(pf, tau, nlse4, 0.f);
+                if (diag) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) pf[c] = (32 * g + c < r) ? 0.f : pf[c];
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) pk[c / 2] = pack_bf16x2(pf[c], pf[c + 1]);
+                tmem::st_32x32b_x16(tS, pk);
+                tmem::wait_st();
+                tmem::fence_before();
+                mbar_arrive(&p_full[g]);
+                if (threadIdx.x == 0) TKB_TR(1, x, 1);
+                mbar_wait(&dp_full, x & 1);
+                if (threadIdx.x == 0) TKB_TR(1, x, 2);
+                tmem::fence_after();
+                uint32_t dpv[32];
+                tmem::ldw_32x32b_x32(tDp, dpv);
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 d4 = lds_f4(dlt4 + 4 * c);
+                    const float2 g01 = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
+                                            make_float2(d4.x, d4.y));
+                    const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
+                                            make_float2(d4.z, d4.w));
+                    const float2 s01 = mul2(make_float2(pf[c], pf[c + 1]), g01);
+                    const float2 s23 = mul2(make_float2(pf[c + 2], pf[c + 3]), g23);
+                    pk[c / 2] = pack_bf16x2(s01.x, s01.y);
+                    pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
+                }
+                tmem::st_32x32b_x16(tDp, pk);
+                tmem::wait_st();
+                tmem::fence_before();
+                mbar_arrive(&ds_full[g]);
+                if (threadIdx.x == 0) TKB_TR(1, x, 3);
+            }
+            x0 += T;
+            // FINISH: dV / dK rows out of TMEM (released at once), bf16 rows to global
+            mbar_wait(&dkv_full, n & 1);
+            tmem::fence_after();
+            const int row = kv0 + r;
+            const size_t off = (size_t)w.batch * p.kv_sb + (size_t)w.head * p.kv_sh + (size_t)row * p.kv_sn + g * (D / 4);
+            uint32_t v[D / 4];
+            if constexpr (D == 128)
+                tmem::ldw_32x32b_x32(tbase + lane_off + C::tmem_dv() + g * (D / 4), v);
+            else
+                tmem::ldw_32x32b_x16(tbase + lane_off + C::tmem_dv() + g * (D / 4), v);
+            tmem::fence_before();
+            mbar_arrive(&dv_free);
+            if (row < p.n) rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dv) + off, 1.f);
+            if constexpr (D == 128)
+                tmem::ldw_32x32b_x32(tbase + lane_off + C::tmem_dk() + g * (D / 4), v);
+            else
+                tmem::ldw_32x32b_x16(tbase + lane_off + C::tmem_dk() + g * (D / 4), v);
+            tmem::fence_before();
+            mbar_arrive(&dk_free);
+            if (row < p.n) rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dk) + off, p.scale);
+            __syncwarp();
+            if (lane == 0) queue.release(n);
+        }
+    }
+
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
+    if (threadIdx.x == 0) lcsf::queue_exit(p.sched);
+}
+
 // ================================================================== bwd_dkdv on CTA pairs (D = 128)
 // The single-CTA bwd_dkdv moves 256 KB through each SM's shared-memory port per step (the
 // SS GEMMs S^T / dP^T read 8 KB per MMA, the TS GEMMs 4 KB, TMA writes 64 KB of Q / dO) —
@@ -941,7 +1249,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             umma::commit_e(&v_empty[x % S]);
         };
         for (int n = 0;; ++n) {
-            const int t = queue.get(n);
+            const int t = queue.get_warp(n);
             if (lane == 0) queue.release(n);
             if (t < 0) break;
             const int nk = nk_of(qtask<CAUSAL>(p, t));
@@ -994,7 +1302,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             mbar_arrive(&a_ready);
             mbar_arrive(&qdo_free);  // SMEM Q / dO may be refilled with the next task's
         };
-        int t = queue.get(0);
+        int t = queue.get_warp(0);
         if (t >= 0) stage_a(0);
         while (t >= 0) {
             const QTask w = qtask<CAUSAL>(p, t);
@@ -1040,7 +1348,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 if (threadIdx.x == 0) TKB_TR(1, (int)it, 2);
             }
             // the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this finish)
-            const int t_next = queue.get(n + 1);
+            const int t_next = queue.get_warp(n + 1);
             if (t_next >= 0) stage_a(n + 1);
             // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM staging -> TMA store
             mbar_wait(&dq_full, n & 1);
@@ -1119,6 +1427,7 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
         int e = set_smem(attn_bwd_dkdv_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
         if (!e) e = set_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes);
         if (!e && D == 128) e = set_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes);
+        if (!e) e = set_smem(attn_bwd_dkdvp_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
         if (e) return e;
         configured = true;
     }
@@ -1129,7 +1438,13 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
             dim3 grid2((p.n_pad / 128 + 1) & ~1, p.heads / p.group, batches);
             attn_bwd_dkdv2_kernel<CAUSAL><<<grid2, kThreads, CfgKV2::kSmemBytes, stream>>>(p);
         } else {
+#ifndef TKB_BWD_GRID_KV
+            const int tasks_kv = (p.n_pad / 128) * (p.heads / p.group) * batches;
+            attn_bwd_dkdvp_kernel<D, CAUSAL>
+                <<<tasks_kv < p.num_sms ? tasks_kv : p.num_sms, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+#else  // A/B baseline: one CTA per kv block
             attn_bwd_dkdv_kernel<D, CAUSAL><<<grid_kv, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+#endif
         }
         int e = (int)cudaGetLastError();
         if (e) return e;

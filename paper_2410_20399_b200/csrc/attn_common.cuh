@@ -48,6 +48,9 @@ struct BwdParams {
     int head_group;    // heads per L2 group of the persistent task order
     int num_sms;       // persistent grid size
     int pairs;         // D = 128: dK/dV on CTA pairs (attn_bwd_dkdv2_kernel)
+    void* dk;          // dK / dV base pointers and element strides (persistent dK/dV kernel:
+    void* dv;          //   direct row stores from registers)
+    long long kv_sb, kv_sh, kv_sn;
     int* sched;        // persistent task counter pair (self-resetting, lcsf::queue_exit)
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)

@@ -279,6 +279,11 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
         p.head_group = (int)(hg < 1 ? 1 : (hg > bh ? bh : hg));
     }
     p.pairs = g_bwd_pairs;
+    p.dk = dk;
+    p.dv = dv;
+    p.kv_sb = skv.b;
+    p.kv_sh = skv.h;
+    p.kv_sn = skv.n;
     int launches = 0;
     int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
                                  s.n, st, g_bwd_phases, &launches);

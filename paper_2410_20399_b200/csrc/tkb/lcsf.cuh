@@ -80,6 +80,10 @@ struct work_queue {
         mbar_wait(&full[s], (n / kSlots) & 1);
         return *reinterpret_cast<volatile int*>(&id[s]);
     }
+    // warp-collective get(): the id comes back warp-uniform (a shuffle from lane 0), so the
+    // task-derived loop bounds and addresses stay in uniform registers — an MMA warp whose
+    // descriptors depend on a per-thread id would pay R2UR / VOTEU per tcgen05.mma
+    TKB_DEVICE int get_warp(int n) { return __shfl_sync(0xffffffffu, get(n), 0); }
     TKB_DEVICE void release(int n) { mbar_arrive(&empty[n % kSlots]); }
 };
 

@@ -22,7 +22,10 @@ ap.add_argument("--uniform", action="store_true", help="U(-1,1) inputs (bench.py
 ap.add_argument("--no-causal", action="store_true")
 ap.add_argument("--only-causal", action="store_true")
 ap.add_argument("--shapes", default="16,16,4096,128;16,16,4096,64;4,16,16384,128;16,16,1024,128")
+ap.add_argument("--pairs", action="store_true", help="D=128 backward dK/dV on CTA pairs")
 args = ap.parse_args()
+if args.pairs:
+    A.set_bwd_pairs(True)
 for sh in args.shapes.split(";"):
     B, H, N, D = map(int, sh.split(","))
     if args.uniform:

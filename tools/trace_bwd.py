@@ -9,15 +9,15 @@ q, k, v, do = (torch.randn(B, H, N, D, device="cuda", dtype=torch.bfloat16) for 
 o, lse = A.attention_fwd(q, k, v, causal=bool(causal))
 slots = 8
 buf = torch.zeros(slots, 4, 32, 8, dtype=torch.int64, device="cuda")
-every = (B * H * ((N + 127) // 128)) // slots
+every = int(os.environ.get("TRACE_EVERY", (B * H * ((N + 127) // 128)) // slots))
 A.attention_bwd(q, k, v, o, do, lse, causal=bool(causal))
 A.debug_set_trace(buf, every, slots)
 A.attention_bwd(q, k, v, o, do, lse, causal=bool(causal))
 torch.cuda.synchronize()
 A.debug_set_trace(None)
 t = buf.cpu()
-names = {0: ["kv.m.top", "kv.m.Sissued", "kv.m.dVissued", "kv.m.dKissued", "kv.m.end", "kv.m.sfree_ok", "kv.m.p0_ok", "kv.m.ds0_ok"],
-         1: ["kv.c.sfull", "kv.c.expdone", "kv.c.dpfull", "kv.c.dSdone"],
+names = {0: ["kv.m.top", "kv.m.dVissued", "kv.m.Sissued", "kv.m.dKissued", "kv.m.end"],
+         1: ["kv.c.sfull", "kv.c.Pdone", "kv.c.dpfull", "kv.c.dSdone"],
          2: ["q.m.dswait", "q.m.dsfull", "q.m.end"], 3: ["q.c.sfull", "q.c.dpfull", "q.c.dSdone"]}
 for slot in (1, 4):
     print(f"--- slot {slot} (item {slot * every})")
