@@ -477,13 +477,37 @@ struct KvTask {
     int j, head, batch;
 };
 
+// SMEM of the persistent dK/dV kernel. Q_{t+1} is needed by S_{t+1}, issued right after dV_t;
+// its slot is the one dK_{t+1-SQ} frees. With SQ = 2 only dP_t and dV_t (1024 clk) separate
+// the two and the L2 -> SMEM latency of the 33 KB reload shows; SQ = 3 gives it a step more.
+// dO_{t+1} (first read by dP_{t+1}, late in step t) and lse / delta need only 2 slots.
+template <int D>
+struct CfgKVP {
+    using T = Tiles<D>;
+    static constexpr int kStagesQ = (D == 128) ? 3 : 4;
+    static constexpr int kStagesDo = (D == 128) ? 2 : 3;
+    static constexpr int kStagesAux = 2;
+    static constexpr int kOffK = 0;
+    static constexpr int kOffV = kOffK + T::kTileBytes;
+    static constexpr int kOffQ = kOffV + T::kTileBytes;
+    static constexpr int kOffDo = kOffQ + kStagesQ * T::kTileBytes;
+    static constexpr int kOffLse = kOffDo + kStagesDo * T::kTileBytes;
+    static constexpr int kOffDelta = kOffLse + kStagesAux * 512;
+    static constexpr int kOffBar = kOffDelta + kStagesAux * 512;
+    // no alignment slack: without static SMEM the dynamic window starts 1024-aligned (checked)
+    static constexpr int kSmemBytes = kOffBar + 512;
+    static_assert(kSmemBytes <= 232448, "smem");
+};
+
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __grid_constant__ BwdParams p) {
-    using C = CfgKV<D>;
+    using C = CfgKVP<D>;
+    using CT = CfgKV<D>;  // TMEM layout
     using TL = Tiles<D>;
-    constexpr int S = C::kStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int SQ = C::kStagesQ, SD = C::kStagesDo, SA = C::kStagesAux;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-byte alignment
     uint8_t* sK = smem + C::kOffK;
     uint8_t* sV = smem + C::kOffV;
     uint8_t* sQ = smem + C::kOffQ;
@@ -498,10 +522,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     mbarrier& dv_free = bars[4];    // the finish has read dV out of TMEM
     mbarrier& dkv_full = bars[5];
     mbarrier& dk_free = bars[6];
-    mbarrier* q_full = bars + 8;     // [S]
-    mbarrier* q_empty = bars + 12;   // [S]
-    mbarrier* do_full = bars + 16;   // [S]
-    mbarrier* do_empty = bars + 20;  // [S]
+    static_assert(SQ <= 4 && SD <= 3 && SA <= 2, "barrier slots");
+    mbarrier* q_full = bars + 8;      // [SQ]
+    mbarrier* q_empty = bars + 12;    // [SQ]
+    mbarrier* do_full = bars + 16;    // [SD]
+    mbarrier* do_empty = bars + 19;   // [SD]
+    mbarrier* aux_full = bars + 22;   // [SA] lse2 / delta
+    mbarrier* aux_empty = bars + 24;  // [SA]
     mbarrier* p_full = bars + 32;    // [kGroups]
     mbarrier* ds_full = bars + 36;   // [kGroups]
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
@@ -538,11 +565,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
             mbar_init(&p_full[g], 128);
             mbar_init(&ds_full[g], 128);
         }
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < SQ; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
+        }
+        for (int s = 0; s < SD; ++s) {
             mbar_init(&do_full[s], 1);
             mbar_init(&do_empty[s], 1);
+        }
+        for (int s = 0; s < SA; ++s) {
+            mbar_init(&aux_full[s], 1);
+            mbar_init(&aux_empty[s], 1);
         }
         fence_barrier_init();
         tma::prefetch_desc(&p.tm_q);
@@ -578,20 +611,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                     const int i = (CAUSAL ? w.j : 0) + t % T1;
                     const int hq = w.head * p.group + t / T1;
                     const size_t bhq = (size_t)w.batch * p.heads + hq;
-                    const int s = x % S;
-                    const uint32_t ph = ((x / S) & 1) ^ 1;
-                    mbar_wait(&do_empty[s], ph);
-                    mbar_arrive_expect_tx(&do_full[s], TL::kTileBytes);
+                    // in pipe order of the GEMMs that free the slots: dK_{x-SQ}, dV_{x-SD}, dK_{x-SA}
+                    const int sq = x % SQ, sd = x % SD, sa = x % SA;
+                    mbar_wait(&q_empty[sq], ((x / SQ) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&q_full[sq], TL::kTileBytes);
                     for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sDo + s * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[s], a * 64,
+                        tma::load_4d(sQ + sq * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[sq], a * 64,
                                      i * 128, hq, w.batch, pol_keep);
-                    mbar_wait(&q_empty[s], ph);
-                    mbar_arrive_expect_tx(&q_full[s], TL::kTileBytes + 1024);
+                    mbar_wait(&do_empty[sd], ((x / SD) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&do_full[sd], TL::kTileBytes);
                     for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sQ + s * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[s], a * 64,
+                        tma::load_4d(sDo + sd * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[sd], a * 64,
                                      i * 128, hq, w.batch, pol_keep);
-                    tma::load_1d(sLse + s * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &q_full[s]);
-                    tma::load_1d(sDelta + s * 128, p.delta + bhq * p.n_pad + i * 128, 512, &q_full[s]);
+                    mbar_wait(&aux_empty[sa], ((x / SA) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&aux_full[sa], 1024);
+                    tma::load_1d(sLse + sa * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &aux_full[sa]);
+                    tma::load_1d(sDelta + sa * 128, p.delta + bhq * p.n_pad + i * 128, 512, &aux_full[sa]);
                 }
                 id = queue.claim(++n, p.sched, tasks);
             }
@@ -601,18 +636,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();
         constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();
         const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-        auto qaddr = [&](int x) { return smem_u32(sQ + (x % S) * TL::kTileBytes); };
-        auto doaddr = [&](int x) { return smem_u32(sDo + (x % S) * TL::kTileBytes); };
+        auto qaddr = [&](int x) { return smem_u32(sQ + (x % SQ) * TL::kTileBytes); };
+        auto doaddr = [&](int x) { return smem_u32(sDo + (x % SD) * TL::kTileBytes); };
         auto issue_s = [&](int x) {
-            mbar_wait(&q_full[x % S], (x / S) & 1);
+            mbar_wait(&q_full[x % SQ], (x / SQ) & 1);
             tmem::fence_after();
-            mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(x), id_s);
+            mm_abt<D>(tbase + CT::tmem_s(), aK, qaddr(x), id_s);
             umma::commit_e(&s_full);
         };
         auto issue_dp = [&](int x) {
-            mbar_wait(&do_full[x % S], (x / S) & 1);
+            mbar_wait(&do_full[x % SD], (x / SD) & 1);
             tmem::fence_after();
-            mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(x), id_s);
+            mm_abt<D>(tbase + CT::tmem_dp(), aV, doaddr(x), id_s);
             umma::commit_e(&dp_full);
         };
         int x0 = 0;  // first global step of the task
@@ -630,21 +665,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 const uint32_t ph = x & 1;
                 TKB_TR(0, x, 0);
                 if (t == 0 && n > 0) mbar_wait(&dv_free, (n - 1) & 1);  // previous task's dV read out
-                mma_tmem_a_groups(tbase + C::tmem_dv(), tbase + C::tmem_s(), doaddr(x), id_kv, t > 0, [&](int g) {
+                mma_tmem_a_groups(tbase + CT::tmem_dv(), tbase + CT::tmem_s(), doaddr(x), id_kv, t > 0, [&](int g) {
                     mbar_wait(&p_full[g], ph);
                     tmem::fence_after();
                 });
                 TKB_TR(0, x, 1);
-                umma::commit_e(&do_empty[x % S]);
+                umma::commit_e(&do_empty[x % SD]);
                 if (t + 1 < T) issue_s(x + 1);  // overwrites P_t, read by dV_t issued before
                 TKB_TR(0, x, 2);
                 if (t == 0 && n > 0) mbar_wait(&dk_free, (n - 1) & 1);
-                mma_tmem_a_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qaddr(x), id_kv, t > 0, [&](int g) {
+                mma_tmem_a_groups(tbase + CT::tmem_dk(), tbase + CT::tmem_dp(), qaddr(x), id_kv, t > 0, [&](int g) {
                     mbar_wait(&ds_full[g], ph);
                     tmem::fence_after();
                 });
                 TKB_TR(0, x, 3);
-                umma::commit_e(&q_empty[x % S]);
+                umma::commit_e(&q_empty[x % SQ]);
+                umma::commit_e(&aux_empty[x % SA]);  // dK_x waited for the last dS of step x
                 if (t + 1 < T) {
                     issue_dp(x + 1);  // overwrites dS_t, read by dK_t issued before
                     if (t + 2 == T) umma::commit_e(&kv_empty);  // the task's last S^T / dP^T issued
@@ -660,8 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         const int g = warp >> 2;
         const int r = wq * 32 + lane;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
-        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
+        const uint32_t tS = tbase + lane_off + CT::tmem_s() + 32 * g;
+        const uint32_t tDp = tbase + lane_off + CT::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
         int x0 = 0;
         for (int n = 0;; ++n) {
@@ -672,11 +708,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
             const int kv0 = w.j * 128;
             for (int t = 0; t < T; ++t) {
                 const int x = x0 + t;
-                const int s = x % S;
+                const int sa = x % SA;
                 const bool diag = CAUSAL && (t % T1 == 0);  // q block i == j
-                const uint32_t nlse4 = smem_u32(sLse + s * 128 + 32 * g);
-                const uint32_t dlt4 = smem_u32(sDelta + s * 128 + 32 * g);
-                mbar_wait(&q_full[s], (x / S) & 1);
+                const uint32_t nlse4 = smem_u32(sLse + sa * 128 + 32 * g);
+                const uint32_t dlt4 = smem_u32(sDelta + sa * 128 + 32 * g);
+                mbar_wait(&aux_full[sa], (x / SA) & 1);
                 mbar_wait(&s_full, x & 1);
                 if (threadIdx.x == 0) TKB_TR(1, x, 0);
                 tmem::fence_after();
@@ -726,16 +762,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
             const size_t off = (size_t)w.batch * p.kv_sb + (size_t)w.head * p.kv_sh + (size_t)row * p.kv_sn + g * (D / 4);
             uint32_t v[D / 4];
             if constexpr (D == 128)
-                tmem::ldw_32x32b_x32(tbase + lane_off + C::tmem_dv() + g * (D / 4), v);
+                tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
             else
-                tmem::ldw_32x32b_x16(tbase + lane_off + C::tmem_dv() + g * (D / 4), v);
+                tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
             tmem::fence_before();
             mbar_arrive(&dv_free);
             if (row < p.n) rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dv) + off, 1.f);
             if constexpr (D == 128)
-                tmem::ldw_32x32b_x32(tbase + lane_off + C::tmem_dk() + g * (D / 4), v);
+                tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
             else
-                tmem::ldw_32x32b_x16(tbase + lane_off + C::tmem_dk() + g * (D / 4), v);
+                tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
             tmem::fence_before();
             mbar_arrive(&dk_free);
             if (row < p.n) rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dk) + off, p.scale);
@@ -1087,13 +1123,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 template <int D>
 struct CfgQ {
     using T = Tiles<D>;
-    static constexpr int kStages = (D == 128) ? 2 : 4;  // K and V ring depth
+    // K / V ring depths. K_j is released by dQ_j, the last GEMM of step j, and needed again
+    // by S_{j+SK}; with SK = 2 only one GEMM (dP_{j+1}) separates them and the L2 -> SMEM
+    // latency of the 32 KB reload is exposed (measured: 2650 instead of 1550 clk per step
+    // with the compute warps idle). V_j is released by dP_j, early in the step.
+    static constexpr int kStagesK = (D == 128) ? 3 : 5;
+    static constexpr int kStagesV = (D == 128) ? 2 : 4;
     static constexpr int kOffQ = 0;
     static constexpr int kOffDo = kOffQ + T::kTileBytes;
     static constexpr int kOffK = kOffDo + T::kTileBytes;
-    static constexpr int kOffV = kOffK + kStages * T::kTileBytes;
-    static constexpr int kOffStage = kOffV + kStages * T::kTileBytes;  // dQ finish staging
-    static constexpr int kOffBar = kOffStage + T::kTileBytes;
+    static constexpr int kOffV = kOffK + kStagesK * T::kTileBytes;
+    static constexpr int kOffBar = kOffV + kStagesV * T::kTileBytes;
     static constexpr int kSmemBytes = kOffBar + 512 + 1024;
     static_assert(kSmemBytes <= 232448, "smem");
     // S | dP | dQ | Q (A operand) | dO (A operand): 128 + 128 + D + D/2 + D/2 <= 512
@@ -1128,14 +1168,14 @@ template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
     using C = CfgQ<D>;
     using TL = Tiles<D>;
-    constexpr int S = C::kStages;
+    constexpr int SK = C::kStagesK;
+    constexpr int SV = C::kStagesV;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem + C::kOffQ;
     uint8_t* sDo = smem + C::kOffDo;
     uint8_t* sK = smem + C::kOffK;
     uint8_t* sV = smem + C::kOffV;
-    uint8_t* sStage = smem + C::kOffStage;
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
     mbarrier& qdo_full = bars[0];   // Q / dO of a task in SMEM (TMA)
     mbarrier& s_full = bars[1];
@@ -1145,10 +1185,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     mbarrier& dp_full = bars[5];
     mbarrier& qa_free = bars[6];    // last S / dP GEMM of a task retired: TMEM Q / dO reusable
     mbarrier& dq_full = bars[7];
-    mbarrier* k_full = bars + 8;    // [S]
-    mbarrier* k_empty = bars + 12;  // [S]
-    mbarrier* v_full = bars + 16;   // [S]
-    mbarrier* v_empty = bars + 20;  // [S]
+    mbarrier* k_full = bars + 8;    // [SK]
+    mbarrier* k_empty = bars + 13;  // [SK]
+    mbarrier* v_full = bars + 18;   // [SV]
+    mbarrier* v_empty = bars + 22;  // [SV]
     mbarrier* ds_full = bars + 32;  // [kGroups] dS chunks (32 keys each)
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
     lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);  // dynamic task claims
@@ -1172,9 +1212,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         mbar_init(&qa_free, 1);
         mbar_init(&dq_full, 1);
         for (int g = 0; g < kGroups; ++g) mbar_init(&ds_full[g], 128);
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < SK; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < SV; ++s) {
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
         }
@@ -1209,17 +1251,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 }
                 const int nk = nk_of(w);
                 for (int jj = 0; jj < nk; ++jj, ++kv) {
-                    const int s = kv % S;
-                    const uint32_t ph = ((kv / S) & 1) ^ 1;
-                    mbar_wait(&k_empty[s], ph);
-                    mbar_arrive_expect_tx(&k_full[s], TL::kTileBytes);
+                    const int sk = kv % SK, sv = kv % SV;
+                    mbar_wait(&k_empty[sk], ((kv / SK) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&k_full[sk], TL::kTileBytes);
                     for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sK + s * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[s], a * 64, jj * 128,
+                        tma::load_4d(sK + sk * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[sk], a * 64, jj * 128,
                                      h / p.group, b, pol_keep);
-                    mbar_wait(&v_empty[s], ph);
-                    mbar_arrive_expect_tx(&v_full[s], TL::kTileBytes);
+                    mbar_wait(&v_empty[sv], ((kv / SV) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&v_full[sv], TL::kTileBytes);
                     for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sV + s * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[s], a * 64, jj * 128,
+                        tma::load_4d(sV + sv * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[sv], a * 64, jj * 128,
                                      h / p.group, b, pol_keep);
                 }
                 // claim the next task once this one's loads are all issued (the atomic counter
@@ -1233,20 +1274,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
         int kv = 0;        // K / V ring position
         uint32_t it = 0;   // global iteration count (s_full / s_free / dp_full / ds_full phases)
-        auto kaddr = [&](int x) { return smem_u32(sK + (x % S) * TL::kTileBytes); };
-        auto vaddr = [&](int x) { return smem_u32(sV + (x % S) * TL::kTileBytes); };
+        auto kaddr = [&](int x) { return smem_u32(sK + (x % SK) * TL::kTileBytes); };
+        auto vaddr = [&](int x) { return smem_u32(sV + (x % SV) * TL::kTileBytes); };
         auto issue_s = [&](int x) {  // S = Q K^T
-            mbar_wait(&k_full[x % S], (x / S) & 1);
+            mbar_wait(&k_full[x % SK], (x / SK) & 1);
             tmem::fence_after();
             mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(x), id_s);
             umma::commit_e(&s_full);
         };
         auto issue_dp = [&](int x) {  // dP = dO V^T
-            mbar_wait(&v_full[x % S], (x / S) & 1);
+            mbar_wait(&v_full[x % SV], (x / SV) & 1);
             tmem::fence_after();
             mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(x), id_s);
             umma::commit_e(&dp_full);
-            umma::commit_e(&v_empty[x % S]);
+            umma::commit_e(&v_empty[x % SV]);
         };
         for (int n = 0;; ++n) {
             const int t = queue.get_warp(n);
@@ -1269,7 +1310,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                     tmem::fence_after();
                 });
                 TKB_TR(0, (int)it, 1);
-                umma::commit_e(&k_empty[kv % S]);
+                umma::commit_e(&k_empty[kv % SK]);
                 if (jj + 1 < nk) {
                     issue_dp(kv + 1);  // overwrites dS_j, read by dQ_j issued before
                     if (jj + 2 == nk) umma::commit_e(&qa_free);  // the task's last S and dP are issued
@@ -1350,25 +1391,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             // the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this finish)
             const int t_next = queue.get_warp(n + 1);
             if (t_next >= 0) stage_a(n + 1);
-            // FINISH: dQ (TMEM fp32) -> bf16 -> SMEM staging -> TMA store
+            // FINISH: dQ (TMEM fp32) -> registers -> bf16 row stores (dQ = scale dS K); the next
+            // task's first dQ GEMM waits for its dS, which these warps produce after this
             mbar_wait(&dq_full, n & 1);
             tmem::fence_after();
-            if (threadIdx.x == 0) tma::wait_group_read<0>();  // the previous task's store has read the staging
-            named_sync(kBarCompute, kComputeThreads);
-            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sStage, r, g, p.scale);  // dQ = scale dS K
-            tma::fence_async_smem();
-            named_sync(kBarCompute, kComputeThreads);
-            if (threadIdx.x == 0) {
-                for (int a = 0; a < TL::kAtoms; ++a)
-                    tma::store_4d(&p.tm_dq, sStage + a * kAtomBytes, a * 64, q0, h, b);
-                tma::commit_group();
+            {
+                uint32_t v[D / 4];
+                if constexpr (D == 128)
+                    tmem::ldw_32x32b_x32(tbase + lane_off + C::tmem_dq() + g * (D / 4), v);
+                else
+                    tmem::ldw_32x32b_x16(tbase + lane_off + C::tmem_dq() + g * (D / 4), v);
+                if (row < p.n)
+                    rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dq) + (size_t)b * p.q_sb +
+                                              (size_t)h * p.q_sh + (size_t)row * p.q_sn + g * (D / 4),
+                                       p.scale);
             }
             __syncwarp();
             if (lane == 0) queue.release(n);  // every warp read task n's id long ago
             t = t_next;
             ++n;
         }
-        if (threadIdx.x == 0) tma::wait_group<0>();
     }
 
     tmem::fence_before();
@@ -1427,7 +1469,7 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
         int e = set_smem(attn_bwd_dkdv_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
         if (!e) e = set_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes);
         if (!e && D == 128) e = set_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes);
-        if (!e) e = set_smem(attn_bwd_dkdvp_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
+        if (!e) e = set_smem(attn_bwd_dkdvp_kernel<D, CAUSAL>, CfgKVP<D>::kSmemBytes);
         if (e) return e;
         configured = true;
     }
@@ -1441,7 +1483,7 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
 #ifndef TKB_BWD_GRID_KV
             const int tasks_kv = (p.n_pad / 128) * (p.heads / p.group) * batches;
             attn_bwd_dkdvp_kernel<D, CAUSAL>
-                <<<tasks_kv < p.num_sms ? tasks_kv : p.num_sms, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
+                <<<tasks_kv < p.num_sms ? tasks_kv : p.num_sms, kThreads, CfgKVP<D>::kSmemBytes, stream>>>(p);
 #else  // A/B baseline: one CTA per kv block
             attn_bwd_dkdv_kernel<D, CAUSAL><<<grid_kv, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
 #endif

@@ -51,6 +51,8 @@ struct BwdParams {
     void* dk;          // dK / dV base pointers and element strides (persistent dK/dV kernel:
     void* dv;          //   direct row stores from registers)
     long long kv_sb, kv_sh, kv_sn;
+    void* dq;          // dQ base and element strides (dQ kernel: direct row stores)
+    long long q_sb, q_sh, q_sn;
     int* sched;        // persistent task counter pair (self-resetting, lcsf::queue_exit)
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)

@@ -284,6 +284,10 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.kv_sb = skv.b;
     p.kv_sh = skv.h;
     p.kv_sn = skv.n;
+    p.dq = dq;
+    p.q_sb = s.b;
+    p.q_sh = s.h;
+    p.q_sn = s.n;
     int launches = 0;
     int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
                                  s.n, st, g_bwd_phases, &launches);
