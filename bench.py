@@ -504,7 +504,9 @@ def load_traffic(kernel):
     try:
         with open(p) as f:
             t = json.load(f)
-        return t.get(kernel, t.get(kernel + "_kernel"))
+        # logical kernel -> the symbol ncu reports (dK/dV runs as the persistent kernel)
+        sym = {"attn_bwd_dkdv": "attn_bwd_dkdvp_kernel"}.get(kernel, kernel + "_kernel")
+        return t.get(sym, t.get(kernel))
     except Exception:
         return None
 
