@@ -43,7 +43,7 @@
 #define TKB_FWD_POLY64 2
 #endif
 #ifndef TKB_FWD_POLY128
-#define TKB_FWD_POLY128 0
+#define TKB_FWD_POLY128 2
 #endif
 #ifndef TKB_FWD_PCHUNKS
 #define TKB_FWD_PCHUNKS 2
@@ -58,9 +58,10 @@ struct Cfg {
     static constexpr int kTile = Tile::kBytes;
     static constexpr int kKvSlots = (D == 128) ? 4 : 8;  // K and V alternate in the ring
     // exp2 of one pair in every group of four columns, on kPolyGroups of every 4 groups, runs as
-    // a polynomial on the FMA pipe: at D = 64 the MMA work per exponential halves and MUFU
-    // (16 / clk / SM) bounds the softmax; at D = 128 the single-warp exp pass is issue-bound
-    // and the polynomial does not pay
+    // a polynomial on the FMA pipe (a quarter of the exponentials at 2): per SM sub-partition
+    // the two softmax warps' 128 ex2 per kv block occupy MUFU (4 lanes / clk) for 2048 clk,
+    // the whole MMA time of the block. At D = 128 this paid only once the row max moved to
+    // FMNMX3 and the row sums to FADD2 (3 instead of 4 issue slots per element)
     static constexpr int kPolyGroups = (D == 64) ? TKB_FWD_POLY64 : TKB_FWD_POLY128;
     static constexpr int kSmemQ = kQStages * kTile;
     static constexpr int kSmemKv = kKvSlots * kTile;
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             // P = exp2(tau * S - m) (exp2, tiles.hpp:217-219); row_sum over fp32 P (tiles.hpp:301-309);
             // bf16 RNE copy into TMEM (copy, tiles.hpp:195-200), handed over chunk by chunk
             const float2 tau2 = make_float2(tau, tau), nm2 = make_float2(-m, -m);
-            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+            float2 l01 = make_float2(0.f, 0.f), l23 = make_float2(0.f, 0.f);  // packed FADD2 row sums
             uint32_t pk[kBlockN / 2];
 #pragma unroll
             for (int c = 0; c < kPChunks; ++c) {
@@ -348,10 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         p2 = ex2_approx(xb.x);
                         p3 = ex2_approx(xb.y);
                     }
-                    l0 += p0;
-                    l1 += p1;
-                    l2 += p2;
-                    l3 += p3;
+                    l01 = add2(l01, make_float2(p0, p1));
+                    l23 = add2(l23, make_float2(p2, p3));
                     pk[j / 2] = pack_bf16x2(p0, p1);
                     pk[j / 2 + 1] = pack_bf16x2(p2, p3);
                 }
@@ -368,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     tmem::st_32x32b_x16(tP + c * 16, pk + c * 16);
                 }
             }
-            l += (l0 + l1) + (l2 + l3);
+            l += (l01.x + l01.y) + (l23.x + l23.y);
             tmem::wait_st();
             tmem::fence_before();
             mbar_arrive(&p_full[s][kPChunks - 1]);

@@ -68,6 +68,13 @@ TKB_DEVICE void named_arrive(int id, int nthreads) {
 
 // Pack two fp32 into bf16x2 with RNE (lo -> bits 0..15, hi -> bits 16..31).
 // Matches round_to_bf16 (tiles.hpp:40-46) for finite inputs.
+// max(a, b, c) in one FMNMX3 (sm_100); NaN handling as fmaxf
+TKB_DEVICE float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 TKB_DEVICE uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

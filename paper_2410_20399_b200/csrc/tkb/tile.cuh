@@ -178,15 +178,17 @@ TKB_DEVICE void mm_AB(const tt_fl<N>& d, const tt_bf<K / 2>& a, const st_bf<K, N
 // ---- row reductions over a thread's row fragment (accumulating forms, tiles.hpp:290-309)
 template <int N>
 TKB_DEVICE void row_max(float& m, const rt_fl<N>& x) {
-    float a = x.v[0], b = x.v[1], c = x.v[2], e = x.v[3];
+    // three-input FMNMX3 (sm_100): two elements per instruction, four independent chains
+    float acc[4] = {x.v[0], x.v[1], x.v[2], x.v[3]};
+    int j = 4;
 #pragma unroll
-    for (int j = 4; j < N; j += 4) {
-        a = fmaxf(a, x.v[j]);
-        b = fmaxf(b, x.v[j + 1]);
-        c = fmaxf(c, x.v[j + 2]);
-        e = fmaxf(e, x.v[j + 3]);
+    for (; j + 8 <= N; j += 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = fmax3(acc[k], x.v[j + 2 * k], x.v[j + 2 * k + 1]);
     }
-    m = fmaxf(m, fmaxf(fmaxf(a, b), fmaxf(c, e)));
+#pragma unroll
+    for (; j < N; ++j) acc[j & 3] = fmaxf(acc[j & 3], x.v[j]);
+    m = fmax3(m, fmax3(acc[0], acc[1], acc[2]), acc[3]);
 }
 template <int N>
 TKB_DEVICE void row_sum(float& l, const rt_fl<N>& x) {
