@@ -453,23 +453,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
 //     last dV / dK (they write the S / dP regions, which hold nothing live by then);
 //   - the finish reads dV / dK out of TMEM, releases them at once (dv_free / dk_free: the
 //     next task's first dV / dK overwrite them) and stores bf16 rows straight from registers.
-TKB_DEVICE void st_global_v4(void* ptr, uint4 v) {
-    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
-}
-
 // TMEM fp32 [lane][D/4 columns of group g] -> registers; the caller releases TMEM, then
-// rows_store_bf16 writes them (x mul) as bf16 to row `dst` (columns [g D/4, (g+1) D/4)).
+// rows_store_bf16 writes them (x mul) as bf16. Warp-collective: lane l holds row
+// row0 + l (columns [g D/4, (g+1) D/4) at `lane0_dst` + l * row_stride). Stored as is, each
+// 16-byte store instruction would touch 32 rows = 32 L2 lines, and the L1 store path
+// (~1 line / clk) then stalls the warps for thousands of cycles per task (measured: -11 %
+// causal, -33 % N = 1024 backward). The rows are first transposed through shuffles so that
+// each instruction writes SEG contiguous bytes of 32 / CH rows (CH = SEG / 16 lanes per
+// row): 4x (D = 128) / 2x (D = 64) fewer lines per warp. Rows >= rows_valid are skipped.
 template <int D>
-TKB_DEVICE void rows_store_bf16(const uint32_t* v, __nv_bfloat16* dst, float mul) {
+TKB_DEVICE void rows_store_bf16(const uint32_t* v, __nv_bfloat16* lane0_dst, long long row_stride, int rows_valid,
+                                float mul) {
+    constexpr int kU32 = D / 8;      // packed bf16 pairs per lane (its row segment)
+    constexpr int kCh = kU32 / 4;    // 16-byte chunks per row segment
+    constexpr int kRpi = 32 / kCh;   // rows per store instruction
+    uint32_t pk[kU32];
 #pragma unroll
-    for (int q = 0; q < D / 32; ++q) {
-        uint4 u;
-        u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * mul, __uint_as_float(v[8 * q + 1]) * mul);
-        u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * mul, __uint_as_float(v[8 * q + 3]) * mul);
-        u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * mul, __uint_as_float(v[8 * q + 5]) * mul);
-        u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * mul, __uint_as_float(v[8 * q + 7]) * mul);
-        st_global_v4(dst + 8 * q, u);
+    for (int j = 0; j < kU32; ++j) pk[j] = pack_bf16x2(__uint_as_float(v[2 * j]) * mul, __uint_as_float(v[2 * j + 1]) * mul);
+    const int lane = laneid();
+    const int c = lane % kCh;
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+        const int src = k * kRpi + lane / kCh;  // the row this lane writes now
+        uint32_t out[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            out[j] = 0;
+#pragma unroll
+            for (int cc = 0; cc < kCh; ++cc) {
+                const uint32_t t = __shfl_sync(0xffffffffu, pk[4 * cc + j], src);
+                out[j] = (cc == c) ? t : out[j];
+            }
+        }
+        if (src < rows_valid) st_global_v4(lane0_dst + (size_t)src * row_stride + 8 * c, make_uint4(out[0], out[1], out[2], out[3]));
     }
 }
 
@@ -522,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     mbarrier& dv_free = bars[4];    // the finish has read dV out of TMEM
     mbarrier& dkv_full = bars[5];
     mbarrier& dk_free = bars[6];
+    mbarrier& staged_full = bars[7];  // a finish has staged dV / dK in two ring slots
     static_assert(SQ <= 4 && SD <= 3 && SA <= 2, "barrier slots");
     mbarrier* q_full = bars + 8;      // [SQ]
     mbarrier* q_empty = bars + 12;    // [SQ]
@@ -561,6 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         mbar_init(&dv_free, kComputeThreads);
         mbar_init(&dkv_full, 1);
         mbar_init(&dk_free, kComputeThreads);
+        mbar_init(&staged_full, kComputeThreads);
         for (int g = 0; g < kGroups; ++g) {
             mbar_init(&p_full[g], 128);
             mbar_init(&ds_full[g], 128);
@@ -596,6 +614,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
             const uint64_t pol_keep = tma::policy_evict_last();
             int x = 0;  // global step (ring position)
             int n = 0;
+            int staged = 0;  // staged finishes stored
+            KvTask prev{0, 0, 0};
             int id = queue.claim(0, p.sched, tasks);
             while (id >= 0) {
                 const KvTask w = decode(id);
@@ -607,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                     tma::load_4d(sK + a * kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, w.head, w.batch, pol_stream);
                     tma::load_4d(sV + a * kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, w.head, w.batch, pol_stream);
                 }
+                const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
                 for (int t = 0; t < T; ++t, ++x) {
                     const int i = (CAUSAL ? w.j : 0) + t % T1;
                     const int hq = w.head * p.group + t / T1;
@@ -618,6 +639,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                     for (int a = 0; a < TL::kAtoms; ++a)
                         tma::load_4d(sQ + sq * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[sq], a * 64,
                                      i * 128, hq, w.batch, pol_keep);
+                    if (after_staged && t == 1) {
+                        // the previous task's finish staged dV / dK in the dO slot of step 1 and the
+                        // Q slot of step 2: store them (this warp, off the compute warps' path)
+                        // and refill the slots once the store has read them
+                        mbar_wait(&staged_full, staged & 1);
+                        ++staged;
+                        uint8_t* stage_v = sQ + ((x + 1) % SQ) * TL::kTileBytes;
+                        uint8_t* stage_k = sDo + (x % SD) * TL::kTileBytes;
+                        for (int a = 0; a < TL::kAtoms; ++a) {
+                            tma::store_4d(&p.tm_dv, stage_v + a * kAtomBytes, a * 64, prev.j * 128, prev.head,
+                                          prev.batch);
+                            tma::store_4d(&p.tm_dk, stage_k + a * kAtomBytes, a * 64, prev.j * 128, prev.head,
+                                          prev.batch);
+                        }
+                        tma::commit_group();
+                        tma::wait_group_read<0>();
+                    }
                     mbar_wait(&do_empty[sd], ((x / SD) & 1) ^ 1);
                     mbar_arrive_expect_tx(&do_full[sd], TL::kTileBytes);
                     for (int a = 0; a < TL::kAtoms; ++a)
@@ -628,8 +666,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                     tma::load_1d(sLse + sa * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &aux_full[sa]);
                     tma::load_1d(sDelta + sa * 128, p.delta + bhq * p.n_pad + i * 128, 512, &aux_full[sa]);
                 }
+                prev = w;
                 id = queue.claim(++n, p.sched, tasks);
             }
+            tma::wait_group<0>();
         }
     } else if (warp == kWarpMma) {
         // ----------------------------------------------------------------- MMA (converged warp)
@@ -715,6 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 mbar_wait(&aux_full[sa], (x / SA) & 1);
                 mbar_wait(&s_full, x & 1);
                 if (threadIdx.x == 0) TKB_TR(1, x, 0);
+                if (threadIdx.x == 0 && t == 0 && n > 0) TKB_TR(1, n - 1, 7);  // next task's first S
                 tmem::fence_after();
                 float pf[32];
                 tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
@@ -755,26 +796,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 if (threadIdx.x == 0) TKB_TR(1, x, 3);
             }
             x0 += T;
-            // FINISH: dV / dK rows out of TMEM (released at once), bf16 rows to global
+            // FINISH. When the next task has >= 3 steps, dV / dK are staged (bf16, SW128) in the
+            // ring slots its step-2 Q and step-1 dO will use — both slots' last data (this task's
+            // final step) are consumed — and TMA-stored; the load warp refills those two slots
+            // only after the store has read them (stage_free). The compute warps are back on the
+            // next task's exponentials after ~500 clk. Otherwise rows are stored from registers
+            // (~2,000 clk per tensor: the per-thread store path is slow).
             mbar_wait(&dkv_full, n & 1);
+            if (threadIdx.x == 0) TKB_TR(1, n, 4);
             tmem::fence_after();
-            const int row = kv0 + r;
-            const size_t off = (size_t)w.batch * p.kv_sb + (size_t)w.head * p.kv_sh + (size_t)row * p.kv_sn + g * (D / 4);
-            uint32_t v[D / 4];
-            if constexpr (D == 128)
-                tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
-            else
-                tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
-            tmem::fence_before();
-            mbar_arrive(&dv_free);
-            if (row < p.n) rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dv) + off, 1.f);
-            if constexpr (D == 128)
-                tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
-            else
-                tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
-            tmem::fence_before();
-            mbar_arrive(&dk_free);
-            if (row < p.n) rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dk) + off, p.scale);
+            const int id_next = queue.get_warp(n + 1);
+            const bool staged = id_next >= 0 && steps(decode(id_next)) >= 3;
+            if (staged) {
+                uint8_t* stage_v = sQ + ((x0 + 2) % SQ) * TL::kTileBytes;
+                uint8_t* stage_k = sDo + ((x0 + 1) % SD) * TL::kTileBytes;
+                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dv(), stage_v, r, g);
+                tmem::fence_before();
+                mbar_arrive(&dv_free);
+                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dk(), stage_k, r, g, p.scale);
+                tmem::fence_before();
+                mbar_arrive(&dk_free);
+                tma::fence_async_smem();
+                mbar_arrive(&staged_full);  // the load warp stores them
+            } else {
+                const int row0 = kv0 + wq * 32;  // row of lane 0
+                const size_t off =
+                    (size_t)w.batch * p.kv_sb + (size_t)w.head * p.kv_sh + (size_t)row0 * p.kv_sn + g * (D / 4);
+                uint32_t v[D / 4];
+                if constexpr (D == 128)
+                    tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
+                else
+                    tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
+                tmem::fence_before();
+                mbar_arrive(&dv_free);
+                rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dv) + off, p.kv_sn, p.n - row0, 1.f);
+                if constexpr (D == 128)
+                    tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
+                else
+                    tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
+                tmem::fence_before();
+                mbar_arrive(&dk_free);
+                rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dk) + off, p.kv_sn, p.n - row0, p.scale);
+            }
+            if (threadIdx.x == 0) TKB_TR(1, n, 6);
             __syncwarp();
             if (lane == 0) queue.release(n);
         }
@@ -1207,7 +1271,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         mbar_init(&s_full, 1);
         mbar_init(&s_free, kComputeThreads);
         mbar_init(&a_ready, kComputeThreads);
-        mbar_init(&qdo_free, kComputeThreads);
+        mbar_init(&qdo_free, 1);
         mbar_init(&dp_full, 1);
         mbar_init(&qa_free, 1);
         mbar_init(&dq_full, 1);
@@ -1341,10 +1405,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             tmem::wait_st();
             tmem::fence_before();
             mbar_arrive(&a_ready);
-            mbar_arrive(&qdo_free);  // SMEM Q / dO may be refilled with the next task's
         };
+        // SMEM Q / dO are released (qdo_free) once copied into TMEM AND once the previous
+        // task's finish, which stages dQ in sQ for its TMA store, has been read out
         int t = queue.get_warp(0);
-        if (t >= 0) stage_a(0);
+        if (t >= 0) {
+            stage_a(0);
+            named_sync(kBarCompute, kComputeThreads);
+            if (threadIdx.x == 0) mbar_arrive(&qdo_free);
+        }
         while (t >= 0) {
             const QTask w = qtask<CAUSAL>(p, t);
             const int b = w.bh / p.heads, h = w.bh - b * p.heads;
@@ -1391,26 +1460,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             // the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this finish)
             const int t_next = queue.get_warp(n + 1);
             if (t_next >= 0) stage_a(n + 1);
-            // FINISH: dQ (TMEM fp32) -> registers -> bf16 row stores (dQ = scale dS K); the next
-            // task's first dQ GEMM waits for its dS, which these warps produce after this
+            // FINISH: dQ (TMEM fp32) -> bf16 -> SW128 staging in sQ (its Q is in TMEM by now)
+            // -> TMA store; sQ / sDo are released to the load warp once the store has read it.
+            // (Per-thread row stores from registers cost ~2,400 clk per task: each store
+            // instruction touches 16-32 L2 lines.) The next task's first dQ GEMM waits for its
+            // dS, which these warps produce after this.
             mbar_wait(&dq_full, n & 1);
             tmem::fence_after();
-            {
-                uint32_t v[D / 4];
-                if constexpr (D == 128)
-                    tmem::ldw_32x32b_x32(tbase + lane_off + C::tmem_dq() + g * (D / 4), v);
-                else
-                    tmem::ldw_32x32b_x16(tbase + lane_off + C::tmem_dq() + g * (D / 4), v);
-                if (row < p.n)
-                    rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dq) + (size_t)b * p.q_sb +
-                                              (size_t)h * p.q_sh + (size_t)row * p.q_sn + g * (D / 4),
-                                       p.scale);
+            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sQ, r, g, p.scale);  // dQ = scale dS K
+            tma::fence_async_smem();
+            named_sync(kBarCompute, kComputeThreads);
+            if (threadIdx.x == 0) {
+                for (int a = 0; a < TL::kAtoms; ++a) tma::store_4d(&p.tm_dq, sQ + a * kAtomBytes, a * 64, q0, h, b);
+                tma::commit_group();
+                tma::wait_group_read<0>();
+                mbar_arrive(&qdo_free);
             }
             __syncwarp();
             if (lane == 0) queue.release(n);  // every warp read task n's id long ago
             t = t_next;
             ++n;
         }
+        if (threadIdx.x == 0) tma::wait_group<0>();
     }
 
     tmem::fence_before();

@@ -68,6 +68,11 @@ TKB_DEVICE void named_arrive(int id, int nthreads) {
 
 // Pack two fp32 into bf16x2 with RNE (lo -> bits 0..15, hi -> bits 16..31).
 // Matches round_to_bf16 (tiles.hpp:40-46) for finite inputs.
+TKB_DEVICE void st_global_v4(void* ptr, uint4 v) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // max(a, b, c) in one FMNMX3 (sm_100); NaN handling as fmaxf
 TKB_DEVICE float fmax3(float a, float b, float c) {
     float d;

@@ -28,6 +28,13 @@ TKB_DEVICE void mbar_arrive(mbarrier* b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
+// Arrive without release semantics: for hand-offs of TMEM data (ordered by the tcgen05
+// fences) where no generic-proxy memory written before the arrive is read by the waiter.
+// A release arrive would first wait for the thread's outstanding global stores.
+TKB_DEVICE void mbar_arrive_relaxed(mbarrier* b) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
 TKB_DEVICE void mbar_arrive_cnt(mbarrier* b, uint32_t cnt) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt)
                  : "memory");

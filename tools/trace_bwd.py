@@ -45,3 +45,12 @@ for slot in range(slots):
     last = max(int(t[slot, 1, it, 3]) for it in range(31))
     if first or fin:
         print(f"slot {slot}: first s_full {first}, last traced dS {last}, finish {fin}")
+
+# persistent dK/dV finish per task n (role 1 events 4-7: dkv_full, dV stored, dK stored, next task's first S)
+for slot in range(min(slots, 2)):
+    for n in range(1, 6):
+        e = [int(t[slot, 1, n, i]) for i in (4, 5, 6, 7)]
+        l5, l6 = int(t[slot, 0, n, 5]), int(t[slot, 0, n, 6])
+        if e[0]:
+            print(f"slot {slot} task {n}: dkv_full {e[0]}  +dV read {l5 - e[0] if l5 else -1}  +dV stored {e[1] - e[0]}"
+                  f"  +dK read {l6 - e[0] if l6 else -1}  +dK stored {e[2] - e[0]}  +next S {e[3] - e[0] if e[3] else -1}")
