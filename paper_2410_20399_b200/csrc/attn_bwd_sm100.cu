@@ -42,6 +42,10 @@
 #include "tkb/tcgen05.cuh"
 #include "tkb/tma.cuh"
 
+#ifndef TKB_BWD_POLY
+#define TKB_BWD_POLY 1  // a quarter of the exponentials on the FMA-pipe polynomial
+#endif
+
 namespace tkb {
 namespace bwd {
 
@@ -177,7 +181,7 @@ TKB_DEVICE void exp_chunk(float* pf, float tau, uint32_t nlse4, float nlse_r) {
         pf[c] = ex2_approx(x01.x);
         pf[c + 1] = ex2_approx(x01.y);
         float2 p23;
-        if ((c & 8) != 0) {
+        if (TKB_BWD_POLY && (c & 8) != 0) {
             p23 = ex2_poly2(x23);
         } else {
             p23.x = ex2_approx(x23.x);
@@ -1492,6 +1496,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 #undef TKB_TR
 
 // Delta = rowsum(dO o O), lse2 = -L log2 e (-inf / 0 on padded rows: P = 0 there).
+// HBM-bound: each thread owns 16 bytes of kPrepRows rows (rows kPrepRows * 16 / (D / 8) apart
+// within the block's row range) and issues all their loads before reducing, so a thread
+// keeps 2 * 16 * kPrepRows bytes in flight.
+constexpr int kPrepRows = 4;
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
@@ -1499,32 +1507,43 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
                                                        float* __restrict__ delta, int heads, int n, int n_pad,
                                                        int64_t sb, int64_t sh, int64_t sn) {
     constexpr int kLanesPerRow = D / 8;
-    constexpr int kRowsPerBlock = 256 / kLanesPerRow;
+    constexpr int kRowsPerPass = 256 / kLanesPerRow;
     const int bh = blockIdx.y;
     const int b = bh / heads, hh = bh % heads;
-    const int row = blockIdx.x * kRowsPerBlock + threadIdx.x / kLanesPerRow;
     const int c = (threadIdx.x % kLanesPerRow) * 8;
-    float acc = 0.f;
-    if (row < n) {
-        const int64_t off = b * sb + hh * sh + (int64_t)row * sn + c;
-        const uint4 ov = *reinterpret_cast<const uint4*>(o + off);
-        const uint4 dv = *reinterpret_cast<const uint4*>(dout + off);
-        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
-        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+    const int row_base = blockIdx.x * kRowsPerPass * kPrepRows + threadIdx.x / kLanesPerRow;
+    uint4 ov[kPrepRows], dv[kPrepRows];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float2 a = __bfloat1622float2(o2[k]);
-            const float2 g = __bfloat1622float2(d2[k]);
-            acc = fmaf(a.x, g.x, acc);
-            acc = fmaf(a.y, g.y, acc);
+    for (int k = 0; k < kPrepRows; ++k) {
+        const int row = row_base + k * kRowsPerPass;
+        ov[k] = make_uint4(0, 0, 0, 0);
+        dv[k] = make_uint4(0, 0, 0, 0);
+        if (row < n) {
+            const int64_t off = b * sb + hh * sh + (int64_t)row * sn + c;
+            ov[k] = __ldg(reinterpret_cast<const uint4*>(o + off));
+            dv[k] = __ldg(reinterpret_cast<const uint4*>(dout + off));
         }
     }
 #pragma unroll
-    for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-    if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
-        const size_t idx = (size_t)bh * n_pad + row;
-        delta[idx] = row < n ? acc : 0.f;
-        lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
+    for (int k = 0; k < kPrepRows; ++k) {
+        const int row = row_base + k * kRowsPerPass;
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov[k]);
+        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[k]);
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 a = __bfloat1622float2(o2[q]);
+            const float2 g = __bfloat1622float2(d2[q]);
+            acc = fmaf(a.x, g.x, acc);
+            acc = fmaf(a.y, g.y, acc);
+        }
+#pragma unroll
+        for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+        if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
+            const size_t idx = (size_t)bh * n_pad + row;
+            delta[idx] = row < n ? acc : 0.f;
+            lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
+        }
     }
 }
 
@@ -1580,7 +1599,7 @@ int launch_all(bool causal, const BwdParams& p, int batches, const void* o, cons
                int* launches) {
     *launches = 0;
     if (phases & 1) {
-        constexpr int kRowsPerBlock = 256 / (D / 8);
+        constexpr int kRowsPerBlock = 256 / (D / 8) * kPrepRows;
         dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, batches * p.heads);
         bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                   reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
