@@ -40,7 +40,7 @@
 #include "tkb/tile.cuh"
 
 #ifndef TKB_FWD_POLY64
-#define TKB_FWD_POLY64 2
+#define TKB_FWD_POLY64 1
 #endif
 #ifndef TKB_FWD_POLY128
 #define TKB_FWD_POLY128 2
