@@ -16,8 +16,6 @@ constexpr int kRowsPerCta = kBlockM * kQStages;
 
 struct FwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_o;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128
-    void* o;                             // O base and element strides (finish: direct row stores)
-    long long o_sb, o_sh, o_sn;
     float* lse;                          // [B*H, N] fp32, may be null
     int* sched;                          // persistent task counter pair (self-resetting)
     long long* trace;                    // optional per-role cycle timeline (tkb_debug_set_trace)

@@ -45,9 +45,6 @@
 #ifndef TKB_FWD_POLY128
 #define TKB_FWD_POLY128 2
 #endif
-#ifndef TKB_FWD_SLOTS128
-#define TKB_FWD_SLOTS128 5
-#endif
 #ifndef TKB_FWD_PCHUNKS
 #define TKB_FWD_PCHUNKS 2
 #endif
@@ -59,12 +56,7 @@ template <int D>
 struct Cfg {
     using Tile = st_bf<128, D>;
     static constexpr int kTile = Tile::kBytes;
-#ifndef TKB_FWD_ROW_STORE
     static constexpr int kKvSlots = (D == 128) ? 4 : 8;  // K and V alternate in the ring
-#else
-    // the finish stores O rows from registers, so the 32 KB of staging atoms hold a fifth slot
-    static constexpr int kKvSlots = (D == 128) ? TKB_FWD_SLOTS128 : 8;  // K and V alternate in the ring
-#endif
     // exp2 of one pair in every group of four columns, on kPolyGroups of every 4 groups, runs as
     // a polynomial on the FMA pipe (a quarter of the exponentials at 2): per SM sub-partition
     // the two softmax warps' 128 ex2 per kv block occupy MUFU (4 lanes / clk) for 2048 clk,
@@ -74,11 +66,7 @@ struct Cfg {
     static constexpr int kSmemQ = kQStages * kTile;
     static constexpr int kSmemKv = kKvSlots * kTile;
     static constexpr int kStageBytes = 128 * 128;  // per-warpgroup O staging: one 128 x 64 atom
-#ifndef TKB_FWD_ROW_STORE
     static constexpr int kSmemBytes = kSmemQ + kSmemKv + kQStages * kStageBytes + 1024;  // + alignment slack
-#else
-    static constexpr int kSmemBytes = kSmemQ + kSmemKv + 1024;  // + alignment slack
-#endif
     static_assert(kSmemBytes + 512 <= 232448, "smem");
     static TKB_DEVICE constexpr uint32_t tmem_s(int s) { return s * 128u; }
     static TKB_DEVICE constexpr uint32_t tmem_o(int s) { return 256u + s * D; }
@@ -103,10 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     auto sKV = [&](int slot) { return Tile{smem + C::kSmemQ + slot * C::kTile}; };
     const gl gQ{&p.tm_q}, gK{&p.tm_k}, gV{&p.tm_v}, gO{&p.tm_o};
 
-#ifndef TKB_FWD_ROW_STORE
     const st_bf<128, 64> sStage[kQStages] = {st_bf<128, 64>{smem + C::kSmemQ + C::kSmemKv},
                                               st_bf<128, 64>{smem + C::kSmemQ + C::kSmemKv + C::kStageBytes}};
-#endif
 
     __shared__ mbarrier q_full[kQStages], q_empty[kQStages], s_full[kQStages], o_full[kQStages];
     __shared__ mbarrier p_full[kQStages][kPChunks];
@@ -393,7 +379,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         tmem::fence_after();
         if (p.lse != nullptr && row < n)
             p.lse[(size_t)(batch * p.heads + head) * n + row] = (m + __log2f(l)) * kLn2;
-#ifndef TKB_FWD_ROW_STORE
         const bool leader = (wq == 0 && lane == 0);
 #pragma unroll 1
         for (int a = 0; a < Tile::kAtoms; ++a) {
@@ -424,35 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 tma::commit_group();
             }
         }
-#else
-        // O / l rows straight from registers to HBM, 32 columns at a time (no staging, no
-        // warpgroup barriers: the next task's first exponentials start sooner)
-        {
-            __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + (size_t)batch * p.o_sb +
-                                  (size_t)head * p.o_sh + (size_t)row * p.o_sn;
-            const float inv_l = 1.f / l;
-#pragma unroll 1
-            for (int c = 0; c < D; c += 32) {
-                rt_fl<32> o;
-                load(o, tO + c);
-                load_wait(o);
-                if (c == D - 32) tmem::fence_before();  // O_s drained: the next task's PV may overwrite it
-                mul(o, inv_l);  // div_row (tiles.hpp:276-281)
-                rt_bf<32> b;
-                copy(b, o);
-                if (row < n) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        st_global_v4(orow + c + 8 * q,
-                                     make_uint4(b.v[4 * q], b.v[4 * q + 1], b.v[4 * q + 2], b.v[4 * q + 3]));
-                }
-            }
-        }
-#endif
         }  // task loop
-#ifndef TKB_FWD_ROW_STORE
         if (wq == 0 && lane == 0) tma::wait_group<0>();
-#endif
     }
 
     tmem::fence_before();

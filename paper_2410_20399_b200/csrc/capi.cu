@@ -200,10 +200,6 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
     int sms = 0;
     if ((rc = device_state(&sms, &p.sched))) return rc;
     p.lse = lse;
-    p.o = o;
-    p.o_sb = s.b;
-    p.o_sh = s.h;
-    p.o_sn = s.n;
     p.trace = g_trace;
     p.trace_every = g_trace_every;
     p.trace_slots = g_trace_slots;
