@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid
 //     tasks, so the next task's first S^T / dP^T GEMMs are issued right behind this task's
 //     last dV / dK (they write the S / dP regions, which hold nothing live by then);
 //   - the finish reads dV / dK out of TMEM, releases them at once (dv_free / dk_free: the
-//     next task's first dV / dK overwrite them) and stores bf16 rows straight from registers.
+//     next task's first dV / dK overwrite them) and stages them in two ring slots for a TMA
+//     store issued by the load warp (see FINISH below).
 // TMEM fp32 [lane][D/4 columns of group g] -> registers; the caller releases TMEM, then
 // rows_store_bf16 writes them (x mul) as bf16. Warp-collective: lane l holds row
 // row0 + l (columns [g D/4, (g+1) D/4) at `lane0_dst` + l * row_stride). Stored as is, each
