@@ -562,12 +562,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     const int hkv = p.heads / p.group;
     const int tasks = nq * hkv * (p.bh / p.heads);
     // task id -> (kv block fastest, kv head, batch): the CTAs running together share heads
+    // With few tasks (grouped-query heads: a task walks its group's query heads) causal
+    // tasks of very different lengths must start longest-first or the last long one sets
+    // the tail: kv block slowest. Otherwise kv block fastest, so the CTAs running together
+    // share heads and their Q / dO stay in L2.
+    const bool heavy_first = CAUSAL && tasks < 4 * p.num_sms;
+    const int hb = hkv * (p.bh / p.heads);
     auto decode = [&](int id) {
         KvTask w;
-        w.j = id % nq;
-        const int r = id / nq;
-        w.head = r % hkv;
-        w.batch = r / hkv;
+        if (heavy_first) {
+            w.j = id / hb;
+            const int r = id - w.j * hb;
+            w.head = r % hkv;
+            w.batch = r / hkv;
+        } else {
+            w.j = id % nq;
+            const int r = id / nq;
+            w.head = r % hkv;
+            w.batch = r / hkv;
+        }
         return w;
     };
     auto steps = [&](const KvTask& w) { return (CAUSAL ? (nq - w.j) : nq) * p.group; };
