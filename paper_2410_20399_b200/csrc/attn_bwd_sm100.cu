@@ -562,25 +562,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     const int hkv = p.heads / p.group;
     const int tasks = nq * hkv * (p.bh / p.heads);
     // task id -> (kv block fastest, kv head, batch): the CTAs running together share heads
-    // With few tasks (grouped-query heads: a task walks its group's query heads) causal
-    // tasks of very different lengths must start longest-first or the last long one sets
-    // the tail: kv block slowest. Otherwise kv block fastest, so the CTAs running together
-    // share heads and their Q / dO stay in L2.
-    const bool heavy_first = CAUSAL && tasks < 4 * p.num_sms;
-    const int hb = hkv * (p.bh / p.heads);
+    // Task order. Non-causal: kv block fastest, so the CTAs running together share heads and
+    // their Q / dO stay in L2. Causal: kv (batch, head) units in L2-sized groups (p.head_group,
+    // as the dQ kernel), inside a group the long tasks (small kv block index) first, so the
+    // queue ends on short tasks; with fewer than 4 tasks per SM (grouped-query heads: a task
+    // walks its group's query heads) one group spans everything — longest-first overall.
+    const int hb = hkv * (p.bh / p.heads);  // (batch, kv head) units
+    const int G = (tasks < 4 * p.num_sms) ? hb : max(1, min(hb, p.head_group / max(1, p.group)));
     auto decode = [&](int id) {
         KvTask w;
-        if (heavy_first) {
-            w.j = id / hb;
-            const int r = id - w.j * hb;
-            w.head = r % hkv;
-            w.batch = r / hkv;
+        int unit;
+        if (CAUSAL) {
+            const int sec = id / (G * nq);
+            const int r = id - sec * G * nq;
+            const int gs = min(G, hb - sec * G);
+            w.j = r / gs;
+            unit = sec * G + (r - w.j * gs);
         } else {
             w.j = id % nq;
-            const int r = id / nq;
-            w.head = r % hkv;
-            w.batch = r / hkv;
+            unit = id / nq;
         }
+        w.head = unit % hkv;
+        w.batch = unit / hkv;
         return w;
     };
     auto steps = [&](const KvTask& w) { return (CAUSAL ? (nq - w.j) : nq) * p.group; };
