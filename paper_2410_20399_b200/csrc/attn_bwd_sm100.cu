@@ -537,7 +537,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
     mbarrier& kv_full = bars[0];
-    mbarrier& s_full = bars[1];
+    // D = 64 leaves 128 TMEM columns free: S^T is double-buffered there (the second buffer at
+    // column 384), so S^T_{t+1} is issued before dV_t and the exponentials of step t+1 do not
+    // wait for the dV GEMM that reads P_t (the D = 64 step is bound by that chain, not by
+    // its 1024 clk of MMA). Per-buffer s_full / p_full keep the phases one apart.
+    constexpr bool kDS = (D == 64);
+    auto s_buf = [](int x) -> uint32_t { return kDS ? ((x & 1) ? 384u : 0u) : CT::tmem_s(); };
+    auto s_full_of = [&](int x) -> mbarrier& { return (kDS && (x & 1)) ? bars[26] : bars[1]; };
+    auto p_full_of = [&](int x) -> mbarrier* { return (kDS && (x & 1)) ? bars + 46 : bars + 32; };
+    auto ph_of = [](int x) -> uint32_t { return kDS ? ((x >> 1) & 1) : (x & 1); };  // per-buffer phase
     mbarrier& kv_empty = bars[2];   // the task's last S^T / dP^T retired: K / V reloadable
     mbarrier& dp_full = bars[3];
     mbarrier& dv_free = bars[4];    // the finish has read dV out of TMEM
@@ -551,7 +559,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     mbarrier* do_empty = bars + 19;   // [SD]
     mbarrier* aux_full = bars + 22;   // [SA] lse2 / delta
     mbarrier* aux_empty = bars + 24;  // [SA]
-    mbarrier* p_full = bars + 32;    // [kGroups]
     mbarrier* ds_full = bars + 36;   // [kGroups]
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
     lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);
@@ -593,7 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
     if (warp == kWarpLoad && lane == 0) {
         queue.init(1 + 16);
         mbar_init(&kv_full, 1);
-        mbar_init(&s_full, 1);
+        mbar_init(&bars[1], 1);
+        mbar_init(&bars[26], 1);
         mbar_init(&kv_empty, 1);
         mbar_init(&dp_full, 1);
         mbar_init(&dv_free, kComputeThreads);
@@ -601,7 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         mbar_init(&dk_free, kComputeThreads);
         mbar_init(&staged_full, kComputeThreads);
         for (int g = 0; g < kGroups; ++g) {
-            mbar_init(&p_full[g], 128);
+            mbar_init(&bars[32 + g], 128);
+            mbar_init(&bars[46 + g], 128);
             mbar_init(&ds_full[g], 128);
         }
         for (int s = 0; s < SQ; ++s) {
@@ -702,8 +711,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         auto issue_s = [&](int x) {
             mbar_wait(&q_full[x % SQ], (x / SQ) & 1);
             tmem::fence_after();
-            mm_abt<D>(tbase + CT::tmem_s(), aK, qaddr(x), id_s);
-            umma::commit_e(&s_full);
+            mm_abt<D>(tbase + s_buf(x), aK, qaddr(x), id_s);
+            umma::commit_e(&s_full_of(x));
         };
         auto issue_dp = [&](int x) {
             mbar_wait(&do_full[x % SD], (x / SD) & 1);
@@ -726,13 +735,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 const uint32_t ph = x & 1;
                 TKB_TR(0, x, 0);
                 if (t == 0 && n > 0) mbar_wait(&dv_free, (n - 1) & 1);  // previous task's dV read out
-                mma_tmem_a_groups(tbase + CT::tmem_dv(), tbase + CT::tmem_s(), doaddr(x), id_kv, t > 0, [&](int g) {
-                    mbar_wait(&p_full[g], ph);
+                if (kDS && t + 1 < T) issue_s(x + 1);  // other buffer: its P_{t-1} went to dV_{t-1}, issued before
+                mma_tmem_a_groups(tbase + CT::tmem_dv(), tbase + s_buf(x), doaddr(x), id_kv, t > 0, [&](int g) {
+                    mbar_wait(&p_full_of(x)[g], ph_of(x));
                     tmem::fence_after();
                 });
                 TKB_TR(0, x, 1);
                 umma::commit_e(&do_empty[x % SD]);
-                if (t + 1 < T) issue_s(x + 1);  // overwrites P_t, read by dV_t issued before
+                if (!kDS && t + 1 < T) issue_s(x + 1);  // overwrites P_t, read by dV_t issued before
                 TKB_TR(0, x, 2);
                 if (t == 0 && n > 0) mbar_wait(&dk_free, (n - 1) & 1);
                 mma_tmem_a_groups(tbase + CT::tmem_dk(), tbase + CT::tmem_dp(), qaddr(x), id_kv, t > 0, [&](int g) {
@@ -757,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         const int g = warp >> 2;
         const int r = wq * 32 + lane;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tbase + lane_off + CT::tmem_s() + 32 * g;
+        const uint32_t tS0 = tbase + lane_off + 32 * g;  // + s_buf(x)
         const uint32_t tDp = tbase + lane_off + CT::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
         int x0 = 0;
@@ -774,7 +784,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 const uint32_t nlse4 = smem_u32(sLse + sa * 128 + 32 * g);
                 const uint32_t dlt4 = smem_u32(sDelta + sa * 128 + 32 * g);
                 mbar_wait(&aux_full[sa], (x / SA) & 1);
-                mbar_wait(&s_full, x & 1);
+                mbar_wait(&s_full_of(x), ph_of(x));
+                const uint32_t tS = tS0 + s_buf(x);
                 if (threadIdx.x == 0) TKB_TR(1, x, 0);
                 if (threadIdx.x == 0 && t == 0 && n > 0) TKB_TR(1, n - 1, 7);  // next task's first S
                 tmem::fence_after();
@@ -791,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 tmem::st_32x32b_x16(tS, pk);
                 tmem::wait_st();
                 tmem::fence_before();
-                mbar_arrive(&p_full[g]);
+                mbar_arrive(&p_full_of(x)[g]);
                 if (threadIdx.x == 0) TKB_TR(1, x, 1);
                 mbar_wait(&dp_full, x & 1);
                 if (threadIdx.x == 0) TKB_TR(1, x, 2);
