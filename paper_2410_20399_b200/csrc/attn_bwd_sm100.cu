@@ -1278,14 +1278,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
     mbarrier& s_free = bars[2];
     mbarrier& a_ready = bars[3];    // Q / dO of a task copied into TMEM
     mbarrier& qdo_free = bars[4];   // SMEM Q / dO copied out: the next task's may load
-    mbarrier& dp_full = bars[5];
+    // D = 64 leaves 128 TMEM columns free: dP is double-buffered there (second buffer at
+    // column 384), so dP_{j+1} is issued before dQ_j instead of after it and the dS of step
+    // j+1 does not wait for the dQ GEMM that reads dS_j. Per-buffer dp_full / ds_full.
+    constexpr bool kDP = (D == 64);
+    auto dp_buf = [](uint32_t it) -> uint32_t { return kDP ? ((it & 1) ? 384u : C::tmem_dp()) : C::tmem_dp(); };
+    auto dp_full_of = [&](uint32_t it) -> mbarrier& { return (kDP && (it & 1)) ? bars[26] : bars[5]; };
+    auto ds_full_of = [&](uint32_t it) -> mbarrier* { return (kDP && (it & 1)) ? bars + 36 : bars + 32; };
+    auto ph_of = [](uint32_t it) -> uint32_t { return kDP ? ((it >> 1) & 1) : (it & 1); };
     mbarrier& qa_free = bars[6];    // last S / dP GEMM of a task retired: TMEM Q / dO reusable
     mbarrier& dq_full = bars[7];
     mbarrier* k_full = bars + 8;    // [SK]
     mbarrier* k_empty = bars + 13;  // [SK]
     mbarrier* v_full = bars + 18;   // [SV]
     mbarrier* v_empty = bars + 22;  // [SV]
-    mbarrier* ds_full = bars + 32;  // [kGroups] dS chunks (32 keys each)
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
     lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);  // dynamic task claims
 
@@ -1304,10 +1310,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         mbar_init(&s_free, kComputeThreads);
         mbar_init(&a_ready, kComputeThreads);
         mbar_init(&qdo_free, 1);
-        mbar_init(&dp_full, 1);
+        mbar_init(&bars[5], 1);
+        mbar_init(&bars[26], 1);
         mbar_init(&qa_free, 1);
         mbar_init(&dq_full, 1);
-        for (int g = 0; g < kGroups; ++g) mbar_init(&ds_full[g], 128);
+        for (int g = 0; g < kGroups; ++g) {
+            mbar_init(&bars[32 + g], 128);
+            mbar_init(&bars[36 + g], 128);
+        }
         for (int s = 0; s < SK; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
@@ -1378,11 +1388,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(x), id_s);
             umma::commit_e(&s_full);
         };
-        auto issue_dp = [&](int x) {  // dP = dO V^T
+        auto issue_dp = [&](int x, uint32_t itx) {  // dP = dO V^T (iteration itx)
             mbar_wait(&v_full[x % SV], (x / SV) & 1);
             tmem::fence_after();
-            mm_tmem_abt<D>(tbase + C::tmem_dp(), tbase + C::tmem_doa(), vaddr(x), id_s);
-            umma::commit_e(&dp_full);
+            mm_tmem_abt<D>(tbase + dp_buf(itx), tbase + C::tmem_doa(), vaddr(x), id_s);
+            umma::commit_e(&dp_full_of(itx));
             umma::commit_e(&v_empty[x % SV]);
         };
         for (int n = 0;; ++n) {
@@ -1392,23 +1402,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             const int nk = nk_of(qtask<CAUSAL>(p, t));
             mbar_wait(&a_ready, n & 1);  // this task's Q / dO are in TMEM
             issue_s(kv);
-            issue_dp(kv);
+            issue_dp(kv, it);
             if (nk == 1) umma::commit_e(&qa_free);  // the task's only S and dP are issued
             for (int jj = 0; jj < nk; ++jj, ++kv, ++it) {
                 if (jj + 1 < nk) {
                     mbar_wait(&s_free, it & 1);  // S_j read out by the compute warps
                     issue_s(kv + 1);
+                    if (kDP) {  // the other dP buffer: its dS_{j-1} went to dQ_{j-1}, issued before
+                        issue_dp(kv + 1, it + 1);
+                        if (jj + 2 == nk) umma::commit_e(&qa_free);  // the task's last S and dP are issued
+                    }
                 }
                 TKB_TR(0, (int)it, 0);
                 // dQ += dS K, one 32-key chunk per column group as it lands
-                mma_tmem_a_groups(tbase + C::tmem_dq(), tbase + C::tmem_dp(), kaddr(kv), id_q, jj > 0, [&](int g) {
-                    mbar_wait(&ds_full[g], it & 1);
+                mma_tmem_a_groups(tbase + C::tmem_dq(), tbase + dp_buf(it), kaddr(kv), id_q, jj > 0, [&](int g) {
+                    mbar_wait(&ds_full_of(it)[g], ph_of(it));
                     tmem::fence_after();
                 });
                 TKB_TR(0, (int)it, 1);
                 umma::commit_e(&k_empty[kv % SK]);
-                if (jj + 1 < nk) {
-                    issue_dp(kv + 1);  // overwrites dS_j, read by dQ_j issued before
+                if (!kDP && jj + 1 < nk) {
+                    issue_dp(kv + 1, it + 1);  // overwrites dS_j, read by dQ_j issued before
                     if (jj + 2 == nk) umma::commit_e(&qa_free);  // the task's last S and dP are issued
                 }
                 TKB_TR(0, (int)it, 2);
@@ -1422,7 +1436,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         const int r = wq * 32 + lane;  // q row == TMEM lane
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
         const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
-        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
+        const uint32_t tDp0 = tbase + lane_off + 32 * g;  // + dp_buf(it)
         const float tau = p.scale_log2;
         uint32_t it = 0;
         int n = 0;
@@ -1470,7 +1484,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 #pragma unroll
                     for (int c = 0; c < 32; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
                 }
-                mbar_wait(&dp_full, it & 1);
+                mbar_wait(&dp_full_of(it), ph_of(it));
+                const uint32_t tDp = tDp0 + dp_buf(it);
                 if (threadIdx.x == 0) TKB_TR(1, (int)it, 1);
                 tmem::fence_after();
                 uint32_t dpv[32];
@@ -1486,7 +1501,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 tmem::st_32x32b_x16(tDp, pk);  // inside the 32 dP columns this thread has read
                 tmem::wait_st();
                 tmem::fence_before();
-                mbar_arrive(&ds_full[g]);
+                mbar_arrive(&ds_full_of(it)[g]);
                 if (threadIdx.x == 0) TKB_TR(1, (int)it, 2);
             }
             // the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this finish)
