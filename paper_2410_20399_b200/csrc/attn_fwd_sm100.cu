@@ -97,6 +97,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     __shared__ mbarrier q_full[kQStages], q_empty[kQStages], s_full[kQStages], o_full[kQStages];
     __shared__ mbarrier p_full[kQStages][kPChunks];
     __shared__ lcsf::ring<C::kKvSlots> kv;
+    // D = 64: the 128 free TMEM columns hold a third S buffer; S / P rotate over three buffers
+    // in QK issue order, so QK_{i+1}(s) is issued before PV_i(s) and the next block's
+    // exponentials do not wait for the PV -> QK round trip (per-buffer s_full / p_full;
+    // pv_done marks each PV_s for the lazy O rescale)
+    constexpr bool k3 = (D == 64);
+    __shared__ mbarrier s_full3[3], p_full3[3][kPChunks], pv_done[kQStages];
     __shared__ lcsf::work_queue queue;
     __shared__ uint32_t tmem_slot;
 
@@ -129,6 +135,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         if (!CAUSAL) return w.nkv;
         return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, n) - 1) / kBlockN + 1);
     };
+    // k3: index of (tile s, block i) in the task's QK issue order, its buffer and TMEM column
+    auto qk_index = [](int s, int i, int nk0, int nk1) { return min(i, nk0) + min(i, nk1) + ((s == 1 && i < nk0) ? 1 : 0); };
+    auto sbuf_col = [](uint32_t b) -> uint32_t { return b == 0 ? 0u : (b == 1 ? 128u : 384u); };
 
     if (warp == kWarpLoad && lane == 0) {
         queue.init(1 + 8);  // the MMA warp and the 8 softmax warps
@@ -137,7 +146,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             mbar_init(&q_empty[s], 1);
             mbar_init(&s_full[s], 1);
             mbar_init(&o_full[s], 1);
+            mbar_init(&pv_done[s], 1);
             for (int c = 0; c < kPChunks; ++c) mbar_init(&p_full[s][c], WARPGROUP_THREADS);
+        }
+        for (int b = 0; b < 3; ++b) {
+            mbar_init(&s_full3[b], 1);
+            for (int c = 0; c < kPChunks; ++c) mbar_init(&p_full3[b][c], WARPGROUP_THREADS);
         }
         kv.init(1, 1);
         fence_barrier_init();
@@ -205,6 +219,83 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                                          sKV(vslot), c * kPChunkCols, acc || c > 0);
             }
         };
+        if constexpr (k3) {
+            lcsf::ring_state<C::kKvSlots> st;
+            uint32_t qbase = 0;  // QK index of the task's first block (buffer = index % 3)
+            for (int nt = 0;; ++nt) {
+                const int t = queue.get(nt);
+                if (lane == 0) queue.release(nt);
+                if (t < 0) break;
+                const Task w = decode(t);
+                const int nkv = w.nkv;
+                const int nk[kQStages] = {tile_blocks(w, 0), tile_blocks(w, 1)};
+                auto gidx = [&](int s, int i) { return qbase + (uint32_t)qk_index(s, i, nk[0], nk[1]); };
+                auto qk3 = [&](int s, int i, int kslot) {
+                    const uint32_t g = gidx(s, i);
+                    mm_ABt(tt_fl<128>{tbase + sbuf_col(g % 3)}, sQ[s], sKV(kslot));
+                    umma::commit_e(&s_full3[g % 3]);
+                };
+                auto pv3 = [&](int s, int i, int vslot) {  // O_s (+)= P_s(i) V
+                    const uint32_t g = gidx(s, i);
+#pragma unroll
+                    for (int c = 0; c < kPChunks; ++c) {
+                        mbar_wait(&p_full3[g % 3][c], (g / 3) & 1);
+                        tmem::fence_after();
+                        mma_AB_k<D, kPChunkCols>(
+                            tt_fl<D>{tbase + C::tmem_o(s)},
+                            tt_bf<kPChunkCols / 2>{tbase + sbuf_col(g % 3) + 64 + c * (kPChunkCols / 2)}, sKV(vslot),
+                            c * kPChunkCols, i > 0 || c > 0);
+                    }
+                    umma::commit_e(&pv_done[s]);
+                };
+                mbar_wait(&q_full[0], nt & 1);
+                mbar_wait(&q_full[1], nt & 1);
+                kv.wait_full(st);
+                tmem::fence_after();
+#pragma unroll
+                for (int s = 0; s < kQStages; ++s) {
+                    qk3(s, 0, st.slot);
+                    if (nk[s] == 1) umma::commit_e(&q_empty[s]);
+                }
+                umma::commit_e(&kv.empty[st.slot]);
+                st.advance();
+                for (int i = 1; i < nkv; ++i) {
+                    const int vslot = st.slot;
+                    kv.wait_full(st);  // V_{i-1}
+                    st.advance();
+                    const int kslot = st.slot;
+                    kv.wait_full(st);  // K_i (tile 1 always has block i here)
+                    tmem::fence_after();
+                    // QK_i(s) before PV_{i-1}(s): its buffer held block index - 3, whose PV was
+                    // issued earlier; the other tile's QK_i follows PV_{i-1}(0), which read its buffer
+#pragma unroll
+                    for (int s = 0; s < kQStages; ++s) {
+                        if (i < nk[s]) {
+                            qk3(s, i, kslot);
+                            if (i == nk[s] - 1) umma::commit_e(&q_empty[s]);
+                        }
+                        if (i - 1 < nk[s]) {
+                            pv3(s, i - 1, vslot);
+                            if (i - 1 == nk[s] - 1) umma::commit_e(&o_full[s]);
+                        }
+                    }
+                    umma::commit_e(&kv.empty[vslot]);
+                    umma::commit_e(&kv.empty[kslot]);
+                    st.advance();
+                }
+                const int vslot = st.slot;
+                kv.wait_full(st);
+#pragma unroll
+                for (int s = 0; s < kQStages; ++s) {
+                    if (nk[s] != nkv) continue;
+                    pv3(s, nkv - 1, vslot);
+                    umma::commit_e(&o_full[s]);
+                }
+                umma::commit_e(&kv.empty[vslot]);
+                st.advance();
+                qbase += (uint32_t)(nk[0] + nk[1]);
+            }
+        } else {
         lcsf::ring_state<C::kKvSlots> st;
         uint32_t it[kQStages] = {0, 0};  // PVs issued per tile: p_full phases
         for (int nt = 0;; ++nt) {
@@ -268,15 +359,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             umma::commit_e(&kv.empty[vslot]);
             st.advance();
         }
+        }
     } else {
         // ----------------------------- SOFTMAX + FINISH ------------------------------------
         const int s = warp / 4;                  // query tile of this warpgroup
         const int wq = warp % 4;                 // TMEM lane quarter
         const int row_in_tile = wq * 32 + lane;  // == TMEM lane
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tbase + lane_off + C::tmem_s(s);
-        const uint32_t tP = tS + 64;
+        const uint32_t tS_fixed = tbase + lane_off + C::tmem_s(s);
         const uint32_t tO = tbase + lane_off + C::tmem_o(s);
+        uint32_t qbase = 0;  // k3: QK index of this task's first block
+        uint32_t pvc = 0;    // k3: pv_done completions consumed
         const float tau = p.scale_log2;
 
         uint32_t sc = 0;  // s_full completions seen
@@ -292,9 +385,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const int head = w.head, batch = w.batch;
         float m = -INFINITY;  // running max of tau * S (the value actually subtracted)
         float l = 0.f;        // running normaliser (fp32 sum of fp32 P, kernels.hpp:324)
+        const int nk0 = tile_blocks(w, 0), nk1 = tile_blocks(w, 1);
         for (int i = 0; i < nkv; ++i) {
-            mbar_wait(&s_full[s], sc & 1);
-            ++sc;
+            uint32_t tS = tS_fixed;
+            mbarrier* pf = p_full[s];
+            if constexpr (k3) {
+                const uint32_t gi = qbase + (uint32_t)qk_index(s, i, nk0, nk1);
+                const uint32_t b = gi % 3;
+                mbar_wait(&s_full3[b], (gi / 3) & 1);
+                tS = tbase + lane_off + sbuf_col(b);
+                pf = p_full3[b];
+            } else {
+                mbar_wait(&s_full[s], sc & 1);
+                ++sc;
+            }
+            const uint32_t tP = tS + 64;
             tmem::fence_after();
             rt_fl<kBlockN> x;
             load(x, tS);
@@ -310,6 +415,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             float mx = -INFINITY;
             row_max(mx, x);  // tiles.hpp:290-298
             const float m_new = fmaxf(m, mx * tau);
+            if (k3 && i > 0) {  // PV_{i-1}(s) done: O_s is stable for the rescale below
+                mbar_wait(&pv_done[s], pvc & 1);
+                ++pvc;
+                tmem::fence_after();
+            }
             // Rescale lazily: only when some row of the warp grew by > 2^8 (warp-uniform
             // because tcgen05.ld/st are warp-collective). The final O / l is unchanged.
             if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
@@ -357,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 if (c > 0) {  // chunk c-1 is in TMEM: hand it to the MMA warp
                     tmem::wait_st();
                     tmem::fence_before();
-                    mbar_arrive(&p_full[s][c - 1]);
+                    mbar_arrive(&pf[c - 1]);
                 }
                 if constexpr (kPChunks == 1) {
                     tmem::st_32x32b_x64(tP, pk);
@@ -370,12 +480,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             l += (l01.x + l01.y) + (l23.x + l23.y);
             tmem::wait_st();
             tmem::fence_before();
-            mbar_arrive(&p_full[s][kPChunks - 1]);
+            mbar_arrive(&pf[kPChunks - 1]);
         }
+        if constexpr (k3) qbase += (uint32_t)(nk0 + nk1);
 
         // FINISH (kernels.hpp:335-342): O / l -> bf16 -> this warpgroup's SMEM staging atom ->
         // TMA store (one 64-column atom at a time); plus L for the backward
         mbar_wait(&o_full[s], nt & 1);
+        if constexpr (k3) {  // the last PV_s's pv_done (complete with o_full)
+            mbar_wait(&pv_done[s], pvc & 1);
+            ++pvc;
+        }
         tmem::fence_after();
         if (p.lse != nullptr && row < n)
             p.lse[(size_t)(batch * p.heads + head) * n + row] = (m + __log2f(l)) * kLn2;
