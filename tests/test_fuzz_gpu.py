@@ -26,7 +26,7 @@ def _case(seed):
                 D=r.choice([64, 128]), causal=r.random() < 0.5, bnhd=r.random() < 0.3)
 
 
-CASES = [_case(s) for s in range(24)]
+CASES = [_case(s) for s in range(48)]
 
 
 @pytest.mark.parametrize("c", CASES, ids=[f"B{c['B']}H{c['H']}kv{c['HKV']}N{c['N']}D{c['D']}"
@@ -47,6 +47,15 @@ def test_fuzz_fwd_bwd(cuda_dev, c):
     o, lse = A.attention_fwd(qd, kd, vd, causal=causal)
     dq, dk, dv = A.attention_bwd(qd, kd, vd, o, dod, lse, causal=causal)
     torch.cuda.synchronize()
+    if D == 128:  # the opt-in CTA-pair dK/dV kernel on the same inputs
+        A.set_bwd_pairs(True)
+        try:
+            _, dk2, dv2 = A.attention_bwd(qd, kd, vd, o, dod, lse, causal=causal)
+            torch.cuda.synchronize()
+        finally:
+            A.set_bwd_pairs(False)
+        assert (dk2.float() - dk.float()).abs().max().item() <= 1e-2
+        assert (dv2.float() - dv.float()).abs().max().item() <= 1e-2
     g = H // HKV
     ke, ve = np.repeat(k, g, axis=1).reshape(-1, N, D), np.repeat(v, g, axis=1).reshape(-1, N, D)
     ro, rl = orc.attn_fwd(q.reshape(-1, N, D), ke, ve, causal=causal)
