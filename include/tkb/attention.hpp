@@ -122,7 +122,7 @@ inline void attention_bwd(const AttentionConfig& cfg, const AttentionGlobals& g,
                        cuda_stream));
 }
 
-// D = 128 backward dK/dV on 2-CTA clusters (tcgen05 cta_group::2); process-wide, default off.
+// D = 128 backward dK/dV on 2-CTA clusters (tcgen05 cta_group::2); calling thread only, default off.
 inline void set_bwd_pairs(bool on) { check(tkb_set_bwd_pairs(on ? 1 : 0)); }
 
 // Multi-GPU driver helper: this rank's contiguous share of the batch x head grid.

@@ -22,9 +22,16 @@
  *     over the unmasked keys (natural log).
  *   - causal: key j is visible to query i iff j <= i (top-left aligned).
  *   - All entry points are asynchronous on `stream` (a cudaStream_t), never
- *     allocate, never throw, and are safe to call from several host threads on
- *     distinct (device, stream) pairs. The last error message of the calling
- *     thread is returned by tkb_last_error().
+ *     throw, and are safe to call from several host threads, on any mix of
+ *     devices and streams. The last error message of the calling thread is
+ *     returned by tkb_last_error().
+ *   - Allocation: the library owns one 64 KB block per device (the persistent
+ *     schedulers' task counters, one slot per stream), made by tkb_device_init()
+ *     or by the first call on that device; nothing else is ever allocated.
+ *     Call tkb_device_init() up front to keep the first call capturable in a
+ *     CUDA graph. A captured graph must not be replayed concurrently with
+ *     itself (its kernels share the capturing stream's counter slot).
+ *   - check_finite (desc) reads its result back and synchronises the stream.
  */
 #ifndef TKB_ATTN_H
 #define TKB_ATTN_H
@@ -36,7 +43,7 @@
 extern "C" {
 #endif
 
-#define TKB_ABI_VERSION 2
+#define TKB_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define TKB_API __attribute__((visibility("default")))
@@ -65,7 +72,7 @@ typedef struct tkb_attn_desc {
     int32_t causal;       /* 0 / 1 */
     int32_t check_finite; /* 1: scan inputs first and fail with TKB_ERR_CONFIG on inf/nan
                              (kernels.hpp:277-284); synchronises the stream */
-    float softmax_scale;  /* <= 0: D^-1/2 */
+    float softmax_scale;  /* 0: D^-1/2; must be finite and >= 0 */
     int32_t kv_heads;     /* Hkv: 0 = H (multi-head); H % Hkv == 0 (grouped-query, Hkv = 1: multi-query).
                              k/v/dk/dv are [B, Hkv, N, D]; query head h reads kv head h / (H / Hkv) */
     /* element strides of q/o/do/dq; 0 = contiguous [B,H,N,D] */
@@ -90,8 +97,8 @@ TKB_API int tkb_attn_validate(const tkb_attn_desc* desc);
 TKB_API int tkb_attn_fwd(const tkb_attn_desc* desc, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* stream);
 
-/* Bytes of caller-provided device workspace the backward needs (fp32 dQ accumulator,
- * delta = rowsum(dO * O), dQ ordering semaphores). */
+/* Bytes of caller-provided device workspace the backward needs: two fp32 [B*H, N_pad]
+ * vectors, delta = rowsum(dO * O) and -L log2(e) (N_pad = N rounded up to 128). */
 TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* desc);
 
 /* Backward from the saved lse: dq, dk, dv (bf16, same layout as q). Deterministic:
@@ -130,21 +137,29 @@ TKB_API int tkb_gemm(const tkb_gemm_desc* desc, const void* a, const void* b, vo
  * contiguous, balanced [begin, end) of `units` for `rank` of `world`. No collective. */
 TKB_API int tkb_shard_range(int64_t units, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
 
+/* One-time per-device state (SM count, the schedulers' counter pool). Optional: the first
+ * call on a device does it otherwise. Thread-safe. */
+TKB_API int tkb_device_init(int device);
+
 /* Debug timeline of the kernels (the reference's Timeline, lcsf.hpp:165-224): device
  * buffer of slots x 4 roles x 32 iterations x 8 events int64 cycle stamps; the backward
  * traces every `every`-th work item, the persistent forward every `every`-th CTA.
- * NULL disables. Not thread-safe; debugging only. */
+ * NULL disables. Applies to later calls from the calling host thread only. */
 TKB_API int tkb_debug_set_trace(void* device_buf, int every, int slots);
 
 /* Debug / profiling: run only some backward stages (bit 0 prep, bit 1 dK/dV kernel,
- * bit 2 dQ kernel; default 7). Results are only complete with 7. Not thread-safe. */
+ * bit 2 dQ kernel; default 7). Results are only complete with 7. Applies to later calls
+ * from the calling host thread only. */
 TKB_API int tkb_debug_set_bwd_phases(int mask);
 
-/* Backward dK/dV kernel selection at D = 128 (process-wide; not thread-safe): 0 = one CTA
+/* Backward dK/dV kernel selection at D = 128 (calling host thread only): 0 = one CTA
  * per kv block (default), 1 = CTA pairs (clusters of 2, tcgen05 cta_group::2, M = 256
  * MMAs over two kv blocks; half the per-SM operand traffic). Same results, bit for bit
  * within each variant's own summation order. */
 TKB_API int tkb_set_bwd_pairs(int on);
+
+/* Hits / misses of the calling thread's TMA descriptor cache (debug, tests). */
+TKB_API int tkb_debug_map_cache_stats(unsigned long long* hits, unsigned long long* misses);
 
 /* Number of kernels the last successful fwd / bwd call on this thread launched. */
 TKB_API int tkb_last_launch_count(void);

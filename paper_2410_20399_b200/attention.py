@@ -93,6 +93,8 @@ _SIGS = {
     "tkb_gemm": (ctypes.c_int, [ctypes.POINTER(GemmDesc), _VP, _VP, _VP, _VP]),
     "tkb_shard_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "tkb_device_init": (ctypes.c_int, [ctypes.c_int]),
+    "tkb_debug_map_cache_stats": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.POINTER(ctypes.c_ulonglong)]),
     "tkb_last_launch_count": (ctypes.c_int, []),
     "tkb_debug_set_trace": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int]),
     "tkb_debug_set_bwd_phases": (ctypes.c_int, [ctypes.c_int]),
@@ -196,6 +198,24 @@ def _tables(sin_tab, cos_tab, N, D, device):
     for t in (sin_tab, cos_tab):
         if not t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != (N, D // 2) or not t.is_contiguous():
             raise ShapeError("sin / cos tables must be contiguous fp32 CUDA tensors [N, D/2]")
+        if t.device != device:
+            raise ConfigError("sin / cos tables must be on the tensors' device")
+
+
+def _bf16_cuda(t, name, device=None):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.bfloat16:
+        raise ConfigError(f"{name} must be a bf16 CUDA tensor (no CPU fallback)")
+    if device is not None and t.device != device:
+        raise ConfigError(f"{name} must be on {device}")
+
+
+def _out_like(t, name, ref_shape, ref_strides, device):
+    """A caller-supplied output: bf16, on `device`, with the expected shape and strides."""
+    _bf16_cuda(t, name, device)
+    if tuple(t.shape) != tuple(ref_shape) or _bhnd(t, name) != ref_strides:
+        raise ShapeError(f"{name} must have shape {tuple(ref_shape)} and the matching input's strides")
 
 
 def rotary(x, sin_tab, cos_tab, out=None):
@@ -203,15 +223,14 @@ def rotary(x, sin_tab, cos_tab, out=None):
     (x[..., p, i], x[..., p, i + D/2]) rotated by the [N, D/2] sin / cos table angles."""
     import torch
 
-    if not x.is_cuda or x.dtype != torch.bfloat16:
-        raise ConfigError("rotary: x must be a bf16 CUDA tensor")
+    _bf16_cuda(x, "x")
     st = _bhnd(x, "x")
     B, H, N, D = x.shape
     _tables(sin_tab, cos_tab, N, D, x.device)
     if out is None:
         out = torch.empty_strided(x.shape, x.stride(), dtype=torch.bfloat16, device=x.device)
-    elif _bhnd(out, "out") != st:
-        raise ShapeError("out must share x's strides")
+    else:
+        _out_like(out, "out", x.shape, st, x.device)
     d = AttentionConfig(B, H, N, D).desc(strides=st)
     _check(lib().tkb_rotary(ctypes.byref(d), x.data_ptr(), sin_tab.data_ptr(), cos_tab.data_ptr(), out.data_ptr(),
                             _stream(torch, x.device)))
@@ -222,10 +241,16 @@ def rotary_qk(q, k, sin_tab, cos_tab):
     """The attention prologue: rotated copies of Q and K from one launch."""
     import torch
 
+    _bf16_cuda(q, "q")
+    _bf16_cuda(k, "k", q.device)
     st = _bhnd(q, "q")
-    hkv = k.shape[1]
     kst = _bhnd(k, "k")
     B, H, N, D = q.shape
+    if k.shape[0] != B or k.shape[2] != N or k.shape[3] != D:
+        raise ShapeError("k must be [B, Hkv, N, D] matching q's B, N, D")
+    hkv = k.shape[1]
+    if hkv < 1 or H % hkv:
+        raise ConfigError(f"heads ({H}) must be a multiple of kv heads ({hkv})")
     _tables(sin_tab, cos_tab, N, D, q.device)
     qr = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
     kr = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
@@ -243,27 +268,36 @@ def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None,
     HBM-bound launch; the rotated tensors are temporaries)."""
     import torch
 
+    _bf16_cuda(q, "q")
+    _bf16_cuda(k, "k", q.device)
+    _bf16_cuda(v, "v", q.device)
+    _check_kv(q, k, v)
     if rotary_tables is not None:
         q, k = rotary_qk(q, k, *rotary_tables)
-
-    if not (q.is_cuda and k.is_cuda and v.is_cuda):
-        raise ConfigError("attention_fwd runs on the GPU only (no CPU fallback)")
-    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
-        raise ConfigError("q, k, v must be bf16")
     st = _bhnd(q, "q")
     hkv, kst = _check_kv(q, k, v)
     B, H, N, D = q.shape
     if out is None:
         out = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
-    elif _bhnd(out, "out") != st:
-        raise ShapeError("out must share q's strides")
+    else:
+        _out_like(out, "out", q.shape, st, q.device)
     if return_lse and lse is None:
         lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
+    if lse is not None:
+        _check_lse(lse, B, H, N, q.device)
     cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite, kv_heads=hkv)
     d = cfg.desc(strides=st, kv_strides=kst)
     _check(lib().tkb_attn_fwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr() if lse is not None else None, _stream(torch, q.device)))
     return (out, lse) if return_lse else out
+
+
+def _check_lse(lse, B, H, N, device):
+    import torch
+
+    if (not isinstance(lse, torch.Tensor) or not lse.is_cuda or lse.device != device or lse.dtype != torch.float32
+            or tuple(lse.shape) != (B, H, N) or not lse.is_contiguous()):
+        raise ShapeError(f"lse must be a contiguous fp32 CUDA tensor [B, H, N] = {(B, H, N)} on {device}")
 
 
 def bwd_workspace_bytes(B, H, N, D, causal=False):
@@ -278,26 +312,31 @@ def attention_bwd(q, k, v, o, dout, lse, causal=False, softmax_scale=None, dq=No
     import torch
 
     for t, name in ((q, "q"), (k, "k"), (v, "v"), (o, "o"), (dout, "dout")):
-        if not t.is_cuda or t.dtype != torch.bfloat16:
-            raise ConfigError(f"{name} must be a bf16 CUDA tensor")
+        _bf16_cuda(t, name, q.device)
     st = _bhnd(q, "q")
     hkv, kst = _check_kv(q, k, v)
     for t, name in ((o, "o"), (dout, "dout")):
         if t.shape != q.shape or _bhnd(t, name) != st:
             raise ShapeError(f"{name} must match q's shape and strides")
     B, H, N, D = q.shape
-    if lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, N) or not lse.is_contiguous():
-        raise ShapeError("lse must be contiguous fp32 [B, H, N]")
-    dq = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device) if dq is None else dq
-    dk = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device) if dk is None else dk
-    dv = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device) if dv is None else dv
-    if _bhnd(dq, "dq") != st or _bhnd(dk, "dk") != kst or _bhnd(dv, "dv") != kst:
-        raise ShapeError("dq must share q's strides and dk/dv k's")
+    _check_lse(lse, B, H, N, q.device)
+    if dq is None:
+        dq = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+    if dk is None:
+        dk = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
+    if dv is None:
+        dv = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
+    _out_like(dq, "dq", q.shape, st, q.device)
+    _out_like(dk, "dk", k.shape, kst, q.device)
+    _out_like(dv, "dv", k.shape, kst, q.device)
     cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite, kv_heads=hkv)
     d = cfg.desc(strides=st, kv_strides=kst)
     ws_bytes = int(lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(d)))
-    if workspace is None or workspace.numel() * workspace.element_size() < ws_bytes:
+    if workspace is None:
         workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    elif (not workspace.is_cuda or workspace.device != q.device or not workspace.is_contiguous()
+          or workspace.numel() * workspace.element_size() < ws_bytes):
+        raise BoundsError(f"workspace must be a contiguous CUDA buffer of >= {ws_bytes} bytes on {q.device}")
     _check(lib().tkb_attn_bwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                               dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                               workspace.data_ptr(), ws_bytes, _stream(torch, q.device)))
@@ -361,8 +400,21 @@ def debug_set_bwd_phases(mask=7):
 
 def set_bwd_pairs(on=True):
     """D = 128 backward: run dK/dV on CTA pairs (cta_group::2 clusters) instead of one CTA
-    per kv block. Process-wide switch; results match the oracle either way."""
+    per kv block. Applies to this host thread's later calls; results match the oracle
+    either way."""
     lib().tkb_set_bwd_pairs(1 if on else 0)
+
+
+def device_init(device=0):
+    """One-time per-device library state (the schedulers' counter pool); optional."""
+    _check(lib().tkb_device_init(int(device)))
+
+
+def map_cache_stats():
+    """(hits, misses) of this thread's TMA descriptor cache."""
+    h, m = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+    lib().tkb_debug_map_cache_stats(ctypes.byref(h), ctypes.byref(m))
+    return h.value, m.value
 
 
 def last_launch_count():

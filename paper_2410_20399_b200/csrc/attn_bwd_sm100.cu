@@ -193,258 +193,14 @@ TKB_DEVICE void exp_chunk(float* pf, float tau, uint32_t nlse4, float nlse_r) {
 }
 
 // ================================================================== bwd_dkdv (KV-stationary)
+// TMEM of the dK/dV kernels: S^T | dV | dP^T (P^T / dS^T packed into S^T / dP^T) | dK.
 template <int D>
-struct CfgKV {
-    using T = Tiles<D>;
-    static constexpr int kStages = (D == 128) ? 2 : 3;  // Q and dO ring depth
-    static constexpr int kOffK = 0;
-    static constexpr int kOffV = kOffK + T::kTileBytes;
-    static constexpr int kOffQ = kOffV + T::kTileBytes;
-    static constexpr int kOffDo = kOffQ + kStages * T::kTileBytes;
-    static constexpr int kOffLse = kOffDo + kStages * T::kTileBytes;  // kStages x 128 fp32
-    static constexpr int kOffDelta = kOffLse + kStages * 512;         // kStages x 128 fp32
-    static constexpr int kOffBar = kOffDelta + kStages * 512;
-    static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // + alignment slack
-    static_assert(kSmemBytes <= 232448, "smem");
+struct TmemKV {
     static __device__ __forceinline__ constexpr uint32_t tmem_s() { return 0u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dv() { return 128u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 128u + D; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dk() { return 256u + D; }
 };
-
-template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdv_kernel(const __grid_constant__ BwdParams p) {
-    using C = CfgKV<D>;
-    using TL = Tiles<D>;
-    constexpr int S = C::kStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem + C::kOffK;
-    uint8_t* sV = smem + C::kOffV;
-    uint8_t* sQ = smem + C::kOffQ;
-    uint8_t* sDo = smem + C::kOffDo;
-    float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
-    float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
-    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
-    mbarrier& kv_full = bars[0];
-    mbarrier& s_full = bars[1];
-    mbarrier& dp_full = bars[3];
-    mbarrier& dkv_full = bars[5];
-    mbarrier* q_full = bars + 8;     // [S]
-    mbarrier* q_empty = bars + 12;   // [S]
-    mbarrier* do_full = bars + 16;   // [S]
-    mbarrier* do_empty = bars + 20;  // [S]
-    mbarrier* p_full = bars + 32;    // [kGroups] P^T chunks (32 queries each)
-    mbarrier* ds_full = bars + 36;   // [kGroups] dS^T chunks
-    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
-
-    const int warp = warpid();
-    const int lane = laneid();
-    const int j = blockIdx.x;  // kv block; causal: small j visits the most q blocks, dispatched first
-    const int head = blockIdx.y;  // kv head (== query head unless grouped-query)
-    const int batch = blockIdx.z;
-    const int kv0 = j * 128;
-    const int nq = p.n_pad / 128;
-    const int T1 = CAUSAL ? (nq - j) : nq;  // q blocks visited per query head: i = j + t (causal) or t
-    const int T = T1 * p.group;             // steps: the group's query heads one after the other, so
-                                            // dK/dV sum over them in TMEM (grouped-query attention)
-    auto qblock = [&](int t) { return CAUSAL ? (j + t % T1) : t % T1; };
-    auto qhead = [&](int t) { return head * p.group + t / T1; };
-    auto qbh = [&](int t) { return batch * p.heads + qhead(t); };
-    long long* tr = trace_slot(p, (batch * gridDim.y + head) * gridDim.x + j, 0);
-    const long long t_start = clock64();
-
-    if (warp == kWarpLoad && lane == 0) {
-        mbar_init(&kv_full, 1);
-        mbar_init(&s_full, 1);
-        mbar_init(&dp_full, 1);
-        mbar_init(&dkv_full, 1);
-        for (int g = 0; g < kGroups; ++g) {
-            mbar_init(&p_full[g], 128);  // the 4 warps of one column group
-            mbar_init(&ds_full[g], 128);
-        }
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], 1);
-            mbar_init(&do_full[s], 1);
-            mbar_init(&do_empty[s], 1);
-        }
-        fence_barrier_init();
-        tma::prefetch_desc(&p.tm_q);
-        tma::prefetch_desc(&p.tm_k);
-        tma::prefetch_desc(&p.tm_v);
-        tma::prefetch_desc(&p.tm_do);
-    }
-    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
-    tmem::fence_before();
-    __syncthreads();
-    tmem::fence_after();
-    const uint32_t tbase = tmem_slot;
-
-    if (warp == kWarpLoad) {
-        if (lane == 0) {
-            // ------------------------------------------------------------- LOAD
-            const uint64_t pol_stream = tma::policy_evict_first();
-            const uint64_t pol_keep = tma::policy_evict_last();
-            mbar_arrive_expect_tx(&kv_full, 2 * TL::kTileBytes);
-            for (int a = 0; a < TL::kAtoms; ++a) {
-                tma::load_4d(sK + a * kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, head, batch, pol_stream);
-                tma::load_4d(sV + a * kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, head, batch, pol_stream);
-            }
-            for (int t = 0; t < T; ++t) {
-                const int i = qblock(t), s = t % S;
-                const uint32_t ph = ((t / S) & 1) ^ 1;
-                mbar_wait(&do_empty[s], ph);  // freed by dV_{t-S}, the first GEMM of its step
-                const int hq = qhead(t);
-                const size_t bhq = (size_t)qbh(t);
-                mbar_arrive_expect_tx(&do_full[s], TL::kTileBytes);
-                for (int a = 0; a < TL::kAtoms; ++a)
-                    tma::load_4d(sDo + s * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[s], a * 64, i * 128,
-                                 hq, batch, pol_keep);
-                mbar_wait(&q_empty[s], ph);  // freed by dK_{t-S}
-                mbar_arrive_expect_tx(&q_full[s], TL::kTileBytes + 1024);
-                for (int a = 0; a < TL::kAtoms; ++a)
-                    tma::load_4d(sQ + s * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[s], a * 64, i * 128,
-                                 hq, batch, pol_keep);
-                tma::load_1d(sLse + s * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &q_full[s]);
-                tma::load_1d(sDelta + s * 128, p.delta + bhq * p.n_pad + i * 128, 512, &q_full[s]);
-            }
-        }
-    } else if (warp == kWarpMma) {
-        // ----------------------------------------------------------------- MMA
-        // converged warp; one elected lane issues each tcgen05 op
-        constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S^T, dP^T
-        constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();    // dV, dK
-        const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-        auto qaddr = [&](int t) { return smem_u32(sQ + (t % S) * TL::kTileBytes); };
-        auto doaddr = [&](int t) { return smem_u32(sDo + (t % S) * TL::kTileBytes); };
-        mbar_wait(&kv_full, 0);
-        mbar_wait(&q_full[0], 0);
-        tmem::fence_after();
-        mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(0), id_s);
-        umma::commit_e(&s_full);
-        mbar_wait(&do_full[0], 0);
-        tmem::fence_after();
-        mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(0), id_s);
-        umma::commit_e(&dp_full);
-        for (int t = 0; t < T; ++t) {
-            const uint32_t ph = t & 1;
-            // dV += P_t^T dO_t, one 32-query chunk per column group as it lands
-            TKB_TR(0, t, 0);
-            mma_tmem_a_groups(tbase + C::tmem_dv(), tbase + C::tmem_s(), doaddr(t), id_kv, t > 0, [&](int g) {
-                mbar_wait(&p_full[g], ph);
-                tmem::fence_after();
-            });
-            TKB_TR(0, t, 1);
-            umma::commit_e(&do_empty[t % S]);
-            // S_{t+1}: overwrites P_t, read by dV_t which was issued before
-            if (t + 1 < T) {
-                mbar_wait(&q_full[(t + 1) % S], ((t + 1) / S) & 1);
-                tmem::fence_after();
-                mm_abt<D>(tbase + C::tmem_s(), aK, qaddr(t + 1), id_s);
-                umma::commit_e(&s_full);
-            }
-            // dK += dS_t^T Q_t
-            TKB_TR(0, t, 2);
-            mma_tmem_a_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qaddr(t), id_kv, t > 0, [&](int g) {
-                mbar_wait(&ds_full[g], ph);
-                tmem::fence_after();
-            });
-            TKB_TR(0, t, 3);
-            umma::commit_e(&q_empty[t % S]);
-            // dP_{t+1}: overwrites dS_t, read by dK_t which was issued before
-            if (t + 1 < T) {
-                mbar_wait(&do_full[(t + 1) % S], ((t + 1) / S) & 1);
-                tmem::fence_after();
-                mm_abt<D>(tbase + C::tmem_dp(), aV, doaddr(t + 1), id_s);
-                umma::commit_e(&dp_full);
-            }
-            TKB_TR(0, t, 4);
-        }
-        umma::commit_e(&dkv_full);
-    } else {
-        // ----------------------------------------------------------------- COMPUTE
-        const int wq = warp & 3;
-        const int g = warp >> 2;       // q group: columns [32g, 32g+32)
-        const int r = wq * 32 + lane;  // kv row == TMEM lane
-        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
-        const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
-        const float tau = p.scale_log2;
-        for (int t = 0; t < T; ++t) {
-            const int i = qblock(t);  // (t / T1 is 0 unless grouped-query: one division per step)
-            const int s = t % S;
-            const bool diag = CAUSAL && (i == j);
-            const uint32_t nlse4 = smem_u32(sLse + s * 128 + 32 * g);  // shared-space addresses
-            const uint32_t dlt4 = smem_u32(sDelta + s * 128 + 32 * g);
-            // P^T = exp2(tau S^T - lse2)
-            mbar_wait(&q_full[s], (t / S) & 1);
-            mbar_wait(&s_full, t & 1);
-            if (threadIdx.x == 0) TKB_TR(1, t, 0);
-            tmem::fence_after();
-            float pf[32];
-            tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
-            exp_chunk<false>(pf, tau, nlse4, 0.f);
-            if (diag) {  // key kv0 + r visible to query kv0 + 32g + c iff r <= 32g + c
-#pragma unroll
-                for (int c = 0; c < 32; ++c) pf[c] = (32 * g + c < r) ? 0.f : pf[c];
-            }
-            uint32_t pk[16];
-#pragma unroll
-            for (int c = 0; c < 32; c += 2) pk[c / 2] = pack_bf16x2(pf[c], pf[c + 1]);
-            tmem::st_32x32b_x16(tS, pk);  // inside the 32 columns this thread has read
-            tmem::wait_st();
-            tmem::fence_before();
-            mbar_arrive(&p_full[g]);
-            if (threadIdx.x == 0) TKB_TR(1, t, 1);
-            // dS^T = P^T o (dP^T - Delta) * scale
-            mbar_wait(&dp_full, t & 1);
-            if (threadIdx.x == 0) TKB_TR(1, t, 2);
-            tmem::fence_after();
-            uint32_t dpv[32];
-            tmem::ldw_32x32b_x32(tDp, dpv);
-#pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                const float4 d4 = lds_f4(dlt4 + 4 * c);
-                const float2 g01 =
-                    sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(d4.x, d4.y));
-                const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
-                                        make_float2(d4.z, d4.w));
-                // dS^T / scale: the softmax scale is applied to dK once, in the finish stage
-                const float2 s01 = mul2(make_float2(pf[c], pf[c + 1]), g01);
-                const float2 s23 = mul2(make_float2(pf[c + 2], pf[c + 3]), g23);
-                pk[c / 2] = pack_bf16x2(s01.x, s01.y);
-                pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
-            }
-            tmem::st_32x32b_x16(tDp, pk);
-            tmem::wait_st();
-            tmem::fence_before();
-            mbar_arrive(&ds_full[g]);
-            if (threadIdx.x == 0) TKB_TR(1, t, 3);
-        }
-        // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q and dO rings are free) -> TMA store
-        mbar_wait(&dkv_full, 0);
-        tmem::fence_after();
-        uint8_t* stage_v = sQ;
-        uint8_t* stage_k = sDo;
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dv(), stage_v, r, g);
-        tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dk(), stage_k, r, g, p.scale);  // dK = scale dS^T Q
-        tma::fence_async_smem();
-        named_sync(kBarCompute, kComputeThreads);
-        if (threadIdx.x == 0) {
-            for (int a = 0; a < TL::kAtoms; ++a) {
-                tma::store_4d(&p.tm_dv, stage_v + a * kAtomBytes, a * 64, kv0, head, batch);
-                tma::store_4d(&p.tm_dk, stage_k + a * kAtomBytes, a * 64, kv0, head, batch);
-            }
-            tma::commit_group();
-            tma::wait_group_read<0>();
-        }
-    }
-
-    tmem::fence_before();
-    __syncthreads();
-    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
-}
 
 // ================================================================== bwd_dkdv, persistent
 // bwd_dkdv with one CTA per SM walking (kv block, kv head, batch) tasks from the atomic
@@ -523,7 +279,7 @@ struct CfgKVP {
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __grid_constant__ BwdParams p) {
     using C = CfgKVP<D>;
-    using CT = CfgKV<D>;  // TMEM layout
+    using CT = TmemKV<D>;
     using TL = Tiles<D>;
     constexpr int SQ = C::kStagesQ, SD = C::kStagesDo, SA = C::kStagesAux;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1543,92 +1299,84 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 // within the block's row range) and issues all their loads before reducing, so a thread
 // keeps 2 * 16 * kPrepRows bytes in flight.
 constexpr int kPrepRows = 4;
+// Linear blocks (bh, row block) are walked grid-stride with a 64-bit index: B * H is not
+// bounded by gridDim.y's 65535.
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ lse2,
                                                        float* __restrict__ delta, int heads, int n, int n_pad,
-                                                       int64_t sb, int64_t sh, int64_t sn) {
+                                                       int row_blocks, int64_t total_blocks, int64_t sb, int64_t sh,
+                                                       int64_t sn) {
     constexpr int kLanesPerRow = D / 8;
     constexpr int kRowsPerPass = 256 / kLanesPerRow;
-    const int bh = blockIdx.y;
-    const int b = bh / heads, hh = bh % heads;
     const int c = (threadIdx.x % kLanesPerRow) * 8;
-    const int row_base = blockIdx.x * kRowsPerPass * kPrepRows + threadIdx.x / kLanesPerRow;
-    uint4 ov[kPrepRows], dv[kPrepRows];
+    for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
+        const int64_t bh = blk / row_blocks;
+        const int rb = (int)(blk - bh * row_blocks);
+        const int64_t b = bh / heads, hh = bh % heads;
+        const int row_base = rb * kRowsPerPass * kPrepRows + threadIdx.x / kLanesPerRow;
+        uint4 ov[kPrepRows], dv[kPrepRows];
 #pragma unroll
-    for (int k = 0; k < kPrepRows; ++k) {
-        const int row = row_base + k * kRowsPerPass;
-        ov[k] = make_uint4(0, 0, 0, 0);
-        dv[k] = make_uint4(0, 0, 0, 0);
-        if (row < n) {
-            const int64_t off = b * sb + hh * sh + (int64_t)row * sn + c;
-            ov[k] = __ldg(reinterpret_cast<const uint4*>(o + off));
-            dv[k] = __ldg(reinterpret_cast<const uint4*>(dout + off));
+        for (int k = 0; k < kPrepRows; ++k) {
+            const int row = row_base + k * kRowsPerPass;
+            ov[k] = make_uint4(0, 0, 0, 0);
+            dv[k] = make_uint4(0, 0, 0, 0);
+            if (row < n) {
+                const int64_t off = b * sb + hh * sh + (int64_t)row * sn + c;
+                ov[k] = __ldg(reinterpret_cast<const uint4*>(o + off));
+                dv[k] = __ldg(reinterpret_cast<const uint4*>(dout + off));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPrepRows; ++k) {
+            const int row = row_base + k * kRowsPerPass;
+            const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov[k]);
+            const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[k]);
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 a = __bfloat1622float2(o2[q]);
+                const float2 g = __bfloat1622float2(d2[q]);
+                acc = fmaf(a.x, g.x, acc);
+                acc = fmaf(a.y, g.y, acc);
+            }
+#pragma unroll
+            for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+            if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
+                const size_t idx = (size_t)bh * n_pad + row;
+                delta[idx] = row < n ? acc : 0.f;
+                lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
+            }
         }
     }
-#pragma unroll
-    for (int k = 0; k < kPrepRows; ++k) {
-        const int row = row_base + k * kRowsPerPass;
-        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov[k]);
-        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[k]);
-        float acc = 0.f;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float2 a = __bfloat1622float2(o2[q]);
-            const float2 g = __bfloat1622float2(d2[q]);
-            acc = fmaf(a.x, g.x, acc);
-            acc = fmaf(a.y, g.y, acc);
-        }
-#pragma unroll
-        for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-        if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
-            const size_t idx = (size_t)bh * n_pad + row;
-            delta[idx] = row < n ? acc : 0.f;
-            lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
-        }
-    }
-}
-
-template <class Kern>
-int set_smem(Kern k, int bytes) {
-    return (int)cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 template <int D, bool CAUSAL>
 int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases, int* launches) {
-    static bool configured = false;
-    if (!configured) {
-        int e = set_smem(attn_bwd_dkdv_kernel<D, CAUSAL>, CfgKV<D>::kSmemBytes);
-        if (!e) e = set_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes);
-        if (!e && D == 128) e = set_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes);
-        if (!e) e = set_smem(attn_bwd_dkdvp_kernel<D, CAUSAL>, CfgKVP<D>::kSmemBytes);
-        if (e) return e;
-        configured = true;
-    }
-    dim3 grid(p.n_pad / 128, p.heads, batches);                 // dQ: one CTA per query block
-    dim3 grid_kv(p.n_pad / 128, p.heads / p.group, batches);    // dK/dV: one CTA per kv block
+    static std::atomic<unsigned long long> set_dq{0}, set_kv2{0}, set_kvp{0};  // per device
+    if (int e = ensure_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes, set_dq)) return e;
+    if (int e = ensure_smem(attn_bwd_dkdvp_kernel<D, CAUSAL>, CfgKVP<D>::kSmemBytes, set_kvp)) return e;
+    if (D == 128)
+        if (int e = ensure_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes, set_kv2)) return e;
     if (phases & 2) {
         if (D == 128 && p.pairs) {  // CTA pairs: kv blocks rounded up to an even count
             dim3 grid2((p.n_pad / 128 + 1) & ~1, p.heads / p.group, batches);
             attn_bwd_dkdv2_kernel<CAUSAL><<<grid2, kThreads, CfgKV2::kSmemBytes, stream>>>(p);
         } else {
-#ifndef TKB_BWD_GRID_KV
-            const int tasks_kv = (p.n_pad / 128) * (p.heads / p.group) * batches;
+            const int64_t tasks_kv = (int64_t)(p.n_pad / 128) * (p.heads / p.group) * batches;
             attn_bwd_dkdvp_kernel<D, CAUSAL>
-                <<<tasks_kv < p.num_sms ? tasks_kv : p.num_sms, kThreads, CfgKVP<D>::kSmemBytes, stream>>>(p);
-#else  // A/B baseline: one CTA per kv block
-            attn_bwd_dkdv_kernel<D, CAUSAL><<<grid_kv, kThreads, CfgKV<D>::kSmemBytes, stream>>>(p);
-#endif
+                <<<(unsigned)(tasks_kv < p.num_sms ? tasks_kv : p.num_sms), kThreads, CfgKVP<D>::kSmemBytes,
+                   stream>>>(p);
         }
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;
     }
     if (phases & 4) {
-        const int tasks = p.bh * (p.n_pad / 128);
+        const int64_t tasks = (int64_t)p.bh * (p.n_pad / 128);
         attn_bwd_dq_kernel<D, CAUSAL>
-            <<<tasks < p.num_sms ? tasks : p.num_sms, kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
+            <<<(unsigned)(tasks < p.num_sms ? tasks : p.num_sms), kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;
@@ -1643,10 +1391,12 @@ int launch_all(bool causal, const BwdParams& p, int batches, const void* o, cons
     *launches = 0;
     if (phases & 1) {
         constexpr int kRowsPerBlock = 256 / (D / 8) * kPrepRows;
-        dim3 g1((p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock, batches * p.heads);
-        bwd_prep_kernel<D><<<g1, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                  reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
-                                                  p.heads, p.n, p.n_pad, sb, sh, sn);
+        const int row_blocks = (p.n_pad + kRowsPerBlock - 1) / kRowsPerBlock;
+        const int64_t total = (int64_t)row_blocks * batches * p.heads;
+        const int64_t cap = (int64_t)p.num_sms * 16;  // 16 x 256 threads per SM in flight
+        bwd_prep_kernel<D><<<(unsigned)(total < cap ? total : cap), 256, 0, stream>>>(
+            reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
+            p.heads, p.n, p.n_pad, row_blocks, total, sb, sh, sn);
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;

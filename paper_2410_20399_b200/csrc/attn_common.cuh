@@ -3,9 +3,27 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace tkb {
+
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device. The attribute
+// is per device (cuKernelSetAttribute takes a CUdevice), so it is tracked per device
+// ordinal in a lock-free bit mask owned by the caller (one per kernel instantiation);
+// concurrent first calls from several host threads both set it, which is idempotent.
+template <class Kern>
+inline int ensure_smem(Kern kern, int bytes, std::atomic<unsigned long long>& done_mask) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;  // ordinals >= 64: set on every launch
+    if (bit && (done_mask.load(std::memory_order_acquire) & bit)) return 0;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return (int)e;
+    done_mask.fetch_or(bit, std::memory_order_release);
+    return 0;
+}
 
 // Tile shapes (compile time; the reference's runtime AttentionConfig knobs
 // kv_rows / qo_rows / num_workers, kernels.hpp:168-176, become these).
@@ -26,7 +44,8 @@ struct FwdParams {
     int group;                           // query heads per kv head (grouped-query attention; 1 = MHA)
     int bh;                              // batches * heads          (set by launch_attn_fwd)
     int m_blocks;                        // 256-row query blocks     (set by launch_attn_fwd)
-    int tasks;                           // bh * m_blocks            (set by launch_attn_fwd)
+    int tasks;                           // bh * m_blocks            (set by launch_attn_fwd;
+                                         //   tkb_attn_validate keeps B*H*ceil(N/128) < 2^31)
     int head_group;                      // heads per L2 group       (set by launch_attn_fwd)
     float scale_log2;                    // softmax_scale * log2(e)
 };

@@ -538,12 +538,8 @@ template <int D, bool CAUSAL>
 int launch(const FwdParams& p, int num_sms, cudaStream_t stream) {
     using C = Cfg<D>;
     auto kern = attn_fwd_kernel<D, CAUSAL>;
-    static bool configured = false;  // per instantiation; attribute setting is idempotent
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-        if (e != cudaSuccess) return (int)e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> smem_set{0};  // per instantiation, per device
+    if (int e = ensure_smem(kern, C::kSmemBytes, smem_set)) return e;
     kern<<<p.tasks < num_sms ? p.tasks : num_sms, kThreads, C::kSmemBytes, stream>>>(p);
     return (int)cudaGetLastError();
 }

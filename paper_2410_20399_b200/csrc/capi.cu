@@ -6,7 +6,11 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
+#include <vector>
 
 #include "attn_common.cuh"
 #include "host/tmap.hpp"
@@ -24,23 +28,128 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
-long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_trace)
-int g_trace_every = 1, g_trace_slots = 0;
-int g_bwd_phases = 7;  // debug: bit 0 prep, bit 1 dK/dV kernel, bit 2 dQ kernel
-int g_bwd_pairs = 0;   // D = 128 dK/dV on CTA pairs (tkb_set_bwd_pairs)
-
-// Per-device persistent-scheduler counters: 64 pairs used round-robin so kernels
-// running concurrently on different streams do not share a counter; each pair is
-// reset to zero by the last CTA of the grid that used it (lcsf::queue_exit).
-constexpr int kMaxDevices = 64;
-constexpr int kSchedPairs = 64;
-int* g_sched[kMaxDevices] = {};
-unsigned g_sched_next[kMaxDevices] = {};
-int g_num_sms[kMaxDevices] = {};
+// Debug / selection knobs: per host thread, so a profiling thread cannot change what the
+// calls of another thread compute (tkb_debug_set_*, tkb_set_bwd_pairs).
+thread_local long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_trace)
+thread_local int g_trace_every = 1, g_trace_slots = 0;
+thread_local int g_bwd_phases = 7;  // debug: bit 0 prep, bit 1 dK/dV kernel, bit 2 dQ kernel
+thread_local int g_bwd_pairs = 0;   // D = 128 dK/dV on CTA pairs (tkb_set_bwd_pairs)
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
+}
+
+// ---------------------------------------------------------------- per-device state
+// The persistent attention kernels claim tasks from a device counter pair {claims, CTAs
+// done} that the last CTA of the grid resets to zero (lcsf::queue_exit). Two kernels that
+// run concurrently must not share a pair, so each (device, stream) gets its own slot of a
+// pool allocated once per device (tkb_device_init, or lazily on the first call); kernels on
+// one stream are ordered, so they may share its slot. Slot = 4 ints: the counter pair and
+// the check_finite flag. Streams are told apart by cudaStreamGetId (unique for the life of
+// the process; the per-thread default stream has its own id). When more than kSlots
+// streams have been seen, the least recently used slot is recycled.
+constexpr int kMaxDevices = 64;
+constexpr int kSlots = 4096;
+
+struct DeviceState {
+    std::once_flag once;
+    int rc = TKB_OK;
+    std::string err;
+    int sms = 0;
+    int* pool = nullptr;  // kSlots x 4 ints, zeroed
+    std::mutex mu;
+    std::unordered_map<unsigned long long, int> slot_of;  // stream id -> slot
+    std::vector<unsigned long long> owner;                // slot -> stream id
+    std::vector<unsigned long long> last_use;             // slot -> tick
+    unsigned long long tick = 0;
+};
+DeviceState g_dev[kMaxDevices];
+
+int device_init(int dev) {
+    if (dev < 0 || dev >= kMaxDevices) return fail(TKB_ERR_UNSUPPORTED, "device ordinal too large");
+    DeviceState& ds = g_dev[dev];
+    std::call_once(ds.once, [&] {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+        cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaMalloc(&ds.pool, (size_t)kSlots * 4 * sizeof(int));
+        if (e == cudaSuccess) e = cudaMemset(ds.pool, 0, (size_t)kSlots * 4 * sizeof(int));
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            ds.rc = TKB_ERR_CUDA;
+            ds.err = std::string("device state init: ") + cudaGetErrorString(e);
+        }
+        ds.owner.assign(kSlots, ~0ull);
+        ds.last_use.assign(kSlots, 0);
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    });
+    if (ds.rc != TKB_OK) return fail(ds.rc, ds.err);
+    return TKB_OK;
+}
+
+// SM count and this stream's slot on the current device.
+int device_state(cudaStream_t st, int* sms, int** slot) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    if (int rc = device_init(dev)) return rc;
+    DeviceState& ds = g_dev[dev];
+    *sms = ds.sms;
+    if (slot == nullptr) return TKB_OK;
+    unsigned long long id = 0;
+    e = cudaStreamGetId(st, &id);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaStreamGetId: ") + cudaGetErrorString(e));
+    std::lock_guard<std::mutex> lock(ds.mu);
+    int s;
+    auto it = ds.slot_of.find(id);
+    if (it != ds.slot_of.end()) {
+        s = it->second;
+    } else if (ds.slot_of.size() < (size_t)kSlots) {
+        s = (int)ds.slot_of.size();
+        ds.slot_of.emplace(id, s);
+        ds.owner[s] = id;
+    } else {  // recycle the least recently used slot
+        s = 0;
+        for (int i = 1; i < kSlots; ++i)
+            if (ds.last_use[i] < ds.last_use[s]) s = i;
+        ds.slot_of.erase(ds.owner[s]);
+        ds.slot_of.emplace(id, s);
+        ds.owner[s] = id;
+    }
+    ds.last_use[s] = ++ds.tick;
+    *slot = ds.pool + 4 * s;
+    return TKB_OK;
+}
+
+// ---------------------------------------------------------------- TMA descriptor cache
+// CUtensorMap encoding is a pure function of (base, dims, strides, box, swizzle); a call
+// re-encodes 4 (forward) or 9 (backward) maps, so each host thread keeps the most recent
+// ones (direct-mapped on a hash of the key).
+struct MapKey {
+    const void* base;
+    uint64_t dims[4];
+    uint64_t strides[4];
+    uint32_t box_rows;
+    bool operator==(const MapKey& o) const {
+        return base == o.base && box_rows == o.box_rows && std::memcmp(dims, o.dims, sizeof(dims)) == 0 &&
+               std::memcmp(strides, o.strides, sizeof(strides)) == 0;
+    }
+};
+struct MapEntry {
+    bool valid = false;
+    MapKey key;
+    CUtensorMap map;
+};
+constexpr int kMapCache = 64;
+thread_local MapEntry g_maps[kMapCache];
+thread_local unsigned long long g_map_hits = 0, g_map_misses = 0;
+
+size_t map_hash(const MapKey& k) {
+    size_t h = std::hash<const void*>()(k.base) ^ (k.box_rows * 0x9E3779B97F4A7C15ull);
+    for (int i = 0; i < 4; ++i) h = h * 1099511628211ull ^ k.dims[i] ^ (k.strides[i] << 20);
+    return h;
 }
 
 struct Strides {
@@ -90,53 +199,51 @@ int check_device() {
     return cached_ok ? TKB_OK : fail(TKB_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
 }
 
-// 4-D {D, N, H, B} bf16 map with a {64, box_rows, 1, 1} SW128 box (heads = H, or Hkv for k/v).
+// 4-D {D, N, H, B} bf16 map with a {64, box_rows, 1, 1} SW128 box (heads = H, or Hkv for k/v),
+// through the per-thread descriptor cache.
 int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, const Strides& s, int heads = 0,
                   uint32_t box_rows = 128) {
-    uint64_t dims[4] = {(uint64_t)d->head_dim, (uint64_t)d->seq, (uint64_t)(heads > 0 ? heads : d->heads),
-                        (uint64_t)d->batches};
-    uint64_t strides[4] = {1, (uint64_t)s.n, (uint64_t)s.h, (uint64_t)s.b};
+    MapKey key;
+    key.base = base;
+    key.dims[0] = (uint64_t)d->head_dim;
+    key.dims[1] = (uint64_t)d->seq;
+    key.dims[2] = (uint64_t)(heads > 0 ? heads : d->heads);
+    key.dims[3] = (uint64_t)d->batches;
+    key.strides[0] = 1;
+    key.strides[1] = (uint64_t)s.n;
+    key.strides[2] = (uint64_t)s.h;
+    key.strides[3] = (uint64_t)s.b;
+    key.box_rows = box_rows;
+    MapEntry& ent = g_maps[map_hash(key) % kMapCache];
+    if (ent.valid && ent.key == key) {
+        ++g_map_hits;
+        *tm = ent.map;
+        return TKB_OK;
+    }
+    ++g_map_misses;
     uint32_t box[4] = {64, box_rows, 1, 1};
     std::string err;
-    if (!tkb::host::make_tmap(tm, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, dims, strides, box,
+    if (!tkb::host::make_tmap(tm, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, key.dims, key.strides, box,
                               CU_TENSOR_MAP_SWIZZLE_128B, &err))
         return fail(TKB_ERR_SHAPE, "tensor map: " + err);
+    ent.valid = true;
+    ent.key = key;
+    ent.map = *tm;
     return TKB_OK;
 }
 
-// One-time per-device state: SM count and the zeroed scheduler counters.
-int device_state(int* sms, int** sched) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= kMaxDevices) return fail(TKB_ERR_UNSUPPORTED, "device ordinal too large");
-    if (g_sched[dev] == nullptr) {
-        int n = 0;
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        int* buf = nullptr;
-        cudaError_t e = cudaMalloc(&buf, kSchedPairs * 2 * sizeof(int));
-        if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("scheduler alloc: ") + cudaGetErrorString(e));
-        e = cudaMemset(buf, 0, kSchedPairs * 2 * sizeof(int));
-        if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("scheduler init: ") + cudaGetErrorString(e));
-        g_num_sms[dev] = n;
-        g_sched[dev] = buf;
-    }
-    *sms = g_num_sms[dev];
-    *sched = g_sched[dev] + 2 * (int)(__atomic_fetch_add(&g_sched_next[dev], 1u, __ATOMIC_RELAXED) % kSchedPairs);
-    return TKB_OK;
-}
-
+// The reference's non-finite input scan (kernels.hpp:277-284), opt-in: the flag lives in
+// this stream's state slot (no allocation); the result is read back synchronously.
 int finite_check(const tkb_attn_desc* d, const void* const* ptrs, int nptrs, const Strides& s, int heads,
-                 cudaStream_t st) {
-    int* flag = nullptr;
-    cudaError_t e = cudaMallocAsync(&flag, sizeof(int), st);
-    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, "check_finite alloc failed");
-    cudaMemsetAsync(flag, 0, sizeof(int), st);
+                 int* slot, cudaStream_t st) {
+    int* flag = slot + 2;
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("check_finite: ") + cudaGetErrorString(e));
     int rc = tkb::launch_check_finite(ptrs, nptrs, d->batches, heads, d->seq, d->head_dim, s.b, s.h, s.n, flag, st);
     int host = 0;
-    cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(flag, st);
-    e = cudaStreamSynchronize(st);
-    if (rc != 0 || e != cudaSuccess) return fail(TKB_ERR_CUDA, "check_finite launch failed");
+    e = cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (rc != 0 || e != cudaSuccess || e2 != cudaSuccess) return fail(TKB_ERR_CUDA, "check_finite launch failed");
     if (host) return fail(TKB_ERR_CONFIG, "attention inputs must be finite");  // kernels.hpp:280-283
     return TKB_OK;
 }
@@ -163,8 +270,11 @@ TKB_API int tkb_attn_validate(const tkb_attn_desc* d) {
     if (d->head_dim != 64 && d->head_dim != 128) return fail(TKB_ERR_CONFIG, "head_dim must be 64 or 128");
     if (d->batches < 1 || d->heads < 1 || d->seq < 1) return fail(TKB_ERR_CONFIG, "positive extents required");
     if (d->causal != 0 && d->causal != 1) return fail(TKB_ERR_CONFIG, "causal must be 0 or 1");
-    if (!(std::isfinite(d->softmax_scale))) return fail(TKB_ERR_CONFIG, "softmax_scale must be finite");
-    if ((int64_t)d->batches * d->heads > (int64_t)65535 * 65535) return fail(TKB_ERR_CONFIG, "too many heads");
+    if (!std::isfinite(d->softmax_scale) || d->softmax_scale < 0.f)
+        return fail(TKB_ERR_CONFIG, "softmax_scale must be finite and >= 0 (0: D^-1/2)");
+    // the persistent schedulers index (b, h, 128-row block) tasks with 32-bit ints
+    if ((int64_t)d->batches * d->heads * ((d->seq + 127) / 128) > (int64_t)INT32_MAX)
+        return fail(TKB_ERR_CONFIG, "B * H * ceil(N / 128) must be < 2^31");
     if (d->kv_heads < 0 || d->heads % kv_heads_of(d) != 0)
         return fail(TKB_ERR_CONFIG, "heads must be a multiple of kv_heads (grouped-query attention)");
     for (const Strides& s : {strides_of(d), kv_strides_of(d)})
@@ -186,10 +296,13 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
     const Strides s = strides_of(d);
     const Strides skv = kv_strides_of(d);
     const int hkv = kv_heads_of(d);
+    int sms = 0, *slot = nullptr;
+    if ((rc = device_state(st, &sms, &slot))) return rc;
     if (d->check_finite) {
         const void* qp[1] = {q};
         const void* kvp[2] = {k, v};
-        if ((rc = finite_check(d, qp, 1, s, d->heads, st)) || (rc = finite_check(d, kvp, 2, skv, hkv, st)))
+        if ((rc = finite_check(d, qp, 1, s, d->heads, slot, st)) ||
+            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st)))
             return rc;
     }
     tkb::FwdParams p{};
@@ -197,8 +310,7 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
         (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
         return rc;
     p.group = d->heads / hkv;
-    int sms = 0;
-    if ((rc = device_state(&sms, &p.sched))) return rc;
+    p.sched = slot;
     p.lse = lse;
     p.trace = g_trace;
     p.trace_every = g_trace_every;
@@ -240,10 +352,13 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     const Strides s = strides_of(d);
     const Strides skv = kv_strides_of(d);
     const int hkv = kv_heads_of(d);
+    int sms = 0, *slot = nullptr;
+    if ((rc = device_state(st, &sms, &slot))) return rc;
     if (d->check_finite) {
         const void* qp[3] = {q, o, dout};
         const void* kvp[2] = {k, v};
-        if ((rc = finite_check(d, qp, 3, s, d->heads, st)) || (rc = finite_check(d, kvp, 2, skv, hkv, st)))
+        if ((rc = finite_check(d, qp, 3, s, d->heads, slot, st)) ||
+            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st)))
             return rc;
     }
     tkb::BwdParams p{};
@@ -269,8 +384,7 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.scale = scale_of(d);
     p.scale_log2 = p.scale * 1.44269504088896340736f;
     {
-        int sms = 0;
-        if ((rc = device_state(&sms, &p.sched))) return rc;
+        p.sched = slot;
         p.num_sms = sms;
         p.bh = (int)bh;
         // heads whose K / V (4 N D bytes each) fit in ~48 MB of L2 run together
@@ -332,8 +446,8 @@ TKB_API int tkb_rotary(const tkb_attn_desc* d, const void* x, const float* sin_t
     if (((uintptr_t)x | (uintptr_t)out | (uintptr_t)sin_tab | (uintptr_t)cos_tab) & 15)
         return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
     if ((rc = check_device())) return rc;
-    int sms = 0, *sched = nullptr;
-    if ((rc = device_state(&sms, &sched))) return rc;
+    int sms = 0;
+    if ((rc = device_state(reinterpret_cast<cudaStream_t>(stream), &sms, nullptr))) return rc;
     tkb::rope::Params p{};
     p.t[0] = rope_tensor(d, x, out, strides_of(d), d->heads);
     p.sin_tab = sin_tab;
@@ -359,8 +473,8 @@ TKB_API int tkb_rotary_qk(const tkb_attn_desc* d, const void* q, const void* k, 
         15)
         return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
     if ((rc = check_device())) return rc;
-    int sms = 0, *sched = nullptr;
-    if ((rc = device_state(&sms, &sched))) return rc;
+    int sms = 0;
+    if ((rc = device_state(reinterpret_cast<cudaStream_t>(stream), &sms, nullptr))) return rc;
     tkb::rope::Params p{};
     p.t[0] = rope_tensor(d, q, q_out, strides_of(d), d->heads);
     p.t[1] = rope_tensor(d, k, k_out, kv_strides_of(d), kv_heads_of(d));
@@ -393,8 +507,8 @@ TKB_API int tkb_gemm(const tkb_gemm_desc* d, const void* a, const void* b, void*
     if (!a || !b || !c) return fail(TKB_ERR_BOUNDS, "null tensor pointer");
     if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 15) return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
     if ((rc = check_device())) return rc;
-    int sms = 0, *sched = nullptr;
-    if ((rc = device_state(&sms, &sched))) return rc;
+    int sms = 0;
+    if ((rc = device_state(reinterpret_cast<cudaStream_t>(stream), &sms, nullptr))) return rc;
     const uint64_t lda = d->lda ? d->lda : d->k, ldb = d->ldb ? d->ldb : d->n, ldc = d->ldc ? d->ldc : d->n;
     tkb::GemmParams p{};
     std::string err;
@@ -452,6 +566,20 @@ TKB_API int tkb_debug_set_bwd_phases(int mask) {
 
 TKB_API int tkb_set_bwd_pairs(int on) {
     g_bwd_pairs = on ? 1 : 0;
+    return TKB_OK;
+}
+
+TKB_API int tkb_device_init(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) return fail(TKB_ERR_CONFIG, "no such device");
+    return device_init(device);
+}
+
+TKB_API int tkb_debug_map_cache_stats(unsigned long long* hits, unsigned long long* misses) {
+    if (hits) *hits = g_map_hits;
+    if (misses) *misses = g_map_misses;
     return TKB_OK;
 }
 

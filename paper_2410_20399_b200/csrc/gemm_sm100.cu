@@ -195,13 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 }  // namespace gemm
 
 int launch_gemm(const GemmParams& p, int num_sms, cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::kSmemBytes);
-        if (e != cudaSuccess) return (int)e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> smem_set{0};  // per device
+    if (int e = ensure_smem(gemm::gemm_kernel, gemm::kSmemBytes, smem_set)) return e;
     const int tasks = ((p.m + gemm::BM - 1) / gemm::BM) * ((p.n + gemm::BN - 1) / gemm::BN);
     const int grid = tasks < num_sms ? tasks : num_sms;
     gemm::gemm_kernel<<<grid, gemm::kThreads, gemm::kSmemBytes, stream>>>(p);

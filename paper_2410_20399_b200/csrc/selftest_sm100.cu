@@ -17,6 +17,7 @@
 
 #include "host/tmap.hpp"
 #include "tkb/tcgen05.cuh"
+#include "tkb/lcsf.cuh"
 #include "tkb/tile.cuh"
 #include "tkb/tma.cuh"
 
@@ -462,4 +463,29 @@ extern "C" __attribute__((visibility("default"))) int tkb_selftest_pipe_bench(fl
                                                                              long long* cycles, cudaStream_t st) {
     pipe_bench_kernel<<<1, 256, 0, st>>>(out, mode, iters, cycles);
     return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------- deadlock
+// The LCSF contract violation the reference detects as DeadlockError (lcsf.hpp:486-489,
+// tests/test_lcsf.cpp:204-233): a consumer waits on a ring slot whose producer never
+// arrives. mbar_wait's bound (TKB_DEADLOCK_NS; this library is built with 0.2 s) traps.
+// mode 0: the producer is missing (deadlock); mode 1: the producer arrives (completes).
+namespace {
+__global__ void deadlock_kernel(int mode, int* done) {
+    __shared__ lcsf::ring<2> r;
+    if (threadIdx.x == 0) r.init(1, 1);
+    __syncthreads();
+    lcsf::ring_state<2> st;
+    if (mode == 1 && threadIdx.x == 32) mbar_arrive(&r.full[0]);
+    if (threadIdx.x == 0) {
+        r.wait_full(st);
+        *done = 1;
+    }
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_deadlock(int mode, int* done_dev) {
+    deadlock_kernel<<<1, 64>>>(mode, done_dev);
+    cudaError_t e = cudaDeviceSynchronize();
+    return (int)e;
 }

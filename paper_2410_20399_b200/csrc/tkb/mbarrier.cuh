@@ -66,8 +66,12 @@ TKB_DEVICE uint64_t globaltimer_ns() {
 }
 
 // Blocking wait for the phase with the given parity to complete. A wait that has spun
-// for 20 s traps instead of hanging the GPU: the DeadlockError analogue of the reference
-// (lcsf.hpp:486-489). -DTKB_NO_DEADLOCK_TRAP removes the bound.
+// for TKB_DEADLOCK_NS (20 s) traps instead of hanging the GPU: the DeadlockError analogue
+// of the reference (lcsf.hpp:486-489); the launch then fails with a CUDA error that the
+// C ABI reports as TKB_ERR_CUDA. -DTKB_NO_DEADLOCK_TRAP removes the bound.
+#ifndef TKB_DEADLOCK_NS
+#define TKB_DEADLOCK_NS 20000000000ull
+#endif
 TKB_DEVICE void mbar_wait(mbarrier* b, uint32_t parity) {
 #ifndef TKB_NO_DEADLOCK_TRAP
     if (mbar_try_wait(b, parity)) return;
@@ -78,7 +82,7 @@ TKB_DEVICE void mbar_wait(mbarrier* b, uint32_t parity) {
             const uint64_t now = globaltimer_ns();
             if (t0 == 0)
                 t0 = now;
-            else if (now - t0 > 20000000000ull)
+            else if (now - t0 > (uint64_t)(TKB_DEADLOCK_NS))
                 __trap();
         }
     }

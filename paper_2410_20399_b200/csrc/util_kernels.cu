@@ -13,13 +13,14 @@ struct FinitePtrs {
     const __nv_bfloat16* p[5];
 };
 
+// Linear (bh, row block) index walked grid-stride in 64 bits: B * H may exceed gridDim.y's 65535.
 __global__ void check_finite_kernel(FinitePtrs ptrs, int nptrs, int heads, int n, int d, int64_t sb, int64_t sh,
-                                    int64_t sn, int* flag) {
-    const int bh = blockIdx.y;
-    const int b = bh / heads, h = bh % heads;
+                                    int64_t sn, int64_t total_blocks, int row_blocks, int* flag) {
     const int rows_per_block = blockDim.x * 8 / d;  // 8 bf16 per thread per row chunk
-    for (int row0 = blockIdx.x * rows_per_block; row0 < n; row0 += gridDim.x * rows_per_block) {
-        const int r = row0 + (int)(threadIdx.x * 8) / d;
+    for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
+        const int64_t bh = blk / row_blocks;
+        const int64_t b = bh / heads, h = bh % heads;
+        const int r = (int)(blk - bh * row_blocks) * rows_per_block + (int)(threadIdx.x * 8) / d;
         const int c = (threadIdx.x * 8) % d;
         if (r >= n) continue;
         for (int t = 0; t < nptrs; ++t) {
@@ -40,8 +41,12 @@ int launch_check_finite(const void* const* ptrs, int nptrs, int batches, int hea
                         int64_t sh, int64_t sn, int* flag_dev, cudaStream_t stream) {
     FinitePtrs fp{};
     for (int i = 0; i < nptrs && i < 5; ++i) fp.p[i] = reinterpret_cast<const __nv_bfloat16*>(ptrs[i]);
-    dim3 grid((n + 127) / 128 < 64 ? (n + 127) / 128 : 64, batches * heads);
-    check_finite_kernel<<<grid, 256, 0, stream>>>(fp, nptrs, heads, n, d, sb, sh, sn, flag_dev);
+    const int rows_per_block = 256 * 8 / d;
+    const int row_blocks = (n + rows_per_block - 1) / rows_per_block;
+    const int64_t total = (int64_t)row_blocks * batches * heads;
+    const int64_t cap = 148 * 16;
+    check_finite_kernel<<<(unsigned)(total < cap ? total : cap), 256, 0, stream>>>(fp, nptrs, heads, n, d, sb, sh, sn,
+                                                                                 total, row_blocks, flag_dev);
     return (int)cudaGetLastError();
 }
 

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s), s
     assert set(A.exported_symbols()) == set(declared_symbols())
-    assert A.lib().tkb_abi_version() == 2
+    assert A.lib().tkb_abi_version() == 3
 
 
 def test_library_is_built_for_sm100a():
@@ -117,3 +117,29 @@ def test_desc_layout_matches_header():
     import ctypes
     assert ctypes.sizeof(A.AttnDesc) == 8 * 4 + 6 * 8
     assert A.AttnDesc.kv_heads.offset == 28 and A.AttnDesc.kv_stride_b.offset == 56
+
+
+@pytest.mark.parametrize("scale,code", [(0.0, 0), (0.05, 0), (0.2, 0), (-0.1, 1), (float("inf"), 1),
+                                        (float("nan"), 1)])
+def test_softmax_scale_validation(scale, code):
+    """0 selects D^-1/2; a negative or non-finite scale is a ConfigError (never silently replaced)."""
+    d = A.AttentionConfig(1, 2, 256, 64).desc()
+    d.softmax_scale = scale
+    assert A.lib().tkb_attn_validate(ctypes.byref(d)) == code
+
+
+def test_task_count_bound():
+    """The persistent schedulers use 32-bit task ids: B * H * ceil(N / 128) must stay < 2^31
+    (B * H beyond gridDim.y's 65535 is fine: the helper kernels walk it grid-stride)."""
+    A.AttentionConfig(70000, 2, 128, 64).validate()  # B*H = 140000 > 65535
+    with pytest.raises(A.ConfigError):
+        A.AttentionConfig(65536, 256, 16384, 128).validate()  # 2^24 heads x 128 blocks = 2^31
+
+
+def test_device_init_without_a_gpu_fails_cleanly():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(A.Error):
+        A.device_init(0)
+
