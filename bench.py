@@ -9,10 +9,13 @@ larger than the 126 MB L2, so no L2 flush is needed between steps).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl tkb|reference] [--pass fwd|bwd|fwdbwd]
 
-Multi-GPU (torchrun, one process per GPU): the flattened batch x head grid of a
-global problem with B = 16 * world is sharded contiguously across ranks
-(tkb_shard_range); no collective touches the data path ("scaling": "weak").
-Time = max over ranks of the CUDA-event time of the K timed steps.
+Multi-GPU (one process per GPU): under torchrun the ranks come from the environment;
+`--gpus N` without torchrun spawns the N - 1 other ranks itself (rank r on visible device
+r % device_count). The flattened batch x head grid of a global problem with B = 16 * N is
+sharded contiguously across ranks (tkb_shard_range); every (b, h) unit's inputs come from
+its own seed, so a shard equals the same slice of a 1-GPU run. No collective touches the
+data path and NCCL is never initialised: the only cross-rank traffic is a gloo (CPU)
+barrier and the max-over-ranks of the CUDA-event time ("scaling": "weak").
 
 FLOP convention (FlashAttention / SURVEY.md §8(d)): fwd 4 B H N^2 D, bwd 10 B H N^2 D,
 causal x 1/2.
@@ -48,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16, help="batch chunks pipelined in the e2e step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-hashes", default=None, help="write per-unit output hashes (JSON) after the run")
     return ap.parse_args()
 
 
@@ -136,11 +140,13 @@ def cpu_reference_sample(causal, which, seq, head_dim, nthreads=None):
     """Time the reference's CPU path on a bounded sample: one (b,h) head per host thread.
 
     fwd: the UNMODIFIED reference kernel path (oracle/_ref: execute_functional(
-         attention_fwd_kernel)) — it only supports non-causal attention, so it computes
-         the full N^2 (the FLOPs credited are the workload's own, causal-halved).
-    bwd: the reference has no backward; the oracle port's fp64 backward is timed.
+         attention_fwd_kernel)). It only supports non-causal attention, so it computes the
+         full N^2 and is credited with the non-causal FLOPs it executes.
+    bwd: the reference has no backward; the oracle port's fp64 backward is timed (causal
+         work skips the masked pairs, so it is credited with the causal FLOPs).
+    kind is "reference" only when every timed part is the reference's own code.
     """
-    import numpy as np
+    import numpy as np  # noqa: F401
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as orc
@@ -150,6 +156,7 @@ def cpu_reference_sample(causal, which, seq, head_dim, nthreads=None):
     q, k, v = orc.qkv(1234, 1, heads, seq, head_dim)
     dout = orc.fill(99, heads * seq * head_dim).reshape(1, heads, seq, head_dim)
     use_ref = orc.ref_available()
+    fl = 0.0
     t0 = time.perf_counter()
     if "fwd" in which:
         if use_ref:
@@ -158,21 +165,25 @@ def cpu_reference_sample(causal, which, seq, head_dim, nthreads=None):
                                              workers=4, bf16=True, threaded=False)
             with ThreadPoolExecutor(nthreads) as ex:
                 list(ex.map(one, range(heads)))
+            fl += flops(1, heads, seq, head_dim, False, "fwd")
         else:
             orc.attn_fwd(q, k, v, causal=causal, nthreads=nthreads)
+            fl += flops(1, heads, seq, head_dim, causal, "fwd")
     t1 = time.perf_counter()
     if "bwd" in which:
         orc.attn_bwd(q, k, v, dout, causal=causal, nthreads=nthreads)
+        fl += flops(1, heads, seq, head_dim, causal, "bwd")
     t2 = time.perf_counter()
-    fl = flops(1, heads, seq, head_dim, causal, which)
+    ref_only = use_ref and "bwd" not in which
+    fwd_desc = ("reference execute_functional(attention_fwd_kernel) [non-causal only: full N^2 executed and "
+                "credited, bf16-emulated]" if use_ref else "oracle port fp64")
     return {
         "value": fl / (t2 - t0) / 1e12,
         "unit": "TFLOPS",
         "cores": nthreads,
-        "kind": "reference" if (use_ref and "fwd" in which) else "port",
-        "sample": (f"{heads} (b,h) heads of N={seq} D={head_dim}, one per host thread; fwd = "
-                   f"{'reference execute_functional(attention_fwd_kernel) [non-causal only, bf16-emulated]' if use_ref else 'oracle port fp64'}"
-                   f" {t1 - t0:.2f}s; bwd = oracle port fp64 (reference has no backward) {t2 - t1:.2f}s"),
+        "kind": "reference" if ref_only else "port",
+        "sample": (f"{heads} (b,h) heads of N={seq} D={head_dim}, one per host thread; fwd = {fwd_desc} "
+                   f"{t1 - t0:.2f}s; bwd = oracle port fp64 (the reference has no backward) {t2 - t1:.2f}s"),
         "seconds": t2 - t0,
     }
 
@@ -240,6 +251,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+
     import torch
     import torch.distributed as dist
 
@@ -248,10 +262,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    ndev = torch.cuda.device_count()
+    dev_index = local % max(1, ndev)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if world > 1:  # CPU-side group for the barrier and the timing max; no NCCL anywhere
+        dist.init_process_group("gloo", rank=rank, world_size=world)
 
     causal = bool(args.causal)
     b_loc, h, n, d = args.batch, args.heads, args.seq, args.head_dim
@@ -259,12 +275,13 @@ def main():
     units = b_loc * world * h
     u0, u1 = A.shard_range(units, rank, world)
     my_units = u1 - u0
-    gen = torch.Generator(device=dev).manual_seed(1000 + u0)  # per-shard seed: shards == the 1-GPU slices
     shape = (1, my_units, n, d)
-    q = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
-    k = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
-    v = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
-    do = torch.empty(shape, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
+    q, k, v, do = (torch.empty(shape, device=dev, dtype=torch.bfloat16) for _ in range(4))
+    gen = torch.Generator(device=dev)
+    for i, u in enumerate(range(u0, u1)):  # per-unit seeds: shards == the 1-GPU slices
+        gen.manual_seed(1000 + u)
+        for t in (q, k, v, do):
+            t[0, i].uniform_(-1, 1, generator=gen)
     o = torch.empty_like(q)
     lse = torch.empty((1, my_units, n), device=dev, dtype=torch.float32)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
@@ -340,10 +357,12 @@ def main():
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    t = torch.tensor([ms], dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # timing only, not on the data path
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # timing only (gloo, CPU), not on the data path
     ms_max = float(t.item())
+    if args.dump_hashes:
+        dump_hashes(args, world, rank, u0, [o, lse, dq, dk, dv], which)
     gpu_launches = launches["n"]
 
     total_flops = flops(1, units, n, d, causal, which) * args.steps
@@ -412,7 +431,7 @@ def main():
             e2e_step()
         e2.record(stream)
         torch.cuda.synchronize(dev)
-        t2 = torch.tensor([s2.elapsed_time(e2)], device=dev, dtype=torch.float64)
+        t2 = torch.tensor([s2.elapsed_time(e2)], dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         e2e_val = flops(1, units, n, d, causal, which) * e2e_steps / (float(t2.item()) / 1e3) / 1e12
@@ -475,6 +494,7 @@ def main():
             "value": value,
             "unit": "TFLOPS",
             "n_gpus": world,
+            "devices": min(world, ndev),
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps,
@@ -496,6 +516,56 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def dump_hashes(args, world, rank, u0, outs, which):
+    """Per-unit FNV-1a hashes of the step's outputs (O, L, dQ, dK, dV bytes), merged over
+    ranks in the file `args.dump_hashes` (one JSON object: unit -> hash)."""
+    import hashlib
+
+    import torch
+
+    torch.cuda.synchronize()
+    hs = {}
+    for i in range(outs[0].shape[1]):
+        hsh = hashlib.sha1()
+        for t in outs:
+            hsh.update(t[0, i].contiguous().view(torch.uint8).cpu().numpy().tobytes())
+        hs[str(u0 + i)] = hsh.hexdigest()
+    path = f"{args.dump_hashes}.rank{rank}"
+    with open(path, "w") as f:
+        json.dump(hs, f)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    if rank == 0:
+        merged = {}
+        for r in range(world):
+            with open(f"{args.dump_hashes}.rank{r}") as f:
+                merged.update(json.load(f))
+        with open(args.dump_hashes, "w") as f:
+            json.dump(merged, f, sort_keys=True)
+
+
+def spawn_ranks(args):
+    """`--gpus N` without torchrun: run N ranks (this process is rank 0), one process per
+    GPU, rendezvous on 127.0.0.1 for the gloo timing group."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    base = dict(os.environ, WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    kids = []
+    for r in range(1, args.gpus):
+        env = dict(base, RANK=str(r), LOCAL_RANK=str(r))
+        kids.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    os.environ.update(base, RANK="0", LOCAL_RANK="0")
+    rc = main()
+    for kd in kids:
+        rc = kd.wait() or rc
+    return rc
 
 
 def load_traffic(kernel):

@@ -45,6 +45,11 @@ def lib():
                                           ctypes.c_double, _D, _D, ctypes.c_int]
         L.tkb_oracle_attn_bwd.argtypes = [_F, _F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_double, _D, _D, _D, ctypes.c_int]
+        L.tkb_oracle_attn_fwd_rows.argtypes = L.tkb_oracle_attn_fwd.argtypes
+        _I = ctypes.POINTER(ctypes.c_int)
+        L.tkb_oracle_attn_bwd_sampled.argtypes = [_F, _F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_int, ctypes.c_double, _I, ctypes.c_int, _I, ctypes.c_int,
+                                                  _D, _D, _D, ctypes.c_int]
         L.tkb_oracle_rotary.argtypes = [_F, _F, _F, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _D]
         L.tkb_oracle_gemm.argtypes = [_F, _F, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, ctypes.c_int]
         _cache["o"] = L
@@ -131,6 +136,38 @@ def attn_bwd(q, k, v, dout, causal=False, scale=None, nthreads=None):
     dq, dk, dv = (np.empty(q.shape, dtype=np.float64) for _ in range(3))
     lib().tkb_oracle_attn_bwd(_ptr(q, _F), _ptr(k, _F), _ptr(v, _F), _ptr(dout, _F), heads, N, D, int(causal), scale,
                               _ptr(dq, _D), _ptr(dk, _D), _ptr(dv, _D), nthreads or threads())
+    return dq, dk, dv
+
+
+def attn_fwd_rows(q, k, v, causal=False, scale=None, nthreads=None):
+    """attn_fwd with every (head, row) an independent work item (long sequences, few heads)."""
+    q, k, v = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v))
+    N, D = q.shape[-2:]
+    heads = int(np.prod(q.shape[:-2])) if q.ndim > 2 else 1
+    scale = scale if scale else 1.0 / np.sqrt(D)
+    o = np.empty(q.shape, dtype=np.float64)
+    lse = np.empty(q.shape[:-1], dtype=np.float64)
+    lib().tkb_oracle_attn_fwd_rows(_ptr(q, _F), _ptr(k, _F), _ptr(v, _F), heads, N, D, int(causal), scale,
+                                   _ptr(o, _D), _ptr(lse, _D), nthreads or threads())
+    return o, lse
+
+
+def attn_bwd_sampled(q, k, v, dout, qrows, krows, causal=False, scale=None, nthreads=None):
+    """dQ at query rows `qrows` and dK / dV at key rows `krows` of every head ([..., len, D])."""
+    q, k, v, dout = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v, dout))
+    N, D = q.shape[-2:]
+    lead = q.shape[:-2]
+    heads = int(np.prod(lead)) if q.ndim > 2 else 1
+    scale = scale if scale else 1.0 / np.sqrt(D)
+    qr = np.ascontiguousarray(qrows, dtype=np.int32)
+    kr = np.ascontiguousarray(krows, dtype=np.int32)
+    _I = ctypes.POINTER(ctypes.c_int)
+    dq = np.empty(lead + (len(qr), D), dtype=np.float64)
+    dk = np.empty(lead + (len(kr), D), dtype=np.float64)
+    dv = np.empty(lead + (len(kr), D), dtype=np.float64)
+    lib().tkb_oracle_attn_bwd_sampled(_ptr(q, _F), _ptr(k, _F), _ptr(v, _F), _ptr(dout, _F), heads, N, D,
+                                      int(causal), scale, _ptr(qr, _I), len(qr), _ptr(kr, _I), len(kr), _ptr(dq, _D),
+                                      _ptr(dk, _D), _ptr(dv, _D), nthreads or threads())
     return dq, dk, dv
 
 
