@@ -142,14 +142,20 @@ struct MapEntry {
     MapKey key;
     CUtensorMap map;
 };
-constexpr int kMapCache = 64;
+constexpr int kMapCache = 128;
 thread_local MapEntry g_maps[kMapCache];
 thread_local unsigned long long g_map_hits = 0, g_map_misses = 0;
 
+uint64_t mix64(uint64_t z) {  // splitmix64 finaliser: every input bit reaches the low bits
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 size_t map_hash(const MapKey& k) {
-    size_t h = std::hash<const void*>()(k.base) ^ (k.box_rows * 0x9E3779B97F4A7C15ull);
-    for (int i = 0; i < 4; ++i) h = h * 1099511628211ull ^ k.dims[i] ^ (k.strides[i] << 20);
-    return h;
+    uint64_t h = mix64((uint64_t)(uintptr_t)k.base ^ ((uint64_t)k.box_rows << 48));
+    for (int i = 0; i < 4; ++i) h = mix64(h ^ k.dims[i] ^ (k.strides[i] << 24));
+    return (size_t)h;
 }
 
 struct Strides {
