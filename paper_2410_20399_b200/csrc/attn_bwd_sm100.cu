@@ -43,7 +43,7 @@
 #include "tkb/tma.cuh"
 
 #ifndef TKB_BWD_POLY
-#define TKB_BWD_POLY 1  // a quarter of the exponentials on the FMA-pipe polynomial
+#define TKB_BWD_POLY 1  // exponential pairs of every four on the FMA-pipe polynomial (1: a quarter)
 #endif
 
 namespace tkb {
@@ -178,10 +178,16 @@ TKB_DEVICE void exp_chunk(float* pf, float tau, uint32_t nlse4, float nlse_r) {
         const float4 l4 = ROWCONST ? make_float4(nlse_r, nlse_r, nlse_r, nlse_r) : lds_f4(nlse4 + 4 * c);
         const float2 x01 = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau), make_float2(l4.x, l4.y));
         const float2 x23 = fma2(make_float2(pf[c + 2], pf[c + 3]), make_float2(tau, tau), make_float2(l4.z, l4.w));
-        pf[c] = ex2_approx(x01.x);
-        pf[c + 1] = ex2_approx(x01.y);
+        if (((c / 2) & 3) >= 4 - TKB_BWD_POLY) {  // pair index c / 2
+            const float2 p01 = ex2_poly2(x01);
+            pf[c] = p01.x;
+            pf[c + 1] = p01.y;
+        } else {
+            pf[c] = ex2_approx(x01.x);
+            pf[c + 1] = ex2_approx(x01.y);
+        }
         float2 p23;
-        if (TKB_BWD_POLY && (c & 8) != 0) {
+        if (((c / 2 + 1) & 3) >= 4 - TKB_BWD_POLY) {  // pair index c / 2 + 1
             p23 = ex2_poly2(x23);
         } else {
             p23.x = ex2_approx(x23.x);
@@ -189,6 +195,70 @@ TKB_DEVICE void exp_chunk(float* pf, float tau, uint32_t nlse4, float nlse_r) {
         }
         pf[c + 2] = p23.x;
         pf[c + 3] = p23.y;
+    }
+}
+
+// ---- the dK/dV compute thread's view of a column group (S^T / dP^T: lanes = kv rows,
+// columns = queries). A warp of lane quarter wq and column group g reads its 32 lanes x 32
+// columns as two tcgen05.ld.16x256b.x4 (lane blocks 0 and 16 of the quarter): element
+//   e = 16 h2 + 4 r + 2 h + b   (h2, h, b < 2; r < 4)
+// sits at lane 32 wq + 16 h2 + lane / 4 + 8 h, column 32 g + 2 (lane % 4) + 8 r + b. A thread
+// thus touches only 8 distinct columns (queries) — against 32 for one-row-per-thread 32x32b
+// — so it needs 8 lse / Delta values per step instead of 32. Packed bf16 pairs k = e / 2 go
+// back with tcgen05.st.16x128b.x4 (register 2 r + h of block h2 -> lane 16 h2 + lane / 4 + 8 h,
+// packed column (lane % 4) + 4 r = queries 2 (lane % 4) + 8 r + {0, 1}): the TS-MMA A-operand
+// layout of the group's 32-query K chunk, in the group's first 16 columns.
+TKB_DEVICE void grp_load(uint32_t taddr, float* v) {  // taddr: lane 32 wq, column 32 g
+    tmem::ld_16x256b_x4(taddr, reinterpret_cast<uint32_t*>(v));
+    tmem::ld_16x256b_x4(taddr + (16u << 16), reinterpret_cast<uint32_t*>(v) + 16);
+    tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(v));
+}
+TKB_DEVICE void grp_store_packed(uint32_t taddr, const uint32_t* pk) {  // pk[k] = bf16x2(v[2k], v[2k+1])
+    tmem::st_16x128b_x4(taddr, pk);
+    tmem::st_16x128b_x4(taddr + (16u << 16), pk + 8);
+}
+TKB_DEVICE constexpr int grp_row(int e) { return 16 * (e >> 4) + 8 * ((e >> 1) & 1); }  // + lane / 4
+TKB_DEVICE constexpr int grp_col(int e) { return 8 * ((e >> 2) & 3) + (e & 1); }         // + 2 (lane % 4)
+TKB_DEVICE constexpr int grp_vec(int e) { return 2 * ((e >> 2) & 3) + (e & 1); }         // index in its 8 columns
+// Per-column vectors (-lse2, Delta) are stored with each 32-column group permuted so that a
+// thread's 8 columns are contiguous: column 2 j + 8 r + b -> position 8 j + 2 r + b.
+TKB_DEVICE constexpr int perm32(int i) {
+    return (i & ~31) | (((i >> 1) & 3) << 3) | (((i >> 3) & 3) << 1) | (i & 1);
+}
+// the 8 values of this thread's columns (lane % 4 = j): positions [8 j, 8 j + 8) of its group
+TKB_DEVICE void grp_vec_load(uint32_t group_base, float* out) {
+    const uint32_t a = group_base + 32u * (laneid() & 3);
+    const float4 lo = lds_f4(a), hi = lds_f4(a + 16);
+    out[0] = lo.x, out[1] = lo.y, out[2] = lo.z, out[3] = lo.w;
+    out[4] = hi.x, out[5] = hi.y, out[6] = hi.z, out[7] = hi.w;
+}
+// P^T = exp2(tau S^T - lse2) over the group view; a quarter of the exponentials (the last
+// pair of every four) run as a polynomial on the FMA pipe (MUFU relief)
+TKB_DEVICE void grp_exp(float* v, float tau, const float* nlse) {
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        const int c = grp_vec(e);
+        const float2 x = fma2(make_float2(v[e], v[e + 1]), make_float2(tau, tau), make_float2(nlse[c], nlse[c + 1]));
+        float2 y;
+        if (((e >> 1) & 3) >= 4 - TKB_BWD_POLY) {
+            y = ex2_poly2(x);
+        } else {
+            y.x = ex2_approx(x.x);
+            y.y = ex2_approx(x.y);
+        }
+        v[e] = y.x;
+        v[e + 1] = y.y;
+    }
+}
+// dS^T = P^T o (dP^T - Delta) packed to bf16 pairs (the softmax scale is applied at the finish)
+TKB_DEVICE void grp_ds(const float* pf, const uint32_t* dpv, const float* dlt, uint32_t* pk) {
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        const int c = grp_vec(e);
+        const float2 gg = sub2(make_float2(__uint_as_float(dpv[e]), __uint_as_float(dpv[e + 1])),
+                               make_float2(dlt[c], dlt[c + 1]));
+        const float2 d = mul2(make_float2(pf[e], pf[e + 1]), gg);
+        pk[e / 2] = pack_bf16x2(d.x, d.y);
     }
 }
 
@@ -537,25 +607,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 const int x = x0 + t;
                 const int sa = x % SA;
                 const bool diag = CAUSAL && (t % T1 == 0);  // q block i == j
-                const uint32_t nlse4 = smem_u32(sLse + sa * 128 + 32 * g);
-                const uint32_t dlt4 = smem_u32(sDelta + sa * 128 + 32 * g);
                 mbar_wait(&aux_full[sa], (x / SA) & 1);
+                float nlse[8], dlt[8];
+                grp_vec_load(smem_u32(sLse + sa * 128 + 32 * g), nlse);
+                grp_vec_load(smem_u32(sDelta + sa * 128 + 32 * g), dlt);
                 mbar_wait(&s_full_of(x), ph_of(x));
                 const uint32_t tS = tS0 + s_buf(x);
                 if (threadIdx.x == 0) TKB_TR(1, x, 0);
                 if (threadIdx.x == 0 && t == 0 && n > 0) TKB_TR(1, n - 1, 7);  // next task's first S
                 tmem::fence_after();
                 float pf[32];
-                tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
-                exp_chunk<false>(pf, tau, nlse4, 0.f);
-                if (diag) {
+                grp_load(tS, pf);
+                grp_exp(pf, tau, nlse);
+                if (diag) {  // query 32 g + col < kv row: masked
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) pf[c] = (32 * g + c < r) ? 0.f : pf[c];
+                    for (int e = 0; e < 32; ++e)
+                        pf[e] = (32 * g + grp_col(e) + 2 * (lane & 3) < 32 * wq + grp_row(e) + (lane >> 2)) ? 0.f
+                                                                                                   : pf[e];
                 }
                 uint32_t pk[16];
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) pk[c / 2] = pack_bf16x2(pf[c], pf[c + 1]);
-                tmem::st_32x32b_x16(tS, pk);
+                for (int k = 0; k < 16; ++k) pk[k] = pack_bf16x2(pf[2 * k], pf[2 * k + 1]);
+                grp_store_packed(tS, pk);
                 tmem::wait_st();
                 tmem::fence_before();
                 mbar_arrive(&p_full_of(x)[g]);
@@ -564,20 +637,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 if (threadIdx.x == 0) TKB_TR(1, x, 2);
                 tmem::fence_after();
                 uint32_t dpv[32];
-                tmem::ldw_32x32b_x32(tDp, dpv);
-#pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                    const float4 d4 = lds_f4(dlt4 + 4 * c);
-                    const float2 g01 = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
-                                            make_float2(d4.x, d4.y));
-                    const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
-                                            make_float2(d4.z, d4.w));
-                    const float2 s01 = mul2(make_float2(pf[c], pf[c + 1]), g01);
-                    const float2 s23 = mul2(make_float2(pf[c + 2], pf[c + 3]), g23);
-                    pk[c / 2] = pack_bf16x2(s01.x, s01.y);
-                    pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
-                }
-                tmem::st_32x32b_x16(tDp, pk);
+                grp_load(tDp, reinterpret_cast<float*>(dpv));
+                grp_ds(pf, dpv, dlt, pk);
+                grp_store_packed(tDp, pk);
                 tmem::wait_st();
                 tmem::fence_before();
                 mbar_arrive(&ds_full[g]);
@@ -650,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
 //   Q_t  its 64-column half of D, all 128 queries (B of dK += dS^T Q, N = D)
 // (and dO likewise). Causal: the pair visits q blocks >= 2p; block 2p is fully masked for
 // the odd CTA (P = 0 there).
-// TMEM per CTA as bwd_dkdv (kvP order): S^T | dV | dP^T (P^T / dS^T packed into it) | dK.
+// TMEM per CTA: S^T (P^T packed into it) | dV | dP^T (dS^T packed into it) | dK.
 struct CfgKV2 {
     static constexpr int D = 128;
     static constexpr int kTile = 128 * D * 2;   // K / V: 32 KB
@@ -698,7 +760,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
     mbarrier& kv_full = bars[0];     // leader: K / V of both CTAs
     mbarrier& s_full = bars[1];      // both (multicast commit)
-    mbarrier& s_free = bars[2];      // leader: S^T read out in both CTAs
     mbarrier& dp_full = bars[3];     // both
     mbarrier& dkv_full = bars[5];    // both
     // operand rings, full on the leader (both CTAs' TMA), empty on both (multicast commit):
@@ -737,7 +798,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == kWarpLoad && lane == 0) {
         mbar_init(&kv_full, 1);
         mbar_init(&s_full, 1);
-        mbar_init(&s_free, 2 * 16);  // one lane per compute warp of both CTAs
         mbar_init(&dp_full, 1);
         mbar_init(&dkv_full, 1);
         for (int g = 0; g < kGroups; ++g) {
@@ -850,25 +910,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             cluster::wait(&kv_full, 0);
             issue_s(0);
             issue_dp(0);
+            // Per step, in issue (= execution) order: dV_t, S^T_{t+1}, dK_t, dP^T_{t+1} — the
+            // single-CTA kernel's order. S^T_{t+1} overwrites S^T / P^T_t, which dV_t (issued
+            // before) reads first; dP^T_{t+1} overwrites dP^T / dS^T_t after dK_t. The next S^T
+            // thus runs under the softmax of this step's dS and the exponentials of step t + 1
+            // under dK_t / dP^T_{t+1}.
             for (int t = 0; t < T; ++t) {
                 const uint32_t ph = t & 1;
                 TKB_TR(0, t, 0);
-                if (t + 1 < T) {  // S_{t+1} once both CTAs read S_t out
-                    cluster::wait(&s_free, ph);
-                    issue_s(t + 1);
-                }
-                // dV += P_t^T dO_t   (P^T in packed columns [32g + 16, 32g + 32) of the dP region)
-                TKB_TR(0, t, 1);
+                // dV += P_t^T dO_t   (P^T in packed columns [32g, 32g + 16) of the S^T region)
                 cluster::wait(&dot_full[t % S], (t / S) & 1);
-                mma_groups(tbase + C::tmem_dv(), tbase + C::tmem_dp() + 16, dos(t) + C::kHalf, t > 0, p_full, ph);
+                mma_groups(tbase + C::tmem_dv(), tbase + C::tmem_s(), dos(t) + C::kHalf, t > 0, p_full, ph);
                 umma::commit2_e(&dot_empty[t % S]);
-                // dK += dS_t^T Q_t   (dS^T in packed columns [32g, 32g + 16))
+                TKB_TR(0, t, 1);
+                if (t + 1 < T) issue_s(t + 1);
                 TKB_TR(0, t, 2);
+                // dK += dS_t^T Q_t   (dS^T in packed columns [32g, 32g + 16) of the dP^T region)
                 cluster::wait(&qt_full[t % S], (t / S) & 1);
                 mma_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qs(t) + C::kHalf, t > 0, ds_full, ph);
                 umma::commit2_e(&qt_empty[t % S]);
                 TKB_TR(0, t, 3);
-                if (t + 1 < T) issue_dp(t + 1);  // overwrites P_t / dS_t, read by dV_t / dK_t issued before
+                if (t + 1 < T) issue_dp(t + 1);
                 TKB_TR(0, t, 4);
             }
             umma::commit2_e(&dkv_full);
@@ -882,7 +944,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
         const uint32_t tDp = tbase + lane_off + C::tmem_dp() + 32 * g;
         const float tau = p.scale_log2;
-        const uint32_t s_free_l = cluster::map(&s_free, 0);
         const uint32_t p_full_l = cluster::map(&p_full[g], 0);
         const uint32_t ds_full_l = cluster::map(&ds_full[g], 0);
         // all lanes' TMEM accesses retired, then one lane arrives on the leader's barrier
@@ -894,52 +955,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int t = 0; t < T; ++t) {
             const int i = qblock(t);
             const int s = t % S;
-            // key kv0 + r visible to query 128 i + 32 g + c iff c >= lim
-            const int lim = kv0 + r - i * 128 - 32 * g;
             const bool diag = CAUSAL && (i * 128 < kv0 + 128);
-            const uint32_t nlse4 = smem_u32(sLse + s * 128 + 32 * g);
-            const uint32_t dlt4 = smem_u32(sDelta + s * 128 + 32 * g);
             mbar_wait(&aux_full[s], (t / S) & 1);
+            float nlse[8], dlt[8];
+            grp_vec_load(smem_u32(sLse + s * 128 + 32 * g), nlse);
+            grp_vec_load(smem_u32(sDelta + s * 128 + 32 * g), dlt);
             cluster::wait(&s_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 0);
             tmem::fence_after();
             float pf[32];
-            tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
-            warp_arrive(s_free_l);  // S_{t+1} may now overwrite S_t
-            exp_chunk<false>(pf, tau, nlse4, 0.f);
-            if (diag) {
+            grp_load(tS, pf);
+            grp_exp(pf, tau, nlse);
+            if (diag) {  // key kv0 + row visible to query 128 i + 32 g + col iff col >= row + kv0 - 128 i - 32 g
+                const int lim0 = kv0 + wq * 32 + (lane >> 2) - i * 128 - 32 * g - 2 * (lane & 3);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) pf[c] = (c < lim) ? 0.f : pf[c];
+                for (int e = 0; e < 32; ++e) pf[e] = (grp_col(e) < lim0 + grp_row(e)) ? 0.f : pf[e];
             }
+            uint32_t pk[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) pk[k] = pack_bf16x2(pf[2 * k], pf[2 * k + 1]);
+            grp_store_packed(tS, pk);  // P^T over the first 16 of the group's S^T columns
+            tmem::wait_st();
+            warp_arrive(p_full_l);
             if (threadIdx.x == 0) TKB_TR(1, t, 1);
             cluster::wait(&dp_full, t & 1);
             if (threadIdx.x == 0) TKB_TR(1, t, 2);
             tmem::fence_after();
             uint32_t dpv[32];
-            tmem::ldw_32x32b_x32(tDp, dpv);
-            uint32_t pk[16];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                for (int c = 0; c < 16; c += 2) pk[8 * h + c / 2] = pack_bf16x2(pf[16 * h + c], pf[16 * h + c + 1]);
-                tmem::st_32x32b_x8(tDp + 16 + 8 * h, pk + 8 * h);
-            }
-            tmem::wait_st();
-            warp_arrive(p_full_l);
-            // dS^T = P^T o (dP^T - Delta)   (the softmax scale is applied to dK at the finish)
-#pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                const float4 d4 = lds_f4(dlt4 + 4 * c);
-                const float2 g01 =
-                    sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])), make_float2(d4.x, d4.y));
-                const float2 g23 = sub2(make_float2(__uint_as_float(dpv[c + 2]), __uint_as_float(dpv[c + 3])),
-                                        make_float2(d4.z, d4.w));
-                const float2 s01 = mul2(make_float2(pf[c], pf[c + 1]), g01);
-                const float2 s23 = mul2(make_float2(pf[c + 2], pf[c + 3]), g23);
-                pk[c / 2] = pack_bf16x2(s01.x, s01.y);
-                pk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
-            }
-            tmem::st_32x32b_x16(tDp, pk);
+            grp_load(tDp, reinterpret_cast<float*>(dpv));
+            grp_ds(pf, dpv, dlt, pk);
+            grp_store_packed(tDp, pk);
             tmem::wait_st();
             warp_arrive(ds_full_l);
             if (threadIdx.x == 0) TKB_TR(1, t, 3);
@@ -1222,8 +1267,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             const int q0 = w.i * 128;
             const int row = q0 + r;
             const int nk = nk_of(w);
-            const float nlse_r = p.lse2[(size_t)w.bh * p.n_pad + row];  // -lse2; -inf on padded rows -> P = 0
-            const float dlt_r = p.delta[(size_t)w.bh * p.n_pad + row];
+            // -lse2 (-inf on padded rows -> P = 0) and Delta, stored group-permuted (perm32)
+            const float nlse_r = p.lse2[(size_t)w.bh * p.n_pad + perm32(row)];
+            const float dlt_r = p.delta[(size_t)w.bh * p.n_pad + perm32(row)];
             for (int jj = 0; jj < nk; ++jj, ++it) {
                 const int kv0 = jj * 128;
                 mbar_wait(&s_full, it & 1);
@@ -1294,7 +1340,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 }
 #undef TKB_TR
 
-// Delta = rowsum(dO o O), lse2 = -L log2 e (-inf / 0 on padded rows: P = 0 there).
+// Delta = rowsum(dO o O), lse2 = -L log2 e (-inf / 0 on padded rows: P = 0 there), written
+// at perm32(row) within each 32-row group (the dK/dV compute threads' column order).
 // HBM-bound: each thread owns 16 bytes of kPrepRows rows (rows kPrepRows * 16 / (D / 8) apart
 // within the block's row range) and issues all their loads before reducing, so a thread
 // keeps 2 * 16 * kPrepRows bytes in flight.
@@ -1344,7 +1391,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
 #pragma unroll
             for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
             if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
-                const size_t idx = (size_t)bh * n_pad + row;
+                const size_t idx = (size_t)bh * n_pad + perm32(row);  // group-permuted (perm32)
                 delta[idx] = row < n ? acc : 0.f;
                 lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
             }

@@ -126,7 +126,7 @@ int device_state(cudaStream_t st, int* sms, int** slot) {
 // ---------------------------------------------------------------- TMA descriptor cache
 // CUtensorMap encoding is a pure function of (base, dims, strides, box, swizzle); a call
 // re-encodes 4 (forward) or 9 (backward) maps, so each host thread keeps the most recent
-// ones (direct-mapped on a hash of the key).
+// ones (4-way set-associative on a hash of the key, LRU within a set).
 struct MapKey {
     const void* base;
     uint64_t dims[4];
@@ -139,12 +139,13 @@ struct MapKey {
 };
 struct MapEntry {
     bool valid = false;
+    unsigned long long used = 0;  // LRU tick
     MapKey key;
     CUtensorMap map;
 };
-constexpr int kMapCache = 128;
-thread_local MapEntry g_maps[kMapCache];
-thread_local unsigned long long g_map_hits = 0, g_map_misses = 0;
+constexpr int kMapSets = 32, kMapWays = 4;  // 4-way set-associative, LRU within a set
+thread_local MapEntry g_maps[kMapSets][kMapWays];
+thread_local unsigned long long g_map_hits = 0, g_map_misses = 0, g_map_tick = 0;
 
 uint64_t mix64(uint64_t z) {  // splitmix64 finaliser: every input bit reaches the low bits
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -220,11 +221,17 @@ int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, con
     key.strides[2] = (uint64_t)s.h;
     key.strides[3] = (uint64_t)s.b;
     key.box_rows = box_rows;
-    MapEntry& ent = g_maps[map_hash(key) % kMapCache];
-    if (ent.valid && ent.key == key) {
-        ++g_map_hits;
-        *tm = ent.map;
-        return TKB_OK;
+    MapEntry* set = g_maps[map_hash(key) % kMapSets];
+    MapEntry* victim = &set[0];
+    for (int w = 0; w < kMapWays; ++w) {
+        MapEntry& e = set[w];
+        if (e.valid && e.key == key) {
+            ++g_map_hits;
+            e.used = ++g_map_tick;
+            *tm = e.map;
+            return TKB_OK;
+        }
+        if (!e.valid || e.used < victim->used) victim = &e;
     }
     ++g_map_misses;
     uint32_t box[4] = {64, box_rows, 1, 1};
@@ -232,9 +239,10 @@ int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, con
     if (!tkb::host::make_tmap(tm, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, key.dims, key.strides, box,
                               CU_TENSOR_MAP_SWIZZLE_128B, &err))
         return fail(TKB_ERR_SHAPE, "tensor map: " + err);
-    ent.valid = true;
-    ent.key = key;
-    ent.map = *tm;
+    victim->valid = true;
+    victim->used = ++g_map_tick;
+    victim->key = key;
+    victim->map = *tm;
     return TKB_OK;
 }
 

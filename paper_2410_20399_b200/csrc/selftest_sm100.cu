@@ -489,3 +489,64 @@ extern "C" __attribute__((visibility("default"))) int tkb_selftest_deadlock(int 
     cudaError_t e = cudaDeviceSynchronize();
     return (int)e;
 }
+
+// ---------------------------------------------------------------------------- TMEM shapes
+// Pins the 16-lane tcgen05 data-movement maps the backward's dK/dV compute relies on
+// (attn_bwd_sm100.cu, grp_load / grp_store_packed):
+//   ld.16x256b.x4 at lane block L: register 4 r + 2 h + b <- lane L + lane/4 + 8 h, column
+//                                  2 (lane % 4) + 8 r + b
+//   st.16x128b.x4 at lane block L: register 2 r + h -> lane L + lane/4 + 8 h, column lane % 4 + 4 r
+// Returns the number of mismatching elements in *bad.
+namespace {
+__global__ void __launch_bounds__(128, 1) tmem_shape_kernel(int* bad) {
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0) tmem::alloc<64>(&slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t base = slot + ((uint32_t)(warp * 32) << 16);
+    const int row = warp * 32 + lane;
+    uint32_t v[32];
+    for (int c = 0; c < 32; ++c) v[c] = (uint32_t)(row * 64 + c);
+    tmem::st_32x32b_x32(base, v);
+    tmem::wait_st();
+    int errs = 0;
+    for (int blk = 0; blk < 2; ++blk) {
+        uint32_t w[16];
+        tmem::ld_16x256b_x4(base + ((uint32_t)(16 * blk) << 16), w);
+        tmem::wait_ld_x16(w);
+        for (int rr = 0; rr < 4; ++rr)
+            for (int h = 0; h < 2; ++h)
+                for (int b = 0; b < 2; ++b) {
+                    const int R = warp * 32 + 16 * blk + lane / 4 + 8 * h;
+                    const int C = 2 * (lane % 4) + 8 * rr + b;
+                    errs += w[4 * rr + 2 * h + b] != (uint32_t)(R * 64 + C);
+                }
+    }
+    for (int blk = 0; blk < 2; ++blk) {
+        uint32_t pk[8];
+        for (int k = 0; k < 8; ++k) pk[k] = (uint32_t)(100000 * (blk + 1) + 1000 * k + threadIdx.x);
+        tmem::st_16x128b_x4(base + 32 + ((uint32_t)(16 * blk) << 16), pk);
+    }
+    tmem::wait_st();
+    uint32_t got[16];
+    tmem::ld_32x32b_x16(base + 32, got);
+    tmem::wait_ld_x16(got);
+    for (int m = 0; m < 16; ++m) {  // this thread holds lane `lane` of the quarter: its row
+        const int R16 = lane % 16, blk = lane / 16;
+        const int h = R16 / 8, writer = 4 * (R16 % 8) + m % 4, rr = m / 4;
+        const uint32_t want = (uint32_t)(100000 * (blk + 1) + 1000 * (2 * rr + h) + warp * 32 + writer);
+        errs += got[m] != want;
+    }
+    atomicAdd(bad, errs);
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) tmem::dealloc<64>(slot);
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_tmem_shapes(int* bad_dev) {
+    tmem_shape_kernel<<<1, 128>>>(bad_dev);
+    return (int)cudaDeviceSynchronize();
+}

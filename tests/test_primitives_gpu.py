@@ -67,3 +67,12 @@ def test_umma_throughput(cuda_dev, variant):
     per_mma = cyc.item() / (reps * k / 16)
     print(f"variant {variant}: {per_mma:.1f} cycles per 128x128x16 MMA")
     assert per_mma < 1000
+
+
+def test_tmem_16lane_shapes(cuda_dev):
+    """The 16x256b load / 16x128b store register maps the backward's dK/dV compute uses."""
+    lib = _lib.load_selftest()
+    lib.tkb_selftest_tmem_shapes.argtypes = [ctypes.c_void_p]
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    assert lib.tkb_selftest_tmem_shapes(bad.data_ptr()) == 0
+    assert int(bad.item()) == 0
