@@ -39,8 +39,7 @@
 #include "attn_common.cuh"
 #include "tkb/cluster.cuh"
 #include "tkb/lcsf.cuh"
-#include "tkb/tcgen05.cuh"
-#include "tkb/tma.cuh"
+#include "tkb/tile.cuh"
 
 #ifndef TKB_BWD_POLY
 #define TKB_BWD_POLY 1  // exponential pairs of every four on the FMA-pipe polynomial (1: a quarter)
@@ -65,88 +64,28 @@ struct Tiles {
 
 // ------------------------------------------------------------------------------ helpers
 
-constexpr uint32_t kDescHi = umma::desc_hi_sw128(1024);  // SBO = 8 rows x 128 B
-
-// X = A B^T with A [128 rows][D] and B [128 rows][D], both K-major (K = D)
 template <int D>
-TKB_DEVICE void mm_abt(uint32_t dst, uint32_t a, uint32_t b, uint32_t idesc) {
-#pragma unroll
-    for (int k = 0; k < D / 16; ++k) {
-        const uint32_t off = (k / 4) * kAtomBytes + (k % 4) * 32;
-        umma::mma_ss_e(dst, umma::desc_lo(a + off, 16), kDescHi, umma::desc_lo(b + off, 16), kDescHi, idesc, k > 0);
-    }
+using Tile = st_bf<128, D>;  // a 128-row K / V / Q / dO block in SMEM (SW128)
+
+// SW128 SMEM tile row r, columns [g D/4, (g+1) D/4) -> TMEM A-operand columns (bf16 pairs):
+// shared -> register -> TMEM (a TS-MMA operand staged once per task)
+template <int D>
+TKB_DEVICE void smem_rows_to_tmem_a(const Tile<D>& tile, uint32_t tdst, int r, int g) {
+    rt_bf<D / 4> f;
+    load(f, tile, r, g * (D / 4));
+    store(tdst + g * (D / 8), f);
 }
 
-// X = A B^T with A in TMEM (128 lanes x D, bf16 pairs) and B [128 rows][D] K-major (K = D)
+// TMEM fp32 [lane r][D/4 columns of group g] (x mul) -> bf16 -> SW128 SMEM tile row r
 template <int D>
-TKB_DEVICE void mm_tmem_abt(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc) {
-#pragma unroll
-    for (int k = 0; k < D / 16; ++k) {
-        const uint32_t off = (k / 4) * kAtomBytes + (k % 4) * 32;
-        umma::mma_ts_e(dst, a_tmem + k * 8, umma::desc_lo(b + off, 16), kDescHi, idesc, k > 0);
-    }
-}
-
-// acc (+)= A B over K = 128: A = bf16 pairs in TMEM, group g's 32-wide K chunk at packed
-// columns [32g, 32g + 16) of a_tmem (k-steps 2g, 2g+1); B [128 K rows][D] MN-major SMEM.
-// Each chunk is issued as soon as `wait_chunk(g)` returns.
-template <class WaitChunk>
-TKB_DEVICE void mma_tmem_a_groups(uint32_t dst, uint32_t a_tmem, uint32_t b, uint32_t idesc, bool acc,
-                                  WaitChunk&& wait_chunk) {
-#pragma unroll
-    for (int g = 0; g < kGroups; ++g) {
-        wait_chunk(g);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-            const int k = 2 * g + kk;
-            umma::mma_ts_e(dst, a_tmem + 32 * g + 8 * kk, umma::desc_lo(b + k * 2048, kAtomBytes), kDescHi, idesc,
-                           acc || g > 0 || kk > 0);
-        }
-    }
-}
-
-// SW128 smem tile row r, columns [g D/4, (g+1) D/4) -> TMEM A-operand columns (bf16 pairs)
-template <int D>
-TKB_DEVICE void smem_rows_to_tmem_a(const uint8_t* tile, uint32_t tdst, int r, int g) {
-    constexpr int kChunks = D / 32;  // 16-byte chunks per quarter row
-    uint32_t v[kChunks * 4];
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-        const int gc = g * kChunks + q;
-        const int atom = gc / 8, ch = gc % 8;
-        const uint4 u = *reinterpret_cast<const uint4*>(tile + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16));
-        v[4 * q] = u.x;
-        v[4 * q + 1] = u.y;
-        v[4 * q + 2] = u.z;
-        v[4 * q + 3] = u.w;
-    }
-    if constexpr (D == 128)
-        tmem::st_32x32b_x16(tdst + g * 16, v);
-    else
-        tmem::st_32x32b_x8(tdst + g * 8, v);
-}
-
-// TMEM fp32 [lane r][D] (x mul) -> bf16 -> SW128 smem tile: row r, columns [g D/4, (g+1) D/4)
-template <int D>
-TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, uint8_t* stage, int r, int g, float mul = 1.f) {
-    constexpr int kCols = D / 4;
-    const int col = g * kCols;
-    uint32_t v[kCols];
-    if constexpr (D == 128)
-        tmem::ldw_32x32b_x32(tsrc + col, v);
-    else
-        tmem::ldw_32x32b_x16(tsrc + col, v);
-#pragma unroll
-    for (int q = 0; q < kCols / 8; ++q) {
-        const int gc = col / 8 + q;  // 16-byte chunk index within the row
-        const int atom = gc / 8, ch = gc % 8;
-        uint4 u;
-        u.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * mul, __uint_as_float(v[8 * q + 1]) * mul);
-        u.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * mul, __uint_as_float(v[8 * q + 3]) * mul);
-        u.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * mul, __uint_as_float(v[8 * q + 5]) * mul);
-        u.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * mul, __uint_as_float(v[8 * q + 7]) * mul);
-        *reinterpret_cast<uint4*>(stage + atom * kAtomBytes + r * 128 + ((ch ^ (r & 7)) * 16)) = u;
-    }
+TKB_DEVICE void tmem_rows_to_smem_bf16(uint32_t tsrc, const Tile<D>& stage, int r, int g, float m = 1.f) {
+    rt_fl<D / 4> f;
+    load(f, tsrc + g * (D / 4));
+    load_wait(f);
+    mul(f, m);
+    rt_bf<D / 4> h;
+    copy(h, f);
+    store(stage, h, r, g * (D / 4));
 }
 
 TKB_DEVICE long long* trace_slot(const BwdParams& p, int lin, int kernel) {
@@ -284,42 +223,6 @@ struct TmemKV {
 //   - the finish reads dV / dK out of TMEM, releases them at once (dv_free / dk_free: the
 //     next task's first dV / dK overwrite them) and stages them in two ring slots for a TMA
 //     store issued by the load warp (see FINISH below).
-// TMEM fp32 [lane][D/4 columns of group g] -> registers; the caller releases TMEM, then
-// rows_store_bf16 writes them (x mul) as bf16. Warp-collective: lane l holds row
-// row0 + l (columns [g D/4, (g+1) D/4) at `lane0_dst` + l * row_stride). Stored as is, each
-// 16-byte store instruction would touch 32 rows = 32 L2 lines, and the L1 store path
-// (~1 line / clk) then stalls the warps for thousands of cycles per task (measured: -11 %
-// causal, -33 % N = 1024 backward). The rows are first transposed through shuffles so that
-// each instruction writes SEG contiguous bytes of 32 / CH rows (CH = SEG / 16 lanes per
-// row): 4x (D = 128) / 2x (D = 64) fewer lines per warp. Rows >= rows_valid are skipped.
-template <int D>
-TKB_DEVICE void rows_store_bf16(const uint32_t* v, __nv_bfloat16* lane0_dst, long long row_stride, int rows_valid,
-                                float mul) {
-    constexpr int kU32 = D / 8;      // packed bf16 pairs per lane (its row segment)
-    constexpr int kCh = kU32 / 4;    // 16-byte chunks per row segment
-    constexpr int kRpi = 32 / kCh;   // rows per store instruction
-    uint32_t pk[kU32];
-#pragma unroll
-    for (int j = 0; j < kU32; ++j) pk[j] = pack_bf16x2(__uint_as_float(v[2 * j]) * mul, __uint_as_float(v[2 * j + 1]) * mul);
-    const int lane = laneid();
-    const int c = lane % kCh;
-#pragma unroll
-    for (int k = 0; k < kCh; ++k) {
-        const int src = k * kRpi + lane / kCh;  // the row this lane writes now
-        uint32_t out[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            out[j] = 0;
-#pragma unroll
-            for (int cc = 0; cc < kCh; ++cc) {
-                const uint32_t t = __shfl_sync(0xffffffffu, pk[4 * cc + j], src);
-                out[j] = (cc == c) ? t : out[j];
-            }
-        }
-        if (src < rows_valid) st_global_v4(lane0_dst + (size_t)src * row_stride + 8 * c, make_uint4(out[0], out[1], out[2], out[3]));
-    }
-}
-
 struct KvTask {
     int j, head, batch;
 };
@@ -529,22 +432,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         }
     } else if (warp == kWarpMma) {
         // ----------------------------------------------------------------- MMA (converged warp)
-        constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();
-        constexpr uint32_t id_kv = umma::idesc_bf16<128, D, false, true>();
-        const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-        auto qaddr = [&](int x) { return smem_u32(sQ + (x % SQ) * TL::kTileBytes); };
-        auto doaddr = [&](int x) { return smem_u32(sDo + (x % SD) * TL::kTileBytes); };
-        auto issue_s = [&](int x) {
+        const Tile<D> tK{sK}, tV{sV};
+        auto tQ = [&](int x) { return Tile<D>{sQ + (x % SQ) * TL::kTileBytes}; };
+        auto tDo = [&](int x) { return Tile<D>{sDo + (x % SD) * TL::kTileBytes}; };
+        auto issue_s = [&](int x) {  // S^T = K Q^T
             mbar_wait(&q_full[x % SQ], (x / SQ) & 1);
             tmem::fence_after();
-            mm_abt<D>(tbase + s_buf(x), aK, qaddr(x), id_s);
-            umma::commit_e(&s_full_of(x));
+            mm_ABt(tt_fl<128>{tbase + s_buf(x)}, tK, tQ(x));
+            mma_commit(&s_full_of(x));
         };
-        auto issue_dp = [&](int x) {
+        auto issue_dp = [&](int x) {  // dP^T = V dO^T
             mbar_wait(&do_full[x % SD], (x / SD) & 1);
             tmem::fence_after();
-            mm_abt<D>(tbase + CT::tmem_dp(), aV, doaddr(x), id_s);
-            umma::commit_e(&dp_full);
+            mm_ABt(tt_fl<128>{tbase + CT::tmem_dp()}, tV, tDo(x));
+            mma_commit(&dp_full);
         };
         int x0 = 0;  // first global step of the task
         for (int n = 0;; ++n) {
@@ -555,36 +456,40 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
             mbar_wait(&kv_full, n & 1);
             issue_s(x0);
             issue_dp(x0);
-            if (T == 1) umma::commit_e(&kv_empty);
+            if (T == 1) mma_commit(&kv_empty);
             for (int t = 0; t < T; ++t) {
                 const int x = x0 + t;
                 const uint32_t ph = x & 1;
                 TKB_TR(0, x, 0);
                 if (t == 0 && n > 0) mbar_wait(&dv_free, (n - 1) & 1);  // previous task's dV read out
                 if (kDS && t + 1 < T) issue_s(x + 1);  // other buffer: its P_{t-1} went to dV_{t-1}, issued before
-                mma_tmem_a_groups(tbase + CT::tmem_dv(), tbase + s_buf(x), doaddr(x), id_kv, t > 0, [&](int g) {
-                    mbar_wait(&p_full_of(x)[g], ph_of(x));
-                    tmem::fence_after();
-                });
+                // dV += P^T dO (mma_AB: P^T chunks in TMEM as they land, dO read MN-major)
+                mma_AB_groups(tt_fl<D>{tbase + CT::tmem_dv()}, tt_bf<128>{tbase + s_buf(x)}, swap_layout(tDo(x)),
+                              t > 0, [&](int g) {
+                                  mbar_wait(&p_full_of(x)[g], ph_of(x));
+                                  tmem::fence_after();
+                              });
                 TKB_TR(0, x, 1);
-                umma::commit_e(&do_empty[x % SD]);
+                mma_commit(&do_empty[x % SD]);
                 if (!kDS && t + 1 < T) issue_s(x + 1);  // overwrites P_t, read by dV_t issued before
                 TKB_TR(0, x, 2);
                 if (t == 0 && n > 0) mbar_wait(&dk_free, (n - 1) & 1);
-                mma_tmem_a_groups(tbase + CT::tmem_dk(), tbase + CT::tmem_dp(), qaddr(x), id_kv, t > 0, [&](int g) {
-                    mbar_wait(&ds_full[g], ph);
-                    tmem::fence_after();
-                });
+                // dK += dS^T Q
+                mma_AB_groups(tt_fl<D>{tbase + CT::tmem_dk()}, tt_bf<128>{tbase + CT::tmem_dp()}, swap_layout(tQ(x)),
+                              t > 0, [&](int g) {
+                                  mbar_wait(&ds_full[g], ph);
+                                  tmem::fence_after();
+                              });
                 TKB_TR(0, x, 3);
-                umma::commit_e(&q_empty[x % SQ]);
-                umma::commit_e(&aux_empty[x % SA]);  // dK_x waited for the last dS of step x
+                mma_commit(&q_empty[x % SQ]);
+                mma_commit(&aux_empty[x % SA]);  // dK_x waited for the last dS of step x
                 if (t + 1 < T) {
                     issue_dp(x + 1);  // overwrites dS_t, read by dK_t issued before
-                    if (t + 2 == T) umma::commit_e(&kv_empty);  // the task's last S^T / dP^T issued
+                    if (t + 2 == T) mma_commit(&kv_empty);  // the task's last S^T / dP^T issued
                 }
                 TKB_TR(0, x, 4);
             }
-            umma::commit_e(&dkv_full);
+            mma_commit(&dkv_full);
             x0 += T;
         }
     } else {
@@ -660,33 +565,34 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
             if (staged) {
                 uint8_t* stage_v = sQ + ((x0 + 2) % SQ) * TL::kTileBytes;
                 uint8_t* stage_k = sDo + ((x0 + 1) % SD) * TL::kTileBytes;
-                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dv(), stage_v, r, g);
+                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dv(), Tile<D>{stage_v}, r, g);
                 tmem::fence_before();
                 mbar_arrive(&dv_free);
-                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dk(), stage_k, r, g, p.scale);
+                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dk(), Tile<D>{stage_k}, r, g, p.scale);
                 tmem::fence_before();
                 mbar_arrive(&dk_free);
                 tma::fence_async_smem();
                 mbar_arrive(&staged_full);  // the load warp stores them
             } else {
+                // dV / dK rows from registers (register -> global, warp-transposed)
                 const int row0 = kv0 + wq * 32;  // row of lane 0
-                const size_t off =
-                    (size_t)w.batch * p.kv_sb + (size_t)w.head * p.kv_sh + (size_t)row0 * p.kv_sn + g * (D / 4);
-                uint32_t v[D / 4];
-                if constexpr (D == 128)
-                    tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
-                else
-                    tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dv() + g * (D / 4), v);
+                const gv<__nv_bfloat16> gdv{reinterpret_cast<__nv_bfloat16*>(p.dv), p.kv_sb, p.kv_sh, p.kv_sn};
+                const gv<__nv_bfloat16> gdk{reinterpret_cast<__nv_bfloat16*>(p.dk), p.kv_sb, p.kv_sh, p.kv_sn};
+                rt_fl<D / 4> f;
+                rt_bf<D / 4> h;
+                load(f, tbase + lane_off + CT::tmem_dv() + g * (D / 4));
+                load_wait(f);
                 tmem::fence_before();
                 mbar_arrive(&dv_free);
-                rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dv) + off, p.kv_sn, p.n - row0, 1.f);
-                if constexpr (D == 128)
-                    tmem::ldw_32x32b_x32(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
-                else
-                    tmem::ldw_32x32b_x16(tbase + lane_off + CT::tmem_dk() + g * (D / 4), v);
+                copy(h, f);
+                store_rows(gdv, h, w.batch, w.head, row0, g * (D / 4), p.n - row0);
+                load(f, tbase + lane_off + CT::tmem_dk() + g * (D / 4));
+                load_wait(f);
                 tmem::fence_before();
                 mbar_arrive(&dk_free);
-                rows_store_bf16<D>(v, reinterpret_cast<__nv_bfloat16*>(p.dk) + off, p.kv_sn, p.n - row0, p.scale);
+                mul(f, p.scale);  // dK = scale dS^T Q
+                copy(h, f);
+                store_rows(gdk, h, w.batch, w.head, row0, g * (D / 4), p.n - row0);
             }
             if (threadIdx.x == 0) TKB_TR(1, n, 6);
             __syncwarp();
@@ -732,17 +638,6 @@ struct CfgKV2 {
     static __device__ __forceinline__ constexpr uint32_t tmem_dp() { return 256u; }
     static __device__ __forceinline__ constexpr uint32_t tmem_dk() { return 384u; }
 };
-
-// X^T (+)= A[128 own rows][128] B_half[64 rows][128]^T over the pair: A atoms 16 KB apart,
-// B (a 64-row half tile) atoms 8 KB apart; both K-major
-TKB_DEVICE void mm2_abt(uint32_t dst, uint32_t a, uint32_t b, uint32_t idesc) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t offa = (k / 4) * kAtomBytes + (k % 4) * 32;
-        const uint32_t offb = (k / 4) * (kAtomBytes / 2) + (k % 4) * 32;
-        umma::mma2_ss_e(dst, umma::desc_lo(a + offa, 16), kDescHi, umma::desc_lo(b + offb, 16), kDescHi, idesc, k > 0);
-    }
-}
 
 template <bool CAUSAL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -873,39 +768,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     } else if (warp == kWarpMma) {
         if (leader) {
             // ------------------------------------------------------------- MMA (leader, converged)
-            constexpr uint32_t id_s = umma::idesc_bf16_m256<128, false, false>();  // S^T, dP^T
-            constexpr uint32_t id_kv = umma::idesc_bf16_m256<128, false, true>();  // dV, dK
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-            auto qs = [&](int t) { return smem_u32(sQ + (t % S) * C::kTile); };
-            auto dos = [&](int t) { return smem_u32(sDo + (t % S) * C::kTile); };
-            // acc (+)= A[TMEM packed chunks] B_t[128 query rows][64 D cols] (MN-major, one atom)
-            auto mma_groups = [&](uint32_t dst, uint32_t a_tmem, uint32_t b, bool acc, mbarrier* ready,
-                                  uint32_t ph) {
-#pragma unroll
-                for (int g = 0; g < kGroups; ++g) {
+            const Tile<128> tK{sK}, tV{sV};
+            // per ring slot: Q_s / dO_s = this CTA's 64-query half (all D), Q_t / dO_t = its
+            // 64-column half of D (all 128 queries)
+            auto qs = [&](int t) { return st_bf<64, 128>{sQ + (t % S) * C::kTile}; };
+            auto dos = [&](int t) { return st_bf<64, 128>{sDo + (t % S) * C::kTile}; };
+            auto qt = [&](int t) { return st_bf<128, 64>{sQ + (t % S) * C::kTile + C::kHalf}; };
+            auto dot = [&](int t) { return st_bf<128, 64>{sDo + (t % S) * C::kTile + C::kHalf}; };
+            auto ready_of = [&](mbarrier* ready, uint32_t ph) {
+                return [=](int g) {
                     cluster::wait(&ready[g], ph);
                     tmem::fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) {
-                        const int k = 2 * g + kk;
-                        umma::mma2_ts_e(dst, a_tmem + 32 * g + 8 * kk, umma::desc_lo(b + k * 2048, kAtomBytes),
-                                        kDescHi, id_kv, acc || g > 0 || kk > 0);
-                    }
-                }
+                };
             };
             auto issue_s = [&](int x) {  // S^T_x = K Q_x^T
                 cluster::wait(&qs_full[x % S], (x / S) & 1);
                 tmem::fence_after();
-                mm2_abt(tbase + C::tmem_s(), aK, qs(x), id_s);
-                umma::commit2_e(&s_full);
-                umma::commit2_e(&qs_empty[x % S]);
+                pair::mm_ABt(tt_fl<128>{tbase + C::tmem_s()}, tK, qs(x));
+                pair::mma_commit(&s_full);
+                pair::mma_commit(&qs_empty[x % S]);
             };
             auto issue_dp = [&](int x) {  // dP^T_x = V dO_x^T
                 cluster::wait(&dos_full[x % S], (x / S) & 1);
                 tmem::fence_after();
-                mm2_abt(tbase + C::tmem_dp(), aV, dos(x), id_s);
-                umma::commit2_e(&dp_full);
-                umma::commit2_e(&dos_empty[x % S]);
+                pair::mm_ABt(tt_fl<128>{tbase + C::tmem_dp()}, tV, dos(x));
+                pair::mma_commit(&dp_full);
+                pair::mma_commit(&dos_empty[x % S]);
             };
             cluster::wait(&kv_full, 0);
             issue_s(0);
@@ -920,20 +808,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 TKB_TR(0, t, 0);
                 // dV += P_t^T dO_t   (P^T in packed columns [32g, 32g + 16) of the S^T region)
                 cluster::wait(&dot_full[t % S], (t / S) & 1);
-                mma_groups(tbase + C::tmem_dv(), tbase + C::tmem_s(), dos(t) + C::kHalf, t > 0, p_full, ph);
-                umma::commit2_e(&dot_empty[t % S]);
+                pair::mma_AB_groups(tt_fl<128>{tbase + C::tmem_dv()}, tt_bf<128>{tbase + C::tmem_s()},
+                                    swap_layout(dot(t)), t > 0, ready_of(p_full, ph));
+                pair::mma_commit(&dot_empty[t % S]);
                 TKB_TR(0, t, 1);
                 if (t + 1 < T) issue_s(t + 1);
                 TKB_TR(0, t, 2);
                 // dK += dS_t^T Q_t   (dS^T in packed columns [32g, 32g + 16) of the dP^T region)
                 cluster::wait(&qt_full[t % S], (t / S) & 1);
-                mma_groups(tbase + C::tmem_dk(), tbase + C::tmem_dp(), qs(t) + C::kHalf, t > 0, ds_full, ph);
-                umma::commit2_e(&qt_empty[t % S]);
+                pair::mma_AB_groups(tt_fl<128>{tbase + C::tmem_dk()}, tt_bf<128>{tbase + C::tmem_dp()},
+                                    swap_layout(qt(t)), t > 0, ready_of(ds_full, ph));
+                pair::mma_commit(&qt_empty[t % S]);
                 TKB_TR(0, t, 3);
                 if (t + 1 < T) issue_dp(t + 1);
                 TKB_TR(0, t, 4);
             }
-            umma::commit2_e(&dkv_full);
+            pair::mma_commit(&dkv_full);
         }
     } else {
         // ----------------------------------------------------------------- COMPUTE (both CTAs)
@@ -992,8 +882,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // FINISH: dV, dK (TMEM fp32) -> bf16 -> SMEM (Q and dO rings are free) -> TMA store
         cluster::wait(&dkv_full, 0);
         tmem::fence_after();
-        tmem_rows_to_smem_bf16<128>(tbase + lane_off + C::tmem_dv(), sQ, r, g);
-        tmem_rows_to_smem_bf16<128>(tbase + lane_off + C::tmem_dk(), sDo, r, g, p.scale);  // dK = scale dS^T Q
+        tmem_rows_to_smem_bf16<128>(tbase + lane_off + C::tmem_dv(), Tile<128>{sQ}, r, g);
+        tmem_rows_to_smem_bf16<128>(tbase + lane_off + C::tmem_dk(), Tile<128>{sDo}, r, g, p.scale);  // dK = scale dS^T Q
         tma::fence_async_smem();
         named_sync(kBarCompute, kComputeThreads);
         if (threadIdx.x == 0) {
@@ -1177,24 +1067,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
         }
     } else if (warp == kWarpMma) {
         // ----------------------------------------------------------------- MMA (converged warp)
-        constexpr uint32_t id_s = umma::idesc_bf16<128, 128, false, false>();  // S, dP
-        constexpr uint32_t id_q = umma::idesc_bf16<128, D, false, true>();     // dQ (A = dS in TMEM)
         int kv = 0;        // K / V ring position
         uint32_t it = 0;   // global iteration count (s_full / s_free / dp_full / ds_full phases)
-        auto kaddr = [&](int x) { return smem_u32(sK + (x % SK) * TL::kTileBytes); };
-        auto vaddr = [&](int x) { return smem_u32(sV + (x % SV) * TL::kTileBytes); };
+        auto tK = [&](int x) { return Tile<D>{sK + (x % SK) * TL::kTileBytes}; };
+        auto tV = [&](int x) { return Tile<D>{sV + (x % SV) * TL::kTileBytes}; };
+        const tt_bf<D / 2> tQa{tbase + C::tmem_qa()}, tDoa{tbase + C::tmem_doa()};  // A operands in TMEM
         auto issue_s = [&](int x) {  // S = Q K^T
             mbar_wait(&k_full[x % SK], (x / SK) & 1);
             tmem::fence_after();
-            mm_tmem_abt<D>(tbase + C::tmem_s(), tbase + C::tmem_qa(), kaddr(x), id_s);
-            umma::commit_e(&s_full);
+            mm_ABt(tt_fl<128>{tbase + C::tmem_s()}, tQa, tK(x));
+            mma_commit(&s_full);
         };
         auto issue_dp = [&](int x, uint32_t itx) {  // dP = dO V^T (iteration itx)
             mbar_wait(&v_full[x % SV], (x / SV) & 1);
             tmem::fence_after();
-            mm_tmem_abt<D>(tbase + dp_buf(itx), tbase + C::tmem_doa(), vaddr(x), id_s);
-            umma::commit_e(&dp_full_of(itx));
-            umma::commit_e(&v_empty[x % SV]);
+            mm_ABt(tt_fl<128>{tbase + dp_buf(itx)}, tDoa, tV(x));
+            mma_commit(&dp_full_of(itx));
+            mma_commit(&v_empty[x % SV]);
         };
         for (int n = 0;; ++n) {
             const int t = queue.get_warp(n);
@@ -1204,31 +1093,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             mbar_wait(&a_ready, n & 1);  // this task's Q / dO are in TMEM
             issue_s(kv);
             issue_dp(kv, it);
-            if (nk == 1) umma::commit_e(&qa_free);  // the task's only S and dP are issued
+            if (nk == 1) mma_commit(&qa_free);  // the task's only S and dP are issued
             for (int jj = 0; jj < nk; ++jj, ++kv, ++it) {
                 if (jj + 1 < nk) {
                     mbar_wait(&s_free, it & 1);  // S_j read out by the compute warps
                     issue_s(kv + 1);
                     if (kDP) {  // the other dP buffer: its dS_{j-1} went to dQ_{j-1}, issued before
                         issue_dp(kv + 1, it + 1);
-                        if (jj + 2 == nk) umma::commit_e(&qa_free);  // the task's last S and dP are issued
+                        if (jj + 2 == nk) mma_commit(&qa_free);  // the task's last S and dP are issued
                     }
                 }
                 TKB_TR(0, (int)it, 0);
                 // dQ += dS K, one 32-key chunk per column group as it lands
-                mma_tmem_a_groups(tbase + C::tmem_dq(), tbase + dp_buf(it), kaddr(kv), id_q, jj > 0, [&](int g) {
-                    mbar_wait(&ds_full_of(it)[g], ph_of(it));
-                    tmem::fence_after();
-                });
+                mma_AB_groups(tt_fl<D>{tbase + C::tmem_dq()}, tt_bf<128>{tbase + dp_buf(it)}, swap_layout(tK(kv)),
+                              jj > 0, [&](int g) {
+                                  mbar_wait(&ds_full_of(it)[g], ph_of(it));
+                                  tmem::fence_after();
+                              });
                 TKB_TR(0, (int)it, 1);
-                umma::commit_e(&k_empty[kv % SK]);
+                mma_commit(&k_empty[kv % SK]);
                 if (!kDP && jj + 1 < nk) {
                     issue_dp(kv + 1, it + 1);  // overwrites dS_j, read by dQ_j issued before
-                    if (jj + 2 == nk) umma::commit_e(&qa_free);  // the task's last S and dP are issued
+                    if (jj + 2 == nk) mma_commit(&qa_free);  // the task's last S and dP are issued
                 }
                 TKB_TR(0, (int)it, 2);
             }
-            umma::commit_e(&dq_full);
+            mma_commit(&dq_full);
         }
     } else {
         // ----------------------------------------------------------------- COMPUTE
@@ -1247,8 +1137,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             mbar_wait(&qdo_full, nn & 1);
             if (nn > 0) mbar_wait(&qa_free, (nn - 1) & 1);
             tmem::fence_after();
-            smem_rows_to_tmem_a<D>(sQ, tbase + lane_off + C::tmem_qa(), r, g);
-            smem_rows_to_tmem_a<D>(sDo, tbase + lane_off + C::tmem_doa(), r, g);
+            smem_rows_to_tmem_a<D>(Tile<D>{sQ}, tbase + lane_off + C::tmem_qa(), r, g);
+            smem_rows_to_tmem_a<D>(Tile<D>{sDo}, tbase + lane_off + C::tmem_doa(), r, g);
             tmem::wait_st();
             tmem::fence_before();
             mbar_arrive(&a_ready);
@@ -1316,7 +1206,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
             // dS, which these warps produce after this.
             mbar_wait(&dq_full, n & 1);
             tmem::fence_after();
-            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), sQ, r, g, p.scale);  // dQ = scale dS K
+            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), Tile<D>{sQ}, r, g, p.scale);  // dQ = scale dS K
             tma::fence_async_smem();
             named_sync(kBarCompute, kComputeThreads);
             if (threadIdx.x == 0) {

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 tmem::fence_after();
                 mma_AB_k<D, kPChunkCols>(tt_fl<D>{tbase + C::tmem_o(s)},
                                          tt_bf<kPChunkCols / 2>{tbase + C::tmem_s(s) + 64 + c * (kPChunkCols / 2)},
-                                         sKV(vslot), c * kPChunkCols, acc || c > 0);
+                                         swap_layout(sKV(vslot)), c * kPChunkCols, acc || c > 0);
             }
         };
         if constexpr (k3) {
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 auto qk3 = [&](int s, int i, int kslot) {
                     const uint32_t g = gidx(s, i);
                     mm_ABt(tt_fl<128>{tbase + sbuf_col(g % 3)}, sQ[s], sKV(kslot));
-                    umma::commit_e(&s_full3[g % 3]);
+                    mma_commit(&s_full3[g % 3]);
                 };
                 auto pv3 = [&](int s, int i, int vslot) {  // O_s (+)= P_s(i) V
                     const uint32_t g = gidx(s, i);
@@ -243,10 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         tmem::fence_after();
                         mma_AB_k<D, kPChunkCols>(
                             tt_fl<D>{tbase + C::tmem_o(s)},
-                            tt_bf<kPChunkCols / 2>{tbase + sbuf_col(g % 3) + 64 + c * (kPChunkCols / 2)}, sKV(vslot),
-                            c * kPChunkCols, i > 0 || c > 0);
+                            tt_bf<kPChunkCols / 2>{tbase + sbuf_col(g % 3) + 64 + c * (kPChunkCols / 2)},
+                            swap_layout(sKV(vslot)), c * kPChunkCols, i > 0 || c > 0);
                     }
-                    umma::commit_e(&pv_done[s]);
+                    mma_commit(&pv_done[s]);
                 };
                 mbar_wait(&q_full[0], nt & 1);
                 mbar_wait(&q_full[1], nt & 1);
@@ -255,9 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #pragma unroll
                 for (int s = 0; s < kQStages; ++s) {
                     qk3(s, 0, st.slot);
-                    if (nk[s] == 1) umma::commit_e(&q_empty[s]);
+                    if (nk[s] == 1) mma_commit(&q_empty[s]);
                 }
-                umma::commit_e(&kv.empty[st.slot]);
+                mma_commit(&kv.empty[st.slot]);
                 st.advance();
                 for (int i = 1; i < nkv; ++i) {
                     const int vslot = st.slot;
@@ -272,15 +272,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     for (int s = 0; s < kQStages; ++s) {
                         if (i < nk[s]) {
                             qk3(s, i, kslot);
-                            if (i == nk[s] - 1) umma::commit_e(&q_empty[s]);
+                            if (i == nk[s] - 1) mma_commit(&q_empty[s]);
                         }
                         if (i - 1 < nk[s]) {
                             pv3(s, i - 1, vslot);
-                            if (i - 1 == nk[s] - 1) umma::commit_e(&o_full[s]);
+                            if (i - 1 == nk[s] - 1) mma_commit(&o_full[s]);
                         }
                     }
-                    umma::commit_e(&kv.empty[vslot]);
-                    umma::commit_e(&kv.empty[kslot]);
+                    mma_commit(&kv.empty[vslot]);
+                    mma_commit(&kv.empty[kslot]);
                     st.advance();
                 }
                 const int vslot = st.slot;
@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 for (int s = 0; s < kQStages; ++s) {
                     if (nk[s] != nkv) continue;
                     pv3(s, nkv - 1, vslot);
-                    umma::commit_e(&o_full[s]);
+                    mma_commit(&o_full[s]);
                 }
-                umma::commit_e(&kv.empty[vslot]);
+                mma_commit(&kv.empty[vslot]);
                 st.advance();
                 qbase += (uint32_t)(nk[0] + nk[1]);
             }
@@ -314,10 +314,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #pragma unroll
             for (int s = 0; s < kQStages; ++s) {
                 qk(s, st.slot);
-                umma::commit_e(&s_full[s]);
-                if (nk[s] == 1) umma::commit_e(&q_empty[s]);
+                mma_commit(&s_full[s]);
+                if (nk[s] == 1) mma_commit(&q_empty[s]);
             }
-            umma::commit_e(&kv.empty[st.slot]);
+            mma_commit(&kv.empty[st.slot]);
             st.advance();
             for (int i = 1; i < nkv; ++i) {
                 const int vslot = st.slot;
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     pv(s, vslot, i > 1, it[s] & 1);
                     ++it[s];
                     if (i == nk[s]) {  // that was tile s's last block
-                        umma::commit_e(&o_full[s]);
+                        mma_commit(&o_full[s]);
                         continue;
                     }
                     if (!k_ready) {
@@ -340,11 +340,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         k_ready = true;
                     }
                     qk(s, kslot);
-                    umma::commit_e(&s_full[s]);
-                    if (i == nk[s] - 1) umma::commit_e(&q_empty[s]);  // Q_s's last read: the next task's may load
+                    mma_commit(&s_full[s]);
+                    if (i == nk[s] - 1) mma_commit(&q_empty[s]);  // Q_s's last read: the next task's may load
                 }
-                umma::commit_e(&kv.empty[vslot]);
-                umma::commit_e(&kv.empty[kslot]);
+                mma_commit(&kv.empty[vslot]);
+                mma_commit(&kv.empty[kslot]);
                 st.advance();
             }
             const int vslot = st.slot;
@@ -354,9 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 if (nk[s] != nkv) continue;
                 pv(s, vslot, nkv > 1, it[s] & 1);
                 ++it[s];
-                umma::commit_e(&o_full[s]);
+                mma_commit(&o_full[s]);
             }
-            umma::commit_e(&kv.empty[vslot]);
+            mma_commit(&kv.empty[vslot]);
             st.advance();
         }
         }

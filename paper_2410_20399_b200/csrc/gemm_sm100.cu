@@ -116,8 +116,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
     } else if (warp == 1) {
         // -------------------------------------------------------------------- MMA
-        constexpr uint32_t idesc = umma::idesc_bf16<BM, BN, false, true>();
-        constexpr uint32_t hi = umma::desc_hi_sw128(1024);
         lcsf::ring_state<kStages> st;
         int n = 0;
         for (int t = blockIdx.x; t < tasks; t += gridDim.x, ++n) {
@@ -128,15 +126,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             for (int kt = 0; kt < k_tiles; ++kt) {
                 bar.ab.wait_full(st);
                 tmem::fence_after();
-                const uint32_t a0 = sA(st.slot).addr(), b0 = smem_u32(sB(st.slot));
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k)
-                    umma::mma_ss_e(acc, umma::desc_lo(a0 + k * 32, 16), hi, umma::desc_lo(b0 + k * 16 * 128, kBAtom),
-                                   hi, idesc, (kt > 0 || k > 0) ? 1u : 0u);
-                umma::commit_e(&bar.ab.empty[st.slot]);  // panel consumed -> the producer may refill it
+                // C (+)= A B: A K-major, B = swap_layout of the [BK rows][BN] panel (mma_AB)
+                mma_AB(tt_fl<BN>{acc}, sA(st.slot), swap_layout(st_bf<BK, BN>{sB(st.slot)}), kt > 0);
+                mma_commit(&bar.ab.empty[st.slot]);  // panel consumed -> the producer may refill it
                 st.advance();
             }
-            umma::commit_e(&bar.acc_full[buf]);
+            mma_commit(&bar.acc_full[buf]);
         }
     } else if (warp >= 4) {
         // -------------------------------------------------------------------- FINISH

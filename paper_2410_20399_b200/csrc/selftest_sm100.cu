@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0) {  // converged MMA warp
         tmem::fence_after();
         mm_ABt(tS, sQ, sK);
-        umma::commit_e(&bar_s);
+        mma_commit(&bar_s);
     }
     mbar_wait(&bar_s, 0);
     tmem::fence_after();
@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (warp == 0) {
         tmem::fence_after();
-        mma_AB(tO, tP, sV, false);
-        umma::commit_e(&bar_o);
+        mma_AB(tO, tP, swap_layout(sV), false);
+        mma_commit(&bar_o);
     }
     mbar_wait(&bar_o, 0);
     tmem::fence_after();
@@ -285,6 +285,138 @@ __global__ void __launch_bounds__(128, 1)
     tmem::fence_before();
     __syncthreads();
     if (warp == 0) tmem::dealloc<512>(tslot);
+}
+
+// Tile-API selftest 2: the operand / transfer flavours the backward uses, on one 128 x 128 x
+// 128 product (tests/test_tile_api_gpu.py checks each against torch):
+//   load(rt_bf, gv) / store(st_bf, rt_bf)   A: global -> register -> shared (SW128)
+//   mm_AB(tt_fl, st_bf, swap_layout(st_bf)) C1 = A B   (SS, B read MN-major)
+//   load(rt_bf, st_bf) / store(tt, rt_bf)   A: shared -> register -> TMEM
+//   mm_ABt(tt_fl, tt_bf, st_bf)             C2 = A B^T (TS, A in TMEM)
+//   mma_AB_groups(tt_fl, tt_bf, st_mn)      C3 = A B   (TS, A as four 32-column chunks)
+//   store_rows(gv, rt_bf)                   C3 -> bf16 rows in global (warp-transposed)
+__global__ void __launch_bounds__(128, 1)
+    tile_api2_kernel(const __nv_bfloat16* A, const __grid_constant__ CUtensorMap tmB, float* C1, float* C2,
+                     float* C3, __nv_bfloat16* C3b) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using T = st_bf<128, 128>;
+    const T sA{smem}, sB{smem + T::kBytes};
+    __shared__ mbarrier bar_load, bar_mma;
+    __shared__ uint32_t tslot;
+    const int warp = warpid(), lane = laneid();
+    const int r = warp * 32 + lane;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_load, 1);
+        mbar_init(&bar_mma, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem::alloc<512>(&tslot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const tt_fl<128> tC1{tslot}, tC2{tslot + 384};
+    const tt_bf<64> tA{tslot + 128};
+    const tt_bf<128> tAg{tslot + 256};
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar_load, T::kBytes);
+        load_async(sB, gl{&tmB}, &bar_load, 0, 0, 0, tma::policy_evict_first());
+    }
+    {  // A: global -> register -> shared
+        const gv<const __nv_bfloat16> gA{A, 0, 0, 128};
+        rt_bf<128> a;
+        load(a, gA, 0, 0, r, 0);
+        store(sA, a, r, 0);
+    }
+    tma::fence_async_smem();  // generic-proxy SMEM writes -> visible to the tensor core (async proxy)
+    __syncthreads();
+    {  // A: shared -> register -> TMEM (dense K = 128, and the grouped 4 x 32 layout)
+        rt_bf<128> a;
+        load(a, sA, r, 0);
+        store(tA.quarter(warp), a);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            rt_bf<32> c;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) c.v[j] = a.v[16 * g + j];
+            store(tAg.quarter(warp) + 32 * g, c);
+        }
+        tmem::wait_st();
+    }
+    mbar_wait(&bar_load, 0);
+    tmem::fence_before();
+    __syncthreads();
+    auto read_out = [&](const tt_fl<128>& t, float* out) {
+        rt_fl<128> c;
+        load(c, t.quarter(warp));
+        load_wait(c);
+        for (int j = 0; j < 128; ++j) out[(size_t)r * 128 + j] = c.v[j];
+    };
+    uint32_t ph = 0;
+    // C1 = A B (SS)
+    if (warp == 0) {
+        tmem::fence_after();
+        mm_AB(tC1, sA, swap_layout(sB));
+        mma_commit(&bar_mma);
+    }
+    mbar_wait(&bar_mma, ph);
+    ph ^= 1;
+    tmem::fence_after();
+    read_out(tC1, C1);
+    // C2 = A B^T (A in TMEM)
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem::fence_after();
+        mm_ABt(tC2, tA, sB);
+        mma_commit(&bar_mma);
+    }
+    mbar_wait(&bar_mma, ph);
+    ph ^= 1;
+    tmem::fence_after();
+    read_out(tC2, C2);
+    // C3 = A B (grouped A in TMEM), into tC1
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem::fence_after();
+        mma_AB_groups(tC1, tAg, swap_layout(sB), false, [](int) {});
+        mma_commit(&bar_mma);
+    }
+    mbar_wait(&bar_mma, ph);
+    tmem::fence_after();
+    read_out(tC1, C3);
+    {  // C3 -> bf16 -> global rows (register -> global, warp-collective), 32 columns per pass
+        const gv<__nv_bfloat16> gC{C3b, 0, 0, 128};
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            rt_fl<32> f;
+            load(f, tC1.quarter(warp) + c0);
+            load_wait(f);
+            rt_bf<32> h;
+            copy(h, f);
+            store_rows(gC, h, 0, 0, warp * 32, c0, 32);
+        }
+    }
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0) tmem::dealloc<512>(tslot);
+}
+
+extern "C" __attribute__((visibility("default"))) int tkb_selftest_tile_api2(const void* A, const void* B, float* C1,
+                                                                            float* C2, float* C3, void* C3b,
+                                                                            cudaStream_t stream) {
+    CUtensorMap tb;
+    std::string err;
+    uint64_t dims[4] = {128, 128, 1, 1}, strides[4] = {1, 128, 128 * 128, 128 * 128};
+    uint32_t box[4] = {64, 128, 1, 1};
+    if (!host::make_tmap(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, dims, strides, box,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &err))
+        return -1;
+    const int smem = 2 * 32768 + 1024;
+    cudaFuncSetAttribute(tile_api2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    tile_api2_kernel<<<1, 128, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(A), tb, C1, C2, C3,
+                                                reinterpret_cast<__nv_bfloat16*>(C3b));
+    return (int)cudaGetLastError();
 }
 
 // bf16 RNE of `n` floats through copy(rt_bf, rt_fl) = cvt.rn.bf16x2.f32 (tiles.hpp:40-46, 195-200)

@@ -63,3 +63,25 @@ def test_copy_is_round_to_nearest_even(cuda_dev):
     want = vals.to(torch.bfloat16).float()  # torch's RNE
     assert torch.equal(out.cpu(), want)
     assert out[0].item() == 1.0 and out[3].item() == 1.0078125 and out[4].item() == 1.0
+
+
+def test_tile_api_operand_and_transfer_flavours(cuda_dev):
+    """global -> register -> shared -> register -> TMEM transfers, the SS mm_AB with a
+    swap_layout B, the TS mm_ABt (A in TMEM), the grouped-A mma_AB_groups and the
+    warp-collective store_rows, each against a torch fp32 matmul of the same bf16 operands."""
+    g = torch.Generator().manual_seed(11)
+    A, B = (torch.randn(128, 128, generator=g).to(torch.bfloat16) for _ in range(2))
+    a, b = A.to(cuda_dev), B.to(cuda_dev)
+    C1, C2, C3 = (torch.empty(128, 128, device=cuda_dev) for _ in range(3))
+    C3b = torch.empty(128, 128, device=cuda_dev, dtype=torch.bfloat16)
+    rc = _fn("tkb_selftest_tile_api2", 7)(a.data_ptr(), b.data_ptr(), C1.data_ptr(), C2.data_ptr(), C3.data_ptr(),
+                                          C3b.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ab = A.float() @ B.float()
+    abt = A.float() @ B.float().t()
+    tol = 1e-3 * ab.abs().max().item()
+    assert (C1.cpu() - ab).abs().max().item() <= tol
+    assert (C2.cpu() - abt).abs().max().item() <= tol
+    assert (C3.cpu() - ab).abs().max().item() <= tol
+    assert torch.equal(C3b.cpu(), C3.cpu().to(torch.bfloat16))
