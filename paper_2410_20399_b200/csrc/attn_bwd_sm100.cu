@@ -231,81 +231,70 @@ struct KvTask {
 // its slot is the one dK_{t+1-SQ} frees. With SQ = 2 only dP_t and dV_t (1024 clk) separate
 // the two and the L2 -> SMEM latency of the 33 KB reload shows; SQ = 3 gives it a step more.
 // dO_{t+1} (first read by dP_{t+1}, late in step t) and lse / delta need only 2 slots.
-template <int D>
-struct CfgKVP {
-    using T = Tiles<D>;
-    static constexpr int kStagesQ = (D == 128) ? 3 : 4;
-    static constexpr int kStagesDo = (D == 128) ? 2 : 3;
-    static constexpr int kStagesAux = 2;
-    static constexpr int kOffK = 0;
-    static constexpr int kOffV = kOffK + T::kTileBytes;
-    static constexpr int kOffQ = kOffV + T::kTileBytes;
-    static constexpr int kOffDo = kOffQ + kStagesQ * T::kTileBytes;
-    static constexpr int kOffLse = kOffDo + kStagesDo * T::kTileBytes;
-    static constexpr int kOffDelta = kOffLse + kStagesAux * 512;
-    static constexpr int kOffBar = kOffDelta + kStagesAux * 512;
-    // no alignment slack: without static SMEM the dynamic window starts 1024-aligned (checked)
-    static constexpr int kSmemBytes = kOffBar + 512;
-    static_assert(kSmemBytes <= 232448, "smem");
-};
-
+//
+// The kernel is lcsf::kernel<attn_bwd_dkdv_template<D, Causal>> (tkb/lcsf.cuh).
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __grid_constant__ BwdParams p) {
-    using C = CfgKVP<D>;
+struct attn_bwd_dkdv_template {
     using CT = TmemKV<D>;
     using TL = Tiles<D>;
-    constexpr int SQ = C::kStagesQ, SD = C::kStagesDo, SA = C::kStagesAux;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = smem_raw;
-    if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-byte alignment
-    uint8_t* sK = smem + C::kOffK;
-    uint8_t* sV = smem + C::kOffV;
-    uint8_t* sQ = smem + C::kOffQ;
-    uint8_t* sDo = smem + C::kOffDo;
-    float* sLse = reinterpret_cast<float*>(smem + C::kOffLse);
-    float* sDelta = reinterpret_cast<float*>(smem + C::kOffDelta);
-    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
-    mbarrier& kv_full = bars[0];
+    using globals = BwdParams;
+    static constexpr int SQ = (D == 128) ? 3 : 4;  // Q ring
+    static constexpr int SD = (D == 128) ? 2 : 3;  // dO ring
+    static constexpr int SA = 2;                   // lse / delta ring
+    static constexpr int kThreads = bwd::kThreads;
+    static constexpr int kTmemCols = 512;
+    static constexpr int kProducerWarp = kWarpLoad;
+    static constexpr int kMmaWarp = bwd::kWarpMma;
+    static constexpr int kConsumerWarps = 16;
+    static constexpr int kQueueReaders = 1 + 16;
+    static constexpr bool kAlignSlack = false;  // no static SMEM: the dynamic window starts 1024-aligned
+    static constexpr bool kReleaseEarly = false;
     // D = 64 leaves 128 TMEM columns free: S^T is double-buffered there (the second buffer at
     // column 384), so S^T_{t+1} is issued before dV_t and the exponentials of step t+1 do not
     // wait for the dV GEMM that reads P_t (the D = 64 step is bound by that chain, not by
     // its 1024 clk of MMA). Per-buffer s_full / p_full keep the phases one apart.
-    constexpr bool kDS = (D == 64);
-    auto s_buf = [](int x) -> uint32_t { return kDS ? ((x & 1) ? 384u : 0u) : CT::tmem_s(); };
-    auto s_full_of = [&](int x) -> mbarrier& { return (kDS && (x & 1)) ? bars[26] : bars[1]; };
-    auto p_full_of = [&](int x) -> mbarrier* { return (kDS && (x & 1)) ? bars + 46 : bars + 32; };
-    auto ph_of = [](int x) -> uint32_t { return kDS ? ((x >> 1) & 1) : (x & 1); };  // per-buffer phase
-    mbarrier& kv_empty = bars[2];   // the task's last S^T / dP^T retired: K / V reloadable
-    mbarrier& dp_full = bars[3];
-    mbarrier& dv_free = bars[4];    // the finish has read dV out of TMEM
-    mbarrier& dkv_full = bars[5];
-    mbarrier& dk_free = bars[6];
-    mbarrier& staged_full = bars[7];  // a finish has staged dV / dK in two ring slots
-    static_assert(SQ <= 4 && SD <= 3 && SA <= 2, "barrier slots");
-    mbarrier* q_full = bars + 8;      // [SQ]
-    mbarrier* q_empty = bars + 12;    // [SQ]
-    mbarrier* do_full = bars + 16;    // [SD]
-    mbarrier* do_empty = bars + 19;   // [SD]
-    mbarrier* aux_full = bars + 22;   // [SA] lse2 / delta
-    mbarrier* aux_empty = bars + 24;  // [SA]
-    mbarrier* ds_full = bars + 36;   // [kGroups]
-    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
-    lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);
+    static constexpr bool kDS = (D == 64);
 
-    const int warp = warpid();
-    const int lane = laneid();
-    const int nq = p.n_pad / 128;
-    const int hkv = p.heads / p.group;
-    const int tasks = nq * hkv * (p.bh / p.heads);
-    // task id -> (kv block fastest, kv head, batch): the CTAs running together share heads
+    struct shared {
+        uint8_t k[TL::kTileBytes];
+        uint8_t v[TL::kTileBytes];
+        uint8_t q[SQ][TL::kTileBytes];
+        uint8_t dO[SD][TL::kTileBytes];
+        float lse[SA][128];  // -lse2 per query (perm32 order)
+        float delta[SA][128];
+        mbarrier kv_full, kv_empty;  // K / V in SMEM; the task's last S^T / dP^T retired
+        mbarrier s_full[2];          // [buffer] (one buffer unless kDS)
+        mbarrier dp_full;
+        mbarrier dv_free, dk_free;   // the finish has read dV / dK out of TMEM
+        mbarrier dkv_full;
+        mbarrier staged_full;        // a finish has staged dV / dK in two ring slots
+        mbarrier q_full[SQ], q_empty[SQ];
+        mbarrier do_full[SD], do_empty[SD];
+        mbarrier aux_full[SA], aux_empty[SA];
+        mbarrier p_full[2][kGroups];  // [buffer][column group]
+        mbarrier ds_full[kGroups];
+        lcsf::work_queue queue;
+        uint32_t tmem_slot;
+    };
+    static constexpr int kSmemBytes = (int)sizeof(shared);
+    static_assert(kSmemBytes <= 232448, "smem");
+
+    static TKB_DEVICE uint32_t s_buf(int x) { return kDS ? ((x & 1) ? 384u : 0u) : CT::tmem_s(); }
+    static TKB_DEVICE int buf_of(int x) { return (kDS && (x & 1)) ? 1 : 0; }
+    static TKB_DEVICE uint32_t ph_of(int x) { return kDS ? ((x >> 1) & 1) : (x & 1); }  // per-buffer phase
+
     // Task order. Non-causal: kv block fastest, so the CTAs running together share heads and
     // their Q / dO stay in L2. Causal: kv (batch, head) units in L2-sized groups (p.head_group,
     // as the dQ kernel), inside a group the long tasks (small kv block index) first, so the
     // queue ends on short tasks; with fewer than 4 tasks per SM (grouped-query heads: a task
     // walks its group's query heads) one group spans everything — longest-first overall.
-    const int hb = hkv * (p.bh / p.heads);  // (batch, kv head) units
-    const int G = (tasks < 4 * p.num_sms) ? hb : max(1, min(hb, p.head_group / max(1, p.group)));
-    auto decode = [&](int id) {
+    static TKB_DEVICE int num_tasks(const globals& p) { return (p.n_pad / 128) * (p.heads / p.group) * (p.bh / p.heads); }
+    static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
+    static TKB_DEVICE KvTask decode(const globals& p, int id) {
+        const int nq = p.n_pad / 128;
+        const int hkv = p.heads / p.group;
+        const int hb = hkv * (p.bh / p.heads);  // (batch, kv head) units
+        const int G = (num_tasks(p) < 4 * p.num_sms) ? hb : max(1, min(hb, p.head_group / max(1, p.group)));
         KvTask w;
         int unit;
         if (CAUSAL) {
@@ -321,202 +310,201 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
         w.head = unit % hkv;
         w.batch = unit / hkv;
         return w;
-    };
-    auto steps = [&](const KvTask& w) { return (CAUSAL ? (nq - w.j) : nq) * p.group; };
-    long long* tr = trace_slot(p, (int)blockIdx.x, 0);
-    const long long t_start = clock64();
+    }
+    static TKB_DEVICE int steps(const globals& p, const KvTask& w) {
+        return (CAUSAL ? (p.n_pad / 128 - w.j) : p.n_pad / 128) * p.group;
+    }
+    static TKB_DEVICE Tile<D> tQ(shared& sh, int x) { return Tile<D>{sh.q[x % SQ]}; }
+    static TKB_DEVICE Tile<D> tDo(shared& sh, int x) { return Tile<D>{sh.dO[x % SD]}; }
 
-    if (warp == kWarpLoad && lane == 0) {
-        queue.init(1 + 16);
-        mbar_init(&kv_full, 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[26], 1);
-        mbar_init(&kv_empty, 1);
-        mbar_init(&dp_full, 1);
-        mbar_init(&dv_free, kComputeThreads);
-        mbar_init(&dkv_full, 1);
-        mbar_init(&dk_free, kComputeThreads);
-        mbar_init(&staged_full, kComputeThreads);
+    static TKB_DEVICE void init(shared& sh, const globals& p) {
+        mbar_init(&sh.kv_full, 1);
+        mbar_init(&sh.kv_empty, 1);
+        mbar_init(&sh.s_full[0], 1);
+        mbar_init(&sh.s_full[1], 1);
+        mbar_init(&sh.dp_full, 1);
+        mbar_init(&sh.dv_free, kComputeThreads);
+        mbar_init(&sh.dkv_full, 1);
+        mbar_init(&sh.dk_free, kComputeThreads);
+        mbar_init(&sh.staged_full, kComputeThreads);
         for (int g = 0; g < kGroups; ++g) {
-            mbar_init(&bars[32 + g], 128);
-            mbar_init(&bars[46 + g], 128);
-            mbar_init(&ds_full[g], 128);
+            mbar_init(&sh.p_full[0][g], 128);
+            mbar_init(&sh.p_full[1][g], 128);
+            mbar_init(&sh.ds_full[g], 128);
         }
         for (int s = 0; s < SQ; ++s) {
-            mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], 1);
+            mbar_init(&sh.q_full[s], 1);
+            mbar_init(&sh.q_empty[s], 1);
         }
         for (int s = 0; s < SD; ++s) {
-            mbar_init(&do_full[s], 1);
-            mbar_init(&do_empty[s], 1);
+            mbar_init(&sh.do_full[s], 1);
+            mbar_init(&sh.do_empty[s], 1);
         }
         for (int s = 0; s < SA; ++s) {
-            mbar_init(&aux_full[s], 1);
-            mbar_init(&aux_empty[s], 1);
+            mbar_init(&sh.aux_full[s], 1);
+            mbar_init(&sh.aux_empty[s], 1);
         }
-        fence_barrier_init();
         tma::prefetch_desc(&p.tm_q);
         tma::prefetch_desc(&p.tm_k);
         tma::prefetch_desc(&p.tm_v);
         tma::prefetch_desc(&p.tm_do);
     }
-    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
-    tmem::fence_before();
-    __syncthreads();
-    tmem::fence_after();
-    const uint32_t tbase = tmem_slot;
 
-    if (warp == kWarpLoad) {
-        if (lane == 0) {
-            // ------------------------------------------------------------- LOAD
-            const uint64_t pol_stream = tma::policy_evict_first();
-            const uint64_t pol_keep = tma::policy_evict_last();
-            int x = 0;  // global step (ring position)
-            int n = 0;
+    // ------------------------------------------------------------- LOAD
+    struct producer {
+        struct state {
+            int x = 0;       // global step (ring position)
             int staged = 0;  // staged finishes stored
             KvTask prev{0, 0, 0};
-            int id = queue.claim(0, p.sched, tasks);
-            while (id >= 0) {
-                const KvTask w = decode(id);
-                const int T = steps(w), T1 = T / p.group;
-                const int kv0 = w.j * 128;
-                mbar_wait(&kv_empty, (n & 1) ^ 1u);
-                mbar_arrive_expect_tx(&kv_full, 2 * TL::kTileBytes);
-                for (int a = 0; a < TL::kAtoms; ++a) {
-                    tma::load_4d(sK + a * kAtomBytes, &p.tm_k, &kv_full, a * 64, kv0, w.head, w.batch, pol_stream);
-                    tma::load_4d(sV + a * kAtomBytes, &p.tm_v, &kv_full, a * 64, kv0, w.head, w.batch, pol_stream);
+        };
+        template <class ClaimNext>
+        static TKB_DEVICE void load(const lcsf::args<attn_bwd_dkdv_template>& a, state& ps, int id, int n,
+                                    ClaimNext&&) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const uint64_t pol_stream = tma::policy_evict_first();
+            const uint64_t pol_keep = tma::policy_evict_last();
+            const KvTask w = decode(p, id);
+            const int T = steps(p, w), T1 = T / p.group;
+            const int kv0 = w.j * 128;
+            mbar_wait(&sh.kv_empty, (n & 1) ^ 1u);
+            mbar_arrive_expect_tx(&sh.kv_full, 2 * TL::kTileBytes);
+            load_async(Tile<D>{sh.k}, gl{&p.tm_k}, &sh.kv_full, kv0, w.head, w.batch, pol_stream);
+            load_async(Tile<D>{sh.v}, gl{&p.tm_v}, &sh.kv_full, kv0, w.head, w.batch, pol_stream);
+            const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
+            for (int t = 0; t < T; ++t, ++ps.x) {
+                const int x = ps.x;
+                const int i = (CAUSAL ? w.j : 0) + t % T1;
+                const int hq = w.head * p.group + t / T1;
+                const size_t bhq = (size_t)w.batch * p.heads + hq;
+                // in pipe order of the GEMMs that free the slots: dK_{x-SQ}, dV_{x-SD}, dK_{x-SA}
+                const int sq = x % SQ, sd = x % SD, sa = x % SA;
+                mbar_wait(&sh.q_empty[sq], ((x / SQ) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sh.q_full[sq], TL::kTileBytes);
+                load_async(tQ(sh, x), gl{&p.tm_q}, &sh.q_full[sq], i * 128, hq, w.batch, pol_keep);
+                if (after_staged && t == 1) {
+                    // the previous task's finish staged dV / dK in the dO slot of step 1 and the
+                    // Q slot of step 2: store them (this warp, off the compute warps' path)
+                    // and refill the slots once the store has read them
+                    mbar_wait(&sh.staged_full, ps.staged & 1);
+                    ++ps.staged;
+                    store_async(gl{&p.tm_dv}, tQ(sh, x + 1), ps.prev.j * 128, ps.prev.head, ps.prev.batch);
+                    store_async(gl{&p.tm_dk}, tDo(sh, x), ps.prev.j * 128, ps.prev.head, ps.prev.batch);
+                    tma::commit_group();
+                    tma::wait_group_read<0>();
                 }
-                const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
-                for (int t = 0; t < T; ++t, ++x) {
-                    const int i = (CAUSAL ? w.j : 0) + t % T1;
-                    const int hq = w.head * p.group + t / T1;
-                    const size_t bhq = (size_t)w.batch * p.heads + hq;
-                    // in pipe order of the GEMMs that free the slots: dK_{x-SQ}, dV_{x-SD}, dK_{x-SA}
-                    const int sq = x % SQ, sd = x % SD, sa = x % SA;
-                    mbar_wait(&q_empty[sq], ((x / SQ) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&q_full[sq], TL::kTileBytes);
-                    for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sQ + sq * TL::kTileBytes + a * kAtomBytes, &p.tm_q, &q_full[sq], a * 64,
-                                     i * 128, hq, w.batch, pol_keep);
-                    if (after_staged && t == 1) {
-                        // the previous task's finish staged dV / dK in the dO slot of step 1 and the
-                        // Q slot of step 2: store them (this warp, off the compute warps' path)
-                        // and refill the slots once the store has read them
-                        mbar_wait(&staged_full, staged & 1);
-                        ++staged;
-                        uint8_t* stage_v = sQ + ((x + 1) % SQ) * TL::kTileBytes;
-                        uint8_t* stage_k = sDo + (x % SD) * TL::kTileBytes;
-                        for (int a = 0; a < TL::kAtoms; ++a) {
-                            tma::store_4d(&p.tm_dv, stage_v + a * kAtomBytes, a * 64, prev.j * 128, prev.head,
-                                          prev.batch);
-                            tma::store_4d(&p.tm_dk, stage_k + a * kAtomBytes, a * 64, prev.j * 128, prev.head,
-                                          prev.batch);
-                        }
-                        tma::commit_group();
-                        tma::wait_group_read<0>();
-                    }
-                    mbar_wait(&do_empty[sd], ((x / SD) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&do_full[sd], TL::kTileBytes);
-                    for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sDo + sd * TL::kTileBytes + a * kAtomBytes, &p.tm_do, &do_full[sd], a * 64,
-                                     i * 128, hq, w.batch, pol_keep);
-                    mbar_wait(&aux_empty[sa], ((x / SA) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&aux_full[sa], 1024);
-                    tma::load_1d(sLse + sa * 128, p.lse2 + bhq * p.n_pad + i * 128, 512, &aux_full[sa]);
-                    tma::load_1d(sDelta + sa * 128, p.delta + bhq * p.n_pad + i * 128, 512, &aux_full[sa]);
-                }
-                prev = w;
-                id = queue.claim(++n, p.sched, tasks);
+                mbar_wait(&sh.do_empty[sd], ((x / SD) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sh.do_full[sd], TL::kTileBytes);
+                load_async(tDo(sh, x), gl{&p.tm_do}, &sh.do_full[sd], i * 128, hq, w.batch, pol_keep);
+                mbar_wait(&sh.aux_empty[sa], ((x / SA) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sh.aux_full[sa], 1024);
+                tma::load_1d(sh.lse[sa], p.lse2 + bhq * p.n_pad + i * 128, 512, &sh.aux_full[sa]);
+                tma::load_1d(sh.delta[sa], p.delta + bhq * p.n_pad + i * 128, 512, &sh.aux_full[sa]);
             }
-            tma::wait_group<0>();
+            ps.prev = w;
         }
-    } else if (warp == kWarpMma) {
-        // ----------------------------------------------------------------- MMA (converged warp)
-        const Tile<D> tK{sK}, tV{sV};
-        auto tQ = [&](int x) { return Tile<D>{sQ + (x % SQ) * TL::kTileBytes}; };
-        auto tDo = [&](int x) { return Tile<D>{sDo + (x % SD) * TL::kTileBytes}; };
-        auto issue_s = [&](int x) {  // S^T = K Q^T
-            mbar_wait(&q_full[x % SQ], (x / SQ) & 1);
-            tmem::fence_after();
-            mm_ABt(tt_fl<128>{tbase + s_buf(x)}, tK, tQ(x));
-            mma_commit(&s_full_of(x));
+        static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dkdv_template>&, state&) { tma::wait_group<0>(); }
+    };
+
+    // ------------------------------------------------------------- MMA (converged warp)
+    struct mma {
+        struct state {
+            int x0 = 0;  // first global step of the task
+            long long t_start = 0;
         };
-        auto issue_dp = [&](int x) {  // dP^T = V dO^T
-            mbar_wait(&do_full[x % SD], (x / SD) & 1);
-            tmem::fence_after();
-            mm_ABt(tt_fl<128>{tbase + CT::tmem_dp()}, tV, tDo(x));
-            mma_commit(&dp_full);
-        };
-        int x0 = 0;  // first global step of the task
-        for (int n = 0;; ++n) {
-            const int id = queue.get_warp(n);
-            if (lane == 0) queue.release(n);
-            if (id < 0) break;
-            const int T = steps(decode(id));
-            mbar_wait(&kv_full, n & 1);
+        static TKB_DEVICE void issue(const lcsf::args<attn_bwd_dkdv_template>& a, state& ms, int id, int n) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const uint32_t tbase = a.tmem;
+            long long* tr = trace_slot(p, (int)blockIdx.x, 0);
+            if (n == 0) ms.t_start = clock64();
+            const long long t_start = ms.t_start;
+            const Tile<D> tK{sh.k}, tV{sh.v};
+            auto issue_s = [&](int x) {  // S^T = K Q^T
+                mbar_wait(&sh.q_full[x % SQ], (x / SQ) & 1);
+                tmem::fence_after();
+                mm_ABt(tt_fl<128>{tbase + s_buf(x)}, tK, tQ(sh, x));
+                mma_commit(&sh.s_full[buf_of(x)]);
+            };
+            auto issue_dp = [&](int x) {  // dP^T = V dO^T
+                mbar_wait(&sh.do_full[x % SD], (x / SD) & 1);
+                tmem::fence_after();
+                mm_ABt(tt_fl<128>{tbase + CT::tmem_dp()}, tV, tDo(sh, x));
+                mma_commit(&sh.dp_full);
+            };
+            const int T = steps(p, decode(p, id));
+            const int x0 = ms.x0;
+            mbar_wait(&sh.kv_full, n & 1);
             issue_s(x0);
             issue_dp(x0);
-            if (T == 1) mma_commit(&kv_empty);
+            if (T == 1) mma_commit(&sh.kv_empty);
             for (int t = 0; t < T; ++t) {
                 const int x = x0 + t;
                 const uint32_t ph = x & 1;
                 TKB_TR(0, x, 0);
-                if (t == 0 && n > 0) mbar_wait(&dv_free, (n - 1) & 1);  // previous task's dV read out
+                if (t == 0 && n > 0) mbar_wait(&sh.dv_free, (n - 1) & 1);  // previous task's dV read out
                 if (kDS && t + 1 < T) issue_s(x + 1);  // other buffer: its P_{t-1} went to dV_{t-1}, issued before
                 // dV += P^T dO (mma_AB: P^T chunks in TMEM as they land, dO read MN-major)
-                mma_AB_groups(tt_fl<D>{tbase + CT::tmem_dv()}, tt_bf<128>{tbase + s_buf(x)}, swap_layout(tDo(x)),
+                mma_AB_groups(tt_fl<D>{tbase + CT::tmem_dv()}, tt_bf<128>{tbase + s_buf(x)}, swap_layout(tDo(sh, x)),
                               t > 0, [&](int g) {
-                                  mbar_wait(&p_full_of(x)[g], ph_of(x));
+                                  mbar_wait(&sh.p_full[buf_of(x)][g], ph_of(x));
                                   tmem::fence_after();
                               });
                 TKB_TR(0, x, 1);
-                mma_commit(&do_empty[x % SD]);
+                mma_commit(&sh.do_empty[x % SD]);
                 if (!kDS && t + 1 < T) issue_s(x + 1);  // overwrites P_t, read by dV_t issued before
                 TKB_TR(0, x, 2);
-                if (t == 0 && n > 0) mbar_wait(&dk_free, (n - 1) & 1);
+                if (t == 0 && n > 0) mbar_wait(&sh.dk_free, (n - 1) & 1);
                 // dK += dS^T Q
-                mma_AB_groups(tt_fl<D>{tbase + CT::tmem_dk()}, tt_bf<128>{tbase + CT::tmem_dp()}, swap_layout(tQ(x)),
-                              t > 0, [&](int g) {
-                                  mbar_wait(&ds_full[g], ph);
+                mma_AB_groups(tt_fl<D>{tbase + CT::tmem_dk()}, tt_bf<128>{tbase + CT::tmem_dp()},
+                              swap_layout(tQ(sh, x)), t > 0, [&](int g) {
+                                  mbar_wait(&sh.ds_full[g], ph);
                                   tmem::fence_after();
                               });
                 TKB_TR(0, x, 3);
-                mma_commit(&q_empty[x % SQ]);
-                mma_commit(&aux_empty[x % SA]);  // dK_x waited for the last dS of step x
+                mma_commit(&sh.q_empty[x % SQ]);
+                mma_commit(&sh.aux_empty[x % SA]);  // dK_x waited for the last dS of step x
                 if (t + 1 < T) {
                     issue_dp(x + 1);  // overwrites dS_t, read by dK_t issued before
-                    if (t + 2 == T) mma_commit(&kv_empty);  // the task's last S^T / dP^T issued
+                    if (t + 2 == T) mma_commit(&sh.kv_empty);  // the task's last S^T / dP^T issued
                 }
                 TKB_TR(0, x, 4);
             }
-            mma_commit(&dkv_full);
-            x0 += T;
+            mma_commit(&sh.dkv_full);
+            ms.x0 += T;
         }
-    } else {
-        // ----------------------------------------------------------------- COMPUTE
-        const int wq = warp & 3;
-        const int g = warp >> 2;
-        const int r = wq * 32 + lane;
-        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS0 = tbase + lane_off + 32 * g;  // + s_buf(x)
-        const uint32_t tDp = tbase + lane_off + CT::tmem_dp() + 32 * g;
-        const float tau = p.scale_log2;
-        int x0 = 0;
-        for (int n = 0;; ++n) {
-            const int id = queue.get_warp(n);
-            if (id < 0) break;
-            const KvTask w = decode(id);
-            const int T = steps(w), T1 = T / p.group;
-            const int kv0 = w.j * 128;
+    };
+
+    // ------------------------------------------------------------- COMPUTE + FINISH
+    struct consumer {
+        struct state {
+            int x0 = 0;
+            long long t_start = 0;
+        };
+        static TKB_DEVICE void compute(const lcsf::args<attn_bwd_dkdv_template>& a, state& cs, int id, int n) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const int wq = a.warp & 3;
+            const int g = a.warp >> 2;
+            const int lane = a.lane;
+            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+            const uint32_t tS0 = a.tmem + lane_off + 32 * g;  // + s_buf(x)
+            const uint32_t tDp = a.tmem + lane_off + CT::tmem_dp() + 32 * g;
+            const float tau = p.scale_log2;
+            long long* tr = trace_slot(p, (int)blockIdx.x, 0);
+            if (n == 0) cs.t_start = clock64();
+            const long long t_start = cs.t_start;
+            const KvTask w = decode(p, id);
+            const int T = steps(p, w), T1 = T / p.group;
             for (int t = 0; t < T; ++t) {
-                const int x = x0 + t;
+                const int x = cs.x0 + t;
                 const int sa = x % SA;
                 const bool diag = CAUSAL && (t % T1 == 0);  // q block i == j
-                mbar_wait(&aux_full[sa], (x / SA) & 1);
+                mbar_wait(&sh.aux_full[sa], (x / SA) & 1);
                 float nlse[8], dlt[8];
-                grp_vec_load(smem_u32(sLse + sa * 128 + 32 * g), nlse);
-                grp_vec_load(smem_u32(sDelta + sa * 128 + 32 * g), dlt);
-                mbar_wait(&s_full_of(x), ph_of(x));
+                grp_vec_load(smem_u32(&sh.lse[sa][32 * g]), nlse);
+                grp_vec_load(smem_u32(&sh.delta[sa][32 * g]), dlt);
+                mbar_wait(&sh.s_full[buf_of(x)], ph_of(x));
                 const uint32_t tS = tS0 + s_buf(x);
                 if (threadIdx.x == 0) TKB_TR(1, x, 0);
                 if (threadIdx.x == 0 && t == 0 && n > 0) TKB_TR(1, n - 1, 7);  // next task's first S
@@ -536,9 +524,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 grp_store_packed(tS, pk);
                 tmem::wait_st();
                 tmem::fence_before();
-                mbar_arrive(&p_full_of(x)[g]);
+                mbar_arrive(&sh.p_full[buf_of(x)][g]);
                 if (threadIdx.x == 0) TKB_TR(1, x, 1);
-                mbar_wait(&dp_full, x & 1);
+                mbar_wait(&sh.dp_full, x & 1);
                 if (threadIdx.x == 0) TKB_TR(1, x, 2);
                 tmem::fence_after();
                 uint32_t dpv[32];
@@ -547,32 +535,42 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 grp_store_packed(tDp, pk);
                 tmem::wait_st();
                 tmem::fence_before();
-                mbar_arrive(&ds_full[g]);
+                mbar_arrive(&sh.ds_full[g]);
                 if (threadIdx.x == 0) TKB_TR(1, x, 3);
             }
-            x0 += T;
-            // FINISH. When the next task has >= 3 steps, dV / dK are staged (bf16, SW128) in the
-            // ring slots its step-2 Q and step-1 dO will use — both slots' last data (this task's
-            // final step) are consumed — and TMA-stored; the load warp refills those two slots
-            // only after the store has read them (stage_free). The compute warps are back on the
-            // next task's exponentials after ~500 clk. Otherwise rows are stored from registers
-            // (~2,000 clk per tensor: the per-thread store path is slow).
-            mbar_wait(&dkv_full, n & 1);
+            cs.x0 += T;
+        }
+        // FINISH. When the next task has >= 3 steps, dV / dK are staged (bf16, SW128) in the
+        // ring slots its step-2 Q and step-1 dO will use — both slots' last data (this task's
+        // final step) are consumed — and TMA-stored by the load warp, which refills those two
+        // slots only after the store has read them. The compute warps are back on the next
+        // task's exponentials after ~500 clk. Otherwise rows are stored from registers.
+        static TKB_DEVICE void finish(const lcsf::args<attn_bwd_dkdv_template>& a, state& cs, int id, int n) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const int wq = a.warp & 3;
+            const int g = a.warp >> 2;
+            const int r = wq * 32 + a.lane;
+            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+            const uint32_t tbase = a.tmem;
+            long long* tr = trace_slot(p, (int)blockIdx.x, 0);
+            const long long t_start = cs.t_start;
+            const KvTask w = decode(p, id);
+            const int kv0 = w.j * 128;
+            mbar_wait(&sh.dkv_full, n & 1);
             if (threadIdx.x == 0) TKB_TR(1, n, 4);
             tmem::fence_after();
-            const int id_next = queue.get_warp(n + 1);
-            const bool staged = id_next >= 0 && steps(decode(id_next)) >= 3;
+            const int id_next = a.queue.get_warp(n + 1);
+            const bool staged = id_next >= 0 && steps(p, decode(p, id_next)) >= 3;
             if (staged) {
-                uint8_t* stage_v = sQ + ((x0 + 2) % SQ) * TL::kTileBytes;
-                uint8_t* stage_k = sDo + ((x0 + 1) % SD) * TL::kTileBytes;
-                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dv(), Tile<D>{stage_v}, r, g);
+                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dv(), tQ(sh, cs.x0 + 2), r, g);
                 tmem::fence_before();
-                mbar_arrive(&dv_free);
-                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dk(), Tile<D>{stage_k}, r, g, p.scale);
+                mbar_arrive(&sh.dv_free);
+                tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dk(), tDo(sh, cs.x0 + 1), r, g, p.scale);
                 tmem::fence_before();
-                mbar_arrive(&dk_free);
+                mbar_arrive(&sh.dk_free);
                 tma::fence_async_smem();
-                mbar_arrive(&staged_full);  // the load warp stores them
+                mbar_arrive(&sh.staged_full);  // the load warp stores them
             } else {
                 // dV / dK rows from registers (register -> global, warp-transposed)
                 const int row0 = kv0 + wq * 32;  // row of lane 0
@@ -583,28 +581,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkdvp_kernel(const __gri
                 load(f, tbase + lane_off + CT::tmem_dv() + g * (D / 4));
                 load_wait(f);
                 tmem::fence_before();
-                mbar_arrive(&dv_free);
+                mbar_arrive(&sh.dv_free);
                 copy(h, f);
                 store_rows(gdv, h, w.batch, w.head, row0, g * (D / 4), p.n - row0);
                 load(f, tbase + lane_off + CT::tmem_dk() + g * (D / 4));
                 load_wait(f);
                 tmem::fence_before();
-                mbar_arrive(&dk_free);
+                mbar_arrive(&sh.dk_free);
                 mul(f, p.scale);  // dK = scale dS^T Q
                 copy(h, f);
                 store_rows(gdk, h, w.batch, w.head, row0, g * (D / 4), p.n - row0);
             }
             if (threadIdx.x == 0) TKB_TR(1, n, 6);
-            __syncwarp();
-            if (lane == 0) queue.release(n);
         }
-    }
-
-    tmem::fence_before();
-    __syncthreads();
-    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
-    if (threadIdx.x == 0) lcsf::queue_exit(p.sched);
-}
+        static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dkdv_template>&, state&) {}
+    };
+};
 
 // ================================================================== bwd_dkdv on CTA pairs (D = 128)
 // The single-CTA bwd_dkdv moves 256 KB through each SM's shared-memory port per step (the
@@ -951,224 +943,240 @@ TKB_DEVICE QTask qtask(const BwdParams& p, int t) {
     return w;
 }
 
+// The dQ kernel is lcsf::kernel<attn_bwd_dq_template<D, Causal>> (tkb/lcsf.cuh).
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
+struct attn_bwd_dq_template {
     using C = CfgQ<D>;
     using TL = Tiles<D>;
-    constexpr int SK = C::kStagesK;
-    constexpr int SV = C::kStagesV;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem + C::kOffQ;
-    uint8_t* sDo = smem + C::kOffDo;
-    uint8_t* sK = smem + C::kOffK;
-    uint8_t* sV = smem + C::kOffV;
-    mbarrier* bars = reinterpret_cast<mbarrier*>(smem + C::kOffBar);
-    mbarrier& qdo_full = bars[0];   // Q / dO of a task in SMEM (TMA)
-    mbarrier& s_full = bars[1];
-    mbarrier& s_free = bars[2];
-    mbarrier& a_ready = bars[3];    // Q / dO of a task copied into TMEM
-    mbarrier& qdo_free = bars[4];   // SMEM Q / dO copied out: the next task's may load
+    using globals = BwdParams;
+    static constexpr int SK = C::kStagesK;
+    static constexpr int SV = C::kStagesV;
+    static constexpr int kThreads = bwd::kThreads;
+    static constexpr int kTmemCols = 512;
+    static constexpr int kProducerWarp = kWarpLoad;
+    static constexpr int kMmaWarp = bwd::kWarpMma;
+    static constexpr int kConsumerWarps = 16;
+    static constexpr int kQueueReaders = 1 + 16;  // the MMA warp and the 16 compute warps
+    static constexpr bool kAlignSlack = true;
+    static constexpr bool kReleaseEarly = false;
     // D = 64 leaves 128 TMEM columns free: dP is double-buffered there (second buffer at
     // column 384), so dP_{j+1} is issued before dQ_j instead of after it and the dS of step
     // j+1 does not wait for the dQ GEMM that reads dS_j. Per-buffer dp_full / ds_full.
-    constexpr bool kDP = (D == 64);
-    auto dp_buf = [](uint32_t it) -> uint32_t { return kDP ? ((it & 1) ? 384u : C::tmem_dp()) : C::tmem_dp(); };
-    auto dp_full_of = [&](uint32_t it) -> mbarrier& { return (kDP && (it & 1)) ? bars[26] : bars[5]; };
-    auto ds_full_of = [&](uint32_t it) -> mbarrier* { return (kDP && (it & 1)) ? bars + 36 : bars + 32; };
-    auto ph_of = [](uint32_t it) -> uint32_t { return kDP ? ((it >> 1) & 1) : (it & 1); };
-    mbarrier& qa_free = bars[6];    // last S / dP GEMM of a task retired: TMEM Q / dO reusable
-    mbarrier& dq_full = bars[7];
-    mbarrier* k_full = bars + 8;    // [SK]
-    mbarrier* k_empty = bars + 13;  // [SK]
-    mbarrier* v_full = bars + 18;   // [SV]
-    mbarrier* v_empty = bars + 22;  // [SV]
-    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 28);
-    lcsf::work_queue& queue = *reinterpret_cast<lcsf::work_queue*>(bars + 40);  // dynamic task claims
+    static constexpr bool kDP = (D == 64);
 
-    const int warp = warpid();
-    const int lane = laneid();
-    const int nq = p.n_pad / 128;
-    const int tasks = p.bh * nq;
-    auto nk_of = [&](const QTask& w) { return CAUSAL ? (w.i + 1) : nq; };  // kv blocks visited
-    long long* tr = trace_slot(p, (int)blockIdx.x, 1);
-    const long long t_start = clock64();
+    struct shared {
+        uint8_t q[TL::kTileBytes];
+        uint8_t dO[TL::kTileBytes];
+        uint8_t k[SK][TL::kTileBytes];
+        uint8_t v[SV][TL::kTileBytes];
+        mbarrier qdo_full;   // Q / dO of a task in SMEM (TMA)
+        mbarrier s_full, s_free;
+        mbarrier a_ready;    // Q / dO of a task copied into TMEM
+        mbarrier qdo_free;   // SMEM Q / dO copied out: the next task's may load
+        mbarrier dp_full[2];  // [buffer]
+        mbarrier qa_free;    // last S / dP GEMM of a task retired: TMEM Q / dO reusable
+        mbarrier dq_full;
+        mbarrier k_full[SK], k_empty[SK];
+        mbarrier v_full[SV], v_empty[SV];
+        mbarrier ds_full[2][kGroups];  // [buffer][column group]
+        lcsf::work_queue queue;
+        uint32_t tmem_slot;
+    };
+    static constexpr int kSmemBytes = (int)sizeof(shared) + 1024;  // + alignment slack
+    static_assert(kSmemBytes <= 232448, "smem");
 
-    if (warp == kWarpLoad && lane == 0) {
-        queue.init(1 + 16);  // the MMA warp and the 16 compute warps
-        mbar_init(&qdo_full, 1);
-        mbar_init(&s_full, 1);
-        mbar_init(&s_free, kComputeThreads);
-        mbar_init(&a_ready, kComputeThreads);
-        mbar_init(&qdo_free, 1);
-        mbar_init(&bars[5], 1);
-        mbar_init(&bars[26], 1);
-        mbar_init(&qa_free, 1);
-        mbar_init(&dq_full, 1);
+    static TKB_DEVICE uint32_t dp_buf(uint32_t it) { return kDP ? ((it & 1) ? 384u : C::tmem_dp()) : C::tmem_dp(); }
+    static TKB_DEVICE int buf_of(uint32_t it) { return (kDP && (it & 1)) ? 1 : 0; }
+    static TKB_DEVICE uint32_t ph_of(uint32_t it) { return kDP ? ((it >> 1) & 1) : (it & 1); }
+    static TKB_DEVICE int num_tasks(const globals& p) { return p.bh * (p.n_pad / 128); }
+    static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
+    static TKB_DEVICE int nk_of(const globals& p, const QTask& w) { return CAUSAL ? (w.i + 1) : p.n_pad / 128; }
+    static TKB_DEVICE Tile<D> tK(shared& sh, int x) { return Tile<D>{sh.k[x % SK]}; }
+    static TKB_DEVICE Tile<D> tV(shared& sh, int x) { return Tile<D>{sh.v[x % SV]}; }
+
+    static TKB_DEVICE void init(shared& sh, const globals& p) {
+        mbar_init(&sh.qdo_full, 1);
+        mbar_init(&sh.s_full, 1);
+        mbar_init(&sh.s_free, kComputeThreads);
+        mbar_init(&sh.a_ready, kComputeThreads);
+        mbar_init(&sh.qdo_free, 1);
+        mbar_init(&sh.dp_full[0], 1);
+        mbar_init(&sh.dp_full[1], 1);
+        mbar_init(&sh.qa_free, 1);
+        mbar_init(&sh.dq_full, 1);
         for (int g = 0; g < kGroups; ++g) {
-            mbar_init(&bars[32 + g], 128);
-            mbar_init(&bars[36 + g], 128);
+            mbar_init(&sh.ds_full[0][g], 128);
+            mbar_init(&sh.ds_full[1][g], 128);
         }
         for (int s = 0; s < SK; ++s) {
-            mbar_init(&k_full[s], 1);
-            mbar_init(&k_empty[s], 1);
+            mbar_init(&sh.k_full[s], 1);
+            mbar_init(&sh.k_empty[s], 1);
         }
         for (int s = 0; s < SV; ++s) {
-            mbar_init(&v_full[s], 1);
-            mbar_init(&v_empty[s], 1);
+            mbar_init(&sh.v_full[s], 1);
+            mbar_init(&sh.v_empty[s], 1);
         }
-        fence_barrier_init();
         tma::prefetch_desc(&p.tm_q);
         tma::prefetch_desc(&p.tm_k);
         tma::prefetch_desc(&p.tm_v);
         tma::prefetch_desc(&p.tm_do);
     }
-    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
-    tmem::fence_before();
-    __syncthreads();
-    tmem::fence_after();
-    const uint32_t tbase = tmem_slot;
 
-    if (warp == kWarpLoad) {
-        if (lane == 0) {
-            // ------------------------------------------------------------- LOAD
+    // ------------------------------------------------------------- LOAD
+    struct producer {
+        struct state {
+            int kv = 0;  // K / V ring position, continuous across tasks
+        };
+        // the skeleton claims the next task once this one's loads are all issued (the atomic
+        // counter hands the heavy causal tasks out first and balances them across SMs)
+        template <class ClaimNext>
+        static TKB_DEVICE void load(const lcsf::args<attn_bwd_dq_template>& a, state& ps, int t, int n, ClaimNext&&) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
             const uint64_t pol_stream = tma::policy_evict_first();
             const uint64_t pol_keep = tma::policy_evict_last();
-            int kv = 0;  // K / V ring position, continuous across tasks
-            int n = 0;
-            int t = queue.claim(0, p.sched, tasks);
-            while (t >= 0) {
-                const QTask w = qtask<CAUSAL>(p, t);
-                const int b = w.bh / p.heads, h = w.bh - b * p.heads;
-                mbar_wait(&qdo_free, (n & 1) ^ 1u);  // the previous task's Q / dO are in TMEM
-                mbar_arrive_expect_tx(&qdo_full, 2 * TL::kTileBytes);
-                for (int a = 0; a < TL::kAtoms; ++a) {
-                    tma::load_4d(sQ + a * kAtomBytes, &p.tm_q, &qdo_full, a * 64, w.i * 128, h, b, pol_stream);
-                    tma::load_4d(sDo + a * kAtomBytes, &p.tm_do, &qdo_full, a * 64, w.i * 128, h, b, pol_stream);
-                }
-                const int nk = nk_of(w);
-                for (int jj = 0; jj < nk; ++jj, ++kv) {
-                    const int sk = kv % SK, sv = kv % SV;
-                    mbar_wait(&k_empty[sk], ((kv / SK) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&k_full[sk], TL::kTileBytes);
-                    for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sK + sk * TL::kTileBytes + a * kAtomBytes, &p.tm_k, &k_full[sk], a * 64, jj * 128,
-                                     h / p.group, b, pol_keep);
-                    mbar_wait(&v_empty[sv], ((kv / SV) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&v_full[sv], TL::kTileBytes);
-                    for (int a = 0; a < TL::kAtoms; ++a)
-                        tma::load_4d(sV + sv * TL::kTileBytes + a * kAtomBytes, &p.tm_v, &v_full[sv], a * 64, jj * 128,
-                                     h / p.group, b, pol_keep);
-                }
-                // claim the next task once this one's loads are all issued (the atomic counter
-                // hands the heavy causal tasks out first and balances them across SMs)
-                t = queue.claim(++n, p.sched, tasks);
+            const QTask w = qtask<CAUSAL>(p, t);
+            const int b = w.bh / p.heads, h = w.bh - b * p.heads;
+            mbar_wait(&sh.qdo_free, (n & 1) ^ 1u);  // the previous task's Q / dO are in TMEM
+            mbar_arrive_expect_tx(&sh.qdo_full, 2 * TL::kTileBytes);
+            load_async(Tile<D>{sh.q}, gl{&p.tm_q}, &sh.qdo_full, w.i * 128, h, b, pol_stream);
+            load_async(Tile<D>{sh.dO}, gl{&p.tm_do}, &sh.qdo_full, w.i * 128, h, b, pol_stream);
+            const int nk = nk_of(p, w);
+            for (int jj = 0; jj < nk; ++jj, ++ps.kv) {
+                const int kv = ps.kv;
+                const int sk = kv % SK, sv = kv % SV;
+                mbar_wait(&sh.k_empty[sk], ((kv / SK) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sh.k_full[sk], TL::kTileBytes);
+                load_async(tK(sh, kv), gl{&p.tm_k}, &sh.k_full[sk], jj * 128, h / p.group, b, pol_keep);
+                mbar_wait(&sh.v_empty[sv], ((kv / SV) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sh.v_full[sv], TL::kTileBytes);
+                load_async(tV(sh, kv), gl{&p.tm_v}, &sh.v_full[sv], jj * 128, h / p.group, b, pol_keep);
             }
         }
-    } else if (warp == kWarpMma) {
-        // ----------------------------------------------------------------- MMA (converged warp)
-        int kv = 0;        // K / V ring position
-        uint32_t it = 0;   // global iteration count (s_full / s_free / dp_full / ds_full phases)
-        auto tK = [&](int x) { return Tile<D>{sK + (x % SK) * TL::kTileBytes}; };
-        auto tV = [&](int x) { return Tile<D>{sV + (x % SV) * TL::kTileBytes}; };
-        const tt_bf<D / 2> tQa{tbase + C::tmem_qa()}, tDoa{tbase + C::tmem_doa()};  // A operands in TMEM
-        auto issue_s = [&](int x) {  // S = Q K^T
-            mbar_wait(&k_full[x % SK], (x / SK) & 1);
-            tmem::fence_after();
-            mm_ABt(tt_fl<128>{tbase + C::tmem_s()}, tQa, tK(x));
-            mma_commit(&s_full);
+        static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dq_template>&, state&) {}
+    };
+
+    // ------------------------------------------------------------- MMA (converged warp)
+    struct mma {
+        struct state {
+            int kv = 0;       // K / V ring position
+            uint32_t it = 0;  // global iteration count (s_full / s_free / dp_full / ds_full phases)
+            long long t_start = 0;
         };
-        auto issue_dp = [&](int x, uint32_t itx) {  // dP = dO V^T (iteration itx)
-            mbar_wait(&v_full[x % SV], (x / SV) & 1);
-            tmem::fence_after();
-            mm_ABt(tt_fl<128>{tbase + dp_buf(itx)}, tDoa, tV(x));
-            mma_commit(&dp_full_of(itx));
-            mma_commit(&v_empty[x % SV]);
-        };
-        for (int n = 0;; ++n) {
-            const int t = queue.get_warp(n);
-            if (lane == 0) queue.release(n);
-            if (t < 0) break;
-            const int nk = nk_of(qtask<CAUSAL>(p, t));
-            mbar_wait(&a_ready, n & 1);  // this task's Q / dO are in TMEM
+        static TKB_DEVICE void issue(const lcsf::args<attn_bwd_dq_template>& a, state& ms, int t, int n) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const uint32_t tbase = a.tmem;
+            long long* tr = trace_slot(p, (int)blockIdx.x, 1);
+            if (n == 0) ms.t_start = clock64();
+            const long long t_start = ms.t_start;
+            const tt_bf<D / 2> tQa{tbase + C::tmem_qa()}, tDoa{tbase + C::tmem_doa()};  // A operands in TMEM
+            auto issue_s = [&](int x) {  // S = Q K^T
+                mbar_wait(&sh.k_full[x % SK], (x / SK) & 1);
+                tmem::fence_after();
+                mm_ABt(tt_fl<128>{tbase + C::tmem_s()}, tQa, tK(sh, x));
+                mma_commit(&sh.s_full);
+            };
+            auto issue_dp = [&](int x, uint32_t itx) {  // dP = dO V^T (iteration itx)
+                mbar_wait(&sh.v_full[x % SV], (x / SV) & 1);
+                tmem::fence_after();
+                mm_ABt(tt_fl<128>{tbase + dp_buf(itx)}, tDoa, tV(sh, x));
+                mma_commit(&sh.dp_full[buf_of(itx)]);
+                mma_commit(&sh.v_empty[x % SV]);
+            };
+            int& kv = ms.kv;
+            uint32_t& it = ms.it;
+            const int nk = nk_of(p, qtask<CAUSAL>(p, t));
+            mbar_wait(&sh.a_ready, n & 1);  // this task's Q / dO are in TMEM
             issue_s(kv);
             issue_dp(kv, it);
-            if (nk == 1) mma_commit(&qa_free);  // the task's only S and dP are issued
+            if (nk == 1) mma_commit(&sh.qa_free);  // the task's only S and dP are issued
             for (int jj = 0; jj < nk; ++jj, ++kv, ++it) {
                 if (jj + 1 < nk) {
-                    mbar_wait(&s_free, it & 1);  // S_j read out by the compute warps
+                    mbar_wait(&sh.s_free, it & 1);  // S_j read out by the compute warps
                     issue_s(kv + 1);
                     if (kDP) {  // the other dP buffer: its dS_{j-1} went to dQ_{j-1}, issued before
                         issue_dp(kv + 1, it + 1);
-                        if (jj + 2 == nk) mma_commit(&qa_free);  // the task's last S and dP are issued
+                        if (jj + 2 == nk) mma_commit(&sh.qa_free);  // the task's last S and dP are issued
                     }
                 }
                 TKB_TR(0, (int)it, 0);
-                // dQ += dS K, one 32-key chunk per column group as it lands
-                mma_AB_groups(tt_fl<D>{tbase + C::tmem_dq()}, tt_bf<128>{tbase + dp_buf(it)}, swap_layout(tK(kv)),
-                              jj > 0, [&](int g) {
-                                  mbar_wait(&ds_full_of(it)[g], ph_of(it));
+                // dQ += dS K (mma_AB: one 32-key chunk per column group as it lands, K read MN-major)
+                mma_AB_groups(tt_fl<D>{tbase + C::tmem_dq()}, tt_bf<128>{tbase + dp_buf(it)},
+                              swap_layout(tK(sh, kv)), jj > 0, [&](int g) {
+                                  mbar_wait(&sh.ds_full[buf_of(it)][g], ph_of(it));
                                   tmem::fence_after();
                               });
                 TKB_TR(0, (int)it, 1);
-                mma_commit(&k_empty[kv % SK]);
+                mma_commit(&sh.k_empty[kv % SK]);
                 if (!kDP && jj + 1 < nk) {
                     issue_dp(kv + 1, it + 1);  // overwrites dS_j, read by dQ_j issued before
-                    if (jj + 2 == nk) mma_commit(&qa_free);  // the task's last S and dP are issued
+                    if (jj + 2 == nk) mma_commit(&sh.qa_free);  // the task's last S and dP are issued
                 }
                 TKB_TR(0, (int)it, 2);
             }
-            mma_commit(&dq_full);
+            mma_commit(&sh.dq_full);
         }
-    } else {
-        // ----------------------------------------------------------------- COMPUTE
-        const int wq = warp & 3;
-        const int g = warp >> 2;       // kv group: columns [32g, 32g+32)
-        const int r = wq * 32 + lane;  // q row == TMEM lane
-        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tbase + lane_off + C::tmem_s() + 32 * g;
-        const uint32_t tDp0 = tbase + lane_off + 32 * g;  // + dp_buf(it)
-        const float tau = p.scale_log2;
-        uint32_t it = 0;
-        int n = 0;
-        // Q, dO of task n: SMEM (TMA, swizzled) -> TMEM A operands, once the previous task's last
-        // S / dP GEMMs retired
-        auto stage_a = [&](int nn) {
-            mbar_wait(&qdo_full, nn & 1);
-            if (nn > 0) mbar_wait(&qa_free, (nn - 1) & 1);
+    };
+
+    // ------------------------------------------------------------- COMPUTE + FINISH
+    struct consumer {
+        struct state {
+            uint32_t it = 0;
+            long long t_start = 0;
+        };
+        // Q, dO of task nn: SMEM (TMA, swizzled) -> TMEM A operands, once the previous task's
+        // last S / dP GEMMs retired (shared -> register -> TMEM)
+        static TKB_DEVICE void stage_a(const lcsf::args<attn_bwd_dq_template>& a, int nn) {
+            shared& sh = a.sh;
+            const int wq = a.warp & 3, g = a.warp >> 2, r = wq * 32 + a.lane;
+            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+            mbar_wait(&sh.qdo_full, nn & 1);
+            if (nn > 0) mbar_wait(&sh.qa_free, (nn - 1) & 1);
             tmem::fence_after();
-            smem_rows_to_tmem_a<D>(Tile<D>{sQ}, tbase + lane_off + C::tmem_qa(), r, g);
-            smem_rows_to_tmem_a<D>(Tile<D>{sDo}, tbase + lane_off + C::tmem_doa(), r, g);
+            smem_rows_to_tmem_a<D>(Tile<D>{sh.q}, a.tmem + lane_off + C::tmem_qa(), r, g);
+            smem_rows_to_tmem_a<D>(Tile<D>{sh.dO}, a.tmem + lane_off + C::tmem_doa(), r, g);
             tmem::wait_st();
             tmem::fence_before();
-            mbar_arrive(&a_ready);
-        };
-        // SMEM Q / dO are released (qdo_free) once copied into TMEM AND once the previous
-        // task's finish, which stages dQ in sQ for its TMA store, has been read out
-        int t = queue.get_warp(0);
-        if (t >= 0) {
-            stage_a(0);
-            named_sync(kBarCompute, kComputeThreads);
-            if (threadIdx.x == 0) mbar_arrive(&qdo_free);
+            mbar_arrive(&sh.a_ready);
         }
-        while (t >= 0) {
+        static TKB_DEVICE void compute(const lcsf::args<attn_bwd_dq_template>& a, state& cs, int t, int n) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const int wq = a.warp & 3;
+            const int g = a.warp >> 2;       // kv group: columns [32g, 32g+32)
+            const int r = wq * 32 + a.lane;  // q row == TMEM lane
+            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+            const uint32_t tS = a.tmem + lane_off + C::tmem_s() + 32 * g;
+            const uint32_t tDp0 = a.tmem + lane_off + 32 * g;  // + dp_buf(it)
+            const float tau = p.scale_log2;
+            long long* tr = trace_slot(p, (int)blockIdx.x, 1);
+            if (n == 0) {
+                cs.t_start = clock64();
+                // SMEM Q / dO are released (qdo_free) once copied into TMEM AND once the previous
+                // task's finish, which stages dQ in sQ for its TMA store, has been read out
+                stage_a(a, 0);
+                named_sync(kBarCompute, kComputeThreads);
+                if (threadIdx.x == 0) mbar_arrive(&sh.qdo_free);
+            }
+            const long long t_start = cs.t_start;
             const QTask w = qtask<CAUSAL>(p, t);
-            const int b = w.bh / p.heads, h = w.bh - b * p.heads;
             const int q0 = w.i * 128;
             const int row = q0 + r;
-            const int nk = nk_of(w);
+            const int nk = nk_of(p, w);
             // -lse2 (-inf on padded rows -> P = 0) and Delta, stored group-permuted (perm32)
             const float nlse_r = p.lse2[(size_t)w.bh * p.n_pad + perm32(row)];
             const float dlt_r = p.delta[(size_t)w.bh * p.n_pad + perm32(row)];
+            uint32_t& it = cs.it;
             for (int jj = 0; jj < nk; ++jj, ++it) {
                 const int kv0 = jj * 128;
-                mbar_wait(&s_full, it & 1);
+                mbar_wait(&sh.s_full, it & 1);
                 if (threadIdx.x == 0) TKB_TR(1, (int)it, 0);
                 tmem::fence_after();
                 float pf[32];
                 tmem::ldw_32x32b_x32(tS, reinterpret_cast<uint32_t*>(pf));
                 tmem::fence_before();
-                mbar_arrive(&s_free);
+                mbar_arrive(&sh.s_free);
                 exp_chunk<true>(pf, tau, 0u, nlse_r);
                 // visible keys: kv < n, and causal kv <= row
                 const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 32 * g;  // last visible column
@@ -1176,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
 #pragma unroll
                     for (int c = 0; c < 32; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
                 }
-                mbar_wait(&dp_full_of(it), ph_of(it));
+                mbar_wait(&sh.dp_full[buf_of(it)], ph_of(it));
                 const uint32_t tDp = tDp0 + dp_buf(it);
                 if (threadIdx.x == 0) TKB_TR(1, (int)it, 1);
                 tmem::fence_after();
@@ -1193,41 +1201,52 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(const __grid_c
                 tmem::st_32x32b_x16(tDp, pk);  // inside the 32 dP columns this thread has read
                 tmem::wait_st();
                 tmem::fence_before();
-                mbar_arrive(&ds_full_of(it)[g]);
+                mbar_arrive(&sh.ds_full[buf_of(it)][g]);
                 if (threadIdx.x == 0) TKB_TR(1, (int)it, 2);
             }
-            // the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this finish)
-            const int t_next = queue.get_warp(n + 1);
-            if (t_next >= 0) stage_a(n + 1);
-            // FINISH: dQ (TMEM fp32) -> bf16 -> SW128 staging in sQ (its Q is in TMEM by now)
-            // -> TMA store; sQ / sDo are released to the load warp once the store has read it.
-            // (Per-thread row stores from registers cost ~2,400 clk per task: each store
-            // instruction touches 16-32 L2 lines.) The next task's first dQ GEMM waits for its
-            // dS, which these warps produce after this.
-            mbar_wait(&dq_full, n & 1);
+        }
+        // FINISH: the next task's Q / dO into TMEM first (its S / dP GEMMs then overlap this
+        // finish), then dQ (TMEM fp32) -> bf16 -> SW128 staging in sQ (its Q is in TMEM by now)
+        // -> TMA store; sQ / sDo are released to the load warp once the store has read it.
+        // (Per-thread row stores from registers cost ~2,400 clk per task: each store
+        // instruction touches 16-32 L2 lines.) The next task's first dQ GEMM waits for its
+        // dS, which these warps produce after this.
+        static TKB_DEVICE void finish(const lcsf::args<attn_bwd_dq_template>& a, state& cs, int t, int n) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const int wq = a.warp & 3, g = a.warp >> 2, r = wq * 32 + a.lane;
+            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+            const QTask w = qtask<CAUSAL>(p, t);
+            const int b = w.bh / p.heads, h = w.bh - b * p.heads;
+            const int t_next = a.queue.get_warp(n + 1);
+            if (t_next >= 0) stage_a(a, n + 1);
+            mbar_wait(&sh.dq_full, n & 1);
             tmem::fence_after();
-            tmem_rows_to_smem_bf16<D>(tbase + lane_off + C::tmem_dq(), Tile<D>{sQ}, r, g, p.scale);  // dQ = scale dS K
+            tmem_rows_to_smem_bf16<D>(a.tmem + lane_off + C::tmem_dq(), Tile<D>{sh.q}, r, g, p.scale);  // dQ = scale dS K
             tma::fence_async_smem();
             named_sync(kBarCompute, kComputeThreads);
             if (threadIdx.x == 0) {
-                for (int a = 0; a < TL::kAtoms; ++a) tma::store_4d(&p.tm_dq, sQ + a * kAtomBytes, a * 64, q0, h, b);
+                store_async(gl{&p.tm_dq}, Tile<D>{sh.q}, w.i * 128, h, b);
                 tma::commit_group();
                 tma::wait_group_read<0>();
-                mbar_arrive(&qdo_free);
+                mbar_arrive(&sh.qdo_free);
             }
-            __syncwarp();
-            if (lane == 0) queue.release(n);  // every warp read task n's id long ago
-            t = t_next;
-            ++n;
         }
-        if (threadIdx.x == 0) tma::wait_group<0>();
-    }
+        static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dq_template>&, state&) {
+            if (threadIdx.x == 0) tma::wait_group<0>();
+        }
+    };
+};
+// The backward entry template (attn_bwd_template<D, Causal> beside the
+// forward's attn_fwd_template<D, Causal>): dQ / dK / dV from the saved L as three launches on
+// one stream — bwd_prep_kernel<D> (Delta = rowsum(dO o O), -L log2 e), then the two LCSF
+// kernels lcsf::kernel<dkdv> (KV-stationary) and lcsf::kernel<dq> (Q-stationary).
+template <int D, bool CAUSAL>
+struct attn_bwd_template {
+    using dkdv = attn_bwd_dkdv_template<D, CAUSAL>;
+    using dq = attn_bwd_dq_template<D, CAUSAL>;
+};
 
-    tmem::fence_before();
-    __syncthreads();
-    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
-    if (threadIdx.x == 0) lcsf::queue_exit(p.sched);
-}
 #undef TKB_TR
 
 // Delta = rowsum(dO o O), lse2 = -L log2 e (-inf / 0 on padded rows: P = 0 there), written
@@ -1292,8 +1311,10 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
 template <int D, bool CAUSAL>
 int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases, int* launches) {
     static std::atomic<unsigned long long> set_dq{0}, set_kv2{0}, set_kvp{0};  // per device
-    if (int e = ensure_smem(attn_bwd_dq_kernel<D, CAUSAL>, CfgQ<D>::kSmemBytes, set_dq)) return e;
-    if (int e = ensure_smem(attn_bwd_dkdvp_kernel<D, CAUSAL>, CfgKVP<D>::kSmemBytes, set_kvp)) return e;
+    using DQ = typename attn_bwd_template<D, CAUSAL>::dq;
+    if (int e = ensure_smem(lcsf::kernel<DQ>, DQ::kSmemBytes, set_dq)) return e;
+    using KV = typename attn_bwd_template<D, CAUSAL>::dkdv;
+    if (int e = ensure_smem(lcsf::kernel<KV>, KV::kSmemBytes, set_kvp)) return e;
     if (D == 128)
         if (int e = ensure_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes, set_kv2)) return e;
     if (phases & 2) {
@@ -1302,9 +1323,8 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
             attn_bwd_dkdv2_kernel<CAUSAL><<<grid2, kThreads, CfgKV2::kSmemBytes, stream>>>(p);
         } else {
             const int64_t tasks_kv = (int64_t)(p.n_pad / 128) * (p.heads / p.group) * batches;
-            attn_bwd_dkdvp_kernel<D, CAUSAL>
-                <<<(unsigned)(tasks_kv < p.num_sms ? tasks_kv : p.num_sms), kThreads, CfgKVP<D>::kSmemBytes,
-                   stream>>>(p);
+            lcsf::kernel<KV><<<(unsigned)(tasks_kv < p.num_sms ? tasks_kv : p.num_sms), KV::kThreads,
+                               KV::kSmemBytes, stream>>>(p);
         }
         int e = (int)cudaGetLastError();
         if (e) return e;
@@ -1312,8 +1332,8 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
     }
     if (phases & 4) {
         const int64_t tasks = (int64_t)p.bh * (p.n_pad / 128);
-        attn_bwd_dq_kernel<D, CAUSAL>
-            <<<(unsigned)(tasks < p.num_sms ? tasks : p.num_sms), kThreads, CfgQ<D>::kSmemBytes, stream>>>(p);
+        lcsf::kernel<DQ><<<(unsigned)(tasks < p.num_sms ? tasks : p.num_sms), DQ::kThreads, DQ::kSmemBytes,
+                           stream>>>(p);
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;

@@ -28,10 +28,14 @@
 // so issuing PV_{i-1}(s) before QK_i(s) makes "S_i(s) full" imply "PV_{i-1}(s)
 // done": the softmax may then rescale O_s and overwrite P_s safely.
 //
-// A persistent variant (dynamic task queue, separate correction warpgroup, MMA stream
-// running across task boundaries; git 283279c) measured 3-10% slower at N >= 4096:
-// the two extra warps per SM sub-partition cost the softmax warps issue slots on the
-// critical path.
+// The kernel is lcsf::kernel<attn_fwd_template<D, Causal>> (tkb/lcsf.cuh: the LCSF skeleton
+// owns the persistent task queue, barrier init, TMEM allocation and role dispatch; the
+// template below supplies the layout and the load / mma / compute / finish hooks, as the
+// paper's lcf::kernel<attn_fwd_template<D>>).
+//
+// A variant with a separate correction warpgroup (FA4-style) and an MMA stream running across
+// task boundaries (git 283279c) measured 3-10% slower at N >= 4096: the two extra warps per
+// SM sub-partition cost the softmax warps issue slots on the critical path.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -66,8 +70,6 @@ struct Cfg {
     static constexpr int kSmemQ = kQStages * kTile;
     static constexpr int kSmemKv = kKvSlots * kTile;
     static constexpr int kStageBytes = 128 * 128;  // per-warpgroup O staging: one 128 x 64 atom
-    static constexpr int kSmemBytes = kSmemQ + kSmemKv + kQStages * kStageBytes + 1024;  // + alignment slack
-    static_assert(kSmemBytes + 512 <= 232448, "smem");
     static TKB_DEVICE constexpr uint32_t tmem_s(int s) { return s * 128u; }
     static TKB_DEVICE constexpr uint32_t tmem_o(int s) { return 256u + s * D; }
 };
@@ -81,41 +83,50 @@ constexpr float kRescaleThreshold = 8.0f;        // log2 units: defer O rescale 
 constexpr float kLn2 = 0.69314718055994530942f;
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ FwdParams p) {
+struct attn_fwd_template {
     using C = Cfg<D>;
     using Tile = typename C::Tile;
-    extern __shared__ uint8_t smem_raw[];
-    // SW128 tiles need a 1024-byte aligned base
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const Tile sQ[kQStages] = {Tile{smem}, Tile{smem + C::kTile}};
-    auto sKV = [&](int slot) { return Tile{smem + C::kSmemQ + slot * C::kTile}; };
-    const gl gQ{&p.tm_q}, gK{&p.tm_k}, gV{&p.tm_v}, gO{&p.tm_o};
-
-    const st_bf<128, 64> sStage[kQStages] = {st_bf<128, 64>{smem + C::kSmemQ + C::kSmemKv},
-                                              st_bf<128, 64>{smem + C::kSmemQ + C::kSmemKv + C::kStageBytes}};
-
-    __shared__ mbarrier q_full[kQStages], q_empty[kQStages], s_full[kQStages], o_full[kQStages];
-    __shared__ mbarrier p_full[kQStages][kPChunks];
-    __shared__ lcsf::ring<C::kKvSlots> kv;
+    using globals = FwdParams;
+    static constexpr int kThreads = fwd::kThreads;
+    static constexpr int kTmemCols = 512;
+    static constexpr int kProducerWarp = kWarpLoad;
+    static constexpr int kMmaWarp = fwd::kWarpMma;
+    static constexpr int kConsumerWarps = 8;      // two softmax warpgroups
+    static constexpr int kQueueReaders = 1 + 8;   // the MMA warp and the 8 softmax warps
+    static constexpr bool kAlignSlack = true;
+    static constexpr bool kReleaseEarly = true;   // the softmax warps release a task id on reading it
     // D = 64: the 128 free TMEM columns hold a third S buffer; S / P rotate over three buffers
     // in QK issue order, so QK_{i+1}(s) is issued before PV_i(s) and the next block's
     // exponentials do not wait for the PV -> QK round trip (per-buffer s_full / p_full;
     // pv_done marks each PV_s for the lazy O rescale)
-    constexpr bool k3 = (D == 64);
-    __shared__ mbarrier s_full3[3], p_full3[3][kPChunks], pv_done[kQStages];
-    __shared__ lcsf::work_queue queue;
-    __shared__ uint32_t tmem_slot;
+    static constexpr bool k3 = (D == 64);
 
-    const int warp = warpid();
-    const int lane = laneid();
-    const int n = p.n;
-    const int m_blocks = (n + kRowsPerCta - 1) / kRowsPerCta;
+    struct shared {  // placed 1024-aligned: the tiles first
+        uint8_t q[kQStages][C::kTile];
+        uint8_t kv[C::kKvSlots][C::kTile];
+        uint8_t stage[kQStages][C::kStageBytes];  // per-warpgroup O staging atom
+        mbarrier q_full[kQStages], q_empty[kQStages], s_full[kQStages], o_full[kQStages];
+        mbarrier p_full[kQStages][kPChunks];
+        lcsf::ring<C::kKvSlots> kv_ring;
+        mbarrier s_full3[3], p_full3[3][kPChunks], pv_done[kQStages];
+        lcsf::work_queue queue;
+        uint32_t tmem_slot;
+    };
+    static constexpr int kSmemBytes = (int)sizeof(shared) + 1024;  // + alignment slack
+    static_assert(kSmemBytes <= 232448, "smem");
+
+    static TKB_DEVICE Tile sQ(shared& sh, int s) { return Tile{sh.q[s]}; }
+    static TKB_DEVICE Tile sKV(shared& sh, int slot) { return Tile{sh.kv[slot]}; }
+    static TKB_DEVICE st_bf<128, 64> sStage(shared& sh, int s) { return st_bf<128, 64>{sh.stage[s]}; }
+
     // task t -> (256-row query block, b, h): heads in L2-sized groups, inside a group the heavy
     // (late) causal query blocks first, heads innermost; claimed dynamically (one CTA per SM)
     struct Task {
         int mblk, head, batch, nkv;
     };
-    auto decode = [&](int t) {
+    static TKB_DEVICE Task decode(const globals& p, int t) {
+        const int N = p.n;
+        const int m_blocks = (N + kRowsPerCta - 1) / kRowsPerCta;
         const int G = p.head_group;
         const int sec = t / (G * m_blocks);
         const int r = t - sec * G * m_blocks;
@@ -126,136 +137,130 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         w.mblk = CAUSAL ? (m_blocks - 1 - mi) : mi;
         w.batch = bh / p.heads;
         w.head = bh - w.batch * p.heads;
-        w.nkv = (n + kBlockN - 1) / kBlockN;
-        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, n) - 1) / kBlockN + 1);
+        w.nkv = (N + kBlockN - 1) / kBlockN;
+        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, N) - 1) / kBlockN + 1);
         return w;
-    };
+    }
     // kv blocks query tile s of a task visits (causal: tile 0 skips the block only tile 1 sees)
-    auto tile_blocks = [&](const Task& w, int s) {
+    static TKB_DEVICE int tile_blocks(const globals& p, const Task& w, int s) {
         if (!CAUSAL) return w.nkv;
-        return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, n) - 1) / kBlockN + 1);
-    };
+        return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, p.n) - 1) / kBlockN + 1);
+    }
     // k3: index of (tile s, block i) in the task's QK issue order, its buffer and TMEM column
-    auto qk_index = [](int s, int i, int nk0, int nk1) { return min(i, nk0) + min(i, nk1) + ((s == 1 && i < nk0) ? 1 : 0); };
-    auto sbuf_col = [](uint32_t b) -> uint32_t { return b == 0 ? 0u : (b == 1 ? 128u : 384u); };
+    static TKB_DEVICE int qk_index(int s, int i, int nk0, int nk1) {
+        return min(i, nk0) + min(i, nk1) + ((s == 1 && i < nk0) ? 1 : 0);
+    }
+    static TKB_DEVICE uint32_t sbuf_col(uint32_t b) { return b == 0 ? 0u : (b == 1 ? 128u : 384u); }
 
-    if (warp == kWarpLoad && lane == 0) {
-        queue.init(1 + 8);  // the MMA warp and the 8 softmax warps
+    static TKB_DEVICE int num_tasks(const globals& p) { return p.tasks; }
+    static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
+
+    static TKB_DEVICE void init(shared& sh, const globals& p) {
         for (int s = 0; s < kQStages; ++s) {
-            mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], 1);
-            mbar_init(&s_full[s], 1);
-            mbar_init(&o_full[s], 1);
-            mbar_init(&pv_done[s], 1);
-            for (int c = 0; c < kPChunks; ++c) mbar_init(&p_full[s][c], WARPGROUP_THREADS);
+            mbar_init(&sh.q_full[s], 1);
+            mbar_init(&sh.q_empty[s], 1);
+            mbar_init(&sh.s_full[s], 1);
+            mbar_init(&sh.o_full[s], 1);
+            mbar_init(&sh.pv_done[s], 1);
+            for (int c = 0; c < kPChunks; ++c) mbar_init(&sh.p_full[s][c], WARPGROUP_THREADS);
         }
         for (int b = 0; b < 3; ++b) {
-            mbar_init(&s_full3[b], 1);
-            for (int c = 0; c < kPChunks; ++c) mbar_init(&p_full3[b][c], WARPGROUP_THREADS);
+            mbar_init(&sh.s_full3[b], 1);
+            for (int c = 0; c < kPChunks; ++c) mbar_init(&sh.p_full3[b][c], WARPGROUP_THREADS);
         }
-        kv.init(1, 1);
-        fence_barrier_init();
-        gQ.prefetch();
-        gK.prefetch();
-        gV.prefetch();
-        gO.prefetch();
+        sh.kv_ring.init(1, 1);
+        gl{&p.tm_q}.prefetch();
+        gl{&p.tm_k}.prefetch();
+        gl{&p.tm_v}.prefetch();
+        gl{&p.tm_o}.prefetch();
     }
-    if (warp == kWarpMma) tmem::alloc<512>(&tmem_slot);
-    tmem::fence_before();
-    __syncthreads();
-    tmem::fence_after();
-    const uint32_t tbase = tmem_slot;
 
-    if (warp == kWarpLoad) {
-        // ----------------------------- LOAD (LCSF load stage) -----------------------------
-        if (lane == 0) {
+    // ----------------------------- LOAD (LCSF load stage) -----------------------------
+    struct producer {
+        struct state {
+            lcsf::ring_state<C::kKvSlots> st;
+        };
+        template <class ClaimNext>
+        static TKB_DEVICE void load(const lcsf::args<attn_fwd_template>& a, state& ps, int t, int nt,
+                                    ClaimNext&& claim_next) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
             const uint64_t pol_q = tma::policy_evict_first();
             const uint64_t pol_kv = tma::policy_evict_last();
-            lcsf::ring_state<C::kKvSlots> st;
-            int nt = 0;
-            int t = queue.claim(0, p.sched, p.tasks);
-            while (t >= 0) {
-                const Task w = decode(t);
-                const int q0 = w.mblk * kRowsPerCta;
-                for (int s = 0; s < kQStages; ++s) {  // Q_s is free once the last QK_s of the previous task retired
-                    mbar_wait(&q_empty[s], (nt & 1) ^ 1u);
-                    mbar_arrive_expect_tx(&q_full[s], C::kTile);
-                    load_async(sQ[s], gQ, &q_full[s], q0 + s * kBlockM, w.head, w.batch, pol_q);
-                }
-                const int t_next = queue.claim(nt + 1, p.sched, p.tasks);
-                if (t_next >= 0) {  // warm the next task's Q in L2
-                    const Task w2 = decode(t_next);
-                    for (int s = 0; s < kQStages; ++s)
-                        for (int a = 0; a < Tile::kAtoms; ++a)
-                            tma::prefetch_4d(gQ.tm, a * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.batch);
-                }
-                for (int i = 0; i < w.nkv; ++i) {
+            const gl gQ{&p.tm_q}, gK{&p.tm_k}, gV{&p.tm_v};
+            const Task w = decode(p, t);
+            const int q0 = w.mblk * kRowsPerCta;
+            for (int s = 0; s < kQStages; ++s) {  // Q_s is free once the last QK_s of the previous task retired
+                mbar_wait(&sh.q_empty[s], (nt & 1) ^ 1u);
+                mbar_arrive_expect_tx(&sh.q_full[s], C::kTile);
+                load_async(sQ(sh, s), gQ, &sh.q_full[s], q0 + s * kBlockM, w.head, w.batch, pol_q);
+            }
+            const int t_next = claim_next();
+            if (t_next >= 0) {  // warm the next task's Q in L2
+                const Task w2 = decode(p, t_next);
+                for (int s = 0; s < kQStages; ++s)
+                    for (int at = 0; at < Tile::kAtoms; ++at)
+                        tma::prefetch_4d(gQ.tm, at * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.batch);
+            }
+            for (int i = 0; i < w.nkv; ++i) {
 #pragma unroll
-                    for (int which = 0; which < 2; ++which) {
-                        kv.wait_empty(st);
-                        mbar_arrive_expect_tx(&kv.full[st.slot], C::kTile);
-                        load_async(sKV(st.slot), which == 0 ? gK : gV, &kv.full[st.slot], i * kBlockN,
-                                   w.head / p.group, w.batch, pol_kv);  // grouped-query: kv head = head / group
-                        st.advance();
-                    }
+                for (int which = 0; which < 2; ++which) {
+                    sh.kv_ring.wait_empty(ps.st);
+                    mbar_arrive_expect_tx(&sh.kv_ring.full[ps.st.slot], C::kTile);
+                    load_async(sKV(sh, ps.st.slot), which == 0 ? gK : gV, &sh.kv_ring.full[ps.st.slot],
+                               i * kBlockN, w.head / p.group, w.batch, pol_kv);  // grouped-query: kv head = head / group
+                    ps.st.advance();
                 }
-                t = t_next;
-                ++nt;
             }
         }
-    } else if (warp == kWarpMma) {
-        // ----------------------------- MMA (LCSF compute, tensor part) ---------------------
-        // converged warp; one elected lane issues each tcgen05 op (tile.cuh / tcgen05.cuh)
-        auto qk = [&](int s, int kslot) {  // S_s = Q_s K^T   (mm_ABt, tiles.hpp:349)
-            mm_ABt(tt_fl<128>{tbase + C::tmem_s(s)}, sQ[s], sKV(kslot));
-        };
-        auto pv = [&](int s, int vslot, bool acc, uint32_t phase) {  // O_s += P_s V (mma_AB, tiles.hpp:350-352)
-#pragma unroll
-            for (int c = 0; c < kPChunks; ++c) {
-                mbar_wait(&p_full[s][c], phase);
-                tmem::fence_after();
-                mma_AB_k<D, kPChunkCols>(tt_fl<D>{tbase + C::tmem_o(s)},
-                                         tt_bf<kPChunkCols / 2>{tbase + C::tmem_s(s) + 64 + c * (kPChunkCols / 2)},
-                                         swap_layout(sKV(vslot)), c * kPChunkCols, acc || c > 0);
-            }
-        };
-        if constexpr (k3) {
+        static TKB_DEVICE void drain(const lcsf::args<attn_fwd_template>&, state&) {}
+    };
+
+    // ----------------------------- MMA (LCSF compute, tensor part) ---------------------
+    // converged warp; one elected lane issues each tcgen05 op
+    struct mma {
+        struct state {
             lcsf::ring_state<C::kKvSlots> st;
-            uint32_t qbase = 0;  // QK index of the task's first block (buffer = index % 3)
-            for (int nt = 0;; ++nt) {
-                const int t = queue.get(nt);
-                if (lane == 0) queue.release(nt);
-                if (t < 0) break;
-                const Task w = decode(t);
-                const int nkv = w.nkv;
-                const int nk[kQStages] = {tile_blocks(w, 0), tile_blocks(w, 1)};
-                auto gidx = [&](int s, int i) { return qbase + (uint32_t)qk_index(s, i, nk[0], nk[1]); };
-                auto qk3 = [&](int s, int i, int kslot) {
+            uint32_t qbase = 0;           // k3: QK index of the task's first block (buffer = index % 3)
+            uint32_t it[kQStages] = {0, 0};  // PVs issued per tile: p_full phases
+        };
+        static TKB_DEVICE void issue(const lcsf::args<attn_fwd_template>& a, state& ms, int t, int nt) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const uint32_t tbase = a.tmem;
+            auto& kv = sh.kv_ring;
+            auto& st = ms.st;
+            const Task w = decode(p, t);
+            const int nkv = w.nkv;
+            const int nk[kQStages] = {tile_blocks(p, w, 0), tile_blocks(p, w, 1)};  // causal: tile 0 may stop one early
+            if constexpr (k3) {
+                auto gidx = [&](int s, int i) { return ms.qbase + (uint32_t)qk_index(s, i, nk[0], nk[1]); };
+                auto qk3 = [&](int s, int i, int kslot) {  // S = Q K^T (mm_ABt, tiles.hpp:349)
                     const uint32_t g = gidx(s, i);
-                    mm_ABt(tt_fl<128>{tbase + sbuf_col(g % 3)}, sQ[s], sKV(kslot));
-                    mma_commit(&s_full3[g % 3]);
+                    mm_ABt(tt_fl<128>{tbase + sbuf_col(g % 3)}, sQ(sh, s), sKV(sh, kslot));
+                    mma_commit(&sh.s_full3[g % 3]);
                 };
-                auto pv3 = [&](int s, int i, int vslot) {  // O_s (+)= P_s(i) V
+                auto pv3 = [&](int s, int i, int vslot) {  // O_s (+)= P_s(i) V (mma_AB, tiles.hpp:350-352)
                     const uint32_t g = gidx(s, i);
 #pragma unroll
                     for (int c = 0; c < kPChunks; ++c) {
-                        mbar_wait(&p_full3[g % 3][c], (g / 3) & 1);
+                        mbar_wait(&sh.p_full3[g % 3][c], (g / 3) & 1);
                         tmem::fence_after();
                         mma_AB_k<D, kPChunkCols>(
                             tt_fl<D>{tbase + C::tmem_o(s)},
                             tt_bf<kPChunkCols / 2>{tbase + sbuf_col(g % 3) + 64 + c * (kPChunkCols / 2)},
-                            swap_layout(sKV(vslot)), c * kPChunkCols, i > 0 || c > 0);
+                            swap_layout(sKV(sh, vslot)), c * kPChunkCols, i > 0 || c > 0);
                     }
-                    mma_commit(&pv_done[s]);
+                    mma_commit(&sh.pv_done[s]);
                 };
-                mbar_wait(&q_full[0], nt & 1);
-                mbar_wait(&q_full[1], nt & 1);
+                mbar_wait(&sh.q_full[0], nt & 1);
+                mbar_wait(&sh.q_full[1], nt & 1);
                 kv.wait_full(st);
                 tmem::fence_after();
 #pragma unroll
                 for (int s = 0; s < kQStages; ++s) {
                     qk3(s, 0, st.slot);
-                    if (nk[s] == 1) mma_commit(&q_empty[s]);
+                    if (nk[s] == 1) mma_commit(&sh.q_empty[s]);
                 }
                 mma_commit(&kv.empty[st.slot]);
                 st.advance();
@@ -272,11 +277,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     for (int s = 0; s < kQStages; ++s) {
                         if (i < nk[s]) {
                             qk3(s, i, kslot);
-                            if (i == nk[s] - 1) mma_commit(&q_empty[s]);
+                            if (i == nk[s] - 1) mma_commit(&sh.q_empty[s]);
                         }
                         if (i - 1 < nk[s]) {
                             pv3(s, i - 1, vslot);
-                            if (i - 1 == nk[s] - 1) mma_commit(&o_full[s]);
+                            if (i - 1 == nk[s] - 1) mma_commit(&sh.o_full[s]);
                         }
                     }
                     mma_commit(&kv.empty[vslot]);
@@ -289,258 +294,273 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 for (int s = 0; s < kQStages; ++s) {
                     if (nk[s] != nkv) continue;
                     pv3(s, nkv - 1, vslot);
-                    mma_commit(&o_full[s]);
+                    mma_commit(&sh.o_full[s]);
                 }
                 mma_commit(&kv.empty[vslot]);
                 st.advance();
-                qbase += (uint32_t)(nk[0] + nk[1]);
-            }
-        } else {
-        lcsf::ring_state<C::kKvSlots> st;
-        uint32_t it[kQStages] = {0, 0};  // PVs issued per tile: p_full phases
-        for (int nt = 0;; ++nt) {
-            const int t = queue.get(nt);
-            if (lane == 0) queue.release(nt);
-            if (t < 0) break;
-            const Task w = decode(t);
-            const int nkv = w.nkv;
-            const int nk[kQStages] = {tile_blocks(w, 0), tile_blocks(w, 1)};  // causal: tile 0 may stop one early
-            mbar_wait(&q_full[0], nt & 1);
-            mbar_wait(&q_full[1], nt & 1);
-            kv.wait_full(st);
-            tmem::fence_after();
-            // QK_s(next task) overwrites S_s, whose P was read by the previous task's last PV_s
-            // (issued before); the first PV_s below overwrites O_s only after the softmax drained it
+                ms.qbase += (uint32_t)(nk[0] + nk[1]);
+            } else {
+                auto qk = [&](int s, int kslot) {  // S_s = Q_s K^T   (mm_ABt, tiles.hpp:349)
+                    mm_ABt(tt_fl<128>{tbase + C::tmem_s(s)}, sQ(sh, s), sKV(sh, kslot));
+                };
+                auto pv = [&](int s, int vslot, bool acc, uint32_t phase) {  // O_s += P_s V (mma_AB)
 #pragma unroll
-            for (int s = 0; s < kQStages; ++s) {
-                qk(s, st.slot);
-                mma_commit(&s_full[s]);
-                if (nk[s] == 1) mma_commit(&q_empty[s]);
-            }
-            mma_commit(&kv.empty[st.slot]);
-            st.advance();
-            for (int i = 1; i < nkv; ++i) {
-                const int vslot = st.slot;
+                    for (int c = 0; c < kPChunks; ++c) {
+                        mbar_wait(&sh.p_full[s][c], phase);
+                        tmem::fence_after();
+                        mma_AB_k<D, kPChunkCols>(tt_fl<D>{tbase + C::tmem_o(s)},
+                                                 tt_bf<kPChunkCols / 2>{tbase + C::tmem_s(s) + 64 + c * (kPChunkCols / 2)},
+                                                 swap_layout(sKV(sh, vslot)), c * kPChunkCols, acc || c > 0);
+                    }
+                };
+                mbar_wait(&sh.q_full[0], nt & 1);
+                mbar_wait(&sh.q_full[1], nt & 1);
                 kv.wait_full(st);
-                st.advance();
-                const int kslot = st.slot;
-                bool k_ready = false;
+                tmem::fence_after();
+                // QK_s(next task) overwrites S_s, whose P was read by the previous task's last PV_s
+                // (issued before); the first PV_s below overwrites O_s only after the softmax drained it
 #pragma unroll
                 for (int s = 0; s < kQStages; ++s) {
-                    if (i > nk[s]) continue;  // tile s is done
-                    pv(s, vslot, i > 1, it[s] & 1);
-                    ++it[s];
-                    if (i == nk[s]) {  // that was tile s's last block
-                        mma_commit(&o_full[s]);
-                        continue;
+                    qk(s, st.slot);
+                    mma_commit(&sh.s_full[s]);
+                    if (nk[s] == 1) mma_commit(&sh.q_empty[s]);
+                }
+                mma_commit(&kv.empty[st.slot]);
+                st.advance();
+                for (int i = 1; i < nkv; ++i) {
+                    const int vslot = st.slot;
+                    kv.wait_full(st);
+                    st.advance();
+                    const int kslot = st.slot;
+                    bool k_ready = false;
+#pragma unroll
+                    for (int s = 0; s < kQStages; ++s) {
+                        if (i > nk[s]) continue;  // tile s is done
+                        pv(s, vslot, i > 1, ms.it[s] & 1);
+                        ++ms.it[s];
+                        if (i == nk[s]) {  // that was tile s's last block
+                            mma_commit(&sh.o_full[s]);
+                            continue;
+                        }
+                        if (!k_ready) {
+                            kv.wait_full(st);
+                            tmem::fence_after();
+                            k_ready = true;
+                        }
+                        qk(s, kslot);
+                        mma_commit(&sh.s_full[s]);
+                        if (i == nk[s] - 1) mma_commit(&sh.q_empty[s]);  // Q_s's last read: the next task's may load
                     }
-                    if (!k_ready) {
-                        kv.wait_full(st);
-                        tmem::fence_after();
-                        k_ready = true;
-                    }
-                    qk(s, kslot);
-                    mma_commit(&s_full[s]);
-                    if (i == nk[s] - 1) mma_commit(&q_empty[s]);  // Q_s's last read: the next task's may load
+                    mma_commit(&kv.empty[vslot]);
+                    mma_commit(&kv.empty[kslot]);
+                    st.advance();
+                }
+                const int vslot = st.slot;
+                kv.wait_full(st);
+#pragma unroll
+                for (int s = 0; s < kQStages; ++s) {
+                    if (nk[s] != nkv) continue;
+                    pv(s, vslot, nkv > 1, ms.it[s] & 1);
+                    ++ms.it[s];
+                    mma_commit(&sh.o_full[s]);
                 }
                 mma_commit(&kv.empty[vslot]);
-                mma_commit(&kv.empty[kslot]);
                 st.advance();
             }
-            const int vslot = st.slot;
-            kv.wait_full(st);
-#pragma unroll
-            for (int s = 0; s < kQStages; ++s) {
-                if (nk[s] != nkv) continue;
-                pv(s, vslot, nkv > 1, it[s] & 1);
-                ++it[s];
-                mma_commit(&o_full[s]);
-            }
-            mma_commit(&kv.empty[vslot]);
-            st.advance();
         }
-        }
-    } else {
-        // ----------------------------- SOFTMAX + FINISH ------------------------------------
-        const int s = warp / 4;                  // query tile of this warpgroup
-        const int wq = warp % 4;                 // TMEM lane quarter
-        const int row_in_tile = wq * 32 + lane;  // == TMEM lane
-        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS_fixed = tbase + lane_off + C::tmem_s(s);
-        const uint32_t tO = tbase + lane_off + C::tmem_o(s);
-        uint32_t qbase = 0;  // k3: QK index of this task's first block
-        uint32_t pvc = 0;    // k3: pv_done completions consumed
-        const float tau = p.scale_log2;
+    };
 
-        uint32_t sc = 0;  // s_full completions seen
-        for (int nt = 0;; ++nt) {
-        const int t = queue.get(nt);
-        __syncwarp();
-        if (lane == 0) queue.release(nt);
-        if (t < 0) break;
-        const Task w = decode(t);
-        const int q0 = w.mblk * kRowsPerCta;
-        const int row = q0 + s * kBlockM + row_in_tile;
-        const int nkv = tile_blocks(w, s);
-        const int head = w.head, batch = w.batch;
-        float m = -INFINITY;  // running max of tau * S (the value actually subtracted)
-        float l = 0.f;        // running normaliser (fp32 sum of fp32 P, kernels.hpp:324)
-        const int nk0 = tile_blocks(w, 0), nk1 = tile_blocks(w, 1);
-        for (int i = 0; i < nkv; ++i) {
-            uint32_t tS = tS_fixed;
-            mbarrier* pf = p_full[s];
-            if constexpr (k3) {
-                const uint32_t gi = qbase + (uint32_t)qk_index(s, i, nk0, nk1);
-                const uint32_t b = gi % 3;
-                mbar_wait(&s_full3[b], (gi / 3) & 1);
-                tS = tbase + lane_off + sbuf_col(b);
-                pf = p_full3[b];
-            } else {
-                mbar_wait(&s_full[s], sc & 1);
-                ++sc;
-            }
-            const uint32_t tP = tS + 64;
-            tmem::fence_after();
-            rt_fl<kBlockN> x;
-            load(x, tS);
-            load_wait(x);
-            const int kv0 = i * kBlockN;
-            const bool need_mask = CAUSAL ? (kv0 + kBlockN - 1 > q0 + s * kBlockM) : (kv0 + kBlockN > n);
-            if (need_mask) {
-                const int lim = CAUSAL ? min(row - kv0, n - 1 - kv0) : (n - 1 - kv0);  // last visible column
-#pragma unroll
-                for (int j = 0; j < kBlockN; ++j)
-                    if (j > lim) x.v[j] = -INFINITY;
-            }
-            float mx = -INFINITY;
-            row_max(mx, x);  // tiles.hpp:290-298
-            const float m_new = fmaxf(m, mx * tau);
-            if (k3 && i > 0) {  // PV_{i-1}(s) done: O_s is stable for the rescale below
-                mbar_wait(&pv_done[s], pvc & 1);
-                ++pvc;
-                tmem::fence_after();
-            }
-            // Rescale lazily: only when some row of the warp grew by > 2^8 (warp-uniform
-            // because tcgen05.ld/st are warp-collective). The final O / l is unchanged.
-            if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
-                const float alpha = ex2_approx(m - m_new);  // exp2(-inf) = 0 on the first tile
-                m = m_new;
-                l *= alpha;
-                if (i > 0) {  // mul_row(o, o, alpha) (tiles.hpp:282-287); PV_{i-1} is complete
-#pragma unroll
-                    for (int c = 0; c < D; c += 32) {
-                        rt_fl<32> o;
-                        load(o, tO + c);
-                        load_wait(o);
-                        mul_row(o, alpha);
-                        tmem::st_32x32b_x32(tO + c, reinterpret_cast<const uint32_t*>(o.v));
-                    }
-                    tmem::wait_st();
-                }
-            }
-            // P = exp2(tau * S - m) (exp2, tiles.hpp:217-219); row_sum over fp32 P (tiles.hpp:301-309);
-            // bf16 RNE copy into TMEM (copy, tiles.hpp:195-200), handed over chunk by chunk
-            const float2 tau2 = make_float2(tau, tau), nm2 = make_float2(-m, -m);
-            float2 l01 = make_float2(0.f, 0.f), l23 = make_float2(0.f, 0.f);  // packed FADD2 row sums
-            uint32_t pk[kBlockN / 2];
-#pragma unroll
-            for (int c = 0; c < kPChunks; ++c) {
-#pragma unroll
-                for (int j = c * kPChunkCols; j < (c + 1) * kPChunkCols; j += 4) {
-                    const float2 xa = fma2(make_float2(x.v[j], x.v[j + 1]), tau2, nm2);
-                    const float2 xb = fma2(make_float2(x.v[j + 2], x.v[j + 3]), tau2, nm2);
-                    const float p0 = ex2_approx(xa.x), p1 = ex2_approx(xa.y);
-                    float p2, p3;
-                    if (((j / 4) % 4) < C::kPolyGroups) {  // part of the exponentials on the FMA pipe
-                        const float2 pb = ex2_poly2(xb);
-                        p2 = pb.x;
-                        p3 = pb.y;
-                    } else {
-                        p2 = ex2_approx(xb.x);
-                        p3 = ex2_approx(xb.y);
-                    }
-                    l01 = add2(l01, make_float2(p0, p1));
-                    l23 = add2(l23, make_float2(p2, p3));
-                    pk[j / 2] = pack_bf16x2(p0, p1);
-                    pk[j / 2 + 1] = pack_bf16x2(p2, p3);
-                }
-                if (c > 0) {  // chunk c-1 is in TMEM: hand it to the MMA warp
-                    tmem::wait_st();
-                    tmem::fence_before();
-                    mbar_arrive(&pf[c - 1]);
-                }
-                if constexpr (kPChunks == 1) {
-                    tmem::st_32x32b_x64(tP, pk);
-                } else if constexpr (kPChunks == 2) {
-                    tmem::st_32x32b_x32(tP + c * 32, pk + c * 32);
+    // ----------------------------- SOFTMAX (compute) + FINISH --------------------------
+    // warps 0-3 / 4-7: the softmax warpgroup of query tile 0 / 1, one thread per row
+    struct consumer {
+        struct state {
+            uint32_t qbase = 0;  // k3: QK index of this task's first block
+            uint32_t pvc = 0;    // k3: pv_done completions consumed
+            uint32_t sc = 0;     // s_full completions seen
+            float m = -INFINITY;  // running max of tau * S (the value actually subtracted)
+            float l = 0.f;        // running normaliser (fp32 sum of fp32 P, kernels.hpp:324)
+        };
+        static TKB_DEVICE void compute(const lcsf::args<attn_fwd_template>& a, state& cs, int t, int nt) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const int s = a.warp / 4;                  // query tile of this warpgroup
+            const int wq = a.warp % 4;                 // TMEM lane quarter
+            const int row_in_tile = wq * 32 + a.lane;  // == TMEM lane
+            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+            const uint32_t tbase = a.tmem;
+            const uint32_t tS_fixed = tbase + lane_off + C::tmem_s(s);
+            const uint32_t tO = tbase + lane_off + C::tmem_o(s);
+            const float tau = p.scale_log2;
+            const int N = p.n;
+            const Task w = decode(p, t);
+            const int q0 = w.mblk * kRowsPerCta;
+            const int row = q0 + s * kBlockM + row_in_tile;
+            const int nkv = tile_blocks(p, w, s);
+            float m = -INFINITY;
+            float l = 0.f;
+            const int nk0 = tile_blocks(p, w, 0), nk1 = tile_blocks(p, w, 1);
+            for (int i = 0; i < nkv; ++i) {
+                uint32_t tS = tS_fixed;
+                mbarrier* pf = sh.p_full[s];
+                if constexpr (k3) {
+                    const uint32_t gi = cs.qbase + (uint32_t)qk_index(s, i, nk0, nk1);
+                    const uint32_t b = gi % 3;
+                    mbar_wait(&sh.s_full3[b], (gi / 3) & 1);
+                    tS = tbase + lane_off + sbuf_col(b);
+                    pf = sh.p_full3[b];
                 } else {
-                    tmem::st_32x32b_x16(tP + c * 16, pk + c * 16);
+                    mbar_wait(&sh.s_full[s], cs.sc & 1);
+                    ++cs.sc;
                 }
+                const uint32_t tP = tS + 64;
+                tmem::fence_after();
+                rt_fl<kBlockN> x;
+                load(x, tS);
+                load_wait(x);
+                const int kv0 = i * kBlockN;
+                const bool need_mask = CAUSAL ? (kv0 + kBlockN - 1 > q0 + s * kBlockM) : (kv0 + kBlockN > N);
+                if (need_mask) {
+                    const int lim = CAUSAL ? min(row - kv0, N - 1 - kv0) : (N - 1 - kv0);  // last visible column
+#pragma unroll
+                    for (int j = 0; j < kBlockN; ++j)
+                        if (j > lim) x.v[j] = -INFINITY;
+                }
+                float mx = -INFINITY;
+                row_max(mx, x);  // tiles.hpp:290-298
+                const float m_new = fmaxf(m, mx * tau);
+                if (k3 && i > 0) {  // PV_{i-1}(s) done: O_s is stable for the rescale below
+                    mbar_wait(&sh.pv_done[s], cs.pvc & 1);
+                    ++cs.pvc;
+                    tmem::fence_after();
+                }
+                // Rescale lazily: only when some row of the warp grew by > 2^8 (warp-uniform
+                // because tcgen05.ld/st are warp-collective). The final O / l is unchanged.
+                if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
+                    const float alpha = ex2_approx(m - m_new);  // exp2(-inf) = 0 on the first tile
+                    m = m_new;
+                    l *= alpha;
+                    if (i > 0) {  // mul_row(o, o, alpha) (tiles.hpp:282-287); PV_{i-1} is complete
+#pragma unroll
+                        for (int c = 0; c < D; c += 32) {
+                            rt_fl<32> o;
+                            load(o, tO + c);
+                            load_wait(o);
+                            mul_row(o, alpha);
+                            store(tO + c, o);
+                        }
+                        tmem::wait_st();
+                    }
+                }
+                // P = exp2(tau * S - m) (exp2, tiles.hpp:217-219); row_sum over fp32 P (tiles.hpp:301-309);
+                // bf16 RNE copy into TMEM (copy, tiles.hpp:195-200), handed over chunk by chunk
+                const float2 tau2 = make_float2(tau, tau), nm2 = make_float2(-m, -m);
+                float2 l01 = make_float2(0.f, 0.f), l23 = make_float2(0.f, 0.f);  // packed FADD2 row sums
+                uint32_t pk[kBlockN / 2];
+#pragma unroll
+                for (int c = 0; c < kPChunks; ++c) {
+#pragma unroll
+                    for (int j = c * kPChunkCols; j < (c + 1) * kPChunkCols; j += 4) {
+                        const float2 xa = fma2(make_float2(x.v[j], x.v[j + 1]), tau2, nm2);
+                        const float2 xb = fma2(make_float2(x.v[j + 2], x.v[j + 3]), tau2, nm2);
+                        const float p0 = ex2_approx(xa.x), p1 = ex2_approx(xa.y);
+                        float p2, p3;
+                        if (((j / 4) % 4) < C::kPolyGroups) {  // part of the exponentials on the FMA pipe
+                            const float2 pb = ex2_poly2(xb);
+                            p2 = pb.x;
+                            p3 = pb.y;
+                        } else {
+                            p2 = ex2_approx(xb.x);
+                            p3 = ex2_approx(xb.y);
+                        }
+                        l01 = add2(l01, make_float2(p0, p1));
+                        l23 = add2(l23, make_float2(p2, p3));
+                        pk[j / 2] = pack_bf16x2(p0, p1);
+                        pk[j / 2 + 1] = pack_bf16x2(p2, p3);
+                    }
+                    if (c > 0) {  // chunk c-1 is in TMEM: hand it to the MMA warp
+                        tmem::wait_st();
+                        tmem::fence_before();
+                        mbar_arrive(&pf[c - 1]);
+                    }
+                    if constexpr (kPChunks == 1) {
+                        tmem::st_32x32b_x64(tP, pk);
+                    } else if constexpr (kPChunks == 2) {
+                        tmem::st_32x32b_x32(tP + c * 32, pk + c * 32);
+                    } else {
+                        tmem::st_32x32b_x16(tP + c * 16, pk + c * 16);
+                    }
+                }
+                l += (l01.x + l01.y) + (l23.x + l23.y);
+                tmem::wait_st();
+                tmem::fence_before();
+                mbar_arrive(&pf[kPChunks - 1]);
             }
-            l += (l01.x + l01.y) + (l23.x + l23.y);
-            tmem::wait_st();
-            tmem::fence_before();
-            mbar_arrive(&pf[kPChunks - 1]);
+            if constexpr (k3) cs.qbase += (uint32_t)(nk0 + nk1);
+            cs.m = m;
+            cs.l = l;
         }
-        if constexpr (k3) qbase += (uint32_t)(nk0 + nk1);
 
         // FINISH (kernels.hpp:335-342): O / l -> bf16 -> this warpgroup's SMEM staging atom ->
         // TMA store (one 64-column atom at a time); plus L for the backward
-        mbar_wait(&o_full[s], nt & 1);
-        if constexpr (k3) {  // the last PV_s's pv_done (complete with o_full)
-            mbar_wait(&pv_done[s], pvc & 1);
-            ++pvc;
-        }
-        tmem::fence_after();
-        if (p.lse != nullptr && row < n)
-            p.lse[(size_t)(batch * p.heads + head) * n + row] = (m + __log2f(l)) * kLn2;
-        const bool leader = (wq == 0 && lane == 0);
+        static TKB_DEVICE void finish(const lcsf::args<attn_fwd_template>& a, state& cs, int t, int nt) {
+            const globals& p = a.g;
+            shared& sh = a.sh;
+            const int s = a.warp / 4;
+            const int wq = a.warp % 4;
+            const int row_in_tile = wq * 32 + a.lane;
+            const uint32_t tO = a.tmem + ((uint32_t)(wq * 32) << 16) + C::tmem_o(s);
+            const Task w = decode(p, t);
+            const int q0 = w.mblk * kRowsPerCta;
+            const int row = q0 + s * kBlockM + row_in_tile;
+            const float m = cs.m, l = cs.l;
+            mbar_wait(&sh.o_full[s], nt & 1);
+            if constexpr (k3) {  // the last PV_s's pv_done (complete with o_full)
+                mbar_wait(&sh.pv_done[s], cs.pvc & 1);
+                ++cs.pvc;
+            }
+            tmem::fence_after();
+            if (p.lse != nullptr && row < p.n)
+                p.lse[(size_t)(w.batch * p.heads + w.head) * p.n + row] = (m + __log2f(l)) * kLn2;
+            const bool leader = (wq == 0 && a.lane == 0);
+            const st_bf<128, 64> stage = sStage(sh, s);
 #pragma unroll 1
-        for (int a = 0; a < Tile::kAtoms; ++a) {
-            rt_fl<32> o0, o1;
-            load(o0, tO + a * 64);
-            load(o1, tO + a * 64 + 32);
-            load_wait(o0);
-            load_wait(o1);
-            if (a == Tile::kAtoms - 1) tmem::fence_before();  // O_s drained: the next task's PV may overwrite it
-            div_row(o0, l);  // tiles.hpp:276-281
-            div_row(o1, l);
-            rt_bf<32> b0, b1;
-            copy(b0, o0);
-            copy(b1, o1);
-            if (leader) tma::wait_group_read<0>();  // the staging atom is free again
-            named_sync(1 + s, WARPGROUP_THREADS);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                sts_v4(smem_u32(sStage[s].chunk(row_in_tile, q)),
-                       make_uint4(b0.v[4 * q], b0.v[4 * q + 1], b0.v[4 * q + 2], b0.v[4 * q + 3]));
-                sts_v4(smem_u32(sStage[s].chunk(row_in_tile, 4 + q)),
-                       make_uint4(b1.v[4 * q], b1.v[4 * q + 1], b1.v[4 * q + 2], b1.v[4 * q + 3]));
-            }
-            tma::fence_async_smem();
-            named_sync(1 + s, WARPGROUP_THREADS);
-            if (leader) {
-                tma::store_4d(gO.tm, sStage[s].ptr, a * 64, q0 + s * kBlockM, head, batch);
-                tma::commit_group();
+            for (int at = 0; at < Tile::kAtoms; ++at) {
+                rt_fl<32> o0, o1;
+                load(o0, tO + at * 64);
+                load(o1, tO + at * 64 + 32);
+                load_wait(o0);
+                load_wait(o1);
+                if (at == Tile::kAtoms - 1) tmem::fence_before();  // O_s drained: the next task's PV may overwrite it
+                div_row(o0, l);  // tiles.hpp:276-281
+                div_row(o1, l);
+                rt_bf<32> b0, b1;
+                copy(b0, o0);
+                copy(b1, o1);
+                if (leader) tma::wait_group_read<0>();  // the staging atom is free again
+                named_sync(1 + s, WARPGROUP_THREADS);
+                store(stage, b0, row_in_tile, 0);  // register -> shared (tiles.hpp:453-459)
+                store(stage, b1, row_in_tile, 32);
+                tma::fence_async_smem();
+                named_sync(1 + s, WARPGROUP_THREADS);
+                if (leader) {
+                    store_async(gl{&p.tm_o}, stage, q0 + s * kBlockM, w.head, w.batch, at * 64);  // shared -> global (TMA)
+                    tma::commit_group();
+                }
             }
         }
-        }  // task loop
-        if (wq == 0 && lane == 0) tma::wait_group<0>();
-    }
-
-    tmem::fence_before();
-    __syncthreads();
-    if (warp == kWarpMma) tmem::dealloc<512>(tbase);
-    if (threadIdx.x == 0) lcsf::queue_exit(p.sched);
-}
+        static TKB_DEVICE void drain(const lcsf::args<attn_fwd_template>& a, state&) {
+            if (a.warp % 4 == 0 && a.lane == 0) tma::wait_group<0>();
+        }
+    };
+};
 
 template <int D, bool CAUSAL>
 int launch(const FwdParams& p, int num_sms, cudaStream_t stream) {
-    using C = Cfg<D>;
-    auto kern = attn_fwd_kernel<D, CAUSAL>;
+    using T = attn_fwd_template<D, CAUSAL>;
+    auto kern = lcsf::kernel<T>;
     static std::atomic<unsigned long long> smem_set{0};  // per instantiation, per device
-    if (int e = ensure_smem(kern, C::kSmemBytes, smem_set)) return e;
-    kern<<<p.tasks < num_sms ? p.tasks : num_sms, kThreads, C::kSmemBytes, stream>>>(p);
+    if (int e = ensure_smem(kern, T::kSmemBytes, smem_set)) return e;
+    kern<<<p.tasks < num_sms ? p.tasks : num_sms, T::kThreads, T::kSmemBytes, stream>>>(p);
     return (int)cudaGetLastError();
 }
 

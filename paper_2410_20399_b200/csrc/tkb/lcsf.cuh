@@ -17,8 +17,28 @@
 //                  from a global atomic counter (dynamic, so heavy causal tasks first
 //                  balance across SMs) and broadcasts them through a 2-slot SMEM ring
 //                  to the other roles; the counter resets itself at grid exit.
+//
+// kernel<T>: the LCSF kernel skeleton (the reference's KernelSpec callbacks,
+// lcsf.hpp:112-161, and the paper's lcf::kernel<attn_fwd_template<D>>),
+// persistent and warp-specialised. A template T supplies the layout and the hooks; the
+// skeleton owns the SMEM carve-up, barrier / queue initialisation, the TMEM allocation, the
+// task queue (claims, broadcast, release), the role dispatch and the grid exit:
+//   using globals; struct shared { ... work_queue queue; uint32_t tmem_slot; }
+//   kThreads, kTmemCols, kProducerWarp, kMmaWarp, kConsumerWarps (warps [0, kConsumerWarps)),
+//   kQueueReaders (MMA warp + consumer warps), kAlignSlack (1024-align the dynamic window
+//   vs. require it aligned), kReleaseEarly (consumers release a task id on reading it, or
+//   after their finish)
+//   static void init(shared&, const globals&)          barrier init, descriptor prefetch
+//   static int num_tasks(const globals&); static int* counter(const globals&)
+//   producer::state, producer::load(args, state&, task, n, claim_next), producer::drain
+//       (the LCSF load stage; claim_next() claims task n + 1 when the hook wants it —
+//        e.g. to warm its inputs in L2 — otherwise the skeleton claims after load returns)
+//   mma::state, mma::issue(args, state&, task, n)       the tensor-core half of compute
+//   consumer::state, consumer::compute(args, state&, task, n), consumer::finish(...),
+//   consumer::drain(args, state&)                        compute (softmax etc.) + finish
 #pragma once
 #include "mbarrier.cuh"
+#include "tcgen05.cuh"
 
 namespace tkb {
 namespace lcsf {
@@ -96,6 +116,95 @@ TKB_DEVICE void queue_exit(int* counter) {
         counter[1] = 0;
         __threadfence();
     }
+}
+
+// Everything a hook sees: the kernel parameters, the SMEM layout, the task queue (to peek at
+// the next task), the TMEM base, and the calling thread's warp / lane.
+template <class T>
+struct args {
+    const typename T::globals& g;
+    typename T::shared& sh;
+    work_queue& queue;
+    uint32_t tmem;
+    int warp, lane;
+};
+
+template <class T>
+__global__ void __launch_bounds__(T::kThreads, 1) kernel(const __grid_constant__ typename T::globals g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = smem_raw;
+    if constexpr (T::kAlignSlack) {
+        base += (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;  // SW128 tiles need 1024-byte alignment
+    } else if ((smem_u32(smem_raw) & 1023u) != 0) {
+        __trap();  // no slack budgeted: the dynamic window must start aligned (no static SMEM)
+    }
+    typename T::shared& sh = *reinterpret_cast<typename T::shared*>(base);
+    const int warp = warpid();
+    const int lane = laneid();
+    if (warp == T::kProducerWarp && lane == 0) {
+        sh.queue.init(T::kQueueReaders);
+        T::init(sh, g);
+        fence_barrier_init();
+    }
+    if (warp == T::kMmaWarp) tmem::alloc<T::kTmemCols>(&sh.tmem_slot);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const args<T> a{g, sh, sh.queue, sh.tmem_slot, warp, lane};
+    int* const counter = T::counter(g);
+    const int total = T::num_tasks(g);
+
+    if (warp == T::kProducerWarp) {
+        // ------------------------------------------------------------- LOAD (producer)
+        if (lane == 0) {
+            typename T::producer::state st{};
+            int n = 0;
+            int t = sh.queue.claim(0, counter, total);
+            while (t >= 0) {
+                int next = -2;
+                auto claim_next = [&]() {
+                    if (next == -2) next = sh.queue.claim(n + 1, counter, total);
+                    return next;
+                };
+                T::producer::load(a, st, t, n, claim_next);
+                t = claim_next();
+                ++n;
+            }
+            T::producer::drain(a, st);
+        }
+    } else if (warp == T::kMmaWarp) {
+        // ------------------------------------------------------------- MMA (converged warp)
+        typename T::mma::state st{};
+        for (int n = 0;; ++n) {
+            const int t = sh.queue.get_warp(n);
+            if (lane == 0) sh.queue.release(n);
+            if (t < 0) break;
+            T::mma::issue(a, st, t, n);
+        }
+    } else if (warp < T::kConsumerWarps) {
+        // ------------------------------------------------------------- COMPUTE + FINISH
+        typename T::consumer::state st{};
+        for (int n = 0;; ++n) {
+            const int t = sh.queue.get_warp(n);
+            if (T::kReleaseEarly) {
+                __syncwarp();
+                if (lane == 0) sh.queue.release(n);
+            }
+            if (t < 0) break;
+            T::consumer::compute(a, st, t, n);
+            T::consumer::finish(a, st, t, n);
+            if (!T::kReleaseEarly) {
+                __syncwarp();
+                if (lane == 0) sh.queue.release(n);
+            }
+        }
+        T::consumer::drain(a, st);
+    }
+
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == T::kMmaWarp) tmem::dealloc<T::kTmemCols>(sh.tmem_slot);
+    if (threadIdx.x == 0) queue_exit(counter);
 }
 
 }  // namespace lcsf

@@ -128,11 +128,13 @@ TKB_DEVICE void load_async(const st_bf<R, C>& dst, const gl& src, mbarrier* bar,
 #pragma unroll
     for (int a = 0; a < st_bf<R, C>::kAtoms; ++a) tma::load_4d(dst.atom(a), src.tm, bar, a * 64, row, head, batch, policy);
 }
+// col0: first column of the tile in the tensor (a multiple of 64) when the tile is narrower
 template <int R, int C>
-TKB_DEVICE void store_async(const gl& dst, const st_bf<R, C>& src, int row, int head, int batch) {
+TKB_DEVICE void store_async(const gl& dst, const st_bf<R, C>& src, int row, int head, int batch, int col0 = 0) {
     static_assert(R == 128, "TMA box is 128 rows");
 #pragma unroll
-    for (int a = 0; a < st_bf<R, C>::kAtoms; ++a) tma::store_4d(dst.tm, src.atom(a), a * 64, row, head, batch);
+    for (int a = 0; a < st_bf<R, C>::kAtoms; ++a)
+        tma::store_4d(dst.tm, src.atom(a), col0 + a * 64, row, head, batch);
 }
 
 // ---- load / store: tt <-> rt (tcgen05.ld / st, warp-collective over the lane quarter)
@@ -156,6 +158,13 @@ TKB_DEVICE void load_wait(rt_fl<N>& dst) {
     if constexpr (N == 64) tmem::wait_ld_x64(reinterpret_cast<uint32_t*>(dst.v));
     if constexpr (N == 32) tmem::wait_ld_x32(reinterpret_cast<uint32_t*>(dst.v));
     if constexpr (N == 16) tmem::wait_ld_x16(reinterpret_cast<uint32_t*>(dst.v));
+}
+// fp32 -> TMEM (N columns), e.g. a rescaled accumulator
+template <int N>
+TKB_DEVICE void store(uint32_t taddr, const rt_fl<N>& src) {
+    static_assert(N == 32 || N == 16, "x32/x16");
+    if constexpr (N == 32) tmem::st_32x32b_x32(taddr, reinterpret_cast<const uint32_t*>(src.v));
+    if constexpr (N == 16) tmem::st_32x32b_x16(taddr, reinterpret_cast<const uint32_t*>(src.v));
 }
 // bf16 pairs -> TMEM (N/2 columns), e.g. a TS-MMA A operand or P over S
 template <int N>
