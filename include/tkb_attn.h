@@ -97,7 +97,19 @@ TKB_API int tkb_attn_validate(const tkb_attn_desc* desc);
 TKB_API int tkb_attn_fwd(const tkb_attn_desc* desc, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* stream);
 
-/* Bytes of caller-provided device workspace the backward needs: two fp32 [B*H, N_pad]
+/* Rotary embedding fused into the forward (one launch): q and k are rotated by the fp32
+ * [seq, head_dim/2] sin / cos tables (the pair (x[p][i], x[p][i + D/2]), as tkb_rotary) into
+ * q_rot ([B, H, N, D], q's strides) and k_rot ([B, Hkv, N, D], k's strides) — which the
+ * backward then takes as its q / k — while the attention of the rotated q, k and v runs in
+ * the same kernel. The workspace (tkb_attn_fwd_rotary_workspace_bytes) holds per-block
+ * flags and must be zero-filled once before its first use, then reused as is; calls that
+ * share a workspace must be stream-ordered. */
+TKB_API size_t tkb_attn_fwd_rotary_workspace_bytes(const tkb_attn_desc* desc);
+TKB_API int tkb_attn_fwd_rotary(const tkb_attn_desc* desc, const void* q, const void* k, const void* v,
+                                const float* sin_tab, const float* cos_tab, void* q_rot, void* k_rot, void* o,
+                                float* lse, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Bytes of caller-provided device workspace the backward needs/* Bytes of caller-provided device workspace the backward needs: two fp32 [B*H, N_pad]
  * vectors, delta = rowsum(dO * O) and -L log2(e) (N_pad = N rounded up to 128). */
 TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* desc);
 

@@ -86,6 +86,8 @@ _SIGS = {
     "tkb_attn_validate": (ctypes.c_int, [ctypes.POINTER(AttnDesc)]),
     "tkb_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP]),
     "tkb_attn_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
+    "tkb_attn_fwd_rotary_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
+    "tkb_attn_fwd_rotary": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
     "tkb_attn_bwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
     "tkb_rotary": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP]),
     "tkb_rotary_qk": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
@@ -260,20 +262,34 @@ def rotary_qk(q, k, sin_tab, cos_tab):
     return qr, kr
 
 
+_rope_ws = {}
+
+
+def _rope_workspace(device, stream, nbytes):
+    """Zero-filled once, then reused: the fused rotary forward's block flags (one buffer per
+    (device, stream), so calls sharing it are stream-ordered as the ABI requires)."""
+    import torch
+
+    key = (device, stream)
+    ws = _rope_ws.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _rope_ws[key] = ws
+    return ws
+
+
 def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None, return_lse=True,
-                  check_finite=False, rotary_tables=None):
+                  check_finite=False, rotary_tables=None, return_rotated=False):
     """O = softmax(scale * Q K^T [causal]) V on the B200; returns (O, L) with L fp32 [B, H, N].
     k, v may carry fewer heads than q (grouped-query / multi-query attention).
-    rotary_tables=(sin, cos) applies the rotary embedding to Q and K first (one extra
-    HBM-bound launch; the rotated tensors are temporaries)."""
+    rotary_tables=(sin, cos) ([N, D/2] fp32) applies the rotary embedding to Q and K inside
+    the same launch (tkb_attn_fwd_rotary); return_rotated=True also returns the rotated
+    (Q, K) — the tensors the backward differentiates against."""
     import torch
 
     _bf16_cuda(q, "q")
     _bf16_cuda(k, "k", q.device)
     _bf16_cuda(v, "v", q.device)
-    _check_kv(q, k, v)
-    if rotary_tables is not None:
-        q, k = rotary_qk(q, k, *rotary_tables)
     st = _bhnd(q, "q")
     hkv, kst = _check_kv(q, k, v)
     B, H, N, D = q.shape
@@ -281,14 +297,29 @@ def attention_fwd(q, k, v, causal=False, softmax_scale=None, out=None, lse=None,
         out = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
     else:
         _out_like(out, "out", q.shape, st, q.device)
-    if return_lse and lse is None:
+    if (return_lse or rotary_tables is not None) and lse is None:
         lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
     if lse is not None:
         _check_lse(lse, B, H, N, q.device)
     cfg = AttentionConfig(B, H, N, D, causal, softmax_scale, check_finite, kv_heads=hkv)
     d = cfg.desc(strides=st, kv_strides=kst)
+    stream = _stream(torch, q.device)
+    if rotary_tables is not None:
+        sin_tab, cos_tab = rotary_tables
+        _tables(sin_tab, cos_tab, N, D, q.device)
+        q_rot = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+        k_rot = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
+        nbytes = int(lib().tkb_attn_fwd_rotary_workspace_bytes(ctypes.byref(d)))
+        ws = _rope_workspace(q.device, stream, nbytes)
+        _check(lib().tkb_attn_fwd_rotary(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                         sin_tab.data_ptr(), cos_tab.data_ptr(), q_rot.data_ptr(), k_rot.data_ptr(),
+                                         out.data_ptr(), lse.data_ptr(), ws.data_ptr(), ws.numel(), stream))
+        res = (out, lse) if return_lse else (out,)
+        if return_rotated:
+            res = res + (q_rot, k_rot)
+        return res if len(res) > 1 else res[0]
     _check(lib().tkb_attn_fwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                              lse.data_ptr() if lse is not None else None, _stream(torch, q.device)))
+                              lse.data_ptr() if lse is not None else None, stream))
     return (out, lse) if return_lse else out
 
 

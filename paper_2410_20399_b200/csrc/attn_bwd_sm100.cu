@@ -249,6 +249,7 @@ struct attn_bwd_dkdv_template {
     static constexpr int kQueueReaders = 1 + 16;
     static constexpr bool kAlignSlack = false;  // no static SMEM: the dynamic window starts 1024-aligned
     static constexpr bool kReleaseEarly = false;
+    static constexpr int kAuxWarps = 0, kAuxWarp0 = 0;
     // D = 64 leaves 128 TMEM columns free: S^T is double-buffered there (the second buffer at
     // column 384), so S^T_{t+1} is issued before dV_t and the exponentials of step t+1 do not
     // wait for the dV GEMM that reads P_t (the D = 64 step is bound by that chain, not by
@@ -959,6 +960,7 @@ struct attn_bwd_dq_template {
     static constexpr int kQueueReaders = 1 + 16;  // the MMA warp and the 16 compute warps
     static constexpr bool kAlignSlack = true;
     static constexpr bool kReleaseEarly = false;
+    static constexpr int kAuxWarps = 0, kAuxWarp0 = 0;
     // D = 64 leaves 128 TMEM columns free: dP is double-buffered there (second buffer at
     // column 384), so dP_{j+1} is issued before dQ_j instead of after it and the dS of step
     // j+1 does not wait for the dQ GEMM that reads dS_j. Per-buffer dp_full / ds_full.

@@ -48,6 +48,19 @@ struct FwdParams {
                                          //   tkb_attn_validate keeps B*H*ceil(N/128) < 2^31)
     int head_group;                      // heads per L2 group       (set by launch_attn_fwd)
     float scale_log2;                    // softmax_scale * log2(e)
+    // Fused rotary prologue (attn_fwd_template<D, Causal, true>): the two aux warps of every
+    // CTA rotate 128-row blocks of Q and K from q_src / k_src into q_rot / k_rot (same
+    // strides; tm_q / tm_k map the rotated copies) and publish each block with a flag set to
+    // `epoch`; the load warp waits for a block's flag before its TMA reads it.
+    const float* sin_tab;                // [N, D/2] fp32
+    const float* cos_tab;
+    const void* q_src;                   // bf16, strides q_sb / q_sh / q_sn
+    const void* k_src;                   // bf16, strides k_sb / k_sh / k_sn
+    void* q_rot;
+    void* k_rot;
+    long long q_sb, q_sh, q_sn, k_sb, k_sh, k_sn;
+    unsigned* flags;                     // [B * Hkv * nq128] K blocks, then [B * H * nq128] Q blocks
+    unsigned epoch;                      // this launch's flag value (never 0)
 };
 
 struct BwdParams {
@@ -113,6 +126,7 @@ struct Params {
 int launch_rotary(const rope::Params& p, int num_sms, cudaStream_t stream);
 
 // Launchers (return cudaError_t as int).
-int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream);
+int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream,
+                    bool rope = false);
 
 }  // namespace tkb

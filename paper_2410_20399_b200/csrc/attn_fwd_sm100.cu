@@ -49,6 +49,9 @@
 #ifndef TKB_FWD_POLY128
 #define TKB_FWD_POLY128 2
 #endif
+#ifndef TKB_ROPE_DEBUG
+#define TKB_ROPE_DEBUG 0  // A/B only: 1 = aux warps publish without rotating, 2 = no flag waits
+#endif
 #ifndef TKB_FWD_PCHUNKS
 #define TKB_FWD_PCHUNKS 2
 #endif
@@ -82,12 +85,19 @@ constexpr int kPChunkCols = kBlockN / kPChunks;  // keys per chunk
 constexpr float kRescaleThreshold = 8.0f;        // log2 units: defer O rescale while max grows < 2^8
 constexpr float kLn2 = 0.69314718055994530942f;
 
-template <int D, bool CAUSAL>
+// ROPE: the fused rotary prologue (rotary_kernel, kernels.hpp:357-513): two aux warps per
+// CTA rotate Q and K into q_rot / k_rot block by block, ahead of and overlapped with the
+// attention tasks (the same pass over Q / K a separate rotary launch would make, but its
+// HBM traffic and issue slots now hide under the tensor-bound attention); the load warp
+// TMA-reads a rotated block once its flag carries this launch's epoch.
+template <int D, bool CAUSAL, bool ROPE = false>
 struct attn_fwd_template {
     using C = Cfg<D>;
     using Tile = typename C::Tile;
     using globals = FwdParams;
-    static constexpr int kThreads = fwd::kThreads;
+    static constexpr int kAuxWarps = ROPE ? 2 : 0;
+    static constexpr int kAuxWarp0 = 10;
+    static constexpr int kThreads = fwd::kThreads + 32 * kAuxWarps;
     static constexpr int kTmemCols = 512;
     static constexpr int kProducerWarp = kWarpLoad;
     static constexpr int kMmaWarp = fwd::kWarpMma;
@@ -153,6 +163,10 @@ struct attn_fwd_template {
     static TKB_DEVICE uint32_t sbuf_col(uint32_t b) { return b == 0 ? 0u : (b == 1 ? 128u : 384u); }
 
     static TKB_DEVICE int num_tasks(const globals& p) { return p.tasks; }
+    // K-block flags come first in p.flags: B * Hkv * nq128 of them
+    static TKB_DEVICE size_t rope_kflags(const globals& p) {
+        return (size_t)(p.bh / p.heads) * (p.heads / p.group) * ((p.n + 127) / 128);
+    }
     static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
 
     static TKB_DEVICE void init(shared& sh, const globals& p) {
@@ -190,6 +204,11 @@ struct attn_fwd_template {
             const gl gQ{&p.tm_q}, gK{&p.tm_k}, gV{&p.tm_v};
             const Task w = decode(p, t);
             const int q0 = w.mblk * kRowsPerCta;
+            const int nq = (p.n + 127) / 128;
+            const int bkv = w.batch * (p.heads / p.group) + w.head / p.group;
+            if constexpr (ROPE && TKB_ROPE_DEBUG != 2)  // the task's rotated Q blocks (rows past N: none)
+                lcsf::flags_wait_all(p.flags + rope_kflags(p) + (size_t)(w.batch * p.heads + w.head) * nq + 2 * w.mblk,
+                                     min(2, nq - 2 * w.mblk), p.epoch);
             for (int s = 0; s < kQStages; ++s) {  // Q_s is free once the last QK_s of the previous task retired
                 mbar_wait(&sh.q_empty[s], (nt & 1) ^ 1u);
                 mbar_arrive_expect_tx(&sh.q_full[s], C::kTile);
@@ -203,6 +222,8 @@ struct attn_fwd_template {
                         tma::prefetch_4d(gQ.tm, at * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.batch);
             }
             for (int i = 0; i < w.nkv; ++i) {
+                if constexpr (ROPE && TKB_ROPE_DEBUG != 2)
+                    lcsf::flag_wait(p.flags + (size_t)bkv * nq + i, p.epoch);  // rotated K block
 #pragma unroll
                 for (int which = 0; which < 2; ++which) {
                     sh.kv_ring.wait_empty(ps.st);
@@ -552,11 +573,105 @@ struct attn_fwd_template {
             if (a.warp % 4 == 0 && a.lane == 0) tma::wait_group<0>();
         }
     };
+
+    // ----------------------------- AUX: the fused rotary prologue ---------------------
+    // Work items = (batch, up to 4 heads, 128-row block), claimed from counter[3] batch by
+    // batch (K items of a batch before its Q items, the attention's consumption order); one
+    // warp rotates an item: lane = (row, 8-pair chunk) and, per (row, chunk), the sin / cos
+    // table entries are loaded once and applied to all of the item's heads (the tables do
+    // not depend on the head), with every load of the step issued before any math. fp32 math
+    // on the bf16 inputs and fp32 tables, bf16 RNE out: the separate tkb_rotary kernel's
+    // arithmetic (oracle_rotary, oracles.hpp:66-90), so both paths agree bit for bit.
+    static constexpr int kRopeHeads = 4;
+    struct aux {
+        static TKB_DEVICE void run(const lcsf::args<attn_fwd_template>& a, int) {
+            if constexpr (ROPE) {
+                const globals& p = a.g;
+                const int lane = a.lane;
+                const int N = p.n;
+                const int nq = (N + 127) / 128;
+                const int H = p.heads, hkv = H / p.group, B = p.bh / H;
+                const int q4 = (H + kRopeHeads - 1) / kRopeHeads, k4 = (hkv + kRopeHeads - 1) / kRopeHeads;
+                const int per_batch = (q4 + k4) * nq;
+                const int items = B * per_batch;
+                constexpr int half = D / 2;
+                constexpr int kChunks = D / 16;          // 8-pair chunks per row
+                constexpr int kRowsPerPass = 32 / kChunks;
+                const int c = lane % kChunks;
+                for (;;) {
+                    int it = 0;
+                    if (lane == 0) it = atomicAdd(p.sched + 3, 1);
+                    it = __shfl_sync(0xffffffffu, it, 0);
+                    if (it >= items) break;
+                    const int b = it / per_batch;
+                    int r = it - b * per_batch;
+                    const bool is_k = r < k4 * nq;
+                    if (!is_k) r -= k4 * nq;
+                    const int quad = r / nq;
+                    // causal: a head's heavy (late) Q blocks first, as the attention claims them
+                    const int blk = (!is_k && CAUSAL) ? nq - 1 - (r - quad * nq) : r - quad * nq;
+                    const int h0 = quad * kRopeHeads;
+                    const int nh = min(kRopeHeads, (is_k ? hkv : H) - h0);
+                    const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(is_k ? p.k_src : p.q_src);
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(is_k ? p.k_rot : p.q_rot);
+                    const long long sb = is_k ? p.k_sb : p.q_sb, shd = is_k ? p.k_sh : p.q_sh,
+                                    sn = is_k ? p.k_sn : p.q_sn;
+                    const int row_end = TKB_ROPE_DEBUG == 1 ? 0 : min(N, blk * 128 + 128);
+                    for (int row = blk * 128 + lane / kChunks; row < row_end; row += kRowsPerPass) {
+                        const float4* sp = reinterpret_cast<const float4*>(p.sin_tab + (size_t)row * half + 8 * c);
+                        const float4* cp = reinterpret_cast<const float4*>(p.cos_tab + (size_t)row * half + 8 * c);
+                        const long long base = b * sb + row * sn + 8 * c;
+                        uint4 x1[kRopeHeads], x2[kRopeHeads];
+#pragma unroll
+                        for (int j = 0; j < kRopeHeads; ++j) {
+                            if (j < nh) {
+                                const __nv_bfloat16* xr = src + base + (h0 + j) * shd;
+                                x1[j] = *reinterpret_cast<const uint4*>(xr);
+                                x2[j] = *reinterpret_cast<const uint4*>(xr + half);
+                            }
+                        }
+                        const float4 s0 = __ldg(sp), s1 = __ldg(sp + 1), c0 = __ldg(cp), c1 = __ldg(cp + 1);
+                        const float sn8[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                        const float cs8[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                        for (int j = 0; j < kRopeHeads; ++j) {
+                            if (j >= nh) continue;
+                            const uint32_t av[4] = {x1[j].x, x1[j].y, x1[j].z, x1[j].w};
+                            const uint32_t bv[4] = {x2[j].x, x2[j].y, x2[j].z, x2[j].w};
+                            uint32_t o1[4], o2[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {  // packed f32x2: the same roundings as fmaf(x1, c, -(x2 s))
+                                const float2 u = make_float2(__uint_as_float(av[q] << 16), __uint_as_float(av[q] & 0xFFFF0000u));
+                                const float2 v = make_float2(__uint_as_float(bv[q] << 16), __uint_as_float(bv[q] & 0xFFFF0000u));
+                                const float2 sp2 = make_float2(sn8[2 * q], sn8[2 * q + 1]);
+                                const float2 cp2 = make_float2(cs8[2 * q], cs8[2 * q + 1]);
+                                const float2 vs = mul2(v, sp2), us = mul2(u, sp2);
+                                const float2 r1 = fma2(u, cp2, make_float2(-vs.x, -vs.y));
+                                const float2 r2 = fma2(v, cp2, us);
+                                o1[q] = pack_bf16x2(r1.x, r1.y);
+                                o2[q] = pack_bf16x2(r2.x, r2.y);
+                            }
+                            __nv_bfloat16* orow = dst + base + (h0 + j) * shd;
+                            *reinterpret_cast<uint4*>(orow) = make_uint4(o1[0], o1[1], o1[2], o1[3]);
+                            *reinterpret_cast<uint4*>(orow + half) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+                        }
+                    }
+                    lcsf::flag_writer_fence();
+                    __syncwarp();
+                    if (lane < nh) {
+                        const size_t f = is_k ? (size_t)(b * hkv + h0 + lane) * nq + blk
+                                              : rope_kflags(p) + (size_t)(b * H + h0 + lane) * nq + blk;
+                        lcsf::flag_publish(p.flags + f, p.epoch);
+                    }
+                }
+            }
+        }
+    };
 };
 
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, bool ROPE>
 int launch(const FwdParams& p, int num_sms, cudaStream_t stream) {
-    using T = attn_fwd_template<D, CAUSAL>;
+    using T = attn_fwd_template<D, CAUSAL, ROPE>;
     auto kern = lcsf::kernel<T>;
     static std::atomic<unsigned long long> smem_set{0};  // per instantiation, per device
     if (int e = ensure_smem(kern, T::kSmemBytes, smem_set)) return e;
@@ -567,16 +682,25 @@ int launch(const FwdParams& p, int num_sms, cudaStream_t stream) {
 }  // namespace fwd
 
 // Fills the persistent task fields of p and launches one CTA per SM (at most one per task).
-int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream) {
+// rope: the fused rotary prologue (attn_fwd_template<D, Causal, true>).
+int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream,
+                    bool rope) {
     p.bh = batches * p.heads;
     p.m_blocks = (p.n + kRowsPerCta - 1) / kRowsPerCta;
     p.tasks = p.bh * p.m_blocks;
     const long long kv_bytes = 4ll * p.n * head_dim / p.group;  // K / V of one query head's kv head
     long long g = (48ll << 20) / (kv_bytes > 0 ? kv_bytes : 1);  // heads whose K / V fit ~48 MB of L2
     p.head_group = (int)(g < 1 ? 1 : (g > p.bh ? p.bh : g));
+    if (rope) {
+        if (head_dim == 128)
+            return causal ? fwd::launch<128, true, true>(p, num_sms, stream)
+                          : fwd::launch<128, false, true>(p, num_sms, stream);
+        return causal ? fwd::launch<64, true, true>(p, num_sms, stream) : fwd::launch<64, false, true>(p, num_sms, stream);
+    }
     if (head_dim == 128)
-        return causal ? fwd::launch<128, true>(p, num_sms, stream) : fwd::launch<128, false>(p, num_sms, stream);
-    return causal ? fwd::launch<64, true>(p, num_sms, stream) : fwd::launch<64, false>(p, num_sms, stream);
+        return causal ? fwd::launch<128, true, false>(p, num_sms, stream)
+                      : fwd::launch<128, false, false>(p, num_sms, stream);
+    return causal ? fwd::launch<64, true, false>(p, num_sms, stream) : fwd::launch<64, false, false>(p, num_sms, stream);
 }
 
 }  // namespace tkb

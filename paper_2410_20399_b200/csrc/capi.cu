@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -334,6 +335,78 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.scale_log2 = scale_of(d) * 1.44269504088896340736f;
     int e = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd launch: ") + cudaGetErrorString((cudaError_t)e));
+    g_launches = 1;
+    return TKB_OK;
+}
+
+// Fused rotary + forward (the rotary prologue of SURVEY §8(f) rank 2 folded into the forward
+// launch): flags of the rotated blocks live in a caller-provided workspace that must be zero
+// once before its first use; every launch publishes a new epoch, so it is never cleared again.
+TKB_API size_t tkb_attn_fwd_rotary_workspace_bytes(const tkb_attn_desc* d) {
+    if (!d || d->seq < 1 || d->batches < 1 || d->heads < 1) return 0;
+    const size_t nq = (size_t)(d->seq + 127) / 128;
+    const size_t hkv = (size_t)kv_heads_of(d);
+    const size_t bytes = 4 * nq * (size_t)d->batches * (hkv + (size_t)d->heads);
+    return (bytes + 255) & ~(size_t)255;
+}
+
+TKB_API int tkb_attn_fwd_rotary(const tkb_attn_desc* d, const void* q, const void* k, const void* v,
+                                const float* sin_tab, const float* cos_tab, void* q_rot, void* k_rot, void* o,
+                                float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    int rc = tkb_attn_validate(d);
+    if (rc) return rc;
+    if (!q || !k || !v || !o || !sin_tab || !cos_tab || !q_rot || !k_rot || !workspace)
+        return fail(TKB_ERR_BOUNDS, "null pointer");
+    if (workspace_bytes < tkb_attn_fwd_rotary_workspace_bytes(d)) return fail(TKB_ERR_BOUNDS, "workspace too small");
+    if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)q_rot | (uintptr_t)k_rot |
+         (uintptr_t)sin_tab | (uintptr_t)cos_tab | (uintptr_t)workspace) &
+        15)
+        return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
+    if (q_rot == q || k_rot == k) return fail(TKB_ERR_CONFIG, "q_rot / k_rot must not alias q / k");
+    if ((rc = check_device())) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const Strides s = strides_of(d);
+    const Strides skv = kv_strides_of(d);
+    const int hkv = kv_heads_of(d);
+    int sms = 0, *slot = nullptr;
+    if ((rc = device_state(st, &sms, &slot))) return rc;
+    if (d->check_finite) {
+        const void* qp[1] = {q};
+        const void* kvp[2] = {k, v};
+        if ((rc = finite_check(d, qp, 1, s, d->heads, slot, st)) ||
+            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st)))
+            return rc;
+    }
+    tkb::FwdParams p{};
+    // the attention reads the rotated copies through TMA
+    if ((rc = make_bhnd_map(&p.tm_q, q_rot, d, s)) || (rc = make_bhnd_map(&p.tm_k, k_rot, d, skv, hkv)) ||
+        (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
+        return rc;
+    p.group = d->heads / hkv;
+    p.sched = slot;
+    p.lse = lse;
+    p.trace = g_trace;
+    p.trace_every = g_trace_every;
+    p.trace_slots = g_trace_slots;
+    p.n = d->seq;
+    p.heads = d->heads;
+    p.scale_log2 = scale_of(d) * 1.44269504088896340736f;
+    p.sin_tab = sin_tab;
+    p.cos_tab = cos_tab;
+    p.q_src = q;
+    p.k_src = k;
+    p.q_rot = q_rot;
+    p.k_rot = k_rot;
+    p.q_sb = s.b, p.q_sh = s.h, p.q_sn = s.n;
+    p.k_sb = skv.b, p.k_sh = skv.h, p.k_sn = skv.n;
+    p.flags = reinterpret_cast<unsigned*>(workspace);
+    static std::atomic<unsigned> epoch{0};
+    unsigned e = epoch.fetch_add(1) + 1;
+    if (e == 0) e = epoch.fetch_add(1) + 1;  // 0 is the zeroed workspace: never a live epoch
+    p.epoch = e;
+    const int err = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st, true);
+    if (err != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd (rotary) launch: ") + cudaGetErrorString((cudaError_t)err));
     g_launches = 1;
     return TKB_OK;
 }

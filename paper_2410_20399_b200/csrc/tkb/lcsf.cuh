@@ -36,6 +36,8 @@
 //   mma::state, mma::issue(args, state&, task, n)       the tensor-core half of compute
 //   consumer::state, consumer::compute(args, state&, task, n), consumer::finish(...),
 //   consumer::drain(args, state&)                        compute (softmax etc.) + finish
+//   kAuxWarps, kAuxWarp0, aux::run(args, index)         optional warps outside the task queue
+//                                                        (e.g. a prologue producing inputs)
 #pragma once
 #include "mbarrier.cuh"
 #include "tcgen05.cuh"
@@ -108,14 +110,73 @@ struct work_queue {
 };
 
 // Grid exit: the last CTA resets the task counter so the next launch starts at zero.
-// counter[0] = claims beyond the grid, counter[1] = CTAs finished.
+// counter[0] = claims beyond the grid, counter[1] = CTAs finished, counter[3] = a second
+// (auxiliary) work counter some kernels use (the fused rotary prologue's block claims).
 TKB_DEVICE void queue_exit(int* counter) {
     __threadfence();
     if (atomicAdd(&counter[1], 1) == (int)gridDim.x - 1) {
         counter[0] = 0;
         counter[1] = 0;
+        counter[3] = 0;
         __threadfence();
     }
+}
+
+// Cross-CTA block flags (a producer publishes a global-memory block for other CTAs' TMA
+// loads): the writer's generic-proxy stores are made visible to the async proxy and the
+// flag is a gpu-scope release; the reader acquires the flag, then fences the async proxy
+// before its TMA reads the block. The wait is bounded like mbar_wait (TKB_DEADLOCK_NS).
+// writer: every thread that wrote part of the block calls flag_writer_fence(), then the warp
+// syncs, then one thread publishes (the release is cumulative over the synced writes)
+TKB_DEVICE void flag_writer_fence() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+TKB_DEVICE void flag_publish(unsigned* f, unsigned v) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+TKB_DEVICE unsigned flag_load(const unsigned* f) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+TKB_DEVICE void flag_wait(const unsigned* f, unsigned v) {
+    if (flag_load(f) != v) {
+        uint64_t t0 = globaltimer_ns();
+        while (flag_load(f) != v) {
+#ifndef TKB_NO_DEADLOCK_TRAP
+            if (globaltimer_ns() - t0 > (uint64_t)(TKB_DEADLOCK_NS)) __trap();
+#endif
+            __nanosleep(64);
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Wait for a run of flags [f, f + n) to all carry v: relaxed polls (up to 16 in flight per
+// round), then one acquire fence for the lot — one L2 round trip per round instead of one
+// per flag.
+TKB_DEVICE void flags_wait_all(const unsigned* f, int n, unsigned v) {
+    uint64_t t0 = 0;
+    for (int i0 = 0; i0 < n;) {
+        unsigned x[16];
+        const int m = min(16, n - i0);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < m) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x[j]) : "l"(f + i0 + j) : "memory");
+        int ok = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) ok += (j < m && x[j] == v) ? 1 : 0;
+        if (ok == m) {
+            i0 += m;
+            continue;
+        }
+        if (t0 == 0) t0 = globaltimer_ns();
+#ifndef TKB_NO_DEADLOCK_TRAP
+        else if (globaltimer_ns() - t0 > (uint64_t)(TKB_DEADLOCK_NS)) __trap();
+#endif
+        __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Everything a hook sees: the kernel parameters, the SMEM layout, the task queue (to peek at
@@ -199,6 +260,9 @@ __global__ void __launch_bounds__(T::kThreads, 1) kernel(const __grid_constant__
             }
         }
         T::consumer::drain(a, st);
+    }
+    if constexpr (T::kAuxWarps > 0) {
+        if (warp >= T::kAuxWarp0 && warp < T::kAuxWarp0 + T::kAuxWarps) T::aux::run(a, warp - T::kAuxWarp0);
     }
 
     tmem::fence_before();

@@ -113,3 +113,54 @@ def test_attention_with_rotary_prologue(cuda_dev, causal):
     got = o.float().cpu().numpy().reshape(-1, N, D)
     assert orc.max_abs(got, ro) <= 2e-2 and orc.rel_l2(got, ro) <= 1e-2
     assert orc.max_abs(lse.cpu().numpy().reshape(-1, N), rl) <= 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,H,HKV,N,D,causal", [(2, 4, 4, 1000, 128, True), (1, 8, 2, 200, 64, False),
+                                                (2, 8, 1, 4096, 128, True), (1, 2, 2, 129, 64, True)])
+def test_fused_rotary_forward_equals_the_two_launch_path(cuda_dev, B, H, HKV, N, D, causal):
+    """tkb_attn_fwd_rotary (one launch: the aux warps rotate Q / K block by block while the
+    attention of the rotated blocks runs) gives bit-identical rotated Q / K to tkb_rotary_qk
+    and bit-identical O / L to tkb_attn_fwd on them; repeated calls (new epochs over the same
+    flag workspace) stay identical."""
+    from paper_2410_20399_b200 import attention as A
+
+    g = torch.Generator(device="cuda").manual_seed(N + D)
+    q = torch.empty(B, H, N, D, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1, generator=g)
+    k = torch.empty(B, HKV, N, D, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1, generator=g)
+    v = torch.empty(B, HKV, N, D, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1, generator=g)
+    pos = torch.arange(N, device="cuda", dtype=torch.float64)[:, None]
+    freq = 10000.0 ** (-torch.arange(D // 2, device="cuda", dtype=torch.float64) / (D // 2))
+    sin, cos = (f(pos * freq[None, :]).float().contiguous() for f in (torch.sin, torch.cos))
+    qr, kr = A.rotary_qk(q, k, sin, cos)
+    o_ref, l_ref = A.attention_fwd(qr, kr, v, causal=causal)
+    for _ in range(3):
+        o, lse, q_rot, k_rot = A.attention_fwd(q, k, v, causal=causal, rotary_tables=(sin, cos), return_rotated=True)
+        torch.cuda.synchronize()
+        assert torch.equal(q_rot, qr) and torch.equal(k_rot, kr)
+        assert torch.equal(o, o_ref) and torch.equal(lse, l_ref)
+
+
+@pytest.mark.gpu
+def test_fused_rotary_backward_chain(cuda_dev):
+    """Training with the fused prologue: the backward runs on the rotated Q / K the forward
+    returned (dQ, dK are gradients w.r.t. the rotated tensors) and matches the oracle."""
+    from paper_2410_20399_b200 import attention as A
+
+    B, H, N, D = 1, 2, 300, 64
+    q = orc.fill(60, B * H * N * D).reshape(B, H, N, D)
+    k = orc.fill(61, B * H * N * D).reshape(B, H, N, D)
+    v = orc.fill(62, B * H * N * D).reshape(B, H, N, D)
+    do = orc.fill(63, B * H * N * D).reshape(B, H, N, D)
+    ang = np.arange(N)[:, None] * (10000.0 ** (-np.arange(D // 2) / (D // 2)))[None, :]
+    s, c = np.sin(ang).astype(np.float32), np.cos(ang).astype(np.float32)
+    o, lse, qr, kr = A.attention_fwd(_dev(q), _dev(k), _dev(v), causal=True,
+                                      rotary_tables=(_dev(s, torch.float32), _dev(c, torch.float32)),
+                                      return_rotated=True)
+    dq, dk, dv = A.attention_bwd(qr, kr, _dev(v), o, _dev(do), lse, causal=True)
+    torch.cuda.synchronize()
+    rq, rk = qr.float().cpu().numpy(), kr.float().cpu().numpy()
+    rdq, rdk, rdv = orc.attn_bwd(rq, rk, v, do, causal=True)
+    for got, ref in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        g = got.float().cpu().numpy()
+        assert orc.max_abs(g, ref) <= 2e-2 and orc.rel_l2(g, ref) <= 1e-2
