@@ -222,8 +222,9 @@ struct attn_fwd_template {
                         tma::prefetch_4d(gQ.tm, at * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.batch);
             }
             for (int i = 0; i < w.nkv; ++i) {
-                if constexpr (ROPE && TKB_ROPE_DEBUG != 2)
-                    lcsf::flag_wait(p.flags + (size_t)bkv * nq + i, p.epoch);  // rotated K block
+                // the rotated K block (checking 8 blocks at a time, or the whole task's range at
+                // its start, measured slower: the load warp then waits for blocks it does not need yet)
+                if constexpr (ROPE && TKB_ROPE_DEBUG != 2) lcsf::flag_wait(p.flags + (size_t)bkv * nq + i, p.epoch);
 #pragma unroll
                 for (int which = 0; which < 2; ++which) {
                     sh.kv_ring.wait_empty(ps.st);
