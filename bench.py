@@ -227,11 +227,26 @@ def run_reference(args):
     return 0
 
 
+L2_BYTES = 126 * 2 ** 20
+
+
+def needs_flush(args):
+    """Inputs that fit in L2 get an L2 flush between timed steps (timing rules)."""
+    return 4 * args.batch * args.heads * args.seq * args.head_dim * 2 < 2 * L2_BYTES
+
+
 def workload_config(args, world):
+    shape = (args.batch, args.heads, args.seq, args.head_dim)
+    named = {(16, 16, 4096, 128): "BASELINE configs[1]+[2]", (1, 8, 1024, 64): "BASELINE configs[0]",
+             (32, 32, 16384, 128): "BASELINE configs[4] per GPU at N=1 (1/8 of it per GPU at 8 GPUs: B=4)",
+             (4, 32, 16384, 128): "BASELINE configs[4] per-GPU shard at 8 GPUs"}.get(shape, "BASELINE configs[3] sweep point"
+                                                                                  if args.heads == 16 and args.batch == 16
+                                                                                  else "custom")
+    tensor_mb = args.batch * args.heads * args.seq * args.head_dim * 2 / 2 ** 20
     return {
         "workload": f"attention {'fwd+bwd' if args.which == 'fwdbwd' else args.which} "
                     f"{'causal' if args.causal else 'non-causal'} B={args.batch}/GPU H={args.heads} "
-                    f"N={args.seq} D={args.head_dim} bf16 (BASELINE configs[1]+[2])",
+                    f"N={args.seq} D={args.head_dim} bf16 ({named})",
         "batch_per_gpu": args.batch,
         "global_batch": args.batch * world,
         "heads": args.heads,
@@ -239,7 +254,9 @@ def workload_config(args, world):
         "head_dim": args.head_dim,
         "causal": bool(args.causal),
         "parallelism": f"bh-shard{world}",
-        "l2": "inputs larger than L2 (268 MB per tensor); no flush",
+        "l2": (f"L2 flushed between timed steps (inputs {tensor_mb:.1f} MB per tensor fit in the 126 MB L2); "
+               "value = sum of the steps' own device time" if needs_flush(args)
+               else f"inputs larger than L2 ({tensor_mb:.0f} MB per tensor); no flush"),
     }
 
 
@@ -290,15 +307,24 @@ def main():
     which = args.which
 
     launches = {"n": 0}
+    marks = []  # in-step CUDA events (timed region only): [before fwd, between, after bwd] per step
 
-    def step():
+    def step(mark=False):
         cnt = 0
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if mark else None
+        if mark:
+            evs[0].record(stream)
         if "fwd" in which:
             A.attention_fwd(q, k, v, causal=causal, out=o, lse=lse)
             cnt += A.last_launch_count()
+        if mark:
+            evs[1].record(stream)
         if "bwd" in which:
             A.attention_bwd(q, k, v, o, do, lse, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws)
             cnt += A.last_launch_count()
+        if mark:
+            evs[2].record(stream)
+            marks.append(evs)
         launches["n"] += cnt
 
     if "bwd" in which and "fwd" not in which:
@@ -349,14 +375,20 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
+        flush = needs_flush(args)
+        scrub = torch.empty(2 * L2_BYTES // 4, device=dev, dtype=torch.float32) if flush else None
         start.record(stream)
         for _ in range(args.steps):
-            step()
+            if flush:
+                scrub.fill_(1.0)  # evict the inputs from L2 (outside the step's own events)
+            step(mark=True)
         end.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
+    if needs_flush(args):  # the steps' own device time, flushes excluded
+        ms = sum(m[0].elapsed_time(m[2]) for m in marks)
     t = torch.tensor([ms], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # timing only (gloo, CPU), not on the data path
@@ -460,11 +492,38 @@ def main():
             peak = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
             unit = "GB/s"
         per_kernel = {}
+        io_bytes = {"attn_fwd": 8 * my_units * n * d + 4 * my_units * n,  # SURVEY §8(d) algorithmic bytes
+                    "attn_bwd_dkdv": 0, "attn_bwd_dq": 0, "bwd_prep": work["bwd_prep"][1]}
         for kname, ms_k in kern_ms.items():
             b_k, amt = work[kname]
             rate = amt / (ms_k / 1e3) / (1e12 if b_k == "tensor" else 1e9)
             per_kernel[kname] = {"ms": ms_k, "bound": b_k, "achieved": rate,
                                  "unit": "TFLOP/s" if b_k == "tensor" else "GB/s"}
+            if kname == "attn_fwd":  # memory side of the forward (short sequences are HBM / latency bound)
+                per_kernel[kname]["us"] = ms_k * 1e3
+                per_kernel[kname]["algorithmic_gbs"] = io_bytes[kname] / (ms_k / 1e3) / 1e9
+        # In-step times: the forward and backward calls of the timed steps themselves (events
+        # between the calls), against the measured peak sustained under this load; the dominant
+        # kernel's in-step time is its share of its pass from the isolated (burst) timings.
+        in_step = None
+        if marks:
+            fwd_in = statistics.mean(m[0].elapsed_time(m[1]) for m in marks)
+            bwd_in = statistics.mean(m[1].elapsed_time(m[2]) for m in marks)
+            in_step = {"attn_fwd_ms": fwd_in, "bwd_ms": bwd_in}
+            bwd_iso = sum(kern_ms.get(x, 0.0) for x in ("bwd_prep", "attn_bwd_dkdv", "attn_bwd_dq"))
+            dom_in = (fwd_in if dom == "attn_fwd" else bwd_in * kern_ms[dom] / bwd_iso) if (
+                dom == "attn_fwd" or bwd_iso > 0) else None
+            if dom_in and bound == "tensor":
+                sust = float(peaks.get("bf16_tflops_sustained", 1400.0))
+                ach_in = amount / (dom_in / 1e3) / 1e12
+                in_step.update({"dominant_ms": dom_in, "dominant_achieved": ach_in,
+                                "dominant_frac_of_burst": ach_in / peak, "dominant_frac_of_sustained": ach_in / sust})
+            if "fwd" in which and fwd_in > 0:
+                in_step["fwd_tflops"] = flops(1, my_units, n, d, causal, "fwd") / (fwd_in / 1e3) / 1e12
+            if "bwd" in which and bwd_in > 0:
+                bt = flops(1, my_units, n, d, causal, "bwd") / (bwd_in / 1e3) / 1e12
+                in_step["bwd_tflops"] = bt
+                in_step["bwd_frac_of_sustained"] = bt / float(peaks.get("bf16_tflops_sustained", 1400.0))
         roofline = {
             "bound": bound,
             "kernel": dom,
@@ -480,6 +539,8 @@ def main():
                                   if bound == "tensor" else None),
             "traffic": load_traffic(dom),
             "per_kernel": per_kernel,
+            "per_kernel_timing": "isolated launches before the soak (burst clocks)",
+            "in_step": in_step,
         }
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -575,7 +636,8 @@ def load_traffic(kernel):
         with open(p) as f:
             t = json.load(f)
         # logical kernel -> the symbol ncu reports (dK/dV runs as the persistent kernel)
-        sym = {"attn_bwd_dkdv": "attn_bwd_dkdvp_kernel"}.get(kernel, kernel + "_kernel")
+        sym = {"attn_bwd_dkdv": "attn_bwd_dkdv_template", "attn_fwd": "attn_fwd_template",
+               "attn_bwd_dq": "attn_bwd_dq_template"}.get(kernel, kernel + "_kernel")
         return t.get(sym, t.get(kernel))
     except Exception:
         return None

@@ -1,4 +1,6 @@
 set -x
-timeout 300 python -m pytest tests/test_primitives_gpu.py -q -x 2>&1 | tail -3
-timeout 900 python -m pytest tests -q -m gpu -x -k "bwd or fuzz or gqa or long or pairs or cpp or smoke" 2>&1 | tail -5
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_r2b.log 2>&1; tail -1 gpurun_out/bench_r2b.log
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu --durations=5 > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -8 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/smoke.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo bench rc=$?; tail -1 gpurun_out/bench.log

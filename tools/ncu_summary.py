@@ -52,8 +52,11 @@ def main(rep, launches, tag):
     seen = set()
     for d, u in rows:
         name = d.get("Kernel Name", "?")
-        short = name.split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
-        key = f"{short}<{name.split('<')[1].split('>')[0]}>" if "<" in name else short
+        # lcsf::kernel<attn_fwd_template<128, 1, 0>> -> attn_fwd_template<128, 1, 0>
+        inner = name.split("kernel<", 1)[1] if name.startswith("void kernel<") or "::kernel<" in name else name
+        base = inner.split("(")[0].replace("void ", "")
+        short = base.split("::")[-1].split("<")[0]
+        key = f"{short}<{base.split('<')[1].split('>')[0]}>" if "<" in base else short
         if key in seen:
             continue
         seen.add(key)
