@@ -122,6 +122,33 @@ inline void attention_bwd(const AttentionConfig& cfg, const AttentionGlobals& g,
                        cuda_stream));
 }
 
+// Variable-length batches (tkb_attn_fwd_varlen / tkb_attn_bwd_varlen): cfg.batches sequences,
+// cfg.seq = the longest; tensors packed token-major [T, H, D] / [T, Hkv, D], contiguous;
+// cu_seqlens is a device int32 [batches + 1]; lse fp32 [batches, heads, seq]. Workspaces are
+// caller-owned device buffers (128-byte aligned) of the *_workspace_bytes sizes.
+inline std::size_t attention_fwd_varlen_workspace_bytes(const AttentionConfig& cfg) {
+    const tkb_attn_desc d = cfg.desc();
+    return tkb_attn_fwd_varlen_workspace_bytes(&d);
+}
+inline std::size_t attention_bwd_varlen_workspace_bytes(const AttentionConfig& cfg) {
+    const tkb_attn_desc d = cfg.desc();
+    return tkb_attn_bwd_varlen_workspace_bytes(&d);
+}
+inline void attention_fwd_varlen(const AttentionConfig& cfg, const int32_t* cu_seqlens, int64_t total_tokens,
+                                 const AttentionGlobals& g, void* workspace, std::size_t workspace_bytes,
+                                 void* cuda_stream = nullptr) {
+    const tkb_attn_desc d = cfg.desc();
+    check(tkb_attn_fwd_varlen(&d, cu_seqlens, total_tokens, g.q, g.k, g.v, g.o, g.lse, workspace, workspace_bytes,
+                              cuda_stream));
+}
+inline void attention_bwd_varlen(const AttentionConfig& cfg, const int32_t* cu_seqlens, int64_t total_tokens,
+                                 const AttentionGlobals& g, const AttentionGrads& gr, void* workspace,
+                                 std::size_t workspace_bytes, void* cuda_stream = nullptr) {
+    const tkb_attn_desc d = cfg.desc();
+    check(tkb_attn_bwd_varlen(&d, cu_seqlens, total_tokens, g.q, g.k, g.v, g.o, gr.dout, g.lse, gr.dq, gr.dk,
+                              gr.dv, workspace, workspace_bytes, cuda_stream));
+}
+
 // D = 128 backward dK/dV on 2-CTA clusters (tcgen05 cta_group::2); calling thread only, default off.
 inline void set_bwd_pairs(bool on) { check(tkb_set_bwd_pairs(on ? 1 : 0)); }
 

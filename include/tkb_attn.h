@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define TKB_ABI_VERSION 3
+#define TKB_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define TKB_API __attribute__((visibility("default")))
@@ -109,7 +109,7 @@ TKB_API int tkb_attn_fwd_rotary(const tkb_attn_desc* desc, const void* q, const 
                                 const float* sin_tab, const float* cos_tab, void* q_rot, void* k_rot, void* o,
                                 float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Bytes of caller-provided device workspace the backward needs/* Bytes of caller-provided device workspace the backward needs: two fp32 [B*H, N_pad]
+/* Bytes of caller-provided device workspace the backward needs: two fp32 [B*H, N_pad]
  * vectors, delta = rowsum(dO * O) and -L log2(e) (N_pad = N rounded up to 128). */
 TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* desc);
 
@@ -118,6 +118,32 @@ TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* desc);
 TKB_API int tkb_attn_bwd(const tkb_attn_desc* desc, const void* q, const void* k, const void* v, const void* o,
                  const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
                  size_t workspace_bytes, void* stream);
+
+/* Variable-length batches (the paper guards out-of-bounds rows,
+ * PAPER.md:1017,1056): B sequences of different lengths packed token-major. Sequence b is
+ * rows [cu_seqlens[b], cu_seqlens[b+1]) of
+ *   q, o, dout, dq   [T, H, D]    (desc.stride_n / stride_h: token / head strides, 0 = H*D / D)
+ *   k, v, dk, dv     [T, Hkv, D]  (desc.kv_stride_n / kv_stride_h, 0 = Hkv*D / D)
+ * with T = total_tokens >= cu_seqlens[B]; desc.batches = B, desc.seq = the maximum length
+ * (every cu_seqlens[b+1] - cu_seqlens[b] must be <= desc.seq; 0 is allowed); stride_b and
+ * kv_stride_b must be 0. cu_seqlens: int32 device array [B + 1], non-decreasing, cu[0] = 0.
+ * Each sequence attends only to itself (causal: top-left aligned within the sequence). Every
+ * sequence gets its own TMA maps (built on the device into the workspace, one extra small
+ * launch), so a tile never reads or writes a neighbouring sequence's rows: rows past a
+ * sequence's end are zero-filled on load and clipped on store. lse is fp32 [B, H, desc.seq];
+ * rows past a sequence's length are left untouched. Workspaces: 128-byte aligned, of
+ * tkb_attn_fwd_varlen_workspace_bytes / tkb_attn_bwd_varlen_workspace_bytes(desc) bytes
+ * (no zero-fill needed; calls sharing one must be stream-ordered). Results equal the
+ * fixed-length entry points run on each sequence alone, bit for bit. */
+TKB_API size_t tkb_attn_fwd_varlen_workspace_bytes(const tkb_attn_desc* desc);
+TKB_API int tkb_attn_fwd_varlen(const tkb_attn_desc* desc, const int32_t* cu_seqlens, int64_t total_tokens,
+                                const void* q, const void* k, const void* v, void* o, float* lse, void* workspace,
+                                size_t workspace_bytes, void* stream);
+TKB_API size_t tkb_attn_bwd_varlen_workspace_bytes(const tkb_attn_desc* desc);
+TKB_API int tkb_attn_bwd_varlen(const tkb_attn_desc* desc, const int32_t* cu_seqlens, int64_t total_tokens,
+                                const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                                size_t workspace_bytes, void* stream);
 
 /* Rotary position embedding (replaces rotary_kernel, kernels.hpp:357-513; oracle
  * oracles.hpp:66-90): for position p and i < D/2 the pair (x[p][i], x[p][i + D/2]) is

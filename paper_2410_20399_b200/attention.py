@@ -89,6 +89,12 @@ _SIGS = {
     "tkb_attn_fwd_rotary_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
     "tkb_attn_fwd_rotary": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
     "tkb_attn_bwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc)] + [_VP] * 10 + [ctypes.c_size_t, _VP]),
+    "tkb_attn_fwd_varlen_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
+    "tkb_attn_bwd_varlen_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(AttnDesc)]),
+    "tkb_attn_fwd_varlen": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, ctypes.c_int64] + [_VP] * 6
+                            + [ctypes.c_size_t, _VP]),
+    "tkb_attn_bwd_varlen": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, ctypes.c_int64] + [_VP] * 10
+                            + [ctypes.c_size_t, _VP]),
     "tkb_rotary": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP]),
     "tkb_rotary_qk": (ctypes.c_int, [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "tkb_gemm_validate": (ctypes.c_int, [ctypes.POINTER(GemmDesc)]),
@@ -371,6 +377,124 @@ def attention_bwd(q, k, v, o, dout, lse, causal=False, softmax_scale=None, dq=No
     _check(lib().tkb_attn_bwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                               dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                               workspace.data_ptr(), ws_bytes, _stream(torch, q.device)))
+    return dq, dk, dv
+
+
+# ------------------------------------------------- variable-length batches
+
+
+def _thd(t, name):
+    """A packed token-major [T, H, D] tensor: (head stride, token stride), D contiguous."""
+    if t.dim() != 3:
+        raise ShapeError(f"{name} must be [T, H, D] (packed variable-length batch)")
+    if t.stride(2) != 1:
+        raise ShapeError(f"{name}: head_dim must be contiguous")
+    return t.stride(1), t.stride(0)
+
+
+def _varlen_args(q, k, v, cu_seqlens, max_seqlen):
+    import torch
+
+    _bf16_cuda(q, "q")
+    _bf16_cuda(k, "k", q.device)
+    _bf16_cuda(v, "v", q.device)
+    qs = _thd(q, "q")
+    ks = _thd(k, "k")
+    if _thd(v, "v") != ks or tuple(v.shape) != tuple(k.shape):
+        raise ShapeError("k and v must share shape and strides")
+    T, H, D = q.shape
+    if k.shape[0] != T or k.shape[2] != D:
+        raise ShapeError("k, v must be [T, Hkv, D] matching q's T and D")
+    hkv = k.shape[1]
+    if hkv < 1 or H % hkv:
+        raise ConfigError(f"heads ({H}) must be a multiple of kv heads ({hkv})")
+    if (not isinstance(cu_seqlens, torch.Tensor) or not cu_seqlens.is_cuda or cu_seqlens.device != q.device
+            or cu_seqlens.dtype != torch.int32 or cu_seqlens.dim() != 1 or not cu_seqlens.is_contiguous()
+            or cu_seqlens.numel() < 2):
+        raise ShapeError("cu_seqlens must be a contiguous int32 CUDA tensor [B + 1] on q's device")
+    B = cu_seqlens.numel() - 1
+    if int(max_seqlen) < 1:
+        raise ConfigError("max_seqlen must be >= 1")
+    return T, B, H, D, hkv, qs, ks
+
+
+def _varlen_desc(B, H, max_seqlen, D, causal, softmax_scale, check_finite, hkv, qs, ks):
+    cfg = AttentionConfig(B, H, int(max_seqlen), D, causal, softmax_scale, check_finite, kv_heads=hkv)
+    d = cfg.desc()
+    d.stride_b, d.stride_h, d.stride_n = 0, qs[0], qs[1]
+    d.kv_stride_b, d.kv_stride_h, d.kv_stride_n = 0, ks[0], ks[1]
+    return d
+
+
+def _workspace(workspace, nbytes, device):
+    import torch
+
+    if workspace is None:
+        return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    if (not workspace.is_cuda or workspace.device != device or not workspace.is_contiguous()
+            or workspace.numel() * workspace.element_size() < nbytes or workspace.data_ptr() % 128):
+        raise BoundsError(f"workspace must be a contiguous 128-byte aligned CUDA buffer of >= {nbytes} bytes "
+                          f"on {device}")
+    return workspace
+
+
+def attention_fwd_varlen(q, k, v, cu_seqlens, max_seqlen, causal=False, softmax_scale=None, out=None, lse=None,
+                         return_lse=True, check_finite=False, workspace=None):
+    """Forward over a packed variable-length batch: sequence b is rows [cu[b], cu[b+1]) of
+    q [T, H, D] and k, v [T, Hkv, D]; it attends only to itself (causal: within the
+    sequence). Returns (O [T, H, D], L fp32 [B, H, max_seqlen]); L rows past a sequence's
+    length are not written. max_seqlen must be >= every length (tkb_attn_fwd_varlen)."""
+    import torch
+
+    T, B, H, D, hkv, qs, ks = _varlen_args(q, k, v, cu_seqlens, max_seqlen)
+    if out is None:
+        out = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+    else:
+        _bf16_cuda(out, "out", q.device)
+        if tuple(out.shape) != tuple(q.shape) or _thd(out, "out") != qs:
+            raise ShapeError("out must match q's shape and strides")
+    if return_lse and lse is None:
+        lse = torch.empty((B, H, int(max_seqlen)), dtype=torch.float32, device=q.device)
+    if lse is not None:
+        _check_lse(lse, B, H, int(max_seqlen), q.device)
+    d = _varlen_desc(B, H, max_seqlen, D, causal, softmax_scale, check_finite, hkv, qs, ks)
+    ws_bytes = int(lib().tkb_attn_fwd_varlen_workspace_bytes(ctypes.byref(d)))
+    workspace = _workspace(workspace, ws_bytes, q.device)
+    _check(lib().tkb_attn_fwd_varlen(ctypes.byref(d), cu_seqlens.data_ptr(), T, q.data_ptr(), k.data_ptr(),
+                                     v.data_ptr(), out.data_ptr(), lse.data_ptr() if lse is not None else None,
+                                     workspace.data_ptr(), ws_bytes, _stream(torch, q.device)))
+    return (out, lse) if return_lse else out
+
+
+def attention_bwd_varlen(q, k, v, o, dout, lse, cu_seqlens, max_seqlen, causal=False, softmax_scale=None,
+                         dq=None, dk=None, dv=None, workspace=None, check_finite=False):
+    """dQ, dK, dV of a packed variable-length batch from the saved L [B, H, max_seqlen]
+    (tkb_attn_bwd_varlen); deterministic like attention_bwd."""
+    import torch
+
+    T, B, H, D, hkv, qs, ks = _varlen_args(q, k, v, cu_seqlens, max_seqlen)
+    for t, name in ((o, "o"), (dout, "dout")):
+        _bf16_cuda(t, name, q.device)
+        if tuple(t.shape) != tuple(q.shape) or _thd(t, name) != qs:
+            raise ShapeError(f"{name} must match q's shape and strides")
+    _check_lse(lse, B, H, int(max_seqlen), q.device)
+    if dq is None:
+        dq = torch.empty_strided(q.shape, q.stride(), dtype=torch.bfloat16, device=q.device)
+    if dk is None:
+        dk = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
+    if dv is None:
+        dv = torch.empty_strided(k.shape, k.stride(), dtype=torch.bfloat16, device=q.device)
+    for t, name, ref, rs in ((dq, "dq", q, qs), (dk, "dk", k, ks), (dv, "dv", k, ks)):
+        _bf16_cuda(t, name, q.device)
+        if tuple(t.shape) != tuple(ref.shape) or _thd(t, name) != rs:
+            raise ShapeError(f"{name} must match the shape and strides of its input")
+    d = _varlen_desc(B, H, max_seqlen, D, causal, softmax_scale, check_finite, hkv, qs, ks)
+    ws_bytes = int(lib().tkb_attn_bwd_varlen_workspace_bytes(ctypes.byref(d)))
+    workspace = _workspace(workspace, ws_bytes, q.device)
+    _check(lib().tkb_attn_bwd_varlen(ctypes.byref(d), cu_seqlens.data_ptr(), T, q.data_ptr(), k.data_ptr(),
+                                     v.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(), dq.data_ptr(),
+                                     dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(), ws_bytes,
+                                     _stream(torch, q.device)))
     return dq, dk, dv
 
 

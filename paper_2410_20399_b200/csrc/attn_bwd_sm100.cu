@@ -225,6 +225,7 @@ struct TmemKV {
 //     store issued by the load warp (see FINISH below).
 struct KvTask {
     int j, head, batch;
+    SeqView sv;  // this batch's length and TMA row coordinates (variable-length batches)
 };
 
 // SMEM of the persistent dK/dV kernel. Q_{t+1} is needed by S_{t+1}, issued right after dV_t;
@@ -310,10 +311,18 @@ struct attn_bwd_dkdv_template {
         }
         w.head = unit % hkv;
         w.batch = unit / hkv;
+        w.sv = seq_view(p.cu_seqlens, p.vmaps, kBwdMaps, p.n, w.batch);
         return w;
     }
     static TKB_DEVICE int steps(const globals& p, const KvTask& w) {
-        return (CAUSAL ? (p.n_pad / 128 - w.j) : p.n_pad / 128) * p.group;
+        const int nb = (w.sv.n + 127) / 128;  // query blocks of this sequence
+        return (CAUSAL ? (nb - w.j) : nb) * p.group;
+    }
+    // variable-length batches: kv blocks past a short sequence have no work
+    static TKB_DEVICE bool skip(const globals& p, int id) {
+        if (p.cu_seqlens == nullptr) return false;
+        const KvTask w = decode(p, id);
+        return w.j * 128 >= w.sv.n;
     }
     static TKB_DEVICE Tile<D> tQ(shared& sh, int x) { return Tile<D>{sh.q[x % SQ]}; }
     static TKB_DEVICE Tile<D> tDo(shared& sh, int x) { return Tile<D>{sh.dO[x % SD]}; }
@@ -356,7 +365,7 @@ struct attn_bwd_dkdv_template {
         struct state {
             int x = 0;       // global step (ring position)
             int staged = 0;  // staged finishes stored
-            KvTask prev{0, 0, 0};
+            KvTask prev{};
         };
         template <class ClaimNext>
         static TKB_DEVICE void load(const lcsf::args<attn_bwd_dkdv_template>& a, state& ps, int id, int n,
@@ -368,10 +377,17 @@ struct attn_bwd_dkdv_template {
             const KvTask w = decode(p, id);
             const int T = steps(p, w), T1 = T / p.group;
             const int kv0 = w.j * 128;
+            if (w.sv.maps != nullptr) {  // this sequence's maps (varlen_maps_kernel); dV / dK: its finish
+                for (int m = 0; m < kBwdMaps; ++m) tma::acquire_map(w.sv.maps + m);
+            }
             mbar_wait(&sh.kv_empty, (n & 1) ^ 1u);
             mbar_arrive_expect_tx(&sh.kv_full, 2 * TL::kTileBytes);
-            load_async(Tile<D>{sh.k}, gl{&p.tm_k}, &sh.kv_full, kv0, w.head, w.batch, pol_stream);
-            load_async(Tile<D>{sh.v}, gl{&p.tm_v}, &sh.kv_full, kv0, w.head, w.batch, pol_stream);
+            w.sv.with_map(p.tm_k, kMapK, [&](const CUtensorMap* m) {
+                load_async(Tile<D>{sh.k}, gl{m}, &sh.kv_full, kv0, w.head, w.sv.bcoord, pol_stream);
+            });
+            w.sv.with_map(p.tm_v, kMapV, [&](const CUtensorMap* m) {
+                load_async(Tile<D>{sh.v}, gl{m}, &sh.kv_full, kv0, w.head, w.sv.bcoord, pol_stream);
+            });
             const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
             for (int t = 0; t < T; ++t, ++ps.x) {
                 const int x = ps.x;
@@ -382,21 +398,31 @@ struct attn_bwd_dkdv_template {
                 const int sq = x % SQ, sd = x % SD, sa = x % SA;
                 mbar_wait(&sh.q_empty[sq], ((x / SQ) & 1) ^ 1);
                 mbar_arrive_expect_tx(&sh.q_full[sq], TL::kTileBytes);
-                load_async(tQ(sh, x), gl{&p.tm_q}, &sh.q_full[sq], i * 128, hq, w.batch, pol_keep);
+                w.sv.with_map(p.tm_q, kMapQ, [&](const CUtensorMap* m) {
+                    load_async(tQ(sh, x), gl{m}, &sh.q_full[sq], i * 128, hq, w.sv.bcoord, pol_keep);
+                });
                 if (after_staged && t == 1) {
                     // the previous task's finish staged dV / dK in the dO slot of step 1 and the
                     // Q slot of step 2: store them (this warp, off the compute warps' path)
                     // and refill the slots once the store has read them
                     mbar_wait(&sh.staged_full, ps.staged & 1);
                     ++ps.staged;
-                    store_async(gl{&p.tm_dv}, tQ(sh, x + 1), ps.prev.j * 128, ps.prev.head, ps.prev.batch);
-                    store_async(gl{&p.tm_dk}, tDo(sh, x), ps.prev.j * 128, ps.prev.head, ps.prev.batch);
+                    const int prow = ps.prev.j * 128;
+                    const KvTask& pw = ps.prev;
+                    pw.sv.with_map(p.tm_dv, kMapDv, [&](const CUtensorMap* m) {
+                        store_async(gl{m}, tQ(sh, x + 1), prow, pw.head, pw.sv.bcoord);
+                    });
+                    pw.sv.with_map(p.tm_dk, kMapDk, [&](const CUtensorMap* m) {
+                        store_async(gl{m}, tDo(sh, x), prow, pw.head, pw.sv.bcoord);
+                    });
                     tma::commit_group();
                     tma::wait_group_read<0>();
                 }
                 mbar_wait(&sh.do_empty[sd], ((x / SD) & 1) ^ 1);
                 mbar_arrive_expect_tx(&sh.do_full[sd], TL::kTileBytes);
-                load_async(tDo(sh, x), gl{&p.tm_do}, &sh.do_full[sd], i * 128, hq, w.batch, pol_keep);
+                w.sv.with_map(p.tm_do, kMapDo, [&](const CUtensorMap* m) {
+                    load_async(tDo(sh, x), gl{m}, &sh.do_full[sd], i * 128, hq, w.sv.bcoord, pol_keep);
+                });
                 mbar_wait(&sh.aux_empty[sa], ((x / SA) & 1) ^ 1);
                 mbar_arrive_expect_tx(&sh.aux_full[sa], 1024);
                 tma::load_1d(sh.lse[sa], p.lse2 + bhq * p.n_pad + i * 128, 512, &sh.aux_full[sa]);
@@ -575,8 +601,11 @@ struct attn_bwd_dkdv_template {
             } else {
                 // dV / dK rows from registers (register -> global, warp-transposed)
                 const int row0 = kv0 + wq * 32;  // row of lane 0
-                const gv<__nv_bfloat16> gdv{reinterpret_cast<__nv_bfloat16*>(p.dv), p.kv_sb, p.kv_sh, p.kv_sn};
-                const gv<__nv_bfloat16> gdk{reinterpret_cast<__nv_bfloat16*>(p.dk), p.kv_sb, p.kv_sh, p.kv_sn};
+                // variable-length batches: the sequence's first packed row is the base, batch 0
+                const size_t base = (size_t)w.sv.off * p.kv_sn;
+                const int bidx = p.cu_seqlens ? 0 : w.batch;
+                const gv<__nv_bfloat16> gdv{reinterpret_cast<__nv_bfloat16*>(p.dv) + base, p.kv_sb, p.kv_sh, p.kv_sn};
+                const gv<__nv_bfloat16> gdk{reinterpret_cast<__nv_bfloat16*>(p.dk) + base, p.kv_sb, p.kv_sh, p.kv_sn};
                 rt_fl<D / 4> f;
                 rt_bf<D / 4> h;
                 load(f, tbase + lane_off + CT::tmem_dv() + g * (D / 4));
@@ -584,14 +613,14 @@ struct attn_bwd_dkdv_template {
                 tmem::fence_before();
                 mbar_arrive(&sh.dv_free);
                 copy(h, f);
-                store_rows(gdv, h, w.batch, w.head, row0, g * (D / 4), p.n - row0);
+                store_rows(gdv, h, bidx, w.head, row0, g * (D / 4), w.sv.n - row0);
                 load(f, tbase + lane_off + CT::tmem_dk() + g * (D / 4));
                 load_wait(f);
                 tmem::fence_before();
                 mbar_arrive(&sh.dk_free);
                 mul(f, p.scale);  // dK = scale dS^T Q
                 copy(h, f);
-                store_rows(gdk, h, w.batch, w.head, row0, g * (D / 4), p.n - row0);
+                store_rows(gdk, h, bidx, w.head, row0, g * (D / 4), w.sv.n - row0);
             }
             if (threadIdx.x == 0) TKB_TR(1, n, 6);
         }
@@ -925,7 +954,8 @@ struct CfgQ {
 };
 
 struct QTask {
-    int i, bh;  // query block, batch * heads + head
+    int i, bh;   // query block, batch * heads + head
+    SeqView sv;  // this batch's length and TMA row coordinates (variable-length batches)
 };
 
 // task t -> (query block, b*h): heads in groups of p.head_group whose K / V stay in L2,
@@ -941,6 +971,7 @@ TKB_DEVICE QTask qtask(const BwdParams& p, int t) {
     QTask w;
     w.bh = sec * G + (r - mi * gs);
     w.i = CAUSAL ? (nq - 1 - mi) : mi;
+    w.sv = seq_view(p.cu_seqlens, p.vmaps, kBwdMaps, p.n, w.bh / p.heads);
     return w;
 }
 
@@ -992,7 +1023,13 @@ struct attn_bwd_dq_template {
     static TKB_DEVICE uint32_t ph_of(uint32_t it) { return kDP ? ((it >> 1) & 1) : (it & 1); }
     static TKB_DEVICE int num_tasks(const globals& p) { return p.bh * (p.n_pad / 128); }
     static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
-    static TKB_DEVICE int nk_of(const globals& p, const QTask& w) { return CAUSAL ? (w.i + 1) : p.n_pad / 128; }
+    static TKB_DEVICE int nk_of(const globals&, const QTask& w) { return CAUSAL ? (w.i + 1) : (w.sv.n + 127) / 128; }
+    // variable-length batches: query blocks past a short sequence have no work
+    static TKB_DEVICE bool skip(const globals& p, int t) {
+        if (p.cu_seqlens == nullptr) return false;
+        const QTask w = qtask<CAUSAL>(p, t);
+        return w.i * 128 >= w.sv.n;
+    }
     static TKB_DEVICE Tile<D> tK(shared& sh, int x) { return Tile<D>{sh.k[x % SK]}; }
     static TKB_DEVICE Tile<D> tV(shared& sh, int x) { return Tile<D>{sh.v[x % SV]}; }
 
@@ -1041,18 +1078,30 @@ struct attn_bwd_dq_template {
             const int b = w.bh / p.heads, h = w.bh - b * p.heads;
             mbar_wait(&sh.qdo_free, (n & 1) ^ 1u);  // the previous task's Q / dO are in TMEM
             mbar_arrive_expect_tx(&sh.qdo_full, 2 * TL::kTileBytes);
-            load_async(Tile<D>{sh.q}, gl{&p.tm_q}, &sh.qdo_full, w.i * 128, h, b, pol_stream);
-            load_async(Tile<D>{sh.dO}, gl{&p.tm_do}, &sh.qdo_full, w.i * 128, h, b, pol_stream);
+            const int bc = w.sv.bcoord;
+            if (w.sv.maps != nullptr) {  // this sequence's maps (varlen_maps_kernel)
+                for (int m : {kMapQ, kMapK, kMapV, kMapDo}) tma::acquire_map(w.sv.maps + m);
+            }
+            w.sv.with_map(p.tm_q, kMapQ, [&](const CUtensorMap* m) {
+                load_async(Tile<D>{sh.q}, gl{m}, &sh.qdo_full, w.i * 128, h, bc, pol_stream);
+            });
+            w.sv.with_map(p.tm_do, kMapDo, [&](const CUtensorMap* m) {
+                load_async(Tile<D>{sh.dO}, gl{m}, &sh.qdo_full, w.i * 128, h, bc, pol_stream);
+            });
             const int nk = nk_of(p, w);
             for (int jj = 0; jj < nk; ++jj, ++ps.kv) {
                 const int kv = ps.kv;
                 const int sk = kv % SK, sv = kv % SV;
                 mbar_wait(&sh.k_empty[sk], ((kv / SK) & 1) ^ 1);
                 mbar_arrive_expect_tx(&sh.k_full[sk], TL::kTileBytes);
-                load_async(tK(sh, kv), gl{&p.tm_k}, &sh.k_full[sk], jj * 128, h / p.group, b, pol_keep);
+                w.sv.with_map(p.tm_k, kMapK, [&](const CUtensorMap* m) {
+                    load_async(tK(sh, kv), gl{m}, &sh.k_full[sk], jj * 128, h / p.group, bc, pol_keep);
+                });
                 mbar_wait(&sh.v_empty[sv], ((kv / SV) & 1) ^ 1);
                 mbar_arrive_expect_tx(&sh.v_full[sv], TL::kTileBytes);
-                load_async(tV(sh, kv), gl{&p.tm_v}, &sh.v_full[sv], jj * 128, h / p.group, b, pol_keep);
+                w.sv.with_map(p.tm_v, kMapV, [&](const CUtensorMap* m) {
+                    load_async(tV(sh, kv), gl{m}, &sh.v_full[sv], jj * 128, h / p.group, bc, pol_keep);
+                });
             }
         }
         static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dq_template>&, state&) {}
@@ -1181,7 +1230,7 @@ struct attn_bwd_dq_template {
                 mbar_arrive(&sh.s_free);
                 exp_chunk<true>(pf, tau, 0u, nlse_r);
                 // visible keys: kv < n, and causal kv <= row
-                const int lim = (CAUSAL ? min(row, p.n - 1) : (p.n - 1)) - kv0 - 32 * g;  // last visible column
+                const int lim = (CAUSAL ? min(row, w.sv.n - 1) : (w.sv.n - 1)) - kv0 - 32 * g;  // last visible column
                 if (lim < 31) {  // diagonal / ragged tail block only
 #pragma unroll
                     for (int c = 0; c < 32; ++c) pf[c] = (c > lim) ? 0.f : pf[c];
@@ -1228,7 +1277,10 @@ struct attn_bwd_dq_template {
             tma::fence_async_smem();
             named_sync(kBarCompute, kComputeThreads);
             if (threadIdx.x == 0) {
-                store_async(gl{&p.tm_dq}, Tile<D>{sh.q}, w.i * 128, h, b);
+                if (w.sv.maps != nullptr) tma::acquire_map(w.sv.maps + kMapDq);
+                w.sv.with_map(p.tm_dq, kMapDq, [&](const CUtensorMap* m) {
+                    store_async(gl{m}, Tile<D>{sh.q}, w.i * 128, h, w.sv.bcoord);
+                });
                 tma::commit_group();
                 tma::wait_group_read<0>();
                 mbar_arrive(&sh.qdo_free);
@@ -1263,7 +1315,8 @@ template <int D>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ lse2,
-                                                       float* __restrict__ delta, int heads, int n, int n_pad,
+                                                       float* __restrict__ delta, const int* __restrict__ cu,
+                                                       int heads, int n, int n_pad,
                                                        int row_blocks, int64_t total_blocks, int64_t sb, int64_t sh,
                                                        int64_t sn) {
     constexpr int kLanesPerRow = D / 8;
@@ -1273,6 +1326,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
         const int64_t bh = blk / row_blocks;
         const int rb = (int)(blk - bh * row_blocks);
         const int64_t b = bh / heads, hh = bh % heads;
+        const SeqView sv = seq_view(cu, nullptr, 0, n, (int)b);  // varlen: rows [cu[b], cu[b+1]), sb = 0
         const int row_base = rb * kRowsPerPass * kPrepRows + threadIdx.x / kLanesPerRow;
         uint4 ov[kPrepRows], dv[kPrepRows];
 #pragma unroll
@@ -1280,8 +1334,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
             const int row = row_base + k * kRowsPerPass;
             ov[k] = make_uint4(0, 0, 0, 0);
             dv[k] = make_uint4(0, 0, 0, 0);
-            if (row < n) {
-                const int64_t off = b * sb + hh * sh + (int64_t)row * sn + c;
+            if (row < sv.n) {
+                const int64_t off = b * sb + hh * sh + (int64_t)(sv.off + row) * sn + c;
                 ov[k] = __ldg(reinterpret_cast<const uint4*>(o + off));
                 dv[k] = __ldg(reinterpret_cast<const uint4*>(dout + off));
             }
@@ -1303,8 +1357,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
             for (int s = kLanesPerRow / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
             if (row < n_pad && (threadIdx.x % kLanesPerRow) == 0) {
                 const size_t idx = (size_t)bh * n_pad + perm32(row);  // group-permuted (perm32)
-                delta[idx] = row < n ? acc : 0.f;
-                lse2[idx] = row < n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
+                delta[idx] = row < sv.n ? acc : 0.f;
+                lse2[idx] = row < sv.n ? -lse[(size_t)bh * n + row] * 1.44269504088896340736f : -INFINITY;
             }
         }
     }
@@ -1320,7 +1374,7 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
     if (D == 128)
         if (int e = ensure_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes, set_kv2)) return e;
     if (phases & 2) {
-        if (D == 128 && p.pairs) {  // CTA pairs: kv blocks rounded up to an even count
+        if (D == 128 && p.pairs && p.cu_seqlens == nullptr) {  // CTA pairs: kv blocks rounded up to an even count
             dim3 grid2((p.n_pad / 128 + 1) & ~1, p.heads / p.group, batches);
             attn_bwd_dkdv2_kernel<CAUSAL><<<grid2, kThreads, CfgKV2::kSmemBytes, stream>>>(p);
         } else {
@@ -1355,7 +1409,7 @@ int launch_all(bool causal, const BwdParams& p, int batches, const void* o, cons
         const int64_t cap = (int64_t)p.num_sms * 16;  // 16 x 256 threads per SM in flight
         bwd_prep_kernel<D><<<(unsigned)(total < cap ? total : cap), 256, 0, stream>>>(
             reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2, delta,
-            p.heads, p.n, p.n_pad, row_blocks, total, sb, sh, sn);
+            p.cu_seqlens, p.heads, p.n, p.n_pad, row_blocks, total, sb, sh, sn);
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;

@@ -32,14 +32,66 @@ constexpr int kBlockN = 128;   // key/value rows per KV tile
 constexpr int kQStages = 2;    // query tiles per CTA (ping-pong softmax warpgroups)
 constexpr int kRowsPerCta = kBlockM * kQStages;
 
+// Variable-length batches (tkb_attn_fwd_varlen / tkb_attn_bwd_varlen): sequence b is rows
+// [cu[b], cu[b+1]) of packed [T, H, D] tensors. Each sequence gets its own TMA maps
+// ({D, n_b, H, 1} over base + cu[b] sn, written on the device by varlen_maps_kernel with
+// tensormap.replace into the caller's workspace, [B][kMaps] CUtensorMaps): a tile past a
+// sequence's end is zero-filled on load and clipped on store exactly like the ragged tail of
+// a fixed-length head, so no tile reads or writes a neighbouring sequence's rows.
+// Fixed-length problems (cu == nullptr): n = n_max, bcoord = batch, off = 0, maps = null
+// (the kernel-parameter maps over [B, H, N, D]).
+struct SeqView {
+    int n;                    // rows of this sequence
+    int bcoord;               // TMA outermost coordinate (batch; 0 with per-sequence maps)
+    int off;                  // first packed row of the sequence (cu[b]; 0 fixed-length)
+    const CUtensorMap* maps;  // this sequence's maps (varlen) or null
+    // Run f(const CUtensorMap*) on map idx of this sequence (varlen) or on the kernel-parameter
+    // map `fixed`. Two call sites, not one pointer select: a descriptor pointer that may be
+    // either a parameter or a global address makes the compiler materialise the parameter's
+    // address generically, and the fixed-length TMA through it faulted (illegal instruction).
+    template <class F>
+    __device__ __forceinline__ void with_map(const CUtensorMap& fixed, int idx, F&& f) const {
+        if (maps != nullptr)
+            f(maps + idx);
+        else
+            f(&fixed);
+    }
+};
+__device__ __forceinline__ SeqView seq_view(const int* cu, const CUtensorMap* vmaps, int kmaps, int n_max, int b) {
+    SeqView v;
+    if (cu == nullptr) {
+        v.n = n_max, v.bcoord = b, v.off = 0, v.maps = nullptr;
+    } else {
+        const int s0 = __ldg(cu + b), s1 = __ldg(cu + b + 1);
+        v.n = s1 - s0, v.bcoord = 0, v.off = s0, v.maps = vmaps + (size_t)b * kmaps;
+    }
+    return v;
+}
+// per-sequence map slots
+constexpr int kFwdMaps = 4;  // q, k, v, o
+constexpr int kBwdMaps = 7;  // q, k, v, do, dq, dk, dv
+enum { kMapQ = 0, kMapK = 1, kMapV = 2, kMapO = 3, kMapDo = 3, kMapDq = 4, kMapDk = 5, kMapDv = 6 };
+
+// Builds [B][nmaps] per-sequence maps from host-encoded templates over the packed tensors
+// ({D, n_max, H, 1}): base += cu[b] * row_bytes, rows = n_b.
+struct VarlenMapTemplates {
+    CUtensorMap tmpl[kBwdMaps];
+    unsigned long long base[kBwdMaps];
+    long long row_bytes[kBwdMaps];
+    int nmaps;
+};
+int launch_varlen_maps(const VarlenMapTemplates& t, const int* cu, int batches, CUtensorMap* out, cudaStream_t stream);
+
 struct FwdParams {
     CUtensorMap tm_q, tm_k, tm_v, tm_o;  // 4-D {D, N, H, B}, box {64, 128, 1, 1}, SW128
     float* lse;                          // [B*H, N] fp32, may be null
+    const int* cu_seqlens;               // varlen: [B + 1] packed row offsets (null: fixed N)
+    const CUtensorMap* vmaps;            // varlen: [B][kFwdMaps] per-sequence maps (workspace)
     int* sched;                          // persistent task counter pair (self-resetting)
     long long* trace;                    // optional per-role cycle timeline (tkb_debug_set_trace)
     int trace_every;
     int trace_slots;
-    int n;                               // sequence length
+    int n;                               // sequence length (varlen: the maximum)
     int heads;
     int group;                           // query heads per kv head (grouped-query attention; 1 = MHA)
     int bh;                              // batches * heads          (set by launch_attn_fwd)
@@ -69,6 +121,8 @@ struct BwdParams {
     CUtensorMap tm_q64, tm_do64;          // Q / dO with a {64, 64, 1, 1} box (CTA-pair query halves)
     const float* lse2;                    // [B*H, Npad] -L * log2(e); -inf on padded rows (workspace)
     const float* delta;                   // [B*H, Npad] rowsum(dO * O) (workspace)
+    const int* cu_seqlens;                // varlen: [B + 1] packed row offsets (null: fixed N)
+    const CUtensorMap* vmaps;             // varlen: [B][kBwdMaps] per-sequence maps (workspace)
     long long* trace;                     // optional per-role cycle timeline (tkb_debug_set_trace)
     int trace_every;                      // trace CTAs with linear id % trace_every == 0
     int trace_slots;

@@ -133,6 +133,7 @@ struct attn_fwd_template {
     // (late) causal query blocks first, heads innermost; claimed dynamically (one CTA per SM)
     struct Task {
         int mblk, head, batch, nkv;
+        SeqView sv;  // this batch's length and TMA row coordinates (variable-length batches)
     };
     static TKB_DEVICE Task decode(const globals& p, int t) {
         const int N = p.n;
@@ -147,14 +148,22 @@ struct attn_fwd_template {
         w.mblk = CAUSAL ? (m_blocks - 1 - mi) : mi;
         w.batch = bh / p.heads;
         w.head = bh - w.batch * p.heads;
-        w.nkv = (N + kBlockN - 1) / kBlockN;
-        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, N) - 1) / kBlockN + 1);
+        w.sv = seq_view(p.cu_seqlens, p.vmaps, kFwdMaps, N, w.batch);
+        const int n = w.sv.n;
+        w.nkv = (n + kBlockN - 1) / kBlockN;
+        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, n) - 1) / kBlockN + 1);
         return w;
+    }
+    // variable-length batches: query blocks past a short sequence have no work
+    static TKB_DEVICE bool skip(const globals& p, int t) {
+        if (p.cu_seqlens == nullptr) return false;
+        const Task w = decode(p, t);
+        return w.mblk * kRowsPerCta >= w.sv.n;
     }
     // kv blocks query tile s of a task visits (causal: tile 0 skips the block only tile 1 sees)
     static TKB_DEVICE int tile_blocks(const globals& p, const Task& w, int s) {
         if (!CAUSAL) return w.nkv;
-        return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, p.n) - 1) / kBlockN + 1);
+        return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, w.sv.n) - 1) / kBlockN + 1);
     }
     // k3: index of (tile s, block i) in the task's QK issue order, its buffer and TMEM column
     static TKB_DEVICE int qk_index(int s, int i, int nk0, int nk1) {
@@ -201,8 +210,12 @@ struct attn_fwd_template {
             shared& sh = a.sh;
             const uint64_t pol_q = tma::policy_evict_first();
             const uint64_t pol_kv = tma::policy_evict_last();
-            const gl gQ{&p.tm_q}, gK{&p.tm_k}, gV{&p.tm_v};
             const Task w = decode(p, t);
+            if (w.sv.maps != nullptr) {  // this sequence's maps, written by varlen_maps_kernel
+                tma::acquire_map(w.sv.maps + kMapQ);
+                tma::acquire_map(w.sv.maps + kMapK);
+                tma::acquire_map(w.sv.maps + kMapV);
+            }
             const int q0 = w.mblk * kRowsPerCta;
             const int nq = (p.n + 127) / 128;
             const int bkv = w.batch * (p.heads / p.group) + w.head / p.group;
@@ -212,14 +225,19 @@ struct attn_fwd_template {
             for (int s = 0; s < kQStages; ++s) {  // Q_s is free once the last QK_s of the previous task retired
                 mbar_wait(&sh.q_empty[s], (nt & 1) ^ 1u);
                 mbar_arrive_expect_tx(&sh.q_full[s], C::kTile);
-                load_async(sQ(sh, s), gQ, &sh.q_full[s], q0 + s * kBlockM, w.head, w.batch, pol_q);
+                w.sv.with_map(p.tm_q, kMapQ, [&](const CUtensorMap* m) {
+                    load_async(sQ(sh, s), gl{m}, &sh.q_full[s], q0 + s * kBlockM, w.head, w.sv.bcoord, pol_q);
+                });
             }
             const int t_next = claim_next();
             if (t_next >= 0) {  // warm the next task's Q in L2
                 const Task w2 = decode(p, t_next);
-                for (int s = 0; s < kQStages; ++s)
-                    for (int at = 0; at < Tile::kAtoms; ++at)
-                        tma::prefetch_4d(gQ.tm, at * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.batch);
+                if (w2.sv.maps != nullptr) tma::acquire_map(w2.sv.maps + kMapQ);
+                w2.sv.with_map(p.tm_q, kMapQ, [&](const CUtensorMap* q2) {
+                    for (int s = 0; s < kQStages; ++s)
+                        for (int at = 0; at < Tile::kAtoms; ++at)
+                            tma::prefetch_4d(q2, at * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.sv.bcoord);
+                });
             }
             for (int i = 0; i < w.nkv; ++i) {
                 // the rotated K block (checking 8 blocks at a time, or the whole task's range at
@@ -229,8 +247,10 @@ struct attn_fwd_template {
                 for (int which = 0; which < 2; ++which) {
                     sh.kv_ring.wait_empty(ps.st);
                     mbar_arrive_expect_tx(&sh.kv_ring.full[ps.st.slot], C::kTile);
-                    load_async(sKV(sh, ps.st.slot), which == 0 ? gK : gV, &sh.kv_ring.full[ps.st.slot],
-                               i * kBlockN, w.head / p.group, w.batch, pol_kv);  // grouped-query: kv head = head / group
+                    w.sv.with_map(which == 0 ? p.tm_k : p.tm_v, which == 0 ? kMapK : kMapV, [&](const CUtensorMap* m) {
+                        load_async(sKV(sh, ps.st.slot), gl{m}, &sh.kv_ring.full[ps.st.slot], i * kBlockN,
+                                   w.head / p.group, w.sv.bcoord, pol_kv);  // grouped-query: kv head = head / group
+                    });
                     ps.st.advance();
                 }
             }
@@ -413,8 +433,8 @@ struct attn_fwd_template {
             const uint32_t tS_fixed = tbase + lane_off + C::tmem_s(s);
             const uint32_t tO = tbase + lane_off + C::tmem_o(s);
             const float tau = p.scale_log2;
-            const int N = p.n;
             const Task w = decode(p, t);
+            const int N = w.sv.n;
             const int q0 = w.mblk * kRowsPerCta;
             const int row = q0 + s * kBlockM + row_in_tile;
             const int nkv = tile_blocks(p, w, s);
@@ -541,10 +561,11 @@ struct attn_fwd_template {
                 ++cs.pvc;
             }
             tmem::fence_after();
-            if (p.lse != nullptr && row < p.n)
+            if (p.lse != nullptr && row < w.sv.n)
                 p.lse[(size_t)(w.batch * p.heads + w.head) * p.n + row] = (m + __log2f(l)) * kLn2;
             const bool leader = (wq == 0 && a.lane == 0);
             const st_bf<128, 64> stage = sStage(sh, s);
+            if (leader && w.sv.maps != nullptr) tma::acquire_map(w.sv.maps + kMapO);
 #pragma unroll 1
             for (int at = 0; at < Tile::kAtoms; ++at) {
                 rt_fl<32> o0, o1;
@@ -565,7 +586,9 @@ struct attn_fwd_template {
                 tma::fence_async_smem();
                 named_sync(1 + s, WARPGROUP_THREADS);
                 if (leader) {
-                    store_async(gl{&p.tm_o}, stage, q0 + s * kBlockM, w.head, w.batch, at * 64);  // shared -> global (TMA)
+                    w.sv.with_map(p.tm_o, kMapO, [&](const CUtensorMap* m) {  // shared -> global (TMA; rows
+                        store_async(gl{m}, stage, q0 + s * kBlockM, w.head, w.sv.bcoord, at * 64);  // past n clipped)
+                    });
                     tma::commit_group();
                 }
             }

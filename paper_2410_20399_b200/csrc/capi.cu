@@ -185,6 +185,23 @@ Strides kv_strides_of(const tkb_attn_desc* d) {
     return s;
 }
 
+// Variable-length batches: packed token-major [T, H, D] (q/o/do/dq) and [T, Hkv, D]
+// (k/v/dk/dv); stride_n / stride_h are the token / head strides (0 = H D / D), stride_b unused.
+struct Varlen {
+    const int32_t* cu;  // device [B + 1]
+    int64_t total;      // T = cu[B]
+};
+
+Strides varlen_strides(const tkb_attn_desc* d, bool kv) {
+    const int heads = kv ? kv_heads_of(d) : d->heads;
+    const int64_t sn = kv ? d->kv_stride_n : d->stride_n, sh = kv ? d->kv_stride_h : d->stride_h;
+    Strides s;
+    s.h = sh ? sh : d->head_dim;
+    s.n = sn ? sn : (int64_t)heads * d->head_dim;
+    s.b = 0;
+    return s;
+}
+
 float scale_of(const tkb_attn_desc* d) {
     return d->softmax_scale > 0.f ? d->softmax_scale : (float)(1.0 / std::sqrt((double)d->head_dim));
 }
@@ -247,14 +264,39 @@ int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, con
     return TKB_OK;
 }
 
+// Variable-length batches: the template of one packed tensor ([T, heads, D], strides s) is the
+// map of a single sequence of the maximum length at the tensor's base ({D, n_max, heads, 1});
+// varlen_maps_kernel copies it per sequence, re-pointed at cu[b] with n_b rows.
+int varlen_template(tkb::VarlenMapTemplates* t, int m, const void* base, const tkb_attn_desc* d, const Strides& s,
+                    int heads) {
+    tkb_attn_desc d1 = *d;
+    d1.batches = 1;
+    Strides s1 = s;
+    s1.b = s.n * d->seq;
+    if (int rc = make_bhnd_map(&t->tmpl[m], base, &d1, s1, heads)) return rc;
+    t->base[m] = (unsigned long long)(uintptr_t)base;
+    t->row_bytes[m] = s.n * 2;
+    return TKB_OK;
+}
+
+int varlen_maps(tkb::VarlenMapTemplates& t, const Varlen& vl, int batches, void* out, cudaStream_t st) {
+    const int e = tkb::launch_varlen_maps(t, vl.cu, batches, reinterpret_cast<CUtensorMap*>(out), st);
+    if (e) return fail(TKB_ERR_CUDA, std::string("varlen maps launch: ") + cudaGetErrorString((cudaError_t)e));
+    return TKB_OK;
+}
+
+size_t round256(size_t b) { return (b + 255) & ~(size_t)255; }
+size_t varlen_map_bytes(const tkb_attn_desc* d, int nmaps) { return (size_t)d->batches * nmaps * sizeof(CUtensorMap); }
+
 // The reference's non-finite input scan (kernels.hpp:277-284), opt-in: the flag lives in
 // this stream's state slot (no allocation); the result is read back synchronously.
 int finite_check(const tkb_attn_desc* d, const void* const* ptrs, int nptrs, const Strides& s, int heads,
-                 int* slot, cudaStream_t st) {
+                 int* slot, cudaStream_t st, const Varlen* vl = nullptr) {
     int* flag = slot + 2;
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
     if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("check_finite: ") + cudaGetErrorString(e));
-    int rc = tkb::launch_check_finite(ptrs, nptrs, d->batches, heads, d->seq, d->head_dim, s.b, s.h, s.n, flag, st);
+    int rc = vl ? tkb::launch_check_finite(ptrs, nptrs, 1, heads, (int)vl->total, d->head_dim, 0, s.h, s.n, flag, st)
+                : tkb::launch_check_finite(ptrs, nptrs, d->batches, heads, d->seq, d->head_dim, s.b, s.h, s.n, flag, st);
     int host = 0;
     e = cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaError_t e2 = cudaStreamSynchronize(st);
@@ -298,32 +340,66 @@ TKB_API int tkb_attn_validate(const tkb_attn_desc* d) {
     return TKB_OK;
 }
 
-TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, const void* v, void* o, float* lse,
-                         void* stream) {
+// Variable-length validation on top of tkb_attn_validate: packed layout (no batch strides),
+// cu_seqlens present, T within the 32-bit TMA coordinate range.
+static int varlen_validate(const tkb_attn_desc* d, const Varlen& vl) {
+    if (!vl.cu) return fail(TKB_ERR_BOUNDS, "null cu_seqlens");
+    if ((uintptr_t)vl.cu & 3) return fail(TKB_ERR_SHAPE, "cu_seqlens must be 4-byte aligned");
+    if (vl.total < 0 || vl.total >= (int64_t)INT32_MAX - d->seq)
+        return fail(TKB_ERR_CONFIG, "total_tokens must be in [0, 2^31 - max_seqlen)");
+    if (d->stride_b != 0 || d->kv_stride_b != 0)
+        return fail(TKB_ERR_SHAPE, "variable-length tensors are packed [T, H, D]: batch strides must be 0");
+    for (const Strides& s : {varlen_strides(d, false), varlen_strides(d, true)})
+        if (s.n < d->head_dim || (s.n % 8) || (s.h % 8))
+            return fail(TKB_ERR_SHAPE, "strides must be multiples of 8 elements (16 B) with rows >= head_dim");
+    return TKB_OK;
+}
+
+static int fwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, const void* k, const void* v, void* o,
+             float* lse, void* workspace, size_t workspace_bytes, void* stream) {
     g_launches = 0;
     int rc = tkb_attn_validate(d);
     if (rc) return rc;
+    if (vl && (rc = varlen_validate(d, *vl))) return rc;
+    if (vl && (!workspace || workspace_bytes < round256(varlen_map_bytes(d, tkb::kFwdMaps))))
+        return fail(TKB_ERR_BOUNDS, "varlen workspace missing or too small");
+    if (vl && ((uintptr_t)workspace & 127)) return fail(TKB_ERR_SHAPE, "varlen workspace must be 128-byte aligned");
     if (!q || !k || !v || !o) return fail(TKB_ERR_BOUNDS, "null tensor pointer");
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) & 15)
         return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
     if ((rc = check_device())) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const Strides s = strides_of(d);
-    const Strides skv = kv_strides_of(d);
+    const Strides s = vl ? varlen_strides(d, false) : strides_of(d);
+    const Strides skv = vl ? varlen_strides(d, true) : kv_strides_of(d);
     const int hkv = kv_heads_of(d);
     int sms = 0, *slot = nullptr;
     if ((rc = device_state(st, &sms, &slot))) return rc;
     if (d->check_finite) {
         const void* qp[1] = {q};
         const void* kvp[2] = {k, v};
-        if ((rc = finite_check(d, qp, 1, s, d->heads, slot, st)) ||
-            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st)))
+        if ((rc = finite_check(d, qp, 1, s, d->heads, slot, st, vl)) ||
+            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st, vl)))
             return rc;
     }
     tkb::FwdParams p{};
-    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
-        (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_o, o, d, s)))
+    int launches = 1;
+    if (vl) {  // per-sequence maps into the workspace (one small launch ahead of the attention)
+        tkb::VarlenMapTemplates t{};
+        t.nmaps = tkb::kFwdMaps;
+        if ((rc = varlen_template(&t, tkb::kMapQ, q, d, s, d->heads)) ||
+            (rc = varlen_template(&t, tkb::kMapK, k, d, skv, hkv)) ||
+            (rc = varlen_template(&t, tkb::kMapV, v, d, skv, hkv)) ||
+            (rc = varlen_template(&t, tkb::kMapO, o, d, s, d->heads)) ||
+            (rc = varlen_maps(t, *vl, d->batches, workspace, st)))
+            return rc;
+        p.tm_q = t.tmpl[tkb::kMapQ], p.tm_k = t.tmpl[tkb::kMapK], p.tm_v = t.tmpl[tkb::kMapV], p.tm_o = t.tmpl[tkb::kMapO];
+        p.vmaps = reinterpret_cast<const CUtensorMap*>(workspace);
+        ++launches;
+    } else if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
+               (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_o, o, d, s))) {
         return rc;
+    }
+    p.cu_seqlens = vl ? vl->cu : nullptr;
     p.group = d->heads / hkv;
     p.sched = slot;
     p.lse = lse;
@@ -335,8 +411,25 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, c
     p.scale_log2 = scale_of(d) * 1.44269504088896340736f;
     int e = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd launch: ") + cudaGetErrorString((cudaError_t)e));
-    g_launches = 1;
+    g_launches = launches;
     return TKB_OK;
+}
+
+TKB_API int tkb_attn_fwd(const tkb_attn_desc* d, const void* q, const void* k, const void* v, void* o, float* lse,
+                         void* stream) {
+    return fwd_impl(d, nullptr, q, k, v, o, lse, nullptr, 0, stream);
+}
+
+TKB_API size_t tkb_attn_fwd_varlen_workspace_bytes(const tkb_attn_desc* d) {
+    if (!d || d->batches < 1) return 0;
+    return round256(varlen_map_bytes(d, tkb::kFwdMaps));
+}
+
+TKB_API int tkb_attn_fwd_varlen(const tkb_attn_desc* d, const int32_t* cu_seqlens, int64_t total_tokens,
+                                const void* q, const void* k, const void* v, void* o, float* lse, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    const Varlen vl{cu_seqlens, total_tokens};
+    return fwd_impl(d, &vl, q, k, v, o, lse, workspace, workspace_bytes, stream);
 }
 
 // Fused rotary + forward (the rotary prologue of SURVEY §8(f) rank 2 folded into the forward
@@ -421,40 +514,65 @@ TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* d) {
     return (bytes + 255) & ~(size_t)255;
 }
 
-TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, const void* v, const void* o,
-                         const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
-                         size_t workspace_bytes, void* stream) {
+static int bwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, const void* k, const void* v, const void* o,
+             const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+             void* stream) {
     g_launches = 0;
     int rc = tkb_attn_validate(d);
     if (rc) return rc;
+    if (vl && (rc = varlen_validate(d, *vl))) return rc;
     if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv || !workspace)
         return fail(TKB_ERR_BOUNDS, "null pointer");
-    if (workspace_bytes < tkb_attn_bwd_workspace_bytes(d)) return fail(TKB_ERR_BOUNDS, "workspace too small");
+    const size_t map_bytes = vl ? round256(varlen_map_bytes(d, tkb::kBwdMaps)) : 0;  // per-sequence maps first
+    if (workspace_bytes < tkb_attn_bwd_workspace_bytes(d) + map_bytes)
+        return fail(TKB_ERR_BOUNDS, "workspace too small");
+    if (vl && ((uintptr_t)workspace & 127)) return fail(TKB_ERR_SHAPE, "varlen workspace must be 128-byte aligned");
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
          (uintptr_t)dk | (uintptr_t)dv | (uintptr_t)workspace) &
         15)
         return fail(TKB_ERR_SHAPE, "tensors must be 16-byte aligned");
     if ((rc = check_device())) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const Strides s = strides_of(d);
-    const Strides skv = kv_strides_of(d);
+    const Strides s = vl ? varlen_strides(d, false) : strides_of(d);
+    const Strides skv = vl ? varlen_strides(d, true) : kv_strides_of(d);
     const int hkv = kv_heads_of(d);
     int sms = 0, *slot = nullptr;
     if ((rc = device_state(st, &sms, &slot))) return rc;
     if (d->check_finite) {
         const void* qp[3] = {q, o, dout};
         const void* kvp[2] = {k, v};
-        if ((rc = finite_check(d, qp, 3, s, d->heads, slot, st)) ||
-            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st)))
+        if ((rc = finite_check(d, qp, 3, s, d->heads, slot, st, vl)) ||
+            (rc = finite_check(d, kvp, 2, skv, hkv, slot, st, vl)))
             return rc;
     }
     tkb::BwdParams p{};
-    if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
-        (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
-        (rc = make_bhnd_map(&p.tm_dq, dq, d, s)) || (rc = make_bhnd_map(&p.tm_dk, dk, d, skv, hkv)) ||
-        (rc = make_bhnd_map(&p.tm_dv, dv, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_q64, q, d, s, 0, 64)) ||
-        (rc = make_bhnd_map(&p.tm_do64, dout, d, s, 0, 64)))
+    int map_launches = 0;
+    if (vl) {  // per-sequence maps at the start of the workspace (one small launch ahead)
+        tkb::VarlenMapTemplates t{};
+        t.nmaps = tkb::kBwdMaps;
+        if ((rc = varlen_template(&t, tkb::kMapQ, q, d, s, d->heads)) ||
+            (rc = varlen_template(&t, tkb::kMapK, k, d, skv, hkv)) ||
+            (rc = varlen_template(&t, tkb::kMapV, v, d, skv, hkv)) ||
+            (rc = varlen_template(&t, tkb::kMapDo, dout, d, s, d->heads)) ||
+            (rc = varlen_template(&t, tkb::kMapDq, dq, d, s, d->heads)) ||
+            (rc = varlen_template(&t, tkb::kMapDk, dk, d, skv, hkv)) ||
+            (rc = varlen_template(&t, tkb::kMapDv, dv, d, skv, hkv)) ||
+            (rc = varlen_maps(t, *vl, d->batches, workspace, st)))
+            return rc;
+        p.tm_q = t.tmpl[tkb::kMapQ], p.tm_k = t.tmpl[tkb::kMapK], p.tm_v = t.tmpl[tkb::kMapV];
+        p.tm_do = t.tmpl[tkb::kMapDo], p.tm_dq = t.tmpl[tkb::kMapDq], p.tm_dk = t.tmpl[tkb::kMapDk];
+        p.tm_dv = t.tmpl[tkb::kMapDv];
+        p.vmaps = reinterpret_cast<const CUtensorMap*>(workspace);
+        workspace = static_cast<char*>(workspace) + map_bytes;
+        map_launches = 1;
+    } else if ((rc = make_bhnd_map(&p.tm_q, q, d, s)) || (rc = make_bhnd_map(&p.tm_k, k, d, skv, hkv)) ||
+               (rc = make_bhnd_map(&p.tm_v, v, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_do, dout, d, s)) ||
+               (rc = make_bhnd_map(&p.tm_dq, dq, d, s)) || (rc = make_bhnd_map(&p.tm_dk, dk, d, skv, hkv)) ||
+               (rc = make_bhnd_map(&p.tm_dv, dv, d, skv, hkv)) || (rc = make_bhnd_map(&p.tm_q64, q, d, s, 0, 64)) ||
+               (rc = make_bhnd_map(&p.tm_do64, dout, d, s, 0, 64))) {
         return rc;
+    }
+    p.cu_seqlens = vl ? vl->cu : nullptr;
     p.group = d->heads / hkv;
     const int64_t bh = (int64_t)d->batches * d->heads;
     const int npad = (d->seq + 127) / 128 * 128;
@@ -493,8 +611,27 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, c
     int e = tkb::launch_attn_bwd(d->head_dim, d->causal != 0, p, d->batches, o, dout, lse, lse2, delta, s.b, s.h,
                                  s.n, st, g_bwd_phases, &launches);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_bwd launch: ") + cudaGetErrorString((cudaError_t)e));
-    g_launches = launches;
+    g_launches = launches + map_launches;
     return TKB_OK;
+}
+
+TKB_API int tkb_attn_bwd(const tkb_attn_desc* d, const void* q, const void* k, const void* v, const void* o,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    return bwd_impl(d, nullptr, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, stream);
+}
+
+TKB_API size_t tkb_attn_bwd_varlen_workspace_bytes(const tkb_attn_desc* d) {
+    const size_t b = tkb_attn_bwd_workspace_bytes(d);
+    return b ? b + round256(varlen_map_bytes(d, tkb::kBwdMaps)) : 0;
+}
+
+TKB_API int tkb_attn_bwd_varlen(const tkb_attn_desc* d, const int32_t* cu_seqlens, int64_t total_tokens,
+                                const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                const float* lse, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+    const Varlen vl{cu_seqlens, total_tokens};
+    return bwd_impl(d, &vl, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, stream);
 }
 
 // RotaryConfig::validate (kernels.hpp:367-376) relaxed to the B200 layout: even head_dim,

@@ -30,6 +30,7 @@
 //   after their finish)
 //   static void init(shared&, const globals&)          barrier init, descriptor prefetch
 //   static int num_tasks(const globals&); static int* counter(const globals&)
+//   static bool skip(const globals&, int task)         optional: the task is empty (never dispatched)
 //   producer::state, producer::load(args, state&, task, n, claim_next), producer::drain
 //       (the LCSF load stage; claim_next() claims task n + 1 when the hook wants it —
 //        e.g. to warm its inputs in L2 — otherwise the skeleton claims after load returns)
@@ -86,9 +87,13 @@ struct work_queue {
             mbar_init(&empty[s], consumers);
         }
     }
-    // producer lane: claim the n-th task of this CTA (n = 0 is blockIdx.x) and publish it
-    TKB_DEVICE int claim(int n, int* counter, int total) {
+    // producer lane: claim the n-th task of this CTA (n = 0 is blockIdx.x) and publish it;
+    // ids for which skip(id) holds (empty tasks, e.g. query blocks past a short sequence of a
+    // variable-length batch) are passed over here, so no other role ever sees them
+    template <class Skip>
+    TKB_DEVICE int claim(int n, int* counter, int total, Skip&& skip) {
         int t = (n == 0) ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(counter, 1);
+        while (t < total && skip(t)) t = (int)gridDim.x + atomicAdd(counter, 1);
         if (t >= total) t = -1;
         const int s = n % kSlots;
         mbar_wait(&empty[s], ((n / kSlots) & 1) ^ 1u);
@@ -190,6 +195,16 @@ struct args {
     int warp, lane;
 };
 
+// optional hook: static bool T::skip(const globals&, int task) — the task has no work
+template <class T, class = void>
+struct has_skip {
+    static constexpr bool value = false;
+};
+template <class T>
+struct has_skip<T, decltype((void)T::skip(*(const typename T::globals*)nullptr, 0))> {
+    static constexpr bool value = true;
+};
+
 template <class T>
 __global__ void __launch_bounds__(T::kThreads, 1) kernel(const __grid_constant__ typename T::globals g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -220,11 +235,15 @@ __global__ void __launch_bounds__(T::kThreads, 1) kernel(const __grid_constant__
         if (lane == 0) {
             typename T::producer::state st{};
             int n = 0;
-            int t = sh.queue.claim(0, counter, total);
+            auto skip = [&](int id) {
+                if constexpr (has_skip<T>::value) return T::skip(g, id);
+                return false;
+            };
+            int t = sh.queue.claim(0, counter, total, skip);
             while (t >= 0) {
                 int next = -2;
                 auto claim_next = [&]() {
-                    if (next == -2) next = sh.queue.claim(n + 1, counter, total);
+                    if (next == -2) next = sh.queue.claim(n + 1, counter, total, skip);
                     return next;
                 };
                 T::producer::load(a, st, t, n, claim_next);

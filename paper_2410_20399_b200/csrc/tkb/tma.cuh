@@ -17,6 +17,14 @@ TKB_DEVICE void prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
 
+// A tensor map written in global memory by an earlier kernel (tensormap.replace, the
+// per-sequence maps of variable-length batches): invalidate this SM's cached copy of the
+// descriptor at that address before the calling thread's next TMA through it.
+TKB_DEVICE void acquire_map(const void* tmap) {
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(tmap))
+                 : "memory");
+}
+
 // L2 cache policies (createpolicy.fractional.L2::evict_*).
 TKB_DEVICE uint64_t policy_evict_first() {
     uint64_t p;

@@ -1,10 +1,14 @@
 // util_kernels.cu — small helper kernels of the hot path's boundary.
 //   check_finite: the reference's "task 0 scans all inputs for non-finite"
 //   (kernels.hpp:277-284), as an opt-in device scan (tkb_attn_desc.check_finite).
+//   varlen_maps: the per-sequence TMA maps of a variable-length batch (tensormap.replace).
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+
+#include "attn_common.cuh"
 
 namespace tkb {
 namespace {
@@ -35,7 +39,36 @@ __global__ void check_finite_kernel(FinitePtrs ptrs, int nptrs, int heads, int n
     }
 }
 
+// One thread per (sequence b, tensor m): copy the host-encoded template of tensor m (rows =
+// the maximum length over the packed tensor's base) into out[b][m], then point it at the
+// sequence — base += cu[b] * row_bytes, rows = n_b (>= 1; an empty sequence's map is never
+// used) — and release it to the tensor-map proxy. The kernels acquire each map before use.
+__global__ void varlen_maps_kernel(const __grid_constant__ VarlenMapTemplates t, const int* __restrict__ cu,
+                                   int batches, CUtensorMap* __restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= batches * t.nmaps) return;
+    const int b = idx / t.nmaps, m = idx - b * t.nmaps;
+    CUtensorMap* dst = out + idx;
+    const uint4* src = reinterpret_cast<const uint4*>(&t.tmpl[m]);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(CUtensorMap) / sizeof(uint4)); ++i) d[i] = src[i];
+    const int s0 = cu[b], s1 = cu[b + 1];
+    const unsigned rows = (unsigned)max(s1 - s0, 1);
+    const unsigned long long addr = t.base[m] + (unsigned long long)s0 * (unsigned long long)t.row_bytes[m];
+    asm volatile("tensormap.replace.tile.global_address.global.b1024.b64 [%0], %1;" ::"l"(dst), "l"(addr) : "memory");
+    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 1, %1;" ::"l"(dst), "r"(rows) : "memory");
+    asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+}
+
 }  // namespace
+
+int launch_varlen_maps(const VarlenMapTemplates& t, const int* cu, int batches, CUtensorMap* out, cudaStream_t stream) {
+    const int total = batches * t.nmaps;
+    if (total == 0) return 0;
+    varlen_maps_kernel<<<(total + 127) / 128, 128, 0, stream>>>(t, cu, batches, out);
+    return (int)cudaGetLastError();
+}
 
 int launch_check_finite(const void* const* ptrs, int nptrs, int batches, int heads, int n, int d, int64_t sb,
                         int64_t sh, int64_t sn, int* flag_dev, cudaStream_t stream) {

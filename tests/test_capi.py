@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s), s
     assert set(A.exported_symbols()) == set(declared_symbols())
-    assert A.lib().tkb_abi_version() == 3
+    assert A.lib().tkb_abi_version() == 4
 
 
 def test_library_is_built_for_sm100a():
@@ -143,3 +143,40 @@ def test_device_init_without_a_gpu_fails_cleanly():
     with pytest.raises(A.Error):
         A.device_init(0)
 
+
+
+def _varlen_call(d, cu=1 << 12, total=100, ptr=1 << 16, ws=1 << 20, ws_bytes=1 << 20):
+    return A.lib().tkb_attn_fwd_varlen(ctypes.byref(d), cu, total, ptr, ptr, ptr, ptr, None, ws, ws_bytes, None)
+
+
+def test_varlen_validation_without_a_gpu():
+    """Variable-length batches (tkb_attn_fwd_varlen): packed [T, H, D] only (batch strides 0),
+    cu_seqlens present and aligned, T inside the 32-bit TMA coordinate range — all checked
+    before any device work."""
+    d = A.AttentionConfig(3, 4, 512, 128).desc()
+    d.stride_b = 4 * 128 * 512
+    assert _varlen_call(d) == 2  # ShapeError: batch stride on a packed tensor
+    d = A.AttentionConfig(3, 4, 512, 128).desc()
+    assert A.lib().tkb_attn_fwd_varlen(ctypes.byref(d), None, 100, 1 << 16, 1 << 16, 1 << 16, 1 << 16, None,
+                                       1 << 20, 1 << 20, None) == 3  # BoundsError: null cu_seqlens
+    assert _varlen_call(d, ws=None) == 3 and _varlen_call(d, ws_bytes=3 * 4 * 128 - 1) == 3  # workspace
+    assert _varlen_call(d, ws=(1 << 20) + 64) == 2  # workspace not 128-byte aligned
+    # per-sequence maps: 4 (fwd) / 7 (bwd) 128-byte CUtensorMaps per sequence, rounded to 256
+    assert A.lib().tkb_attn_fwd_varlen_workspace_bytes(ctypes.byref(d)) == 1536
+    assert (A.lib().tkb_attn_bwd_varlen_workspace_bytes(ctypes.byref(d))
+            == A.lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(d)) + 2816)
+    assert _varlen_call(d, cu=(1 << 12) + 2) == 2  # misaligned cu_seqlens
+    assert _varlen_call(d, total=-1) == 1 and _varlen_call(d, total=1 << 31) == 1  # ConfigError
+    d.stride_n = 4 * 128 + 4  # token stride not a multiple of 8 elements
+    assert _varlen_call(d) == 2
+    d = A.AttentionConfig(3, 4, 512, 96).desc()
+    assert _varlen_call(d) == 1  # head_dim
+    d = A.AttentionConfig(3, 4, 512, 128).desc()
+    assert A.lib().tkb_attn_bwd_varlen(ctypes.byref(d), 1 << 12, 100, *([None] * 10), 0, None) == 3
+
+
+def test_varlen_python_mirror_rejects_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    x = torch.zeros(10, 2, 64, dtype=torch.bfloat16)
+    with pytest.raises(A.ConfigError):
+        A.attention_fwd_varlen(x, x, x, torch.tensor([0, 10], dtype=torch.int32), 10)
