@@ -1308,7 +1308,10 @@ struct attn_bwd_template {
 // HBM-bound: each thread owns 16 bytes of kPrepRows rows (rows kPrepRows * 16 / (D / 8) apart
 // within the block's row range) and issues all their loads before reducing, so a thread
 // keeps 2 * 16 * kPrepRows bytes in flight.
-constexpr int kPrepRows = 4;
+#ifndef TKB_PREP_ROWS
+#define TKB_PREP_ROWS 4
+#endif
+constexpr int kPrepRows = TKB_PREP_ROWS;
 // Linear blocks (bh, row block) are walked grid-stride with a 64-bit index: B * H is not
 // bounded by gridDim.y's 65535.
 template <int D>
