@@ -36,16 +36,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <type_traits>
-
 #include "attn_common.cuh"
 #include "tkb/cluster.cuh"
 #include "tkb/lcsf.cuh"
 #include "tkb/tile.cuh"
 
-#ifndef TKB_BWD_Q64
-#define TKB_BWD_Q64 0  // 1: D = 128 dK/dV on 64-query sub-steps with K / V in TMEM (experiment: 15 % slower)
-#endif
 #ifndef TKB_BWD_POLY
 #define TKB_BWD_POLY 1  // exponential pairs of every four on the FMA-pipe polynomial (1: a quarter)
 #endif
@@ -630,364 +625,6 @@ struct attn_bwd_dkdv_template {
             if (threadIdx.x == 0) TKB_TR(1, n, 6);
         }
         static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dkdv_template>&, state&) {}
-    };
-};
-
-// ================================================================== bwd_dkdv, 64-query sub-steps (D = 128)
-// The single-CTA kernel above runs S^T = K Q^T and dP^T = V dO^T as SS MMAs: each re-reads the
-// 4 KB K / V slice from SMEM per K-step, so a 128-query step moves 256 KB through the 128 B/clk
-// SMEM port (2048 clk — the step's whole MMA time). Here K and V are copied into TMEM once per
-// task and those two GEMMs become TS MMAs that read only Q / dO from SMEM. TMEM then holds
-// K | V (64 bf16-pair columns each) | S^T | dP^T | dV | dK, which leaves 64 columns for S^T and
-// dP^T: the queries advance in 64-row sub-steps (N = 64 MMAs, 2 KB of B per 32 clk), and a
-// 128-query block costs 192 KB of port traffic instead of 256 KB. Per sub-step x:
-//   S^T_x = K Q_x^T (TS) -> P^T_x (bf16, in place) -> dV += P^T_x dO_x (TS, dO MN-major)
-//   dP^T_x = V dO_x^T (TS) -> dS^T_x (bf16, in place) -> dK += dS^T_x Q_x (TS, Q MN-major)
-// issued in the order S_x, dP_x | dV_x, S_{x+1}, dK_x, dP_{x+1} | ... (a region is overwritten
-// only by a GEMM issued after the one reading it). Compute thread = (TMEM lane = kv row, 16-query
-// column group g). The K / V SMEM buffers double as the finish's dK / dV staging: finish(n) first
-// copies task n+1's K / V (already loaded) into TMEM, then stages dV / dK there; the load warp
-// TMA-stores them before loading task n+2's K / V. Same tasks, queue and results contract as
-// attn_bwd_dkdv_template (reads the same perm32-ordered lse / Delta workspace).
-template <bool CAUSAL>
-struct attn_bwd_dkdv_q64_template {
-    static constexpr int D = 128;
-    using Base = attn_bwd_dkdv_template<D, CAUSAL>;
-    using TL = Tiles<D>;
-    using globals = BwdParams;
-    using Sub = st_bf<64, D>;  // a 64-query Q / dO sub-block (16 KB, two SW128 atoms)
-    static constexpr int kSubBytes = Sub::kBytes;
-    static constexpr int SQ = 4, SD = 4, SA = 4;  // Q / dO / lse-Delta rings (sub-blocks)
-    static constexpr int kThreads = bwd::kThreads;
-    static constexpr int kTmemCols = 512;
-    static constexpr int kProducerWarp = kWarpLoad;
-    static constexpr int kMmaWarp = bwd::kWarpMma;
-    static constexpr int kConsumerWarps = 16;
-    static constexpr int kQueueReaders = 1 + 16;
-    static constexpr bool kAlignSlack = false;
-    static constexpr bool kReleaseEarly = false;
-    static constexpr int kAuxWarps = 0, kAuxWarp0 = 0;
-    static constexpr uint32_t kTK = 0, kTV = 64, kTS = 128, kTDp = 192, kTDv = 256, kTDk = 384;
-
-    struct shared {
-        uint8_t k[TL::kTileBytes];  // K of the next task to copy into TMEM, then dK staging
-        uint8_t v[TL::kTileBytes];  // V, then dV staging
-        uint8_t q[SQ][kSubBytes];
-        uint8_t dO[SD][kSubBytes];
-        float lse[SA][64];    // -lse2 of the sub-block's queries (perm32 order)
-        float delta[SA][64];  // Delta (perm32 order)
-        mbarrier kv_full;      // K / V of a task in SMEM
-        mbarrier kv_free;      // the first task's K / V are in TMEM: the second task's may load
-        mbarrier staged_full;  // a finish staged dV / dK in sV / sK
-        mbarrier stored;       // the load warp's TMA store of a staged dV / dK has read SMEM
-        mbarrier a_ready;      // a task's K / V are in TMEM
-        mbarrier ka_free;      // the task's last S^T / dP^T retired: TMEM K / V reusable
-        mbarrier s_full, dp_full;
-        mbarrier dv_free, dk_free, dkv_full;
-        mbarrier q_full[SQ], q_empty[SQ];
-        mbarrier do_full[SD], do_empty[SD];
-        mbarrier aux_full[SA], aux_empty[SA];
-        mbarrier p_full[kGroups], ds_full[kGroups];
-        lcsf::work_queue queue;
-        uint32_t tmem_slot;
-    };
-    static constexpr int kSmemBytes = (int)sizeof(shared);
-    static_assert(kSmemBytes <= 232448, "smem");
-
-    static TKB_DEVICE int num_tasks(const globals& p) { return Base::num_tasks(p); }
-    static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
-    static TKB_DEVICE KvTask decode(const globals& p, int id) { return Base::decode(p, id); }
-    static TKB_DEVICE bool skip(const globals& p, int id) { return Base::skip(p, id); }
-    static TKB_DEVICE int sub_steps(const globals& p, const KvTask& w) { return 2 * Base::steps(p, w); }
-    // sub-step t of a task -> (query head, query block, half)
-    struct SubPos {
-        int hq, i, h;
-    };
-    static TKB_DEVICE SubPos sub_pos(const globals& p, const KvTask& w, int T, int t) {
-        const int per_head = T / p.group;  // 2 x query blocks
-        const int r = t % per_head;
-        return SubPos{w.head * p.group + t / per_head, (CAUSAL ? w.j : 0) + r / 2, r & 1};
-    }
-    static TKB_DEVICE Sub tQ(shared& sh, int x) { return Sub{sh.q[x % SQ]}; }
-    static TKB_DEVICE Sub tDo(shared& sh, int x) { return Sub{sh.dO[x % SD]}; }
-
-    static TKB_DEVICE void init(shared& sh, const globals& p) {
-        mbar_init(&sh.kv_full, 1);
-        mbar_init(&sh.kv_free, 1);
-        mbar_init(&sh.staged_full, kComputeThreads);
-        mbar_init(&sh.stored, 1);
-        mbar_init(&sh.a_ready, kComputeThreads);
-        mbar_init(&sh.ka_free, 1);
-        mbar_init(&sh.s_full, 1);
-        mbar_init(&sh.dp_full, 1);
-        mbar_init(&sh.dv_free, kComputeThreads);
-        mbar_init(&sh.dk_free, kComputeThreads);
-        mbar_init(&sh.dkv_full, 1);
-        for (int s = 0; s < SQ; ++s) mbar_init(&sh.q_full[s], 1), mbar_init(&sh.q_empty[s], 1);
-        for (int s = 0; s < SD; ++s) mbar_init(&sh.do_full[s], 1), mbar_init(&sh.do_empty[s], 1);
-        for (int s = 0; s < SA; ++s) mbar_init(&sh.aux_full[s], 1), mbar_init(&sh.aux_empty[s], 1);
-        for (int g = 0; g < kGroups; ++g) mbar_init(&sh.p_full[g], 128), mbar_init(&sh.ds_full[g], 128);
-        tma::prefetch_desc(&p.tm_q64);
-        tma::prefetch_desc(&p.tm_k);
-        tma::prefetch_desc(&p.tm_v);
-        tma::prefetch_desc(&p.tm_do64);
-    }
-
-    // ------------------------------------------------------------- LOAD
-    struct producer {
-        struct state {
-            int x = 0;      // global sub-step (ring position)
-            int tasks = 0;  // tasks loaded
-            KvTask hist[2];  // the last two tasks (their dV / dK are stored two tasks later)
-        };
-        // TMA-store the dV / dK of task m that its finish staged in sV / sK, then release them
-        static TKB_DEVICE void store_staged(const globals& p, shared& sh, state& ps, int m) {
-            mbar_wait(&sh.staged_full, m & 1);
-            const KvTask& pw = ps.hist[m & 1];
-            pw.sv.with_map(p.tm_dv, kMapDv, [&](const CUtensorMap* mp) {
-                store_async(gl{mp}, Tile<D>{sh.v}, pw.j * 128, pw.head, pw.sv.bcoord);
-            });
-            pw.sv.with_map(p.tm_dk, kMapDk, [&](const CUtensorMap* mp) {
-                store_async(gl{mp}, Tile<D>{sh.k}, pw.j * 128, pw.head, pw.sv.bcoord);
-            });
-            tma::commit_group();
-            tma::wait_group_read<0>();
-            mbar_arrive(&sh.stored);
-        }
-        template <class ClaimNext>
-        static TKB_DEVICE void load(const lcsf::args<attn_bwd_dkdv_q64_template>& a, state& ps, int id, int n,
-                                    ClaimNext&&) {
-            const globals& p = a.g;
-            shared& sh = a.sh;
-            const uint64_t pol_stream = tma::policy_evict_first();
-            const uint64_t pol_keep = tma::policy_evict_last();
-            const KvTask w = decode(p, id);
-            const int T = sub_steps(p, w);
-            if (w.sv.maps != nullptr) {  // this sequence's maps (varlen_maps_kernel)
-                for (int m = 0; m < kBwdMaps; ++m) tma::acquire_map(w.sv.maps + m);
-            }
-            // K / V: the first task at once; the second once the first's K / V are in TMEM; task n
-            // >= 2 once the finish of task n - 2 staged its dV / dK in sV / sK and they are stored
-            if (n == 1) mbar_wait(&sh.kv_free, 0);
-            if (n >= 2) store_staged(p, sh, ps, n - 2);
-            mbar_arrive_expect_tx(&sh.kv_full, 2 * TL::kTileBytes);
-            w.sv.with_map(p.tm_k, kMapK, [&](const CUtensorMap* m) {
-                load_async(Tile<D>{sh.k}, gl{m}, &sh.kv_full, w.j * 128, w.head, w.sv.bcoord, pol_stream);
-            });
-            w.sv.with_map(p.tm_v, kMapV, [&](const CUtensorMap* m) {
-                load_async(Tile<D>{sh.v}, gl{m}, &sh.kv_full, w.j * 128, w.head, w.sv.bcoord, pol_stream);
-            });
-            for (int t = 0; t < T; ++t, ++ps.x) {
-                const int x = ps.x;
-                const SubPos sp = sub_pos(p, w, T, t);
-                const int row = sp.i * 128 + 64 * sp.h;
-                const size_t bhq = (size_t)w.batch * p.heads + sp.hq;
-                const int sq = x % SQ, sd = x % SD, sa = x % SA;
-                mbar_wait(&sh.q_empty[sq], ((x / SQ) & 1) ^ 1);
-                mbar_arrive_expect_tx(&sh.q_full[sq], kSubBytes);
-                w.sv.with_map(p.tm_q64, kMapQ64, [&](const CUtensorMap* m) {
-                    load_async(tQ(sh, x), gl{m}, &sh.q_full[sq], row, sp.hq, w.sv.bcoord, pol_keep);
-                });
-                mbar_wait(&sh.do_empty[sd], ((x / SD) & 1) ^ 1);
-                mbar_arrive_expect_tx(&sh.do_full[sd], kSubBytes);
-                w.sv.with_map(p.tm_do64, kMapDo64, [&](const CUtensorMap* m) {
-                    load_async(tDo(sh, x), gl{m}, &sh.do_full[sd], row, sp.hq, w.sv.bcoord, pol_keep);
-                });
-                mbar_wait(&sh.aux_empty[sa], ((x / SA) & 1) ^ 1);
-                mbar_arrive_expect_tx(&sh.aux_full[sa], 512);
-                tma::load_1d(sh.lse[sa], p.lse2 + bhq * p.n_pad + row, 256, &sh.aux_full[sa]);
-                tma::load_1d(sh.delta[sa], p.delta + bhq * p.n_pad + row, 256, &sh.aux_full[sa]);
-            }
-            ps.hist[n & 1] = w;
-            ps.tasks = n + 1;
-        }
-        static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dkdv_q64_template>& a, state& ps) {
-            for (int m = max(0, ps.tasks - 2); m < ps.tasks; ++m) store_staged(a.g, a.sh, ps, m);
-            tma::wait_group<0>();
-        }
-    };
-
-    // ------------------------------------------------------------- MMA (converged warp)
-    struct mma {
-        struct state {
-            int x0 = 0;
-        };
-        static TKB_DEVICE void issue(const lcsf::args<attn_bwd_dkdv_q64_template>& a, state& ms, int id, int n) {
-            const globals& p = a.g;
-            shared& sh = a.sh;
-            const uint32_t tb = a.tmem;
-            const tt_bf<D / 2> tKa{tb + kTK}, tVa{tb + kTV};
-            auto issue_s = [&](int x) {  // S^T = K Q^T (TS: K in TMEM)
-                mbar_wait(&sh.q_full[x % SQ], (x / SQ) & 1);
-                tmem::fence_after();
-                mm_ABt(tt_fl<64>{tb + kTS}, tKa, tQ(sh, x));
-                mma_commit(&sh.s_full);
-            };
-            auto issue_dp = [&](int x) {  // dP^T = V dO^T (TS: V in TMEM)
-                mbar_wait(&sh.do_full[x % SD], (x / SD) & 1);
-                tmem::fence_after();
-                mm_ABt(tt_fl<64>{tb + kTDp}, tVa, tDo(sh, x));
-                mma_commit(&sh.dp_full);
-            };
-            const int T = sub_steps(p, decode(p, id));
-            const int x0 = ms.x0;
-            mbar_wait(&sh.a_ready, n & 1);  // this task's K / V are in TMEM
-            tmem::fence_after();
-            issue_s(x0);
-            issue_dp(x0);
-            if (T == 1) mma_commit(&sh.ka_free);
-            for (int t = 0; t < T; ++t) {
-                const int x = x0 + t;
-                const uint32_t ph = x & 1;
-                if (t == 0 && n > 0) mbar_wait(&sh.dv_free, (n - 1) & 1);  // previous task's dV read out
-                // dV += P^T dO (P^T: 16-query chunks as they land, dO read MN-major)
-                mma_AB_chunks16(tt_fl<D>{tb + kTDv}, tb + kTS, swap_layout(tDo(sh, x)), t > 0, [&](int g) {
-                    mbar_wait(&sh.p_full[g], ph);
-                    tmem::fence_after();
-                });
-                mma_commit(&sh.do_empty[x % SD]);
-                if (t + 1 < T) issue_s(x + 1);  // overwrites P^T_x, read by dV_x issued before
-                if (t == 0 && n > 0) mbar_wait(&sh.dk_free, (n - 1) & 1);
-                // dK += dS^T Q
-                mma_AB_chunks16(tt_fl<D>{tb + kTDk}, tb + kTDp, swap_layout(tQ(sh, x)), t > 0, [&](int g) {
-                    mbar_wait(&sh.ds_full[g], ph);
-                    tmem::fence_after();
-                });
-                mma_commit(&sh.q_empty[x % SQ]);
-                mma_commit(&sh.aux_empty[x % SA]);  // dK_x waited for the last dS of sub-step x
-                if (t + 1 < T) {
-                    issue_dp(x + 1);  // overwrites dS^T_x, read by dK_x issued before
-                    if (t + 2 == T) mma_commit(&sh.ka_free);  // the task's last S^T / dP^T issued
-                }
-            }
-            mma_commit(&sh.dkv_full);
-            ms.x0 += T;
-        }
-    };
-
-    // ------------------------------------------------------------- COMPUTE + FINISH
-    struct consumer {
-        struct state {
-            int x0 = 0;
-        };
-        // K / V of task m: SMEM -> registers -> TMEM A operands, once task m - 1's last S^T /
-        // dP^T retired (thread = row r, D / 4 columns of group g)
-        static TKB_DEVICE void stage(const lcsf::args<attn_bwd_dkdv_q64_template>& a, int m) {
-            shared& sh = a.sh;
-            const int wq = a.warp & 3, g = a.warp >> 2, r = wq * 32 + a.lane;
-            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-            mbar_wait(&sh.kv_full, m & 1);
-            if (m > 0) mbar_wait(&sh.ka_free, (m - 1) & 1);
-            tmem::fence_after();
-            smem_rows_to_tmem_a<D>(Tile<D>{sh.k}, a.tmem + lane_off + kTK, r, g);
-            smem_rows_to_tmem_a<D>(Tile<D>{sh.v}, a.tmem + lane_off + kTV, r, g);
-            tmem::wait_st();
-            tmem::fence_before();
-            mbar_arrive(&sh.a_ready);
-        }
-        // this thread's 16 queries of a 64-query sub-block from a perm32-ordered vector: an
-        // LDS.128 at 32 G + 8 m + 4 h' holds queries 16 h' + 2 m + {0, 1, 8, 9} of group G
-        static TKB_DEVICE void vec16(const float* base, int g, float* out) {
-            const uint32_t a0 = smem_u32(base + 32 * (g >> 1) + 4 * (g & 1));
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const float4 v = lds_f4(a0 + 32u * m);
-                out[2 * m] = v.x, out[2 * m + 1] = v.y, out[2 * m + 8] = v.z, out[2 * m + 9] = v.w;
-            }
-        }
-        static TKB_DEVICE void compute(const lcsf::args<attn_bwd_dkdv_q64_template>& a, state& cs, int id, int n) {
-            const globals& p = a.g;
-            shared& sh = a.sh;
-            const int wq = a.warp & 3;
-            const int g = a.warp >> 2;  // query columns [16 g, 16 g + 16) of the sub-block
-            const int r = wq * 32 + a.lane;
-            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-            const uint32_t tS = a.tmem + lane_off + kTS + 16 * g;
-            const uint32_t tDp = a.tmem + lane_off + kTDp + 16 * g;
-            const float tau = p.scale_log2;
-            if (n == 0) {
-                stage(a, 0);
-                named_sync(kBarCompute, kComputeThreads);
-                if (threadIdx.x == 0) mbar_arrive(&sh.kv_free);  // sK / sV free for the second task
-            }
-            const KvTask w = decode(p, id);
-            const int T = sub_steps(p, w);
-            for (int t = 0; t < T; ++t) {
-                const int x = cs.x0 + t;
-                const int sa = x % SA;
-                const SubPos sp = sub_pos(p, w, T, t);
-                mbar_wait(&sh.aux_full[sa], (x / SA) & 1);
-                float nlse[16], dlt[16];
-                vec16(sh.lse[sa], g, nlse);
-                vec16(sh.delta[sa], g, dlt);
-                mbar_wait(&sh.s_full, x & 1);
-                tmem::fence_after();
-                float pf[16];
-                tmem::ldw_32x32b_x16(tS, reinterpret_cast<uint32_t*>(pf));
-#pragma unroll
-                for (int c = 0; c < 16; c += 2) {  // P^T = exp2(tau S^T - lse2); pairs 3 and 7 on the FMA pipe
-                    const float2 xx = fma2(make_float2(pf[c], pf[c + 1]), make_float2(tau, tau),
-                                           make_float2(nlse[c], nlse[c + 1]));
-                    float2 y;
-                    if (((c >> 1) & 3) >= 4 - TKB_BWD_POLY) {
-                        y = ex2_poly2(xx);
-                    } else {
-                        y.x = ex2_approx(xx.x);
-                        y.y = ex2_approx(xx.y);
-                    }
-                    pf[c] = y.x, pf[c + 1] = y.y;
-                }
-                if (CAUSAL && sp.i == w.j) {  // diagonal block: query < kv row is masked
-                    const int q0 = 64 * sp.h + 16 * g;
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) pf[c] = (q0 + c < r) ? 0.f : pf[c];
-                }
-                uint32_t pk[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) pk[k] = pack_bf16x2(pf[2 * k], pf[2 * k + 1]);
-                tmem::st_32x32b_x8(tS, pk);  // the group's first 8 columns: its 16-query A chunk
-                tmem::wait_st();
-                tmem::fence_before();
-                mbar_arrive(&sh.p_full[g]);
-                mbar_wait(&sh.dp_full, x & 1);
-                tmem::fence_after();
-                uint32_t dpv[16];
-                tmem::ldw_32x32b_x16(tDp, dpv);
-#pragma unroll
-                for (int c = 0; c < 16; c += 2) {  // dS^T = P^T o (dP^T - Delta) (scale at the finish)
-                    const float2 gg = sub2(make_float2(__uint_as_float(dpv[c]), __uint_as_float(dpv[c + 1])),
-                                           make_float2(dlt[c], dlt[c + 1]));
-                    const float2 d = mul2(make_float2(pf[c], pf[c + 1]), gg);
-                    pk[c / 2] = pack_bf16x2(d.x, d.y);
-                }
-                tmem::st_32x32b_x8(tDp, pk);
-                tmem::wait_st();
-                tmem::fence_before();
-                mbar_arrive(&sh.ds_full[g]);
-            }
-            cs.x0 += T;
-        }
-        // FINISH: the next task's K / V into TMEM first (its first S^T / dP^T then overlap this
-        // finish), then dV / dK -> bf16 -> sV / sK (free now) for the load warp's TMA store
-        static TKB_DEVICE void finish(const lcsf::args<attn_bwd_dkdv_q64_template>& a, state&, int, int n) {
-            const globals& p = a.g;
-            shared& sh = a.sh;
-            const int wq = a.warp & 3, g = a.warp >> 2, r = wq * 32 + a.lane;
-            const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-            if (a.queue.get_warp(n + 1) >= 0) stage(a, n + 1);
-            if (n > 0) mbar_wait(&sh.stored, (n - 1) & 1);  // the previous finish's staging was stored
-            mbar_wait(&sh.dkv_full, n & 1);
-            tmem::fence_after();
-            tmem_rows_to_smem_bf16<D>(a.tmem + lane_off + kTDv, Tile<D>{sh.v}, r, g);
-            tmem::fence_before();
-            mbar_arrive(&sh.dv_free);
-            tmem_rows_to_smem_bf16<D>(a.tmem + lane_off + kTDk, Tile<D>{sh.k}, r, g, p.scale);  // dK = scale dS^T Q
-            tmem::fence_before();
-            mbar_arrive(&sh.dk_free);
-            tma::fence_async_smem();
-            mbar_arrive(&sh.staged_full);
-        }
-        static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dkdv_q64_template>&, state&) {}
     };
 };
 
@@ -1660,8 +1297,7 @@ struct attn_bwd_dq_template {
 // kernels lcsf::kernel<dkdv> (KV-stationary) and lcsf::kernel<dq> (Q-stationary).
 template <int D, bool CAUSAL>
 struct attn_bwd_template {
-    using dkdv = typename std::conditional<D == 128 && TKB_BWD_Q64, attn_bwd_dkdv_q64_template<CAUSAL>,
-                                           attn_bwd_dkdv_template<D, CAUSAL>>::type;
+    using dkdv = attn_bwd_dkdv_template<D, CAUSAL>;
     using dq = attn_bwd_dq_template<D, CAUSAL>;
 };
 

@@ -349,22 +349,6 @@ TKB_DEVICE void mma_AB_groups(const tt_fl<N>& d, const tt_bf<128>& a, const st_m
     }
 }
 
-// Grouped-A form for K = 64 (a 64-query sub-block): chunk g (16 K-values) is bf16 in the 8
-// packed columns [a_col + 16 g, a_col + 16 g + 8) (written in place by compute column group g
-// over the 16 fp32 columns it read); issued as soon as wait_chunk(g) returns.
-template <int N, class WaitChunk>
-TKB_DEVICE void mma_AB_chunks16(const tt_fl<N>& d, uint32_t a_col, const st_mn<64, N>& b, bool accumulate,
-                                WaitChunk&& wait_chunk) {
-    constexpr uint32_t idesc = umma::idesc_bf16<128, N, false, true>();
-    constexpr uint32_t hi = umma::desc_hi_sw128(1024);
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        wait_chunk(g);
-        umma::mma_ts_e(d.addr, a_col + 16 * g, umma::desc_lo(detail::mnmajor_step(b, g), st_bf<64, N>::kAtomBytes),
-                       hi, idesc, (accumulate || g > 0) ? 1u : 0u);
-    }
-}
-
 // tcgen05.commit: `bar` gets one arrival when every MMA this thread issued so far retired
 // (warp-converged; the elected lane commits)
 TKB_DEVICE void mma_commit(mbarrier* bar) { umma::commit_e(bar); }
