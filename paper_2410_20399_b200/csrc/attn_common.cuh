@@ -69,9 +69,8 @@ __device__ __forceinline__ SeqView seq_view(const int* cu, const CUtensorMap* vm
 }
 // per-sequence map slots
 constexpr int kFwdMaps = 4;  // q, k, v, o
-constexpr int kBwdMaps = 9;  // q, k, v, do, dq, dk, dv, and q / do with a 64-row box
-enum { kMapQ = 0, kMapK = 1, kMapV = 2, kMapO = 3, kMapDo = 3, kMapDq = 4, kMapDk = 5, kMapDv = 6, kMapQ64 = 7,
-       kMapDo64 = 8 };
+constexpr int kBwdMaps = 7;  // q, k, v, do, dq, dk, dv
+enum { kMapQ = 0, kMapK = 1, kMapV = 2, kMapO = 3, kMapDo = 3, kMapDq = 4, kMapDk = 5, kMapDv = 6 };
 
 // Builds [B][nmaps] per-sequence maps from host-encoded templates over the packed tensors
 // ({D, n_max, H, 1}): base += cu[b] * row_bytes, rows = n_b.

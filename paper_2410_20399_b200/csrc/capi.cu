@@ -268,12 +268,12 @@ int make_bhnd_map(CUtensorMap* tm, const void* base, const tkb_attn_desc* d, con
 // map of a single sequence of the maximum length at the tensor's base ({D, n_max, heads, 1});
 // varlen_maps_kernel copies it per sequence, re-pointed at cu[b] with n_b rows.
 int varlen_template(tkb::VarlenMapTemplates* t, int m, const void* base, const tkb_attn_desc* d, const Strides& s,
-                    int heads, uint32_t box_rows = 128) {
+                    int heads) {
     tkb_attn_desc d1 = *d;
     d1.batches = 1;
     Strides s1 = s;
     s1.b = s.n * d->seq;
-    if (int rc = make_bhnd_map(&t->tmpl[m], base, &d1, s1, heads, box_rows)) return rc;
+    if (int rc = make_bhnd_map(&t->tmpl[m], base, &d1, s1, heads)) return rc;
     t->base[m] = (unsigned long long)(uintptr_t)base;
     t->row_bytes[m] = s.n * 2;
     return TKB_OK;
@@ -557,13 +557,11 @@ static int bwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, con
             (rc = varlen_template(&t, tkb::kMapDq, dq, d, s, d->heads)) ||
             (rc = varlen_template(&t, tkb::kMapDk, dk, d, skv, hkv)) ||
             (rc = varlen_template(&t, tkb::kMapDv, dv, d, skv, hkv)) ||
-            (rc = varlen_template(&t, tkb::kMapQ64, q, d, s, d->heads, 64)) ||
-            (rc = varlen_template(&t, tkb::kMapDo64, dout, d, s, d->heads, 64)) ||
             (rc = varlen_maps(t, *vl, d->batches, workspace, st)))
             return rc;
         p.tm_q = t.tmpl[tkb::kMapQ], p.tm_k = t.tmpl[tkb::kMapK], p.tm_v = t.tmpl[tkb::kMapV];
         p.tm_do = t.tmpl[tkb::kMapDo], p.tm_dq = t.tmpl[tkb::kMapDq], p.tm_dk = t.tmpl[tkb::kMapDk];
-        p.tm_dv = t.tmpl[tkb::kMapDv], p.tm_q64 = t.tmpl[tkb::kMapQ64], p.tm_do64 = t.tmpl[tkb::kMapDo64];
+        p.tm_dv = t.tmpl[tkb::kMapDv];
         p.vmaps = reinterpret_cast<const CUtensorMap*>(workspace);
         workspace = static_cast<char*>(workspace) + map_bytes;
         map_launches = 1;

@@ -124,7 +124,7 @@ struct rt_bf {
 template <int R, int C>
 TKB_DEVICE void load_async(const st_bf<R, C>& dst, const gl& src, mbarrier* bar, int row, int head, int batch,
                            uint64_t policy) {
-    static_assert(R == 128 || R == 64, "TMA box of 128 or 64 rows (the map's box must match R)");
+    static_assert(R == 128, "TMA box is 128 rows");
 #pragma unroll
     for (int a = 0; a < st_bf<R, C>::kAtoms; ++a) tma::load_4d(dst.atom(a), src.tm, bar, a * 64, row, head, batch, policy);
 }
