@@ -294,30 +294,32 @@ struct attn_bwd_dkdv_template {
     static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
     static TKB_DEVICE KvTask decode(const globals& p, int id) {
         const int nq = p.n_pad / 128;
-        const int hkv = p.heads / p.group;
-        const int hb = hkv * (p.bh / p.heads);  // (batch, kv head) units
-        const int G = (num_tasks(p) < 4 * p.num_sms) ? hb : max(1, min(hb, p.head_group / max(1, p.group)));
+        const int hkv = p.kv_hkv.d;
+        const int hb = p.kv_units;  // (batch, kv head) units
+        const int G = p.kv_G;  // fill_bwd_divisors: all units when < 4 tasks per SM, else L2-sized groups
         KvTask w;
         int unit;
-        if (CAUSAL) {
-            const int sec = id / (G * nq);
+        if (CAUSAL) {  // divisions through FastDiv: no MUFU.RCP behind the compute warps' exponentials
+            const int sec = p.kv_sec.div(id);
             const int r = id - sec * G * nq;
-            const int gs = min(G, hb - sec * G);
-            w.j = r / gs;
+            const bool full = hb - sec * G >= G;
+            const int gs = full ? G : hb - sec * G;
+            w.j = full ? p.kv_g.div(r) : p.kv_grem.div(r);
             unit = sec * G + (r - w.j * gs);
         } else {
-            w.j = id % nq;
-            unit = id / nq;
+            unit = p.kv_nq.div(id);
+            w.j = id - unit * nq;
         }
-        w.head = unit % hkv;
-        w.batch = unit / hkv;
+        w.batch = p.kv_hkv.div(unit);
+        w.head = unit - w.batch * hkv;
         w.sv = seq_view(p.cu_seqlens, p.vmaps, kBwdMaps, p.n, w.batch);
         return w;
     }
-    static TKB_DEVICE int steps(const globals& p, const KvTask& w) {
-        const int nb = (w.sv.n + 127) / 128;  // query blocks of this sequence
-        return (CAUSAL ? (nb - w.j) : nb) * p.group;
+    static TKB_DEVICE int q_blocks(const KvTask& w) {  // query blocks a task visits per query head
+        const int nb = (w.sv.n + 127) / 128;              // query blocks of this sequence
+        return CAUSAL ? (nb - w.j) : nb;
     }
+    static TKB_DEVICE int steps(const globals& p, const KvTask& w) { return q_blocks(w) * p.group; }
     // variable-length batches: kv blocks past a short sequence have no work
     static TKB_DEVICE bool skip(const globals& p, int id) {
         if (p.cu_seqlens == nullptr) return false;
@@ -375,7 +377,7 @@ struct attn_bwd_dkdv_template {
             const uint64_t pol_stream = tma::policy_evict_first();
             const uint64_t pol_keep = tma::policy_evict_last();
             const KvTask w = decode(p, id);
-            const int T = steps(p, w), T1 = T / p.group;
+            const int T = steps(p, w), T1 = q_blocks(w);
             const int kv0 = w.j * 128;
             if (w.sv.maps != nullptr) {  // this sequence's maps (varlen_maps_kernel); dV / dK: its finish
                 for (int m = 0; m < kBwdMaps; ++m) tma::acquire_map(w.sv.maps + m);
@@ -389,10 +391,10 @@ struct attn_bwd_dkdv_template {
                 load_async(Tile<D>{sh.v}, gl{m}, &sh.kv_full, kv0, w.head, w.sv.bcoord, pol_stream);
             });
             const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
+            int ti = 0, hq = w.head * p.group;  // step t = (query head hq, its ti-th query block)
             for (int t = 0; t < T; ++t, ++ps.x) {
                 const int x = ps.x;
-                const int i = (CAUSAL ? w.j : 0) + t % T1;
-                const int hq = w.head * p.group + t / T1;
+                const int i = (CAUSAL ? w.j : 0) + ti;
                 const size_t bhq = (size_t)w.batch * p.heads + hq;
                 // in pipe order of the GEMMs that free the slots: dK_{x-SQ}, dV_{x-SD}, dK_{x-SA}
                 const int sq = x % SQ, sd = x % SD, sa = x % SA;
@@ -423,6 +425,7 @@ struct attn_bwd_dkdv_template {
                 w.sv.with_map(p.tm_do, kMapDo, [&](const CUtensorMap* m) {
                     load_async(tDo(sh, x), gl{m}, &sh.do_full[sd], i * 128, hq, w.sv.bcoord, pol_keep);
                 });
+                if (++ti == T1) ti = 0, ++hq;
                 mbar_wait(&sh.aux_empty[sa], ((x / SA) & 1) ^ 1);
                 mbar_arrive_expect_tx(&sh.aux_full[sa], 1024);
                 tma::load_1d(sh.lse[sa], p.lse2 + bhq * p.n_pad + i * 128, 512, &sh.aux_full[sa]);
@@ -522,11 +525,11 @@ struct attn_bwd_dkdv_template {
             if (n == 0) cs.t_start = clock64();
             const long long t_start = cs.t_start;
             const KvTask w = decode(p, id);
-            const int T = steps(p, w), T1 = T / p.group;
-            for (int t = 0; t < T; ++t) {
+            const int T = steps(p, w), T1 = q_blocks(w);
+            for (int t = 0, ti = 0; t < T; ++t, ti = (ti + 1 == T1) ? 0 : ti + 1) {
                 const int x = cs.x0 + t;
                 const int sa = x % SA;
-                const bool diag = CAUSAL && (t % T1 == 0);  // q block i == j
+                const bool diag = CAUSAL && ti == 0;  // q block i == j
                 mbar_wait(&sh.aux_full[sa], (x / SA) & 1);
                 float nlse[8], dlt[8];
                 grp_vec_load(smem_u32(&sh.lse[sa][32 * g]), nlse);
@@ -955,6 +958,7 @@ struct CfgQ {
 
 struct QTask {
     int i, bh;   // query block, batch * heads + head
+    int b;       // batch
     SeqView sv;  // this batch's length and TMA row coordinates (variable-length batches)
 };
 
@@ -964,14 +968,16 @@ template <bool CAUSAL>
 TKB_DEVICE QTask qtask(const BwdParams& p, int t) {
     const int nq = p.n_pad / 128;
     const int G = p.head_group;
-    const int sec = t / (G * nq);
+    const int sec = p.q_sec.div(t);  // FastDiv: no MUFU.RCP behind the compute warps' exponentials
     const int r = t - sec * G * nq;
-    const int gs = min(G, p.bh - sec * G);
-    const int mi = r / gs;
+    const bool full = p.bh - sec * G >= G;
+    const int gs = full ? G : p.bh - sec * G;
+    const int mi = full ? p.q_g.div(r) : p.q_grem.div(r);
     QTask w;
     w.bh = sec * G + (r - mi * gs);
     w.i = CAUSAL ? (nq - 1 - mi) : mi;
-    w.sv = seq_view(p.cu_seqlens, p.vmaps, kBwdMaps, p.n, w.bh / p.heads);
+    w.b = p.q_heads.div(w.bh);
+    w.sv = seq_view(p.cu_seqlens, p.vmaps, kBwdMaps, p.n, w.b);
     return w;
 }
 
@@ -1075,7 +1081,7 @@ struct attn_bwd_dq_template {
             const uint64_t pol_stream = tma::policy_evict_first();
             const uint64_t pol_keep = tma::policy_evict_last();
             const QTask w = qtask<CAUSAL>(p, t);
-            const int b = w.bh / p.heads, h = w.bh - b * p.heads;
+            const int b = w.b, h = w.bh - b * p.heads;
             mbar_wait(&sh.qdo_free, (n & 1) ^ 1u);  // the previous task's Q / dO are in TMEM
             mbar_arrive_expect_tx(&sh.qdo_full, 2 * TL::kTileBytes);
             const int bc = w.sv.bcoord;
@@ -1268,7 +1274,7 @@ struct attn_bwd_dq_template {
             const int wq = a.warp & 3, g = a.warp >> 2, r = wq * 32 + a.lane;
             const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
             const QTask w = qtask<CAUSAL>(p, t);
-            const int b = w.bh / p.heads, h = w.bh - b * p.heads;
+            const int b = w.b, h = w.bh - b * p.heads;
             const int t_next = a.queue.get_warp(n + 1);
             if (t_next >= 0) stage_a(a, n + 1);
             mbar_wait(&sh.dq_full, n & 1);

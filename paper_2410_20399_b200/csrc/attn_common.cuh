@@ -25,6 +25,27 @@ inline int ensure_smem(Kern kern, int bytes, std::atomic<unsigned long long>& do
     return 0;
 }
 
+// Division by a launch-constant divisor without the integer-division sequence (whose
+// MUFU.RCP queues behind the softmax warps' exponentials on the same SM sub-partition: a task
+// decode cost ~1.2 k clk there). Round-up multiplier (Granlund-Montgomery, as CUTLASS's
+// FastDivmod): q = umulhi(n, mul) >> shr, exact for 0 <= n < 2^31 and 1 <= d < 2^31.
+struct FastDiv {
+    uint32_t mul = 0, shr = 0, d = 1;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t divisor) : d(divisor < 1 ? 1 : divisor) {
+        if (d != 1) {
+            uint32_t l = 0;
+            while ((1ull << l) < d) ++l;  // ceil(log2 d)
+            const uint32_t p = 31 + l;
+            mul = (uint32_t)(((1ull << p) + d - 1) / d);
+            shr = p - 32;
+        }
+    }
+    __device__ __forceinline__ int div(int n) const {
+        return d == 1 ? n : (int)(__umulhi((uint32_t)n, mul) >> shr);
+    }
+};
+
 // Tile shapes (compile time; the reference's runtime AttentionConfig knobs
 // kv_rows / qo_rows / num_workers, kernels.hpp:168-176, become these).
 constexpr int kBlockM = 128;   // query rows per tcgen05 M tile (one softmax warpgroup)
@@ -99,6 +120,7 @@ struct FwdParams {
     int tasks;                           // bh * m_blocks            (set by launch_attn_fwd;
                                          //   tkb_attn_validate keeps B*H*ceil(N/128) < 2^31)
     int head_group;                      // heads per L2 group       (set by launch_attn_fwd)
+    FastDiv fd_sec, fd_group, fd_grem, fd_heads;  // task decode divisors (set by launch_attn_fwd)
     float scale_log2;                    // softmax_scale * log2(e)
     // Fused rotary prologue (attn_fwd_template<D, Causal, true>): the two aux warps of every
     // CTA rotate 128-row blocks of Q and K from q_src / k_src into q_rot / k_rot (same
@@ -134,6 +156,11 @@ struct BwdParams {
     int head_group;    // heads per L2 group of the persistent task order
     int num_sms;       // persistent grid size
     int pairs;         // D = 128: dK/dV on CTA pairs (attn_bwd_dkdv2_kernel)
+    int kv_G;          // (batch, kv head) units per L2 group of the dK/dV task order
+    int kv_units;      // (batch, kv head) units = B * Hkv
+    // task decode divisors (set by the host: fill_bwd_divisors)
+    FastDiv kv_sec, kv_g, kv_grem, kv_nq, kv_hkv;  // dK/dV: G*nq, G, last-group size, nq, Hkv
+    FastDiv q_sec, q_g, q_grem, q_heads;           // dQ: head_group*nq, head_group, last-group size, H
     void* dk;          // dK / dV base pointers and element strides (persistent dK/dV kernel:
     void* dv;          //   direct row stores from registers)
     long long kv_sb, kv_sh, kv_sn;
@@ -143,6 +170,27 @@ struct BwdParams {
     float scale;       // softmax_scale
     float scale_log2;  // softmax_scale * log2(e)
 };
+
+// The backward's task-decode divisors (after bh, heads, group, n_pad, head_group, num_sms are set).
+inline void fill_bwd_divisors(BwdParams& p) {
+    const int nq = p.n_pad / 128;
+    const int hkv = p.heads / p.group;
+    const int hb = hkv * (p.bh / p.heads);
+    const long long tasks = (long long)nq * hb;
+    int G = tasks < 4ll * p.num_sms ? hb : p.head_group / (p.group > 1 ? p.group : 1);
+    G = G < 1 ? 1 : (G > hb ? hb : G);
+    p.kv_G = G;
+    p.kv_units = hb;
+    p.kv_sec = FastDiv((uint32_t)(G * nq));
+    p.kv_g = FastDiv((uint32_t)G);
+    p.kv_grem = FastDiv((uint32_t)(hb % G ? hb % G : G));
+    p.kv_nq = FastDiv((uint32_t)nq);
+    p.kv_hkv = FastDiv((uint32_t)hkv);
+    p.q_sec = FastDiv((uint32_t)(p.head_group * nq));
+    p.q_g = FastDiv((uint32_t)p.head_group);
+    p.q_grem = FastDiv((uint32_t)(p.bh % p.head_group ? p.bh % p.head_group : p.head_group));
+    p.q_heads = FastDiv((uint32_t)p.heads);
+}
 
 // Per-role cycle timeline (the Timeline of lcsf.hpp:165-224, recorded on the device):
 // trace[slot][role][iter][event] = clock64() - CTA start, roles MMA / COMPUTE / REDUCE.

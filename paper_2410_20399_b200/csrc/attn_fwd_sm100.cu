@@ -52,6 +52,9 @@
 #ifndef TKB_ROPE_DEBUG
 #define TKB_ROPE_DEBUG 0  // A/B only: 1 = aux warps publish without rotating, 2 = no flag waits
 #endif
+#ifndef TKB_FWD_TRACE
+#define TKB_FWD_TRACE 0  // debug builds: per-task cycle stamps into tkb_debug_set_trace's buffer
+#endif
 #ifndef TKB_FWD_PCHUNKS
 #define TKB_FWD_PCHUNKS 2
 #endif
@@ -84,6 +87,19 @@ constexpr int kPChunks = TKB_FWD_PCHUNKS;       // P handed to the MMA warp in c
 constexpr int kPChunkCols = kBlockN / kPChunks;  // keys per chunk
 constexpr float kRescaleThreshold = 8.0f;        // log2 units: defer O rescale while max grows < 2^8
 constexpr float kLn2 = 0.69314718055994530942f;
+
+// TKB_FWD_TRACE: trace[slot][role][task n < 32][event] = clock64() (the SM's counter, shared by
+// all warps of the CTA), for CTAs with blockIdx.x % trace_every == 0 (roles: 0 load, 1 MMA,
+// 2 softmax tile 0, 3 tile 1)
+TKB_DEVICE void fwd_stamp(const FwdParams& p, int role, int n, int ev) {
+    if constexpr (TKB_FWD_TRACE != 0) {
+        if (p.trace == nullptr || (int)blockIdx.x % p.trace_every || (int)blockIdx.x / p.trace_every >= p.trace_slots ||
+            n >= kTraceIters)
+            return;
+        p.trace[(((size_t)(blockIdx.x / p.trace_every) * kTraceRoles + role) * kTraceIters + n) * kTraceEvents + ev] =
+            clock64();
+    }
+}
 
 // ROPE: the fused rotary prologue (rotary_kernel, kernels.hpp:357-513): two aux warps per
 // CTA rotate Q and K into q_rot / k_rot block by block, ahead of and overlapped with the
@@ -139,14 +155,15 @@ struct attn_fwd_template {
         const int N = p.n;
         const int m_blocks = (N + kRowsPerCta - 1) / kRowsPerCta;
         const int G = p.head_group;
-        const int sec = t / (G * m_blocks);
+        const int sec = p.fd_sec.div(t);  // t / (G * m_blocks)
         const int r = t - sec * G * m_blocks;
-        const int gs = min(G, p.bh - sec * G);
-        const int mi = r / gs;
+        const bool full = p.bh - sec * G >= G;  // the last section may hold fewer heads
+        const int gs = full ? G : p.bh - sec * G;
+        const int mi = full ? p.fd_group.div(r) : p.fd_grem.div(r);
         const int bh = sec * G + (r - mi * gs);
         Task w;
         w.mblk = CAUSAL ? (m_blocks - 1 - mi) : mi;
-        w.batch = bh / p.heads;
+        w.batch = p.fd_heads.div(bh);
         w.head = bh - w.batch * p.heads;
         w.sv = seq_view(p.cu_seqlens, p.vmaps, kFwdMaps, N, w.batch);
         const int n = w.sv.n;
@@ -208,6 +225,7 @@ struct attn_fwd_template {
                                     ClaimNext&& claim_next) {
             const globals& p = a.g;
             shared& sh = a.sh;
+            fwd_stamp(p, 0, nt, 0);
             const uint64_t pol_q = tma::policy_evict_first();
             const uint64_t pol_kv = tma::policy_evict_last();
             const Task w = decode(p, t);
@@ -229,16 +247,12 @@ struct attn_fwd_template {
                     load_async(sQ(sh, s), gl{m}, &sh.q_full[s], q0 + s * kBlockM, w.head, w.sv.bcoord, pol_q);
                 });
             }
+            fwd_stamp(p, 0, nt, 1);  // Q issued (after q_empty)
             const int t_next = claim_next();
-            if (t_next >= 0) {  // warm the next task's Q in L2
-                const Task w2 = decode(p, t_next);
-                if (w2.sv.maps != nullptr) tma::acquire_map(w2.sv.maps + kMapQ);
-                w2.sv.with_map(p.tm_q, kMapQ, [&](const CUtensorMap* q2) {
-                    for (int s = 0; s < kQStages; ++s)
-                        for (int at = 0; at < Tile::kAtoms; ++at)
-                            tma::prefetch_4d(q2, at * 64, w2.mblk * kRowsPerCta + s * kBlockM, w2.head, w2.sv.bcoord);
-                });
-            }
+            fwd_stamp(p, 0, nt, 2);
+            // (warming the next task's Q — or its Q and first K / V block — in L2 ahead of time
+            // measured 1-2 % slower: the loads are not L2-miss bound)
+            (void)t_next;
             for (int i = 0; i < w.nkv; ++i) {
                 // the rotated K block (checking 8 blocks at a time, or the whole task's range at
                 // its start, measured slower: the load warp then waits for blocks it does not need yet)
@@ -251,6 +265,7 @@ struct attn_fwd_template {
                         load_async(sKV(sh, ps.st.slot), gl{m}, &sh.kv_ring.full[ps.st.slot], i * kBlockN,
                                    w.head / p.group, w.sv.bcoord, pol_kv);  // grouped-query: kv head = head / group
                     });
+                    if (i == w.nkv - 1 && which == 1) fwd_stamp(p, 0, nt, 3);
                     ps.st.advance();
                 }
             }
@@ -268,6 +283,7 @@ struct attn_fwd_template {
         };
         static TKB_DEVICE void issue(const lcsf::args<attn_fwd_template>& a, state& ms, int t, int nt) {
             const globals& p = a.g;
+            if (a.lane == 0) fwd_stamp(p, 1, nt, 0);
             shared& sh = a.sh;
             const uint32_t tbase = a.tmem;
             auto& kv = sh.kv_ring;
@@ -356,8 +372,10 @@ struct attn_fwd_template {
                     }
                 };
                 mbar_wait(&sh.q_full[0], nt & 1);
+                if (a.lane == 0) fwd_stamp(p, 1, nt, 3);
                 mbar_wait(&sh.q_full[1], nt & 1);
                 kv.wait_full(st);
+                if (a.lane == 0) fwd_stamp(p, 1, nt, 4);
                 tmem::fence_after();
                 // QK_s(next task) overwrites S_s, whose P was read by the previous task's last PV_s
                 // (issued before); the first PV_s below overwrites O_s only after the softmax drained it
@@ -367,6 +385,7 @@ struct attn_fwd_template {
                     mma_commit(&sh.s_full[s]);
                     if (nk[s] == 1) mma_commit(&sh.q_empty[s]);
                 }
+                if (a.lane == 0) fwd_stamp(p, 1, nt, 1);
                 mma_commit(&kv.empty[st.slot]);
                 st.advance();
                 for (int i = 1; i < nkv; ++i) {
@@ -409,6 +428,7 @@ struct attn_fwd_template {
                 mma_commit(&kv.empty[vslot]);
                 st.advance();
             }
+            if (a.lane == 0) fwd_stamp(p, 1, nt, 2);
         }
     };
 
@@ -427,6 +447,7 @@ struct attn_fwd_template {
             shared& sh = a.sh;
             const int s = a.warp / 4;                  // query tile of this warpgroup
             const int wq = a.warp % 4;                 // TMEM lane quarter
+            if (wq == 0 && a.lane == 0) fwd_stamp(p, 2 + s, nt, 5);
             const int row_in_tile = wq * 32 + a.lane;  // == TMEM lane
             const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
             const uint32_t tbase = a.tmem;
@@ -441,6 +462,8 @@ struct attn_fwd_template {
             float m = -INFINITY;
             float l = 0.f;
             const int nk0 = tile_blocks(p, w, 0), nk1 = tile_blocks(p, w, 1);
+            const bool stamp = (wq == 0 && a.lane == 0);
+            if (stamp) fwd_stamp(p, 2 + s, nt, 0);
             for (int i = 0; i < nkv; ++i) {
                 uint32_t tS = tS_fixed;
                 mbarrier* pf = sh.p_full[s];
@@ -455,6 +478,7 @@ struct attn_fwd_template {
                     ++cs.sc;
                 }
                 const uint32_t tP = tS + 64;
+                if (stamp && i == 0) fwd_stamp(p, 2 + s, nt, 1);
                 tmem::fence_after();
                 rt_fl<kBlockN> x;
                 load(x, tS);
@@ -537,6 +561,7 @@ struct attn_fwd_template {
                 tmem::fence_before();
                 mbar_arrive(&pf[kPChunks - 1]);
             }
+            if (stamp) fwd_stamp(p, 2 + s, nt, 2);
             if constexpr (k3) cs.qbase += (uint32_t)(nk0 + nk1);
             cs.m = m;
             cs.l = l;
@@ -561,6 +586,7 @@ struct attn_fwd_template {
                 ++cs.pvc;
             }
             tmem::fence_after();
+            if (wq == 0 && a.lane == 0) fwd_stamp(p, 2 + s, nt, 3);
             if (p.lse != nullptr && row < w.sv.n)
                 p.lse[(size_t)(w.batch * p.heads + w.head) * p.n + row] = (m + __log2f(l)) * kLn2;
             const bool leader = (wq == 0 && a.lane == 0);
@@ -592,6 +618,7 @@ struct attn_fwd_template {
                     tma::commit_group();
                 }
             }
+            if (leader) fwd_stamp(p, 2 + s, nt, 4);
         }
         static TKB_DEVICE void drain(const lcsf::args<attn_fwd_template>& a, state&) {
             if (a.warp % 4 == 0 && a.lane == 0) tma::wait_group<0>();
@@ -715,6 +742,10 @@ int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num
     const long long kv_bytes = 4ll * p.n * head_dim / p.group;  // K / V of one query head's kv head
     long long g = (48ll << 20) / (kv_bytes > 0 ? kv_bytes : 1);  // heads whose K / V fit ~48 MB of L2
     p.head_group = (int)(g < 1 ? 1 : (g > p.bh ? p.bh : g));
+    p.fd_sec = FastDiv((uint32_t)(p.head_group * p.m_blocks));
+    p.fd_group = FastDiv((uint32_t)p.head_group);
+    p.fd_grem = FastDiv((uint32_t)(p.bh % p.head_group ? p.bh % p.head_group : p.head_group));
+    p.fd_heads = FastDiv((uint32_t)p.heads);
     if (rope) {
         if (head_dim == 128)
             return causal ? fwd::launch<128, true, true>(p, num_sms, stream)

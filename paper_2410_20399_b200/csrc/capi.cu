@@ -598,6 +598,7 @@ static int bwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, con
         p.head_group = (int)(hg < 1 ? 1 : (hg > bh ? bh : hg));
     }
     p.pairs = g_bwd_pairs;
+    tkb::fill_bwd_divisors(p);
     p.dk = dk;
     p.dv = dv;
     p.kv_sb = skv.b;
