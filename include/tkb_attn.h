@@ -134,7 +134,9 @@ TKB_API int tkb_attn_bwd(const tkb_attn_desc* desc, const void* q, const void* k
  * rows past a sequence's length are left untouched. Workspaces: 128-byte aligned, of
  * tkb_attn_fwd_varlen_workspace_bytes / tkb_attn_bwd_varlen_workspace_bytes(desc) bytes
  * (no zero-fill needed; calls sharing one must be stream-ordered). Results equal the
- * fixed-length entry points run on each sequence alone, bit for bit. */
+ * fixed-length entry points run on each sequence alone, bit for bit. With desc.check_finite
+ * the call also reads cu_seqlens back and rejects bad offsets (TKB_ERR_CONFIG / _BOUNDS);
+ * otherwise they are preconditions. */
 TKB_API size_t tkb_attn_fwd_varlen_workspace_bytes(const tkb_attn_desc* desc);
 TKB_API int tkb_attn_fwd_varlen(const tkb_attn_desc* desc, const int32_t* cu_seqlens, int64_t total_tokens,
                                 const void* q, const void* k, const void* v, void* o, float* lse, void* workspace,

@@ -355,6 +355,24 @@ static int varlen_validate(const tkb_attn_desc* d, const Varlen& vl) {
     return TKB_OK;
 }
 
+// With desc.check_finite (the synchronising input check) a variable-length call also reads
+// cu_seqlens back and checks it: cu[0] = 0, non-decreasing, every length <= desc.seq and
+// cu[B] <= total_tokens. Without it these are the caller's preconditions (no device read-back).
+static int varlen_check_offsets(const tkb_attn_desc* d, const Varlen& vl, cudaStream_t st) {
+    std::vector<int32_t> cu((size_t)d->batches + 1);
+    cudaError_t e = cudaMemcpyAsync(cu.data(), vl.cu, cu.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cu_seqlens read-back: ") + cudaGetErrorString(e));
+    if (cu[0] != 0) return fail(TKB_ERR_CONFIG, "cu_seqlens[0] must be 0");
+    for (int b = 0; b < d->batches; ++b) {
+        const int64_t n = (int64_t)cu[b + 1] - cu[b];
+        if (n < 0) return fail(TKB_ERR_CONFIG, "cu_seqlens must be non-decreasing");
+        if (n > d->seq) return fail(TKB_ERR_CONFIG, "a sequence is longer than desc.seq (the maximum length)");
+    }
+    if ((int64_t)cu[d->batches] > vl.total) return fail(TKB_ERR_BOUNDS, "cu_seqlens[B] exceeds total_tokens");
+    return TKB_OK;
+}
+
 static int fwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, const void* k, const void* v, void* o,
              float* lse, void* workspace, size_t workspace_bytes, void* stream) {
     g_launches = 0;
@@ -377,7 +395,7 @@ static int fwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, con
     if (d->check_finite) {
         const void* qp[1] = {q};
         const void* kvp[2] = {k, v};
-        if ((rc = finite_check(d, qp, 1, s, d->heads, slot, st, vl)) ||
+        if ((vl && (rc = varlen_check_offsets(d, *vl, st))) || (rc = finite_check(d, qp, 1, s, d->heads, slot, st, vl)) ||
             (rc = finite_check(d, kvp, 2, skv, hkv, slot, st, vl)))
             return rc;
     }
@@ -541,7 +559,7 @@ static int bwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, con
     if (d->check_finite) {
         const void* qp[3] = {q, o, dout};
         const void* kvp[2] = {k, v};
-        if ((rc = finite_check(d, qp, 3, s, d->heads, slot, st, vl)) ||
+        if ((vl && (rc = varlen_check_offsets(d, *vl, st))) || (rc = finite_check(d, qp, 3, s, d->heads, slot, st, vl)) ||
             (rc = finite_check(d, kvp, 2, skv, hkv, slot, st, vl)))
             return rc;
     }

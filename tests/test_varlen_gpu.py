@@ -155,3 +155,27 @@ def test_varlen_rejects_bad_layouts(cuda_dev):
         A.attention_fwd_varlen(qd, kd, vd, _dev(cu, torch.int64), 20)
     with pytest.raises(A.ShapeError):  # [B, H, N, D] instead of packed [T, H, D]
         A.attention_fwd_varlen(qd[None], kd[None], vd[None], _dev(cu, torch.int32), 20)
+
+
+@pytest.mark.parametrize("bad", ["too_long", "decreasing", "start", "past_total"])
+def test_varlen_check_finite_validates_offsets(cuda_dev, bad):
+    """desc.check_finite (the synchronising input check) also checks cu_seqlens on the host."""
+    lens, H, D = [100, 60], 2, 64
+    q, k, v, do, cu = _packed(3, lens, H, D)
+    qd, kd, vd = _dev(q), _dev(k), _dev(v)
+    A.attention_fwd_varlen(qd, kd, vd, _dev(cu, torch.int32), 100, check_finite=True)  # valid
+    cu_bad = {"too_long": [0, 100, 160], "decreasing": [0, 120, 100], "start": [1, 100, 160],
+              "past_total": [0, 100, 200]}[bad]
+    max_len = 60 if bad == "too_long" else 100
+    err = A.BoundsError if bad == "past_total" else A.ConfigError
+    with pytest.raises(err):
+        A.attention_fwd_varlen(qd, kd, vd, _dev(np.asarray(cu_bad, np.int32), torch.int32), max_len,
+                               check_finite=True)
+
+
+def test_varlen_check_finite_rejects_non_finite(cuda_dev):
+    lens, H, D = [100, 60], 2, 128
+    q, k, v, do, cu = _packed(4, lens, H, D)
+    q[150, 1, 7] = np.inf
+    with pytest.raises(A.ConfigError):
+        A.attention_fwd_varlen(_dev(q), _dev(k), _dev(v), _dev(cu, torch.int32), 100, check_finite=True)
