@@ -215,8 +215,10 @@ struct TmemKV {
 // bwd_dkdv with one CTA per SM walking (kv block, kv head, batch) tasks from the atomic
 // queue, so that a task's prologue / finish overlap its neighbours instead of costing a CTA
 // turnover (~4000 clk start-up + ~4400 clk finish per CTA, ~9 % of a 32-step task):
-//   - K / V of the next task are loaded as soon as this task's last S^T / dP^T retire
-//     (kv_empty), i.e. under its last dV / dK GEMMs and finish;
+//   - K (V) of the next task is loaded as soon as this task's last S^T (dP^T) retired
+//     (k_empty / v_empty), i.e. under its last dV / dK GEMMs and finish; the next task's first
+//     S^T waits for K only (k_full / v_full; measured neutral against one K+V barrier: the
+//     ~3 k clk from this task's last dK to the next first S^T is the 64 KB reload itself);
 //   - the Q / dO rings and the per-step barriers run on a step counter continuous across
 //     tasks, so the next task's first S^T / dP^T GEMMs are issued right behind this task's
 //     last dV / dK (they write the S / dP regions, which hold nothing live by then);
@@ -264,7 +266,8 @@ struct attn_bwd_dkdv_template {
         uint8_t dO[SD][TL::kTileBytes];
         float lse[SA][128];  // -lse2 per query (perm32 order)
         float delta[SA][128];
-        mbarrier kv_full, kv_empty;  // K / V in SMEM; the task's last S^T / dP^T retired
+        mbarrier k_full, v_full;     // K / V of a task in SMEM (separately: S^T needs only K)
+        mbarrier k_empty, v_empty;   // the task's last S^T (K) / dP^T (V) retired: the next task's may load
         mbarrier s_full[2];          // [buffer] (one buffer unless kDS)
         mbarrier dp_full;
         mbarrier dv_free, dk_free;   // the finish has read dV / dK out of TMEM
@@ -330,8 +333,10 @@ struct attn_bwd_dkdv_template {
     static TKB_DEVICE Tile<D> tDo(shared& sh, int x) { return Tile<D>{sh.dO[x % SD]}; }
 
     static TKB_DEVICE void init(shared& sh, const globals& p) {
-        mbar_init(&sh.kv_full, 1);
-        mbar_init(&sh.kv_empty, 1);
+        mbar_init(&sh.k_full, 1);
+        mbar_init(&sh.v_full, 1);
+        mbar_init(&sh.k_empty, 1);
+        mbar_init(&sh.v_empty, 1);
         mbar_init(&sh.s_full[0], 1);
         mbar_init(&sh.s_full[1], 1);
         mbar_init(&sh.dp_full, 1);
@@ -382,13 +387,17 @@ struct attn_bwd_dkdv_template {
             if (w.sv.maps != nullptr) {  // this sequence's maps (varlen_maps_kernel); dV / dK: its finish
                 for (int m = 0; m < kBwdMaps; ++m) tma::acquire_map(w.sv.maps + m);
             }
-            mbar_wait(&sh.kv_empty, (n & 1) ^ 1u);
-            mbar_arrive_expect_tx(&sh.kv_full, 2 * TL::kTileBytes);
+            // K as soon as the previous task's last S^T retired, V once its last dP^T did (one
+            // GEMM later): the next task's first S^T needs only K
+            mbar_wait(&sh.k_empty, (n & 1) ^ 1u);
+            mbar_arrive_expect_tx(&sh.k_full, TL::kTileBytes);
             w.sv.with_map(p.tm_k, kMapK, [&](const CUtensorMap* m) {
-                load_async(Tile<D>{sh.k}, gl{m}, &sh.kv_full, kv0, w.head, w.sv.bcoord, pol_stream);
+                load_async(Tile<D>{sh.k}, gl{m}, &sh.k_full, kv0, w.head, w.sv.bcoord, pol_stream);
             });
+            mbar_wait(&sh.v_empty, (n & 1) ^ 1u);
+            mbar_arrive_expect_tx(&sh.v_full, TL::kTileBytes);
             w.sv.with_map(p.tm_v, kMapV, [&](const CUtensorMap* m) {
-                load_async(Tile<D>{sh.v}, gl{m}, &sh.kv_full, kv0, w.head, w.sv.bcoord, pol_stream);
+                load_async(Tile<D>{sh.v}, gl{m}, &sh.v_full, kv0, w.head, w.sv.bcoord, pol_stream);
             });
             const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
             int ti = 0, hq = w.head * p.group;  // step t = (query head hq, its ti-th query block)
@@ -450,24 +459,27 @@ struct attn_bwd_dkdv_template {
             if (n == 0) ms.t_start = clock64();
             const long long t_start = ms.t_start;
             const Tile<D> tK{sh.k}, tV{sh.v};
+            const int T = steps(p, decode(p, id));
+            const int x0 = ms.x0;
+            const int x_last = x0 + T - 1;
             auto issue_s = [&](int x) {  // S^T = K Q^T
                 mbar_wait(&sh.q_full[x % SQ], (x / SQ) & 1);
                 tmem::fence_after();
                 mm_ABt(tt_fl<128>{tbase + s_buf(x)}, tK, tQ(sh, x));
                 mma_commit(&sh.s_full[buf_of(x)]);
+                if (x == x_last) mma_commit(&sh.k_empty);  // the task's last S^T: K may reload
             };
             auto issue_dp = [&](int x) {  // dP^T = V dO^T
                 mbar_wait(&sh.do_full[x % SD], (x / SD) & 1);
                 tmem::fence_after();
                 mm_ABt(tt_fl<128>{tbase + CT::tmem_dp()}, tV, tDo(sh, x));
                 mma_commit(&sh.dp_full);
+                if (x == x_last) mma_commit(&sh.v_empty);  // the task's last dP^T: V may reload
             };
-            const int T = steps(p, decode(p, id));
-            const int x0 = ms.x0;
-            mbar_wait(&sh.kv_full, n & 1);
+            mbar_wait(&sh.k_full, n & 1);
             issue_s(x0);
+            mbar_wait(&sh.v_full, n & 1);
             issue_dp(x0);
-            if (T == 1) mma_commit(&sh.kv_empty);
             for (int t = 0; t < T; ++t) {
                 const int x = x0 + t;
                 const uint32_t ph = x & 1;
@@ -494,10 +506,7 @@ struct attn_bwd_dkdv_template {
                 TKB_TR(0, x, 3);
                 mma_commit(&sh.q_empty[x % SQ]);
                 mma_commit(&sh.aux_empty[x % SA]);  // dK_x waited for the last dS of step x
-                if (t + 1 < T) {
-                    issue_dp(x + 1);  // overwrites dS_t, read by dK_t issued before
-                    if (t + 2 == T) mma_commit(&sh.kv_empty);  // the task's last S^T / dP^T issued
-                }
+                if (t + 1 < T) issue_dp(x + 1);  // overwrites dS_t, read by dK_t issued before
                 TKB_TR(0, x, 4);
             }
             mma_commit(&sh.dkv_full);
