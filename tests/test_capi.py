@@ -180,3 +180,28 @@ def test_varlen_python_mirror_rejects_cpu_tensors():
     x = torch.zeros(10, 2, 64, dtype=torch.bfloat16)
     with pytest.raises(A.ConfigError):
         A.attention_fwd_varlen(x, x, x, torch.tensor([0, 10], dtype=torch.int32), 10)
+
+
+def test_fastdiv_multiplier_is_exact():
+    """The task decoders divide by launch constants through FastDiv (attn_common.cuh): the
+    round-up multiplier m = ceil(2^(31 + ceil(log2 d)) / d), q = umulhi(n, m) >> (p - 32).
+    Same arithmetic in Python: exact for every tested divisor over dividends up to 2^31 - 1."""
+    import random
+
+    def fastdiv(n, d):
+        if d == 1:
+            return n
+        l = (d - 1).bit_length()  # ceil(log2 d)
+        p = 31 + l
+        m = ((1 << p) + d - 1) // d
+        assert m < (1 << 32)
+        return ((n * m) >> 32) >> (p - 32)
+
+    rng = random.Random(7)
+    divisors = list(range(1, 300)) + [2 ** k + o for k in range(2, 31) for o in (-1, 0, 1)] + \
+        [rng.randrange(1, 2 ** 31) for _ in range(200)]
+    for d in divisors:
+        ns = [0, 1, d - 1, d, d + 1, 2 ** 31 - 1, 2 ** 31 - 2] + [rng.randrange(0, 2 ** 31) for _ in range(50)]
+        for n in ns:
+            if 0 <= n < 2 ** 31:
+                assert fastdiv(n, d) == n // d, (n, d)

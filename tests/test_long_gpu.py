@@ -157,3 +157,23 @@ def test_descriptor_cache_hits(cuda_dev):
         A.attention_fwd(q, k, v, out=o, lse=lse)
     h1, m1 = A.map_cache_stats()
     assert (m1 - m0, h1 - h0) == (0, 12), (h0, m0, h1, m1)  # 4 maps per forward, all hits
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_many_heads_task_decode(cuda_dev, causal):
+    """B*H = 70000 (> gridDim.y's 65535) at a ragged N: task ids up to ~10^5 through the FastDiv
+    task decoders, L2 head groups that do not divide B*H (a short last group), and the
+    grid-stride prep / scan kernels; sampled heads against the fp64 oracle."""
+    B, H, N, D = 35000, 2, 200, 64
+    q, k, v, do = _gpu_inputs(99 + causal, B, H, N, D)
+    o, lse = A.attention_fwd(q, k, v, causal=causal)
+    dq, dk, dv = A.attention_bwd(q, k, v, o, do, lse, causal=causal)
+    torch.cuda.synchronize()
+    idx = np.array([0, 1, 12345, 34999 * 2, 69998, 69999])
+    qh, kh, vh, doh = (_heads(t, idx) for t in (q, k, v, do))
+    ro, rl = orc.attn_fwd(qh, kh, vh, causal=causal)
+    rdq, rdk, rdv = orc.attn_bwd(qh, kh, vh, doh, causal=causal)
+    _assert_close("o", _heads(o, idx), ro)
+    assert orc.max_abs(lse.reshape(B * H, N)[idx].cpu().numpy(), rl) <= LSE_TOL
+    for name, got, ref in (("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+        _assert_close(name, _heads(got, idx), ref)
