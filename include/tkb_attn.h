@@ -29,8 +29,9 @@
  *     schedulers' task counters, one slot per stream), made by tkb_device_init()
  *     or by the first call on that device; nothing else is ever allocated.
  *     Call tkb_device_init() up front to keep the first call capturable in a
- *     CUDA graph. A captured graph must not be replayed concurrently with
- *     itself (its kernels share the capturing stream's counter slot).
+ *     CUDA graph. Calls captured into a graph get a counter slot of their own
+ *     for the graph's lifetime; a graph must not be replayed concurrently with
+ *     itself (its kernels share that slot). check_finite is not capturable.
  *   - check_finite (desc) reads its result back and synchronises the stream.
  */
 #ifndef TKB_ATTN_H

@@ -99,9 +99,23 @@ int device_state(cudaStream_t st, int* sms, int** slot) {
     DeviceState& ds = g_dev[dev];
     *sms = ds.sms;
     if (slot == nullptr) return TKB_OK;
+    // The slot key: the stream's id, or — while the stream is being captured into a CUDA graph,
+    // where cudaStreamGetId is not permitted — the capture's unique id (top bit set). A graph's
+    // kernels then own that slot for the graph's lifetime (never recycled), and the graph must
+    // not be replayed concurrently with itself.
     unsigned long long id = 0;
-    e = cudaStreamGetId(st, &id);
-    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaStreamGetId: ") + cudaGetErrorString(e));
+    bool captured = false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    unsigned long long cap_id = 0;
+    e = cudaStreamGetCaptureInfo(st, &cs, &cap_id);
+    if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaStreamGetCaptureInfo: ") + cudaGetErrorString(e));
+    if (cs == cudaStreamCaptureStatusActive) {
+        id = (1ull << 63) | cap_id;
+        captured = true;
+    } else {
+        e = cudaStreamGetId(st, &id);
+        if (e != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("cudaStreamGetId: ") + cudaGetErrorString(e));
+    }
     std::lock_guard<std::mutex> lock(ds.mu);
     int s;
     auto it = ds.slot_of.find(id);
@@ -111,15 +125,16 @@ int device_state(cudaStream_t st, int* sms, int** slot) {
         s = (int)ds.slot_of.size();
         ds.slot_of.emplace(id, s);
         ds.owner[s] = id;
-    } else {  // recycle the least recently used slot
-        s = 0;
-        for (int i = 1; i < kSlots; ++i)
-            if (ds.last_use[i] < ds.last_use[s]) s = i;
+    } else {  // recycle the least recently used slot (never one a captured graph owns)
+        s = -1;
+        for (int i = 0; i < kSlots; ++i)
+            if (ds.last_use[i] != ~0ull && (s < 0 || ds.last_use[i] < ds.last_use[s])) s = i;
+        if (s < 0) return fail(TKB_ERR_CONTRACT, "scheduler slots exhausted by captured graphs");
         ds.slot_of.erase(ds.owner[s]);
         ds.slot_of.emplace(id, s);
         ds.owner[s] = id;
     }
-    ds.last_use[s] = ++ds.tick;
+    ds.last_use[s] = captured ? ~0ull : ++ds.tick;
     *slot = ds.pool + 4 * s;
     return TKB_OK;
 }
