@@ -227,6 +227,7 @@ struct TmemKV {
 //     store issued by the load warp (see FINISH below).
 struct KvTask {
     int j, head, batch;
+    int chunk;   // query-head chunk (kv_split > 1: grouped-query heads split over tasks)
     SeqView sv;  // this batch's length and TMA row coordinates (variable-length batches)
 };
 
@@ -293,12 +294,12 @@ struct attn_bwd_dkdv_template {
     // as the dQ kernel), inside a group the long tasks (small kv block index) first, so the
     // queue ends on short tasks; with fewer than 4 tasks per SM (grouped-query heads: a task
     // walks its group's query heads) one group spans everything — longest-first overall.
-    static TKB_DEVICE int num_tasks(const globals& p) { return (p.n_pad / 128) * (p.heads / p.group) * (p.bh / p.heads); }
+    static TKB_DEVICE int num_tasks(const globals& p) { return (p.n_pad / 128) * p.kv_units; }
     static TKB_DEVICE int* counter(const globals& p) { return p.sched; }
     static TKB_DEVICE KvTask decode(const globals& p, int id) {
         const int nq = p.n_pad / 128;
         const int hkv = p.kv_hkv.d;
-        const int hb = p.kv_units;  // (batch, kv head) units
+        const int hb = p.kv_units;  // (batch, kv head, query-head chunk) units
         const int G = p.kv_G;  // fill_bwd_divisors: all units when < 4 tasks per SM, else L2-sized groups
         KvTask w;
         int unit;
@@ -313,8 +314,10 @@ struct attn_bwd_dkdv_template {
             unit = p.kv_nq.div(id);
             w.j = id - unit * nq;
         }
-        w.batch = p.kv_hkv.div(unit);
-        w.head = unit - w.batch * hkv;
+        const int bu = p.kv_c.div(unit);  // the chunk runs fastest: a kv head's chunks run together
+        w.chunk = unit - bu * p.kv_split;
+        w.batch = p.kv_hkv.div(bu);
+        w.head = bu - w.batch * hkv;
         w.sv = seq_view(p.cu_seqlens, p.vmaps, kBwdMaps, p.n, w.batch);
         return w;
     }
@@ -322,7 +325,8 @@ struct attn_bwd_dkdv_template {
         const int nb = (w.sv.n + 127) / 128;              // query blocks of this sequence
         return CAUSAL ? (nb - w.j) : nb;
     }
-    static TKB_DEVICE int steps(const globals& p, const KvTask& w) { return q_blocks(w) * p.group; }
+    static TKB_DEVICE int heads_per_task(const globals& p) { return p.kv_c.d == 1 ? p.group : p.group / p.kv_c.d; }
+    static TKB_DEVICE int steps(const globals& p, const KvTask& w) { return q_blocks(w) * heads_per_task(p); }
     // variable-length batches: kv blocks past a short sequence have no work
     static TKB_DEVICE bool skip(const globals& p, int id) {
         if (p.cu_seqlens == nullptr) return false;
@@ -399,8 +403,8 @@ struct attn_bwd_dkdv_template {
             w.sv.with_map(p.tm_v, kMapV, [&](const CUtensorMap* m) {
                 load_async(Tile<D>{sh.v}, gl{m}, &sh.v_full, kv0, w.head, w.sv.bcoord, pol_stream);
             });
-            const bool after_staged = n > 0 && T >= 3;  // the previous finish staged in our slots
-            int ti = 0, hq = w.head * p.group;  // step t = (query head hq, its ti-th query block)
+            const bool after_staged = n > 0 && T >= 3 && p.kv_split == 1;  // the previous finish staged in our slots
+            int ti = 0, hq = w.head * p.group + w.chunk * heads_per_task(p);  // step t = (query head hq, block ti)
             for (int t = 0; t < T; ++t, ++ps.x) {
                 const int x = ps.x;
                 const int i = (CAUSAL ? w.j : 0) + ti;
@@ -600,8 +604,30 @@ struct attn_bwd_dkdv_template {
             if (threadIdx.x == 0) TKB_TR(1, n, 4);
             tmem::fence_after();
             const int id_next = a.queue.get_warp(n + 1);
-            const bool staged = id_next >= 0 && steps(p, decode(p, id_next)) >= 3;
-            if (staged) {
+            const bool staged = p.kv_split == 1 && id_next >= 0 && steps(p, decode(p, id_next)) >= 3;
+            if (p.kv_split > 1) {
+                // grouped-query split: this chunk's fp32 partials, reduced by dkv_reduce_kernel
+                const size_t u = (size_t)(w.batch * (p.heads / p.group) + w.head);
+                const size_t plane = (size_t)p.kv_units / p.kv_split * p.n_pad * D;  // one chunk of one tensor
+                float* part = p.dkv_part + ((size_t)w.chunk * (p.kv_units / p.kv_split) + u) * p.n_pad * D +
+                              (size_t)(kv0 + r) * D + g * (D / 4);
+                rt_fl<D / 4> f;
+                load(f, tbase + lane_off + CT::tmem_dv() + g * (D / 4));
+                load_wait(f);
+                tmem::fence_before();
+                mbar_arrive(&sh.dv_free);
+#pragma unroll
+                for (int c = 0; c < D / 4; c += 4)
+                    *reinterpret_cast<float4*>(part + c) = make_float4(f.v[c], f.v[c + 1], f.v[c + 2], f.v[c + 3]);
+                load(f, tbase + lane_off + CT::tmem_dk() + g * (D / 4));
+                load_wait(f);
+                tmem::fence_before();
+                mbar_arrive(&sh.dk_free);
+                part += plane * p.kv_split;  // the dK planes follow the dV planes
+#pragma unroll
+                for (int c = 0; c < D / 4; c += 4)
+                    *reinterpret_cast<float4*>(part + c) = make_float4(f.v[c], f.v[c + 1], f.v[c + 2], f.v[c + 3]);
+            } else if (staged) {
                 tmem_rows_to_smem_bf16<D>(tbase + lane_off + CT::tmem_dv(), tQ(sh, cs.x0 + 2), r, g);
                 tmem::fence_before();
                 mbar_arrive(&sh.dv_free);
@@ -1382,6 +1408,46 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
     }
 }
 
+// Grouped-query split (kv_split > 1): dV = sum_c dV_c, dK = scale * sum_c dK_c over the chunks in
+// chunk order (deterministic), bf16 into dv / dk with their strides. HBM-bound; 8 columns per
+// thread, grid-stride over (unit, row, column block).
+template <int D>
+__global__ void __launch_bounds__(256) dkv_reduce_kernel(const float* __restrict__ part, int split, int units, int n,
+                                                         int n_pad, int hkv, __nv_bfloat16* dv, __nv_bfloat16* dk,
+                                                         int64_t sb, int64_t sh, int64_t sn, float scale) {
+    constexpr int kCb = D / 8;
+    const int64_t total = (int64_t)units * n * kCb;
+    const size_t plane = (size_t)units * n_pad * D;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int cb = (int)(i % kCb);
+        const int64_t ur = i / kCb;
+        const int row = (int)(ur % n);
+        const int u = (int)(ur / n);
+        const size_t src = ((size_t)u * n_pad + row) * D + cb * 8;
+        const int64_t dst = (int64_t)(u / hkv) * sb + (int64_t)(u % hkv) * sh + (int64_t)row * sn + cb * 8;
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {
+            const float* pp = part + (size_t)which * split * plane + src;
+            float acc[8];
+            {
+                const float4 a = *reinterpret_cast<const float4*>(pp), b = *reinterpret_cast<const float4*>(pp + 4);
+                acc[0] = a.x, acc[1] = a.y, acc[2] = a.z, acc[3] = a.w, acc[4] = b.x, acc[5] = b.y, acc[6] = b.z, acc[7] = b.w;
+            }
+            for (int c = 1; c < split; ++c) {
+                const float4 a = *reinterpret_cast<const float4*>(pp + c * plane);
+                const float4 b = *reinterpret_cast<const float4*>(pp + c * plane + 4);
+                acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+                acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+            }
+            const float m = which ? scale : 1.f;  // dK = scale dS^T Q
+            uint4 o;
+            o.x = pack_bf16x2(acc[0] * m, acc[1] * m), o.y = pack_bf16x2(acc[2] * m, acc[3] * m);
+            o.z = pack_bf16x2(acc[4] * m, acc[5] * m), o.w = pack_bf16x2(acc[6] * m, acc[7] * m);
+            *reinterpret_cast<uint4*>((which ? dk : dv) + dst) = o;
+        }
+    }
+}
+
 template <int D, bool CAUSAL>
 int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases, int* launches) {
     static std::atomic<unsigned long long> set_dq{0}, set_kv2{0}, set_kvp{0};  // per device
@@ -1392,17 +1458,28 @@ int launch_main(const BwdParams& p, int batches, cudaStream_t stream, int phases
     if (D == 128)
         if (int e = ensure_smem(attn_bwd_dkdv2_kernel<CAUSAL>, CfgKV2::kSmemBytes, set_kv2)) return e;
     if (phases & 2) {
-        if (D == 128 && p.pairs && p.cu_seqlens == nullptr) {  // CTA pairs: kv blocks rounded up to an even count
+        if (D == 128 && p.pairs && p.cu_seqlens == nullptr && p.kv_split == 1) {  // CTA pairs: kv blocks rounded up to even
             dim3 grid2((p.n_pad / 128 + 1) & ~1, p.heads / p.group, batches);
             attn_bwd_dkdv2_kernel<CAUSAL><<<grid2, kThreads, CfgKV2::kSmemBytes, stream>>>(p);
         } else {
-            const int64_t tasks_kv = (int64_t)(p.n_pad / 128) * (p.heads / p.group) * batches;
+            const int64_t tasks_kv = (int64_t)(p.n_pad / 128) * p.kv_units;
             lcsf::kernel<KV><<<(unsigned)(tasks_kv < p.num_sms ? tasks_kv : p.num_sms), KV::kThreads,
                                KV::kSmemBytes, stream>>>(p);
         }
         int e = (int)cudaGetLastError();
         if (e) return e;
         ++*launches;
+        if (p.kv_split > 1) {
+            const int hkv = p.heads / p.group;
+            const int units = hkv * batches;
+            const int64_t work = (int64_t)units * p.n * (D / 8);
+            const int64_t cap = (int64_t)p.num_sms * 8;
+            dkv_reduce_kernel<D><<<(unsigned)((work + 255) / 256 < cap ? (work + 255) / 256 : cap), 256, 0, stream>>>(
+                p.dkv_part, p.kv_split, units, p.n, p.n_pad, hkv, reinterpret_cast<__nv_bfloat16*>(p.dv),
+                reinterpret_cast<__nv_bfloat16*>(p.dk), p.kv_sb, p.kv_sh, p.kv_sn, p.scale);
+            if ((e = (int)cudaGetLastError())) return e;
+            ++*launches;
+        }
     }
     if (phases & 4) {
         const int64_t tasks = (int64_t)p.bh * (p.n_pad / 128);

@@ -157,9 +157,11 @@ struct BwdParams {
     int num_sms;       // persistent grid size
     int pairs;         // D = 128: dK/dV on CTA pairs (attn_bwd_dkdv2_kernel)
     int kv_G;          // (batch, kv head) units per L2 group of the dK/dV task order
-    int kv_units;      // (batch, kv head) units = B * Hkv
+    int kv_units;      // dK/dV task units = B * Hkv * kv_split
+    int kv_split;      // grouped-query: query-head chunks per (batch, kv head) (bwd_kv_split)
+    float* dkv_part;   // kv_split > 1: fp32 dV / dK partials [2][kv_split][B * Hkv][n_pad][D] (workspace)
     // task decode divisors (set by the host: fill_bwd_divisors)
-    FastDiv kv_sec, kv_g, kv_grem, kv_nq, kv_hkv;  // dK/dV: G*nq, G, last-group size, nq, Hkv
+    FastDiv kv_sec, kv_g, kv_grem, kv_nq, kv_hkv, kv_c;  // dK/dV: G*nq, G, last-group size, nq, Hkv, split
     FastDiv q_sec, q_g, q_grem, q_heads;           // dQ: head_group*nq, head_group, last-group size, H
     void* dk;          // dK / dV base pointers and element strides (persistent dK/dV kernel:
     void* dv;          //   direct row stores from registers)
@@ -171,13 +173,31 @@ struct BwdParams {
     float scale_log2;  // softmax_scale * log2(e)
 };
 
-// The backward's task-decode divisors (after bh, heads, group, n_pad, head_group, num_sms are set).
+// Grouped-query dK/dV with few kv heads: a (kv block, kv head) task walks all `group` query
+// heads, and with fewer than ~4 such tasks per SM the last wave leaves SMs idle (MQA causal: one
+// j = 0 task holds 32 query heads' work). The query heads are then split into kv_split chunks,
+// each task writes fp32 dV / dK partials and a reduce kernel sums them in chunk order
+// (deterministic). A function of the problem alone (B200's 148 SMs), so the workspace size does
+// not depend on the device; never for variable-length batches.
+constexpr int kSplitSms = 148;
+inline int bwd_kv_split(long long units, int group, int nq, bool varlen) {
+    if (varlen || group < 2) return 1;
+    const long long tasks = (long long)nq * units;
+    int c = 1;
+    while (c < group && group % (2 * c) == 0 && tasks * c < 4ll * kSplitSms) c *= 2;
+    return c;
+}
+
+// The backward's task-decode divisors (after bh, heads, group, n_pad, head_group, num_sms and
+// kv_split are set).
 inline void fill_bwd_divisors(BwdParams& p) {
     const int nq = p.n_pad / 128;
     const int hkv = p.heads / p.group;
-    const int hb = hkv * (p.bh / p.heads);
+    const int hb = hkv * (p.bh / p.heads) * p.kv_split;  // task units: (batch, kv head, chunk)
     const long long tasks = (long long)nq * hb;
-    int G = tasks < 4ll * p.num_sms ? hb : p.head_group / (p.group > 1 ? p.group : 1);
+    // few tasks per SM (or a grouped-query split, which only happens then): one group spanning
+    // everything, i.e. longest-first over the whole causal queue
+    int G = (tasks < 4ll * p.num_sms || p.kv_split > 1) ? hb : p.head_group / (p.group > 1 ? p.group : 1);
     G = G < 1 ? 1 : (G > hb ? hb : G);
     p.kv_G = G;
     p.kv_units = hb;
@@ -186,6 +206,7 @@ inline void fill_bwd_divisors(BwdParams& p) {
     p.kv_grem = FastDiv((uint32_t)(hb % G ? hb % G : G));
     p.kv_nq = FastDiv((uint32_t)nq);
     p.kv_hkv = FastDiv((uint32_t)hkv);
+    p.kv_c = FastDiv((uint32_t)p.kv_split);
     p.q_sec = FastDiv((uint32_t)(p.head_group * nq));
     p.q_g = FastDiv((uint32_t)p.head_group);
     p.q_grem = FastDiv((uint32_t)(p.bh % p.head_group ? p.bh % p.head_group : p.head_group));

@@ -544,6 +544,12 @@ TKB_API size_t tkb_attn_bwd_workspace_bytes(const tkb_attn_desc* d) {
     size_t bytes = 0;
     bytes += bh * npad * 4;  // delta = rowsum(dO * O)
     bytes += bh * npad * 4;  // lse2 (log2 domain, padded)
+    const int hkv = kv_heads_of(d);
+    if (hkv > 0 && d->heads % hkv == 0) {  // grouped-query split: fp32 dV / dK partials per chunk
+        const size_t units = (size_t)d->batches * hkv;
+        const int split = tkb::bwd_kv_split((long long)units, d->heads / hkv, (int)(npad / 128), false);
+        if (split > 1) bytes += 2 * (size_t)split * units * npad * d->head_dim * 4;
+    }
     return (bytes + 255) & ~(size_t)255;
 }
 
@@ -631,6 +637,8 @@ static int bwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, con
         p.head_group = (int)(hg < 1 ? 1 : (hg > bh ? bh : hg));
     }
     p.pairs = g_bwd_pairs;
+    p.kv_split = tkb::bwd_kv_split((long long)d->batches * hkv, p.group, npad / 128, vl != nullptr);
+    p.dkv_part = p.kv_split > 1 ? lse2 + (size_t)bh * npad : nullptr;
     tkb::fill_bwd_divisors(p);
     p.dk = dk;
     p.dv = dv;

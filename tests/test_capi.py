@@ -205,3 +205,21 @@ def test_fastdiv_multiplier_is_exact():
         for n in ns:
             if 0 <= n < 2 ** 31:
                 assert fastdiv(n, d) == n // d, (n, d)
+
+
+def test_workspace_bytes_grouped_query_split():
+    """Grouped-query dK/dV with few kv heads splits the query heads over tasks (bwd_kv_split,
+    attn_common.cuh: doubling while (kv blocks x B x Hkv) x split < 4 x 148) and reserves fp32
+    dV / dK partials per chunk in the backward workspace."""
+    def ws(B, H, hkv, N, D):
+        d = A.AttentionConfig(B, H, N, D, kv_heads=hkv).desc()
+        return A.lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(d))
+
+    base = lambda B, H, N: 2 * B * H * ((N + 127) // 128 * 128) * 4  # noqa: E731 - delta + lse2
+    assert ws(2, 8, 8, 512, 128) == base(2, 8, 512)           # multi-head: no split
+    # MQA, B=2, N=512: 4 kv blocks x 2 units = 8 tasks -> split 8 (the whole group)
+    assert ws(2, 8, 1, 512, 128) == base(2, 8, 512) + 2 * 8 * 2 * 512 * 128 * 4
+    # B=8 H=32 Hkv=1 N=4096: 32 x 8 = 256 tasks -> split 4 (256 x 4 >= 592)
+    assert ws(8, 32, 1, 4096, 128) == base(8, 32, 4096) + 2 * 4 * 8 * 4096 * 128 * 4
+    # plenty of kv heads: 16 x 64 x 8 = 8192 tasks -> no split
+    assert ws(16, 64, 8, 1024, 64) == base(16, 64, 1024)

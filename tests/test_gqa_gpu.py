@@ -76,3 +76,22 @@ def test_gqa_rejects_bad_group(cuda_dev):
     q, k, v, _ = (_dev(x) for x in _inputs(3, 1, 6, 4, 128, 64))
     with pytest.raises(A.ConfigError):
         A.attention_fwd(q, k, v)
+
+
+def test_mqa_split_reduce_launches_and_determinism(cuda_dev):
+    """Few kv heads: the dK/dV tasks split the query heads (fp32 partials + an ordered reduce
+    launch: prep, dK/dV, reduce, dQ); results stay deterministic and match the oracle."""
+    B, H, HKV, N, D = 1, 16, 1, 384, 128
+    q, k, v, do = _inputs(11, B, H, HKV, N, D)
+    qd, kd, vd, dod = (_dev(x) for x in (q, k, v, do))
+    o, lse = A.attention_fwd(qd, kd, vd, causal=True)
+    r1 = A.attention_bwd(qd, kd, vd, o, dod, lse, causal=True)
+    assert A.last_launch_count() == 4
+    r2 = A.attention_bwd(qd, kd, vd, o, dod, lse, causal=True)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(r1, r2))
+    ke, ve = np.repeat(k, H, axis=1), np.repeat(v, H, axis=1)
+    rdq, rdk, rdv = orc.attn_bwd(q.reshape(-1, N, D), ke.reshape(-1, N, D), ve.reshape(-1, N, D),
+                                 do.reshape(-1, N, D), causal=True)
+    _close("dk", r1[1].float().cpu().numpy(), rdk.reshape(B, HKV, H, N, D).sum(axis=2))
+    _close("dv", r1[2].float().cpu().numpy(), rdv.reshape(B, HKV, H, N, D).sum(axis=2))
