@@ -498,6 +498,47 @@ def attention_bwd_varlen(q, k, v, o, dout, lse, cu_seqlens, max_seqlen, causal=F
     return dq, dk, dv
 
 
+# ------------------------------------------------- PyTorch autograd (a training-step caller)
+
+
+def _autograd_fn():
+    import torch
+
+    class _Attention(torch.autograd.Function):
+        """O = attention(q, k, v) whose backward is tkb_attn_bwd from the saved L."""
+
+        @staticmethod
+        def forward(ctx, q, k, v, causal, softmax_scale):
+            o, lse = attention_fwd(q, k, v, causal=causal, softmax_scale=softmax_scale)
+            ctx.save_for_backward(q, k, v, o, lse)
+            ctx.causal, ctx.softmax_scale = causal, softmax_scale
+            return o
+
+        @staticmethod
+        def backward(ctx, do):
+            q, k, v, o, lse = ctx.saved_tensors
+            do = do if do.stride() == o.stride() else do.contiguous()
+            if do.stride() != q.stride():  # dO must share q's layout: bring both to contiguous
+                q, o, do = q.contiguous(), o.contiguous(), do.contiguous()
+            dq, dk, dv = attention_bwd(q, k, v, o, do, lse, causal=ctx.causal, softmax_scale=ctx.softmax_scale)
+            return dq, dk, dv, None, None
+
+    return _Attention
+
+
+_ATTN_FN = None
+
+
+def attention(q, k, v, causal=False, softmax_scale=None):
+    """Differentiable attention for PyTorch code: O = softmax(scale q k^T [causal]) v with the
+    B200 forward, and a backward (dQ, dK, dV) from the saved L — one tkb_attn_fwd launch
+    forward, tkb_attn_bwd backward; bf16 CUDA tensors [B, H, N, D] (k, v may be grouped-query)."""
+    global _ATTN_FN
+    if _ATTN_FN is None:
+        _ATTN_FN = _autograd_fn()
+    return _ATTN_FN.apply(q, k, v, bool(causal), softmax_scale)
+
+
 @dataclass
 class GemmConfig:
     """The reference GemmConfig (kernels.hpp:23-46) minus its CPU-model knobs (m_block /

@@ -114,3 +114,25 @@ def test_bwd_strided_heads(cuda_dev, D, causal):
         g = g.float().cpu().numpy().reshape(-1, 1000, D)
         ma, rl = orc.max_abs(g, r), orc.rel_l2(g, r)
         assert ma <= MAX_ABS and rl <= REL_L2, (name, ma, rl)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_autograd_function_matches_torch(cuda_dev, causal):
+    """attention() (torch.autograd.Function over tkb_attn_fwd / tkb_attn_bwd) inside a small
+    graph: gradients through a loss equal torch fp64 SDPA autograd on the same bf16 values."""
+    B, H, HKV, N, D = 2, 4, 2, 300, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.empty(B, h, N, D, device="cuda").uniform_(-1, 1, generator=g).bfloat16()
+               for h in (H, HKV, HKV))
+    w = torch.empty(B, H, N, D, device="cuda").uniform_(-1, 1, generator=g)
+    qa, ka, va = (x.clone().requires_grad_() for x in (q, k, v))
+    loss = (A.attention(qa, ka, va, causal=causal).float() * w).sum()
+    loss.backward()
+    qr, kr, vr = (x.double().requires_grad_() for x in (q, k, v))
+    kre, vre = kr.repeat_interleave(H // HKV, dim=1), vr.repeat_interleave(H // HKV, dim=1)
+    ref = torch.nn.functional.scaled_dot_product_attention(qr, kre, vre, is_causal=causal)
+    (ref * w.double()).sum().backward()
+    for got, want in ((qa.grad, qr.grad), (ka.grad, kr.grad), (va.grad, vr.grad)):
+        assert got.dtype == torch.bfloat16 and got.shape == want.shape
+        err = (got.double() - want).abs().max().item()
+        assert err <= MAX_ABS * max(1.0, want.abs().max().item() / 4), err
