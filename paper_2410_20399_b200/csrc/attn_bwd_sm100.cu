@@ -1310,21 +1310,30 @@ struct attn_bwd_dq_template {
             const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
             const QTask w = qtask<CAUSAL>(p, t);
             const int b = w.b, h = w.bh - b * p.heads;
+            long long* tr = trace_slot(p, (int)blockIdx.x, 1);
+            const long long t_start = cs.t_start;
+            if (threadIdx.x == 0) TKB_TR(1, n, 3);  // finish start (per task n; events 3-7)
             const int t_next = a.queue.get_warp(n + 1);
             if (t_next >= 0) stage_a(a, n + 1);
+            if (threadIdx.x == 0) TKB_TR(1, n, 4);  // next task's Q / dO in TMEM
             mbar_wait(&sh.dq_full, n & 1);
+            if (threadIdx.x == 0) TKB_TR(1, n, 5);  // last dQ GEMM retired
             tmem::fence_after();
             tmem_rows_to_smem_bf16<D>(a.tmem + lane_off + C::tmem_dq(), Tile<D>{sh.q}, r, g, p.scale);  // dQ = scale dS K
             tma::fence_async_smem();
             named_sync(kBarCompute, kComputeThreads);
+            if (threadIdx.x == 0) TKB_TR(1, n, 6);  // dQ staged
             if (threadIdx.x == 0) {
                 if (w.sv.maps != nullptr) tma::acquire_map(w.sv.maps + kMapDq);
                 w.sv.with_map(p.tm_dq, kMapDq, [&](const CUtensorMap* m) {
                     store_async(gl{m}, Tile<D>{sh.q}, w.i * 128, h, w.sv.bcoord);
                 });
                 tma::commit_group();
+                // (waiting for this read later, after the next task's first step, freed warp 0
+                // ~1.2 k clk per boundary but measured neutral: r2c_ab_bwd_dq_defer.txt)
                 tma::wait_group_read<0>();
                 mbar_arrive(&sh.qdo_free);
+                TKB_TR(1, n, 7);  // store read SMEM
             }
         }
         static TKB_DEVICE void drain(const lcsf::args<attn_bwd_dq_template>&, state&) {

@@ -59,6 +59,19 @@ TKB_DEVICE bool mbar_try_wait(mbarrier* b, uint32_t parity) {
     return ok != 0;
 }
 
+// Non-blocking: has the phase with this parity completed?
+TKB_DEVICE bool mbar_test_wait(mbarrier* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 TKB_DEVICE uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
