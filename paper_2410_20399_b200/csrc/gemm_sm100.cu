@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "attn_common.cuh"
+#include "tkb/cluster.cuh"
 #include "tkb/lcsf.cuh"
 #include "tkb/tile.cuh"
 
@@ -187,10 +188,198 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     if (warp == 1) tmem::dealloc<512>(tbase);
 }
 
+// ------------------------------------------------------------------ CTA pairs (cta_group::2)
+// The same GEMM on 2-CTA clusters: a pair computes a 256 x 256 block of C with M = 256 pair
+// MMAs (tkb/cluster.cuh). Each CTA holds its 128 rows of the A panel and its 128-column half
+// of the B panel (32 KB per stage instead of 48), so per SM a K = 16 step reads 4 + 4 KB of
+// SMEM instead of 4 + 8 and the TMA moves a third less: six stages fit where four did.
+// Both CTAs' TMA complete on the leader's full barrier; the leader's MMA warp issues for the
+// pair and commits multicast (ring slots to both producers, accumulators to both epilogues);
+// each CTA's epilogue drains its own TMEM rows and arrives on the leader's acc_empty.
+namespace pair2 {
+constexpr int BM = 128, BN = 256, BK = 64;  // per CTA: 128 rows; pair tile 256 x 256
+#ifndef TKB_GEMM2_STAGES
+#define TKB_GEMM2_STAGES 6
+#endif
+#ifndef TKB_GEMM2_STAGING
+#define TKB_GEMM2_STAGING 2
+#endif
+constexpr int kStages = TKB_GEMM2_STAGES;
+constexpr int kStagingAtoms = TKB_GEMM2_STAGING;  // output atoms staged in flight (epilogue)
+constexpr int kATile = BM * BK * 2;         // 16 KB
+constexpr int kBHalf = BK * (BN / 2) * 2;   // 16 KB: 2 atoms of 64 K rows x 64 N cols
+constexpr int kBAtom = BK * 128;            // 8 KB
+constexpr int kStage = kATile + kBHalf;
+constexpr int kStaging = BM * 128;
+constexpr int kOffBar = kStages * kStage + kStagingAtoms * kStaging;
+constexpr int kSmemBytes = kOffBar + 256 + 1024;
+static_assert(kSmemBytes <= 232448, "smem");
+constexpr int kThreads = 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    auto sA = [&](int s) { return st_bf<BM, BK>{smem + s * kStage}; };
+    auto sB = [&](int s) { return smem + s * kStage + kATile; };  // this CTA's [BK][BN/2] MN-major half
+    uint8_t* stage_c = smem + kStages * kStage;
+    struct Bars {
+        mbarrier full[kStages], empty[kStages];
+        mbarrier acc_full[2], acc_empty[2];
+        uint32_t tmem_slot;
+    };
+    Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
+    static_assert(sizeof(Bars) <= 256, "barrier area");
+
+    const int warp = warpid();
+    const int lane = laneid();
+    const uint32_t rank = cluster::ctarank();
+    const bool leader = rank == 0;
+    const int r_blocks = (p.m + 2 * BM - 1) / (2 * BM), c_blocks = (p.n + BN - 1) / BN;
+    const int tasks = r_blocks * c_blocks;
+    const int k_tiles = (p.k + BK - 1) / BK;
+    const int pair_id = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bar.full[s], 1);
+            mbar_init(&bar.empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar.acc_full[i], 1);
+            mbar_init(&bar.acc_empty[i], 2 * 4);  // one lane per epilogue warp, both CTAs
+        }
+        fence_barrier_init();
+        tma::prefetch_desc(&p.tm_a);
+        tma::prefetch_desc(&p.tm_b);
+        tma::prefetch_desc(&p.tm_c);
+    }
+    if (warp == 1) tmem::alloc2<512>(&bar.tmem_slot);
+    tmem::fence_before();
+    cluster::sync();  // both CTAs' barriers initialised before any remote arrive / complete_tx
+    tmem::fence_after();
+    const uint32_t tbase = bar.tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------------------------------------------------------- LOAD (both CTAs)
+            lcsf::ring_state<kStages> st;
+            for (int t = pair_id; t < tasks; t += pairs) {
+                int rb, cb;
+                supergroup(t, r_blocks, c_blocks, p.super_m, rb, cb);
+                const int row0 = rb * 2 * BM + (int)rank * BM, col0 = cb * BN + (int)rank * (BN / 2);
+                for (int kt = 0; kt < k_tiles; ++kt) {
+                    mbar_wait(&bar.empty[st.slot], st.phase ^ 1u);
+                    const uint32_t fb = cluster::map(&bar.full[st.slot], 0);
+                    if (leader) mbar_arrive_expect_tx(&bar.full[st.slot], 2 * kStage);
+                    cluster::load_2d(sA(st.slot).ptr, &p.tm_a, fb, kt * BK, row0);
+#pragma unroll
+                    for (int a = 0; a < BN / 128; ++a)
+                        cluster::load_2d(sB(st.slot) + a * kBAtom, &p.tm_b, fb, col0 + a * 64, kt * BK);
+                    st.advance();
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            // -------------------------------------------------------------------- MMA (leader)
+            constexpr uint32_t idesc = umma::idesc_bf16_m256<BN, false, true>();
+            constexpr uint32_t hi = umma::desc_hi_sw128(1024);
+            lcsf::ring_state<kStages> st;
+            int n = 0;
+            for (int t = pair_id; t < tasks; t += pairs, ++n) {
+                const int buf = n & 1;
+                cluster::wait(&bar.acc_empty[buf], ((n >> 1) & 1) ^ 1u);  // both epilogues drained it
+                tmem::fence_after();
+                const uint32_t acc = tbase + buf * BN;
+                for (int kt = 0; kt < k_tiles; ++kt) {
+                    cluster::wait(&bar.full[st.slot], st.phase);
+                    tmem::fence_after();
+                    const uint32_t a0 = sA(st.slot).addr(), b0 = smem_u32(sB(st.slot));
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)  // C (+)= A B: A K-major, B MN-major (its N half per CTA)
+                        umma::mma2_ss_e(acc, umma::desc_lo(a0 + k * 32, 16), hi, umma::desc_lo(b0 + k * 16 * 128, kBAtom),
+                                        hi, idesc, (kt > 0 || k > 0) ? 1u : 0u);
+                    pair::mma_commit(&bar.empty[st.slot]);  // both CTAs may refill this slot
+                    st.advance();
+                }
+                pair::mma_commit(&bar.acc_full[buf]);
+            }
+        }
+    } else if (warp >= 4) {
+        // -------------------------------------------------------------------- FINISH (both CTAs)
+        const int wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const bool lead_thr = (warp == 4 && lane == 0);
+        const uint32_t empty_remote[2] = {cluster::map(&bar.acc_empty[0], 0), cluster::map(&bar.acc_empty[1], 0)};
+        int n = 0;
+        for (int t = pair_id; t < tasks; t += pairs, ++n) {
+            int rb, cb;
+            supergroup(t, r_blocks, c_blocks, p.super_m, rb, cb);
+            const int buf = n & 1;
+            cluster::wait(&bar.acc_full[buf], (n >> 1) & 1);
+            tmem::fence_after();
+            const uint32_t acc = tbase + lane_off + buf * BN;
+#pragma unroll 1
+            for (int a = 0; a < BN / 64; ++a) {
+                rt_fl<32> v0, v1;
+                load(v0, acc + a * 64);
+                load(v1, acc + a * 64 + 32);
+                load_wait(v0);
+                load_wait(v1);
+                if (a == BN / 64 - 1) {  // accumulator drained: the leader's MMA may reuse it
+                    tmem::fence_before();
+                    __syncwarp();
+                    if (lane == 0) cluster::arrive_remote(empty_remote[buf]);
+                }
+                rt_bf<32> b0, b1;
+                copy(b0, v0);
+                copy(b1, v1);
+                // rotating staging atoms: the one written now was last stored kStagingAtoms
+                // stores ago; wait until at most kStagingAtoms - 1 stores are still reading
+                const st_bf<BM, 64> stage{stage_c + (a % kStagingAtoms) * kStaging};
+                if (lead_thr) tma::wait_group_read<kStagingAtoms - 1>();
+                named_sync(kBarEpi, WARPGROUP_THREADS);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    sts_v4(smem_u32(stage.chunk(r, q)), make_uint4(b0.v[4 * q], b0.v[4 * q + 1], b0.v[4 * q + 2],
+                                                                   b0.v[4 * q + 3]));
+                    sts_v4(smem_u32(stage.chunk(r, 4 + q)), make_uint4(b1.v[4 * q], b1.v[4 * q + 1],
+                                                                       b1.v[4 * q + 2], b1.v[4 * q + 3]));
+                }
+                tma::fence_async_smem();
+                named_sync(kBarEpi, WARPGROUP_THREADS);
+                if (lead_thr) {
+                    tma::store_2d(&p.tm_c, stage.ptr, cb * BN + a * 64, rb * 2 * BM + (int)rank * BM);
+                    tma::commit_group();
+                }
+            }
+        }
+        if (lead_thr) tma::wait_group<0>();
+    }
+
+    tmem::fence_before();
+    cluster::sync();  // the peer's TMEM / barriers stay live until both CTAs are done
+    if (warp == 1) tmem::dealloc2<512>(tbase);
+}
+}  // namespace pair2
+
 }  // namespace gemm
 
+#ifndef TKB_GEMM_PAIRS
+#define TKB_GEMM_PAIRS 1
+#endif
+
 int launch_gemm(const GemmParams& p, int num_sms, cudaStream_t stream) {
-    static std::atomic<unsigned long long> smem_set{0};  // per device
+    static std::atomic<unsigned long long> smem_set{0}, smem_set2{0};  // per device
+    if (TKB_GEMM_PAIRS && p.m > gemm::BM) {  // CTA pairs: a 256 x 256 block of C per cluster
+        if (int e = ensure_smem(gemm::pair2::gemm2_kernel, gemm::pair2::kSmemBytes, smem_set2)) return e;
+        const int tasks = ((p.m + 2 * gemm::BM - 1) / (2 * gemm::BM)) * ((p.n + gemm::BN - 1) / gemm::BN);
+        const int pairs = tasks < num_sms / 2 ? tasks : num_sms / 2;
+        gemm::pair2::gemm2_kernel<<<2 * pairs, gemm::pair2::kThreads, gemm::pair2::kSmemBytes, stream>>>(p);
+        return (int)cudaGetLastError();
+    }
     if (int e = ensure_smem(gemm::gemm_kernel, gemm::kSmemBytes, smem_set)) return e;
     const int tasks = ((p.m + gemm::BM - 1) / gemm::BM) * ((p.n + gemm::BN - 1) / gemm::BN);
     const int grid = tasks < num_sms ? tasks : num_sms;

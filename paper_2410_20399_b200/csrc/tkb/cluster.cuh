@@ -84,6 +84,15 @@ TKB_DEVICE void load_4d(void* smem_dst, const void* tmap, uint32_t bar, int c0, 
         : "memory");
 }
 
+// 2-D variant (GEMM panels)
+TKB_DEVICE void load_2d(void* smem_dst, const void* tmap, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
 }  // namespace cluster
 
 namespace tmem {
