@@ -103,8 +103,8 @@ TKB_API int tkb_attn_fwd(const tkb_attn_desc* desc, const void* q, const void* k
  * q_rot ([B, H, N, D], q's strides) and k_rot ([B, Hkv, N, D], k's strides) — which the
  * backward then takes as its q / k — while the attention of the rotated q, k and v runs in
  * the same kernel. The workspace (tkb_attn_fwd_rotary_workspace_bytes) holds per-block
- * flags and must be zero-filled once before its first use, then reused as is; calls that
- * share a workspace must be stream-ordered. */
+ * flags, cleared on the stream before each launch (any initial contents; capturable in a
+ * CUDA graph); calls that share a workspace must be stream-ordered. */
 TKB_API size_t tkb_attn_fwd_rotary_workspace_bytes(const tkb_attn_desc* desc);
 TKB_API int tkb_attn_fwd_rotary(const tkb_attn_desc* desc, const void* q, const void* k, const void* v,
                                 const float* sin_tab, const float* cos_tab, void* q_rot, void* k_rot, void* o,

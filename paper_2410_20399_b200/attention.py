@@ -272,8 +272,8 @@ _rope_ws = {}
 
 
 def _rope_workspace(device, stream, nbytes):
-    """Zero-filled once, then reused: the fused rotary forward's block flags (one buffer per
-    (device, stream), so calls sharing it are stream-ordered as the ABI requires)."""
+    """The fused rotary forward's block flags (cleared by each call on its stream; one buffer
+    per (device, stream), so calls sharing it are stream-ordered as the ABI requires)."""
     import torch
 
     key = (device, stream)

@@ -466,8 +466,8 @@ TKB_API int tkb_attn_fwd_varlen(const tkb_attn_desc* d, const int32_t* cu_seqlen
 }
 
 // Fused rotary + forward (the rotary prologue of SURVEY §8(f) rank 2 folded into the forward
-// launch): flags of the rotated blocks live in a caller-provided workspace that must be zero
-// once before its first use; every launch publishes a new epoch, so it is never cleared again.
+// launch): flags of the rotated blocks live in a caller-provided workspace, cleared on the
+// stream before each launch (so any contents are fine and a captured graph replays correctly).
 TKB_API size_t tkb_attn_fwd_rotary_workspace_bytes(const tkb_attn_desc* d) {
     if (!d || d->seq < 1 || d->batches < 1 || d->heads < 1) return 0;
     const size_t nq = (size_t)(d->seq + 127) / 128;
@@ -527,10 +527,12 @@ TKB_API int tkb_attn_fwd_rotary(const tkb_attn_desc* d, const void* q, const voi
     p.q_sb = s.b, p.q_sh = s.h, p.q_sn = s.n;
     p.k_sb = skv.b, p.k_sh = skv.h, p.k_sn = skv.n;
     p.flags = reinterpret_cast<unsigned*>(workspace);
-    static std::atomic<unsigned> epoch{0};
-    unsigned e = epoch.fetch_add(1) + 1;
-    if (e == 0) e = epoch.fetch_add(1) + 1;  // 0 is the zeroed workspace: never a live epoch
-    p.epoch = e;
+    // The flags are cleared on the stream ahead of every launch and published as 1. (A per-call
+    // host epoch would be frozen into a captured graph: from its second replay on, the load
+    // warp would find last replay's flags already set and read stale rotated blocks.)
+    p.epoch = 1;
+    cudaError_t ce = cudaMemsetAsync(workspace, 0, tkb_attn_fwd_rotary_workspace_bytes(d), st);
+    if (ce != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("rotary flags: ") + cudaGetErrorString(ce));
     const int err = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st, true);
     if (err != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd (rotary) launch: ") + cudaGetErrorString((cudaError_t)err));
     g_launches = 1;

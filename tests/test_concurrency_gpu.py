@@ -104,3 +104,37 @@ def test_cuda_graph_capture(cuda_dev):
         ref = _step(q, k, v, do)
         torch.cuda.synchronize()
         _assert_equal(ref, (o, lse, dq, dk, dv))
+
+
+def test_cuda_graph_capture_rotary_forward(cuda_dev):
+    """The fused rotary forward publishes per-block flags that its load warp waits on; they are
+    cleared on the stream before each launch (a memset node in the graph), so every replay on
+    new inputs waits for its own rotated blocks. A per-call epoch frozen into the graph would
+    let replays 2+ read the previous replay's rotated Q / K."""
+    A.device_init(0)
+    q, k, v, _ = _inputs(400)
+    pos = torch.arange(N, device="cuda", dtype=torch.float64)[:, None]
+    freq = 10000.0 ** (-torch.arange(D // 2, device="cuda", dtype=torch.float64) / (D // 2))
+    sin, cos = (f(pos * freq[None, :]).float().contiguous() for f in (torch.sin, torch.cos))
+    o, lse = torch.empty_like(q), torch.empty((B, H, N), dtype=torch.float32, device="cuda")
+
+    def step():
+        return A.attention_fwd(q, k, v, causal=True, out=o, lse=lse, rotary_tables=(sin, cos), return_rotated=True)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        _, _, q_rot, k_rot = step()
+    for seed in (401, 402, 403):
+        for dst, src in zip((q, k, v), _inputs(seed)):
+            dst.copy_(src)
+        graph.replay()
+        torch.cuda.synchronize()
+        qr, kr = A.rotary_qk(q, k, sin, cos)
+        o_ref, l_ref = A.attention_fwd(qr, kr, v, causal=True)
+        torch.cuda.synchronize()
+        _assert_equal((qr, kr, o_ref, l_ref), (q_rot, k_rot, o, lse))

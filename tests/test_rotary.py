@@ -121,8 +121,8 @@ def test_attention_with_rotary_prologue(cuda_dev, causal):
 def test_fused_rotary_forward_equals_the_two_launch_path(cuda_dev, B, H, HKV, N, D, causal):
     """tkb_attn_fwd_rotary (one launch: the aux warps rotate Q / K block by block while the
     attention of the rotated blocks runs) gives bit-identical rotated Q / K to tkb_rotary_qk
-    and bit-identical O / L to tkb_attn_fwd on them; repeated calls (new epochs over the same
-    flag workspace) stay identical."""
+    and bit-identical O / L to tkb_attn_fwd on them; repeated calls (the flag workspace is
+    cleared by each call) stay identical."""
     from paper_2410_20399_b200 import attention as A
 
     g = torch.Generator(device="cuda").manual_seed(N + D)
