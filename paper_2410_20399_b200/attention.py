@@ -337,8 +337,10 @@ def _check_lse(lse, B, H, N, device):
         raise ShapeError(f"lse must be a contiguous fp32 CUDA tensor [B, H, N] = {(B, H, N)} on {device}")
 
 
-def bwd_workspace_bytes(B, H, N, D, causal=False):
-    cfg = AttentionConfig(B, H, N, D, causal)
+def bwd_workspace_bytes(B, H, N, D, causal=False, kv_heads=None):
+    """Bytes of the backward's workspace (tkb_attn_bwd_workspace_bytes); with few kv heads the
+    grouped-query dK/dV split adds fp32 partials, so pass kv_heads for k / v with fewer heads."""
+    cfg = AttentionConfig(B, H, N, D, causal, kv_heads=kv_heads or H)
     return int(lib().tkb_attn_bwd_workspace_bytes(ctypes.byref(cfg.desc())))
 
 

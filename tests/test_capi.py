@@ -223,3 +223,6 @@ def test_workspace_bytes_grouped_query_split():
     assert ws(8, 32, 1, 4096, 128) == base(8, 32, 4096) + 2 * 4 * 8 * 4096 * 128 * 4
     # plenty of kv heads: 16 x 64 x 8 = 8192 tasks -> no split
     assert ws(16, 64, 8, 1024, 64) == base(16, 64, 1024)
+    # the Python helper takes kv_heads too
+    assert A.bwd_workspace_bytes(2, 8, 512, 128, kv_heads=1) == ws(2, 8, 1, 512, 128)
+    assert A.bwd_workspace_bytes(2, 8, 512, 128) == ws(2, 8, 8, 512, 128)
