@@ -152,7 +152,9 @@ TKB_API int tkb_attn_bwd_varlen(const tkb_attn_desc* desc, const int32_t* cu_seq
  * oracles.hpp:66-90): for position p and i < D/2 the pair (x[p][i], x[p][i + D/2]) is
  * rotated by the angle whose sin / cos are sin_tab / cos_tab [seq, D/2] (fp32, contiguous,
  * shared by every batch and head). x, out: [B, H, N, D] bf16 with desc's strides; out may
- * alias x. D must be a multiple of 16 here (any seq). */
+ * alias x. D must be a multiple of 16 here (any seq). The rotation's transpose — the
+ * backward of the rotary prologue, taking dQ / dK of the rotated Q / K back to the inputs —
+ * is the same call with sin_tab negated (rotation by -angle). */
 TKB_API int tkb_rotary(const tkb_attn_desc* desc, const void* x, const float* sin_tab, const float* cos_tab,
                        void* out, void* stream);
 

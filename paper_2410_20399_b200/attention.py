@@ -507,23 +507,35 @@ def _autograd_fn():
     import torch
 
     class _Attention(torch.autograd.Function):
-        """O = attention(q, k, v) whose backward is tkb_attn_bwd from the saved L."""
+        """O = attention(q, k, v) whose backward is tkb_attn_bwd from the saved L. With rotary
+        tables the forward is the fused rotary launch (tkb_attn_fwd_rotary), the backward runs
+        on the rotated Q / K it returned and takes dQ / dK back through the rotation's transpose
+        — the rotation by -theta, i.e. tkb_rotary_qk with the sin table negated."""
 
         @staticmethod
-        def forward(ctx, q, k, v, causal, softmax_scale):
-            o, lse = attention_fwd(q, k, v, causal=causal, softmax_scale=softmax_scale)
-            ctx.save_for_backward(q, k, v, o, lse)
+        def forward(ctx, q, k, v, causal, softmax_scale, sin_tab, cos_tab):
+            ctx.rope = sin_tab is not None
+            if ctx.rope:
+                o, lse, q, k = attention_fwd(q, k, v, causal=causal, softmax_scale=softmax_scale,
+                                             rotary_tables=(sin_tab, cos_tab), return_rotated=True)
+                ctx.save_for_backward(q, k, v, o, lse, sin_tab, cos_tab)
+            else:
+                o, lse = attention_fwd(q, k, v, causal=causal, softmax_scale=softmax_scale)
+                ctx.save_for_backward(q, k, v, o, lse)
             ctx.causal, ctx.softmax_scale = causal, softmax_scale
             return o
 
         @staticmethod
         def backward(ctx, do):
-            q, k, v, o, lse = ctx.saved_tensors
+            q, k, v, o, lse = ctx.saved_tensors[:5]
             do = do if do.stride() == o.stride() else do.contiguous()
             if do.stride() != q.stride():  # dO must share q's layout: bring both to contiguous
                 q, o, do = q.contiguous(), o.contiguous(), do.contiguous()
             dq, dk, dv = attention_bwd(q, k, v, o, do, lse, causal=ctx.causal, softmax_scale=ctx.softmax_scale)
-            return dq, dk, dv, None, None
+            if ctx.rope:  # d(R x)/dx = R: the gradient goes back through R^T = R(-theta)
+                sin_tab, cos_tab = ctx.saved_tensors[5:]
+                dq, dk = rotary_qk(dq, dk, -sin_tab, cos_tab)
+            return dq, dk, dv, None, None, None, None
 
     return _Attention
 
@@ -531,14 +543,17 @@ def _autograd_fn():
 _ATTN_FN = None
 
 
-def attention(q, k, v, causal=False, softmax_scale=None):
+def attention(q, k, v, causal=False, softmax_scale=None, rotary_tables=None):
     """Differentiable attention for PyTorch code: O = softmax(scale q k^T [causal]) v with the
     B200 forward, and a backward (dQ, dK, dV) from the saved L — one tkb_attn_fwd launch
-    forward, tkb_attn_bwd backward; bf16 CUDA tensors [B, H, N, D] (k, v may be grouped-query)."""
+    forward, tkb_attn_bwd backward; bf16 CUDA tensors [B, H, N, D] (k, v may be grouped-query).
+    rotary_tables=(sin, cos) ([N, D/2] fp32) rotates q and k inside the forward launch; their
+    gradients come back through the inverse rotation (one tkb_rotary_qk launch)."""
     global _ATTN_FN
     if _ATTN_FN is None:
         _ATTN_FN = _autograd_fn()
-    return _ATTN_FN.apply(q, k, v, bool(causal), softmax_scale)
+    sin_tab, cos_tab = rotary_tables if rotary_tables is not None else (None, None)
+    return _ATTN_FN.apply(q, k, v, bool(causal), softmax_scale, sin_tab, cos_tab)
 
 
 @dataclass

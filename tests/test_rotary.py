@@ -164,3 +164,38 @@ def test_fused_rotary_backward_chain(cuda_dev):
     for got, ref in ((dq, rdq), (dk, rdk), (dv, rdv)):
         g = got.float().cpu().numpy()
         assert orc.max_abs(g, ref) <= 2e-2 and orc.rel_l2(g, ref) <= 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("causal,HKV", [(True, 4), (False, 2)])
+def test_autograd_attention_with_rotary_matches_torch(cuda_dev, causal, HKV):
+    """attention(q, k, v, rotary_tables=...) — the fused rotary forward, the backward on the
+    rotated Q / K, and dQ / dK back through the rotation's transpose (tkb_rotary_qk with -sin) —
+    against torch fp64 autograd through rotate -> SDPA on the same bf16 values."""
+    from paper_2410_20399_b200 import attention as A
+
+    B, H, N, D = 2, 4, 300, 128
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = (torch.empty(B, h, N, D, device="cuda").uniform_(-1, 1, generator=g).bfloat16()
+               for h in (H, HKV, HKV))
+    w = torch.empty(B, H, N, D, device="cuda").uniform_(-1, 1, generator=g)
+    pos = torch.arange(N, device="cuda", dtype=torch.float64)[:, None]
+    freq = 10000.0 ** (-torch.arange(D // 2, device="cuda", dtype=torch.float64) / (D // 2))
+    sin64, cos64 = torch.sin(pos * freq[None, :]), torch.cos(pos * freq[None, :])
+    sin, cos = sin64.float().contiguous(), cos64.float().contiguous()
+    qa, ka, va = (x.clone().requires_grad_() for x in (q, k, v))
+    loss = (A.attention(qa, ka, va, causal=causal, rotary_tables=(sin, cos)).float() * w).sum()
+    loss.backward()
+
+    def rot(x):  # oracle_rotary (oracles.hpp:66-90) in fp64
+        x1, x2 = x[..., : D // 2], x[..., D // 2:]
+        return torch.cat([x1 * cos64 - x2 * sin64, x2 * cos64 + x1 * sin64], dim=-1)
+
+    qr, kr, vr = (x.double().requires_grad_() for x in (q, k, v))
+    kre, vre = rot(kr).repeat_interleave(H // HKV, dim=1), vr.repeat_interleave(H // HKV, dim=1)
+    ref = torch.nn.functional.scaled_dot_product_attention(rot(qr), kre, vre, is_causal=causal)
+    (ref * w.double()).sum().backward()
+    for got, want in ((qa.grad, qr.grad), (ka.grad, kr.grad), (va.grad, vr.grad)):
+        assert got.dtype == torch.bfloat16 and got.shape == want.shape
+        err = (got.double() - want).abs().max().item()
+        assert err <= 2e-2 * max(1.0, want.abs().max().item() / 4), err
