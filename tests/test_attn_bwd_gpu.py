@@ -136,3 +136,24 @@ def test_autograd_function_matches_torch(cuda_dev, causal):
         assert got.dtype == torch.bfloat16 and got.shape == want.shape
         err = (got.double() - want).abs().max().item()
         assert err <= MAX_ABS * max(1.0, want.abs().max().item() / 4), err
+
+
+def test_autograd_function_bnhd_views(cuda_dev):
+    """attention() on [B, N, H, D] storage seen as [B, H, N, D] views (the layout of a fused QKV
+    projection): the forward reads the strided views through TMA, dO arrives contiguous from the
+    loss and the backward brings q / o / dO to one layout; gradients equal torch fp64 SDPA."""
+    B, H, N, D = 2, 4, 260, 64
+    g = torch.Generator(device="cuda").manual_seed(9)
+    base = [torch.empty(B, N, H, D, device="cuda").uniform_(-1, 1, generator=g).bfloat16() for _ in range(3)]
+    w = torch.empty(B, H, N, D, device="cuda").uniform_(-1, 1, generator=g)
+    qa, ka, va = (x.clone().requires_grad_() for x in base)
+    loss = (A.attention(qa.transpose(1, 2), ka.transpose(1, 2), va.transpose(1, 2), causal=True).float() * w).sum()
+    loss.backward()
+    qr, kr, vr = (x.double().requires_grad_() for x in base)
+    ref = torch.nn.functional.scaled_dot_product_attention(qr.transpose(1, 2), kr.transpose(1, 2), vr.transpose(1, 2),
+                                                           is_causal=True)
+    (ref * w.double()).sum().backward()
+    for got, want in ((qa.grad, qr.grad), (ka.grad, kr.grad), (va.grad, vr.grad)):
+        assert got.shape == want.shape
+        err = (got.double() - want).abs().max().item()
+        assert err <= MAX_ABS * max(1.0, want.abs().max().item() / 4), err
