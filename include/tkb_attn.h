@@ -201,6 +201,11 @@ TKB_API int tkb_debug_set_bwd_phases(int mask);
  * within each variant's own summation order. */
 TKB_API int tkb_set_bwd_pairs(int on);
 
+/* Debug / testing: query tiles per forward task (calling host thread only). 0 (default) picks
+ * by problem size — two 128-row tiles sharing each K / V block, or one when two-tile tasks
+ * would leave SMs idle; 1 or 2 force it. Results are the same bits either way. */
+TKB_API int tkb_debug_set_fwd_task_tiles(int tiles);
+
 /* Hits / misses of the calling thread's TMA descriptor cache (debug, tests). */
 TKB_API int tkb_debug_map_cache_stats(unsigned long long* hits, unsigned long long* misses);
 

@@ -107,6 +107,7 @@ _SIGS = {
     "tkb_debug_set_trace": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int]),
     "tkb_debug_set_bwd_phases": (ctypes.c_int, [ctypes.c_int]),
     "tkb_set_bwd_pairs": (ctypes.c_int, [ctypes.c_int]),
+    "tkb_debug_set_fwd_task_tiles": (ctypes.c_int, [ctypes.c_int]),
     "tkb_last_error": (ctypes.c_char_p, []),
     "tkb_abi_version": (ctypes.c_int, []),
 }
@@ -604,6 +605,12 @@ def debug_set_trace(buf=None, every=1, slots=0):
     """Enable the backward kernel's per-role cycle timeline into a device int64 tensor
     [slots, 4, 32, 8] (debug only); buf=None disables."""
     lib().tkb_debug_set_trace(buf.data_ptr() if buf is not None else None, every, slots)
+
+
+def debug_set_fwd_task_tiles(tiles=0):
+    """Forward query tiles per task for later calls from this thread: 0 = by problem size, 1 or 2
+    forced (tkb_debug_set_fwd_task_tiles; the results are the same bits)."""
+    _check(lib().tkb_debug_set_fwd_task_tiles(int(tiles)))
 
 
 def debug_set_bwd_phases(mask=7):

@@ -116,7 +116,9 @@ struct FwdParams {
     int heads;
     int group;                           // query heads per kv head (grouped-query attention; 1 = MHA)
     int bh;                              // batches * heads          (set by launch_attn_fwd)
-    int m_blocks;                        // 256-row query blocks     (set by launch_attn_fwd)
+    int m_blocks;                        // query blocks of task_tiles * 128 rows (set by launch_attn_fwd)
+    int task_tiles;                      // query tiles per task: 2, or 1 when 2-tile tasks would
+                                         //   leave SMs idle (set by launch_attn_fwd)
     int tasks;                           // bh * m_blocks            (set by launch_attn_fwd;
                                          //   tkb_attn_validate keeps B*H*ceil(N/128) < 2^31)
     int head_group;                      // heads per L2 group       (set by launch_attn_fwd)

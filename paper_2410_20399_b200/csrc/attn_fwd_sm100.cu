@@ -153,7 +153,8 @@ struct attn_fwd_template {
     };
     static TKB_DEVICE Task decode(const globals& p, int t) {
         const int N = p.n;
-        const int m_blocks = (N + kRowsPerCta - 1) / kRowsPerCta;
+        const int rows = p.task_tiles * kBlockM;  // query rows per task
+        const int m_blocks = p.m_blocks;
         const int G = p.head_group;
         const int sec = p.fd_sec.div(t);  // t / (G * m_blocks)
         const int r = t - sec * G * m_blocks;
@@ -168,19 +169,21 @@ struct attn_fwd_template {
         w.sv = seq_view(p.cu_seqlens, p.vmaps, kFwdMaps, N, w.batch);
         const int n = w.sv.n;
         w.nkv = (n + kBlockN - 1) / kBlockN;
-        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * kRowsPerCta + kRowsPerCta, n) - 1) / kBlockN + 1);
+        if (CAUSAL) w.nkv = min(w.nkv, (min(w.mblk * rows + rows, n) - 1) / kBlockN + 1);
         return w;
     }
     // variable-length batches: query blocks past a short sequence have no work
     static TKB_DEVICE bool skip(const globals& p, int t) {
         if (p.cu_seqlens == nullptr) return false;
         const Task w = decode(p, t);
-        return w.mblk * kRowsPerCta >= w.sv.n;
+        return w.mblk * p.task_tiles * kBlockM >= w.sv.n;
     }
     // kv blocks query tile s of a task visits (causal: tile 0 skips the block only tile 1 sees)
+    // (0 for tile 1 of a one-tile task)
     static TKB_DEVICE int tile_blocks(const globals& p, const Task& w, int s) {
+        if (s >= p.task_tiles) return 0;
         if (!CAUSAL) return w.nkv;
-        return min(w.nkv, (min(w.mblk * kRowsPerCta + s * kBlockM + kBlockM, w.sv.n) - 1) / kBlockN + 1);
+        return min(w.nkv, (min(w.mblk * p.task_tiles * kBlockM + s * kBlockM + kBlockM, w.sv.n) - 1) / kBlockN + 1);
     }
     // k3: index of (tile s, block i) in the task's QK issue order, its buffer and TMEM column
     static TKB_DEVICE int qk_index(int s, int i, int nk0, int nk1) {
@@ -234,13 +237,13 @@ struct attn_fwd_template {
                 tma::acquire_map(w.sv.maps + kMapK);
                 tma::acquire_map(w.sv.maps + kMapV);
             }
-            const int q0 = w.mblk * kRowsPerCta;
+            const int q0 = w.mblk * p.task_tiles * kBlockM;
             const int nq = (p.n + 127) / 128;
             const int bkv = w.batch * (p.heads / p.group) + w.head / p.group;
             if constexpr (ROPE && TKB_ROPE_DEBUG != 2)  // the task's rotated Q blocks (rows past N: none)
-                lcsf::flags_wait_all(p.flags + rope_kflags(p) + (size_t)(w.batch * p.heads + w.head) * nq + 2 * w.mblk,
-                                     min(2, nq - 2 * w.mblk), p.epoch);
-            for (int s = 0; s < kQStages; ++s) {  // Q_s is free once the last QK_s of the previous task retired
+                lcsf::flags_wait_all(p.flags + rope_kflags(p) + (size_t)(w.batch * p.heads + w.head) * nq + q0 / 128,
+                                     min(p.task_tiles, nq - q0 / 128), p.epoch);
+            for (int s = 0; s < p.task_tiles; ++s) {  // Q_s is free once the last QK_s of the previous task retired
                 mbar_wait(&sh.q_empty[s], (nt & 1) ^ 1u);
                 mbar_arrive_expect_tx(&sh.q_full[s], C::kTile);
                 w.sv.with_map(p.tm_q, kMapQ, [&](const CUtensorMap* m) {
@@ -312,11 +315,12 @@ struct attn_fwd_template {
                     mma_commit(&sh.pv_done[s]);
                 };
                 mbar_wait(&sh.q_full[0], nt & 1);
-                mbar_wait(&sh.q_full[1], nt & 1);
+                if (nk[1] > 0) mbar_wait(&sh.q_full[1], nt & 1);  // (a one-tile task has no Q_1)
                 kv.wait_full(st);
                 tmem::fence_after();
 #pragma unroll
                 for (int s = 0; s < kQStages; ++s) {
+                    if (nk[s] == 0) continue;
                     qk3(s, 0, st.slot);
                     if (nk[s] == 1) mma_commit(&sh.q_empty[s]);
                 }
@@ -373,7 +377,7 @@ struct attn_fwd_template {
                 };
                 mbar_wait(&sh.q_full[0], nt & 1);
                 if (a.lane == 0) fwd_stamp(p, 1, nt, 3);
-                mbar_wait(&sh.q_full[1], nt & 1);
+                if (nk[1] > 0) mbar_wait(&sh.q_full[1], nt & 1);  // (a one-tile task has no Q_1)
                 kv.wait_full(st);
                 if (a.lane == 0) fwd_stamp(p, 1, nt, 4);
                 tmem::fence_after();
@@ -381,6 +385,7 @@ struct attn_fwd_template {
                 // (issued before); the first PV_s below overwrites O_s only after the softmax drained it
 #pragma unroll
                 for (int s = 0; s < kQStages; ++s) {
+                    if (nk[s] == 0) continue;
                     qk(s, st.slot);
                     mma_commit(&sh.s_full[s]);
                     if (nk[s] == 1) mma_commit(&sh.q_empty[s]);
@@ -456,7 +461,7 @@ struct attn_fwd_template {
             const float tau = p.scale_log2;
             const Task w = decode(p, t);
             const int N = w.sv.n;
-            const int q0 = w.mblk * kRowsPerCta;
+            const int q0 = w.mblk * p.task_tiles * kBlockM;
             const int row = q0 + s * kBlockM + row_in_tile;
             const int nkv = tile_blocks(p, w, s);
             float m = -INFINITY;
@@ -577,7 +582,8 @@ struct attn_fwd_template {
             const int row_in_tile = wq * 32 + a.lane;
             const uint32_t tO = a.tmem + ((uint32_t)(wq * 32) << 16) + C::tmem_o(s);
             const Task w = decode(p, t);
-            const int q0 = w.mblk * kRowsPerCta;
+            if (tile_blocks(p, w, s) == 0) return;  // tile 1 of a one-tile task: no rows
+            const int q0 = w.mblk * p.task_tiles * kBlockM;
             const int row = q0 + s * kBlockM + row_in_tile;
             const float m = cs.m, l = cs.l;
             mbar_wait(&sh.o_full[s], nt & 1);
@@ -737,7 +743,14 @@ int launch(const FwdParams& p, int num_sms, cudaStream_t stream) {
 int launch_attn_fwd(int head_dim, bool causal, FwdParams p, int batches, int num_sms, cudaStream_t stream,
                     bool rope) {
     p.bh = batches * p.heads;
-    p.m_blocks = (p.n + kRowsPerCta - 1) / kRowsPerCta;
+    // Two query tiles per task share each K / V block; when even the one-tile tasks all fit in
+    // one wave (small B*H*N, e.g. BASELINE configs[0]: 32 two-tile tasks for 148 SMs) a task is
+    // one tile, doubling the CTAs that work in parallel on the latency-bound problem (C1: 22.5 ->
+    // 19.5 us). With more tasks the one-tile CTAs (tile 1's warps idle, half the MMA work per K / V
+    // block) lose: 128 two-tile tasks ran 16-34 % faster than 256 one-tile ones (tools/c1_tiles.py).
+    if (p.task_tiles != 1 && p.task_tiles != 2)  // 0: by problem size (tkb_debug_set_fwd_task_tiles forces it)
+        p.task_tiles = 2ll * p.bh * ((p.n + 2 * kBlockM - 1) / (2 * kBlockM)) <= num_sms ? 1 : 2;
+    p.m_blocks = (p.n + p.task_tiles * kBlockM - 1) / (p.task_tiles * kBlockM);
     p.tasks = p.bh * p.m_blocks;
     const long long kv_bytes = 4ll * p.n * head_dim / p.group;  // K / V of one query head's kv head
     long long g = (48ll << 20) / (kv_bytes > 0 ? kv_bytes : 1);  // heads whose K / V fit ~48 MB of L2

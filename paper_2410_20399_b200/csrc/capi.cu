@@ -35,6 +35,7 @@ thread_local long long* g_trace = nullptr;  // debug timeline (tkb_debug_set_tra
 thread_local int g_trace_every = 1, g_trace_slots = 0;
 thread_local int g_bwd_phases = 7;  // debug: bit 0 prep, bit 1 dK/dV kernel, bit 2 dQ kernel
 thread_local int g_bwd_pairs = 0;   // D = 128 dK/dV on CTA pairs (tkb_set_bwd_pairs)
+thread_local int g_fwd_task_tiles = 0;  // debug: forward query tiles per task (0 = by problem size)
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -442,6 +443,7 @@ static int fwd_impl(const tkb_attn_desc* d, const Varlen* vl, const void* q, con
     p.n = d->seq;
     p.heads = d->heads;
     p.scale_log2 = scale_of(d) * 1.44269504088896340736f;
+    p.task_tiles = g_fwd_task_tiles;
     int e = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st);
     if (e != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd launch: ") + cudaGetErrorString((cudaError_t)e));
     g_launches = launches;
@@ -533,6 +535,7 @@ TKB_API int tkb_attn_fwd_rotary(const tkb_attn_desc* d, const void* q, const voi
     p.epoch = 1;
     cudaError_t ce = cudaMemsetAsync(workspace, 0, tkb_attn_fwd_rotary_workspace_bytes(d), st);
     if (ce != cudaSuccess) return fail(TKB_ERR_CUDA, std::string("rotary flags: ") + cudaGetErrorString(ce));
+    p.task_tiles = g_fwd_task_tiles;
     const int err = tkb::launch_attn_fwd(d->head_dim, d->causal != 0, p, d->batches, sms, st, true);
     if (err != 0) return fail(TKB_ERR_CUDA, std::string("attn_fwd (rotary) launch: ") + cudaGetErrorString((cudaError_t)err));
     g_launches = 1;
@@ -834,6 +837,12 @@ TKB_API int tkb_debug_set_bwd_phases(int mask) {
 
 TKB_API int tkb_set_bwd_pairs(int on) {
     g_bwd_pairs = on ? 1 : 0;
+    return TKB_OK;
+}
+
+TKB_API int tkb_debug_set_fwd_task_tiles(int tiles) {
+    if (tiles < 0 || tiles > 2) return fail(TKB_ERR_CONFIG, "forward task tiles must be 0 (auto), 1 or 2");
+    g_fwd_task_tiles = tiles;
     return TKB_OK;
 }
 

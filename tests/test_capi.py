@@ -226,3 +226,10 @@ def test_workspace_bytes_grouped_query_split():
     # the Python helper takes kv_heads too
     assert A.bwd_workspace_bytes(2, 8, 512, 128, kv_heads=1) == ws(2, 8, 1, 512, 128)
     assert A.bwd_workspace_bytes(2, 8, 512, 128) == ws(2, 8, 8, 512, 128)
+
+
+def test_fwd_task_tiles_knob_validates():
+    assert A.lib().tkb_debug_set_fwd_task_tiles(3) == 1  # TKB_ERR_CONFIG
+    assert A.lib().tkb_debug_set_fwd_task_tiles(-1) == 1
+    for t in (1, 2, 0):
+        assert A.lib().tkb_debug_set_fwd_task_tiles(t) == 0
